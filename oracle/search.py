@@ -1,0 +1,198 @@
+"""ORACLE (test infrastructure only) — greedy, batched/pruned greedy, beam search.
+
+* greedy_def: "we use greedy search in all submissions";
+  argmax over raw logits — "remove the log_softmax in the output layer for
+  greedy search" — ties to the lowest id (reading R13).  A
+  sentence finishes on EOS or after cap_i = min(200, tgt_cap_i) generated
+  tokens (reading R12).  Uses O-def (no cache).
+  Pinned: == translate_fast (cached, batched, pruned) token for token;
+  argmax(logits) == argmax(log_softmax(logits)).
+* translate_fast: dynamic batches, cached decoding
+   and batch pruning — "we prune the finished hypotheses in a
+  batch during decoding" — with reading R18: a decision
+  point after every ``prune_every`` steps; if #done >= max(1, ceil(rho B_live))
+  (or all done) the live rows are compacted stably, new_to_old = ascending
+  indices of the not-done rows.  Finished-but-unpruned rows keep computing and
+  their tokens are ignored.  Pinned: outputs invariant to rho and to batching;
+  == greedy_def.
+* beam_search: "the search ends when any candidate predicts the EOS symbol,
+  and there are no candidates with higher scores", reading R15:
+  score = sum of log_softmax (no length penalty, R16); candidates (slot, v)
+  ordered by (score desc, slot*V + v asc), first 2K kept; EOS candidates ranked
+  < K are finalised; the first K non-EOS become the next active set; stop when
+  fin is non-empty and max fin >= max active, or at the cap (actives finalised).
+  Pinned: K >= V^T equals ``exhaustive_best`` (brute force); K = 1 == greedy;
+  early stop on == off.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from synth.config import BOS_ID, EOS_ID
+from .nn import log_softmax
+from .batching import plan_batches
+
+
+def _cap(cfg, c):
+    return int(min(cfg.max_tgt_len, int(c)))
+
+
+# ------------------------------------------------------------------ greedy (def)
+def greedy_def(model, src, cap: int, return_logits: bool = False):
+    enc = model.encode_def(src)
+    prefix = [BOS_ID]
+    out, logits_all = [], []
+    cap = _cap(model.cfg, cap)
+    while True:
+        logits = model.decoder_logits_def(enc, prefix)
+        logits_all.append(logits)
+        w = int(np.argmax(logits))
+        out.append(w)
+        prefix.append(w)
+        if w == EOS_ID or len(out) == cap:
+            break
+    toks = out[:-1] if out[-1] == EOS_ID else out
+    return (toks, np.array(logits_all)) if return_logits else toks
+
+
+# ------------------------------------------------------ greedy (fast, batched)
+def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
+                   prune_every: int = 1, prune_ratio: float = 0.25, log: dict | None = None):
+    """Greedy translation of a Workload; returns list of outputs in input order.
+
+    ``log`` (optional dict) receives 'prunes': [(batch, step, new_to_old)],
+    'gen_tokens', 'steps', 'batches'.
+    """
+    cfg = model.cfg
+    lens = wl.lengths()
+    batches = plan_batches(lens, max_tokens, max_sents)
+    outputs = [None] * wl.n
+    prunes = []
+    gen_tokens = 0
+    steps = 0
+    for bi, idx in enumerate(batches):
+        srcs = [wl.sentence(i) for i in idx]
+        caps = np.array([_cap(cfg, wl.caps[i]) for i in idx])
+        enc, src_len = model.encode_batch(srcs)
+        ckv = model.cross_kv(enc)
+        B = len(idx)
+        cache = model.new_cache(B, int(caps.max()))
+        rows = np.arange(B)                 # live row -> batch slot
+        tok = np.full(B, BOS_ID, dtype=np.int64)
+        done = np.zeros(B, dtype=bool)
+        gen = [[] for _ in range(B)]
+        t = 0
+        while True:
+            logits = model.decoder_step(tok, t, cache, ckv, src_len)
+            nxt = np.argmax(logits, axis=1)
+            for r, s in enumerate(rows):
+                if not done[r]:
+                    gen[s].append(int(nxt[r]))
+                    if nxt[r] == EOS_ID or len(gen[s]) == caps[s]:
+                        done[r] = True
+            tok = nxt
+            t += 1
+            steps += 1
+            if done.all():
+                break
+            if prune_ratio is not None and prune_ratio >= 0 and t % prune_every == 0:
+                need = max(1, math.ceil(prune_ratio * len(rows)))
+                if done.sum() >= need:
+                    keep = np.nonzero(~done)[0]
+                    prunes.append((bi, t - 1, keep.copy()))
+                    rows, tok, done, src_len = rows[keep], tok[keep], done[keep], src_len[keep]
+                    cache = [(K[keep], V[keep]) for K, V in cache]
+                    ckv = [(K[keep], V[keep]) for K, V in ckv]
+        for s, i in enumerate(idx):
+            g = gen[s]
+            gen_tokens += len(g)
+            outputs[i] = g[:-1] if g and g[-1] == EOS_ID else g
+    if log is not None:
+        log.update(prunes=prunes, gen_tokens=gen_tokens, steps=steps, batches=batches)
+    return outputs
+
+
+# ----------------------------------------------------------------- beam search
+def prefix_logprobs(model, enc_kv, src_len, prefixes):
+    """log_softmax of next-token logits for each prefix (cached recompute)."""
+    out = []
+    for pre in prefixes:
+        T = len(pre)
+        cache = model.new_cache(1, T)
+        for t in range(T):
+            logits = model.decoder_step(np.array([pre[t]]), t, cache, enc_kv, src_len)
+        out.append(log_softmax(logits[0]))
+    return out
+
+
+def beam_search(model, src, cap: int, K: int, early_stop: bool = True, step_logprobs=None):
+    """Single-sentence beam search (reading R15).  Returns (tokens, score)."""
+    cfg = model.cfg
+    V = cfg.vocab_size
+    cap = _cap(cfg, cap)
+    enc, src_len = model.encode_batch([src])
+    ckv = model.cross_kv(enc)
+    if step_logprobs is None:
+        def step_logprobs(prefixes):
+            return prefix_logprobs(model, ckv, src_len, prefixes)
+    active = [(0.0, [BOS_ID])]
+    fin = []           # (score, tokens, order)
+    order = 0
+    for t in range(cap):
+        lps = step_logprobs([h[1] for h in active])
+        cand_s = np.concatenate([a[0] + lp for a, lp in zip(active, lps)])
+        # order by (score desc, slot*V + v asc): lexsort keys are ascending, last key primary
+        flat = np.arange(len(cand_s))
+        sel = np.lexsort((flat, -cand_s))[:2 * K]
+        new_active = []
+        for rank, c in enumerate(sel):
+            slot, v = divmod(int(c), V)
+            sc = float(cand_s[c])
+            if v == EOS_ID:
+                if rank < K:
+                    fin.append((sc, active[slot][1] + [v], order)); order += 1
+            elif len(new_active) < K:
+                new_active.append((sc, active[slot][1] + [v]))
+        if t + 1 == cap:
+            for sc, toks in new_active:
+                fin.append((sc, toks, order)); order += 1
+            break
+        active = new_active
+        if not active:
+            break
+        if early_stop and fin and max(f[0] for f in fin) >= max(a[0] for a in active):
+            break
+    best = sorted(fin, key=lambda f: (-f[0], f[2]))[0]
+    toks = best[1][1:]
+    if toks and toks[-1] == EOS_ID:
+        toks = toks[:-1]
+    return toks, best[0]
+
+
+def exhaustive_best(model, src, cap: int):
+    """Brute force over every sequence of length <= cap (EOS-terminated or cap-long)."""
+    cfg = model.cfg
+    cap = _cap(cfg, cap)
+    enc, src_len = model.encode_batch([src])
+    ckv = model.cross_kv(enc)
+    best = (-math.inf, None)
+
+    def rec(prefix, score):
+        nonlocal best
+        lp = prefix_logprobs(model, ckv, src_len, [prefix])[0]
+        for v in range(cfg.vocab_size):
+            s = score + float(lp[v])
+            seq = prefix + [v]
+            if v == EOS_ID or len(seq) - 1 == cap:
+                if s > best[0]:
+                    best = (s, seq[1:])
+            else:
+                rec(seq, s)
+
+    rec([BOS_ID], 0.0)
+    toks = best[1]
+    if toks and toks[-1] == EOS_ID:
+        toks = toks[:-1]
+    return toks, best[0]

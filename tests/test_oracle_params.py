@@ -1,0 +1,51 @@
+"""Pin the architecture reading (shapes / tied E / RPR tables / F=2048) to the
+parameter counts and FP16 sizes printed in PAPER.md (tests/golden/param_counts.txt)."""
+import os
+
+from synth import PRESETS, param_count
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "param_counts.txt")
+
+
+def _golden():
+    rows = {}
+    for line in open(GOLD):
+        line = line.split("#")[0].strip()
+        if line:
+            name, val, *_ = line.split()
+            rows[name] = float(val)
+    return rows
+
+
+def test_param_counts_match_tables():
+    g = _golden()
+    for name in ("teacher-40-6", "student-35-6", "student-35-1", "student-18-1", "student-9-1"):
+        n = param_count(PRESETS[name], include_dlcl=False)
+        assert round(n / 1e6) == g[name], (name, n)
+    ens = (2 * param_count(PRESETS["student-35-6"], False) + 2 * param_count(PRESETS["teacher-40-6"], False))
+    assert round(ens / 1e6) == g["ensemble"]
+
+
+def test_dlcl_adds_negligible_params():
+    # Table 1 prints the same size with and without DLCL
+    for name in ("student-35-6", "teacher-40-6"):
+        c = PRESETS[name]
+        assert round(param_count(c, True) / 1e6) == round(param_count(c, False) / 1e6)
+
+
+def test_fp16_file_sizes():
+    g = _golden()
+    # "291 MiB when stored in 16-bit floats": 152.03M x 2 B = 290.0 MiB
+    mib = param_count(PRESETS["student-35-6"], False) * 2 / 2 ** 20
+    assert abs(mib - g["fp16_mib:student-35-6"]) <= 1.5
+    # Table 3 "MiB" column is MB of FP16 params within ~1% (header / metadata)
+    for name in ("student-35-6", "student-35-1", "student-18-1", "student-9-1"):
+        mb = param_count(PRESETS[name], False) * 2 / 1e6
+        ref = g["fp16_mb:" + name]
+        assert 0 <= ref - mb <= 0.012 * ref, (name, mb, ref)
+
+
+def test_ffn_width_is_2048():
+    # F=2048 is the only power-of-two width reproducing 131M for 35-1
+    hits = [F for F in (1024, 2048, 4096) if round(param_count(PRESETS["student-35-1"].replace(d_ffn=F), False) / 1e6) == 131]
+    assert hits == [2048]
