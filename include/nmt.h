@@ -1,0 +1,183 @@
+/*
+ * nmt.h — C ABI of the B200-native NiuTrans-WNGT2020 translation hot path.
+ *
+ * The path (PAPER.md = arXiv 2109.08008, cited by line):
+ *   encoder: deep pre-norm Transformer with relative position representations
+ *            (Shaw et al., clip 8) and the dynamic linear
+ *            combination of layers x_{l+1} = sum_k W_k^{(l+1)} LN(y_k)
+ *            (Eq. 1-2);
+ *   decoder: incremental greedy decoding with cached self-attention K/V and
+ *            encoder-decoder K/V projected once per sentence,
+ *            tied 32K-vocab projection fused with argmax — no log_softmax for
+ *            greedy — and batch pruning of finished sentences
+ *             over length-sorted dynamic batches
+ *             in FP16 with FP32 reductions
+ *            (PAPER.md:122-123).
+ * Readings where the paper is silent are listed in DESIGN.md ("Readings").
+ *
+ * Conventions
+ *   - Every call returns nmt_status (NMT_OK == 0); details in nmt_last_error().
+ *     No C++ exception crosses the ABI.
+ *   - h_* = host pointer, d_* = device pointer on the model's device.
+ *     The caller owns every buffer passed in; the library never frees them.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are stream-ordered and asynchronous unless documented otherwise.
+ *   - All device memory the path needs is allocated once by nmt_load_weights
+ *     (the paper's memory pool): encode / decode / prune /
+ *     translate never call cudaMalloc.
+ *   - Token ids: PAD 0, UNK 1, BOS 2, EOS 3; sources end with EOS.
+ */
+#ifndef NMT_H_
+#define NMT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NMT_OK = 0,
+  NMT_E_ARG = 1,         /* null / negative / out-of-range argument                 */
+  NMT_E_SHAPE = 2,       /* dimension mismatch or limit exceeded (message has both)  */
+  NMT_E_INPUT = 3,       /* token id outside [0,V) or source longer than max_src_len */
+  NMT_E_STATE = 4,       /* call out of sequence (e.g. step != batch step)           */
+  NMT_E_FORMAT = 5,      /* bad NTSD magic / version                                 */
+  NMT_E_INTEGRITY = 6,   /* missing / duplicate / mis-shaped tensor, truncated blob   */
+  NMT_E_RESOURCE = 7,    /* device allocation failed at load                          */
+  NMT_E_CUDA = 8,        /* CUDA error (message from cudaGetErrorString)              */
+  NMT_E_UNSUPPORTED = 9  /* feature not built (e.g. precision / shape not supported)  */
+} nmt_status;
+
+typedef enum { NMT_FP32 = 0, NMT_FP16 = 1 } nmt_precision;
+
+/* Model hyper-parameters, stored in the NTSD config block. */
+typedef struct {
+  int32_t enc_layers, dec_layers, d_model, n_heads, d_ffn, vocab_size;
+  int32_t max_rel_pos;            /* 8: "maximum relative length was 8"        */
+  int32_t use_dlcl, use_rpr, dlcl_ln;
+  int32_t max_src_len, max_tgt_len; /* 120 / 200                               */
+  int32_t max_pos;                /* 1024                                      */
+  int32_t pad_id, unk_id, bos_id, eos_id;
+  float ln_eps;                   /* 1e-5 (reading R10)                                      */
+} nmt_config;
+
+/* Sizes the arena is allocated for (nmt_load_weights). */
+typedef struct {
+  int32_t max_tokens;   /* padded source tokens per batch: n_sent * s_max <= max_tokens          */
+  int32_t max_sents;    /* sentences per batch (PAPER.md:138 uses 512)                           */
+  int32_t max_tgt_len;  /* <= config max_tgt_len; decode steps per batch                          */
+  int32_t beam;         /* 1 = greedy                                                              */
+} nmt_limits;
+
+typedef struct nmt_model nmt_model;   /* opaque: device weights + arena */
+typedef struct nmt_batch nmt_batch;   /* opaque: one encoded batch living in the model's arena */
+
+/* Load an NTSD blob (host memory, `nbytes`): magic "NTSD", version 1, config block,
+ * named tensors (FP16 or FP32).  Weights are converted to `prec` on the device.
+ * Errors: NMT_E_FORMAT, NMT_E_INTEGRITY (no partial model is returned), NMT_E_RESOURCE. */
+nmt_status nmt_load_weights(const void* h_ntsd, size_t nbytes, int device, nmt_precision prec,
+                            const nmt_limits* lim, nmt_model** out);
+nmt_status nmt_get_config(const nmt_model* m, nmt_config* out);
+void nmt_free_model(nmt_model* m);
+
+/* Encode one batch (encoder output and per-decoder-layer cross K/V
+ * are computed once here and cached).
+ *   d_src     [n_sent][s_max] int32 row-major, PAD-filled, each row EOS-terminated
+ *   h_src_len [n_sent] lengths incl. EOS, 1 <= len <= s_max
+ *   h_tgt_cap [n_sent] per-sentence cap on generated tokens (NULL = max_tgt_len)
+ * Requires n_sent <= max_sents, n_sent*s_max <= max_tokens, s_max <= max_src_len.
+ * Only one batch per model may be live; encoding a new one invalidates the previous. */
+nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_len,
+                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, void* stream,
+                      nmt_batch** out);
+
+/* Copy the batch's encoder output enc [n_sent][s_max][d] as FP32 into d_dst (parity/debug). */
+nmt_status nmt_batch_encoder_output(const nmt_batch* b, float* d_dst, void* stream);
+
+/* Per-step outputs; every pointer optional (NULL = not written). Sizes are n_live rows
+ * of the live batch *before* this step's pruning. */
+typedef struct {
+  int32_t* d_next;    /* [n_live]    argmax token per live row (ties -> lowest id)   */
+  uint8_t* d_done;    /* [n_live]    row finished (EOS or cap) at or before this step */
+  float* d_logits;    /* [n_live][V] FP32 logits (parity / debug; slows the step)      */
+} nmt_step_out;
+
+/* One greedy decode step t for all live rows: embed w_t, cached RPR self-attention
+ * (appends k_t, v_t), cross-attention on the cached encoder K/V, FFN, final LN,
+ * tied vocab projection fused with argmax.  `step` must equal the batch's step count.
+ *   d_prev: [n_live] tokens w_t to feed (teacher forcing); NULL = the tokens this
+ *           batch chose at step t-1 (BOS at t = 0) — the normal, sync-free path. */
+nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, int32_t step,
+                           const nmt_step_out* out, void* stream);
+
+/* Batch pruning (reading R18): if #done >= max(1, ceil(ratio*n_live))
+ * (ratio < 0: never, except when every row is done), compact the live rows stably.
+ *   d_new_to_old [n_live] (optional): ascending pre-prune indices of surviving rows;
+ *                 entries past the new count are -1.  Unchanged identity if no prune.
+ *   h_n_live (optional): new live count — synchronises the stream when non-NULL. */
+nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_new_to_old,
+                           int32_t* h_n_live, void* stream);
+
+/* Number of live rows (synchronises the stream). */
+nmt_status nmt_batch_live(nmt_batch* b, int32_t* h_n_live, void* stream);
+
+/* Results in batch order (synchronous): h_ids [n_sent][max_tgt_len] generated tokens
+ * (EOS included when produced), h_len [n_sent] generated counts. */
+nmt_status nmt_batch_results(nmt_batch* b, int32_t* h_ids, int32_t* h_len, void* stream);
+
+typedef struct {
+  int32_t max_tokens;    /* dynamic-batch token budget, <= limits */
+  int32_t max_sents;     /* sentence cap per batch, <= limits     */
+  int32_t prune_every;   /* decision point every c steps (>= 1)                  */
+  float prune_ratio;     /* rho (0.25); < 0 = never prune                        */
+  int32_t sync_every;    /* host polls the live count every k steps (>= 1)       */
+  const int32_t* h_tgt_cap; /* optional [n] per-sentence caps (synthetic workloads) */
+} nmt_translate_opts;
+
+typedef struct {
+  int64_t sentences, src_tokens, gen_tokens, out_tokens, decode_steps, prunes, batches, launches;
+  double ms_total;
+} nmt_stats;
+
+/* Whole translation with HOST buffers (synchronous): length sort, dynamic batches,
+ * encode, greedy decode with pruning, output in the original order
+ * with the terminating EOS stripped.
+ *   h_ids [h_off[n]] int32 flat EOS-terminated sources, h_off [n+1] int64.
+ *   h_out [out_cap] receives the flat outputs, h_out_off [n+1] their offsets.
+ * Sources longer than max_src_len are rejected (NMT_E_INPUT). */
+nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
+                         const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
+                         int64_t* h_out_off, nmt_stats* stats, void* stream);
+
+/* Same with DEVICE-resident sources and outputs (inputs already in HBM):
+ *   d_ids [h_off[n]] int32 flat sources on the device; h_off [n+1] host offsets (plan);
+ *   d_out [n][out_stride] int32 generated tokens (EOS included if produced),
+ *   d_out_len [n] generated counts; out_stride >= max_tgt_len. Asynchronous
+ *   except for live-count polls (sync_every). */
+nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_t* h_off, int64_t n,
+                                const nmt_translate_opts* opts, int32_t* d_out, int32_t out_stride,
+                                int32_t* d_out_len, nmt_stats* stats, void* stream);
+
+const char* nmt_last_error(void);   /* thread-local; valid until the next nmt_* call */
+
+/* ---- kernel-level entry points used by the unit parity tests ------------------- */
+/* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision
+ * (FP16: tcgen05/TMEM/TMA tensor-core GEMM; FP32: SIMT), all pointers device, row-major
+ * with leading dimensions lda/ldb/ldr/ldc in elements.  `prec` selects the element
+ * type of A, B, bias, R and C.  Asynchronous. */
+nmt_status nmt_dev_gemm(nmt_precision prec, int32_t M, int32_t N, int32_t K, const void* d_A,
+                        int32_t lda, const void* d_B, int32_t ldb, const void* d_bias,
+                        const void* d_R, int32_t ldr, void* d_C, int32_t ldc, int32_t relu,
+                        void* stream);
+/* Fused vocab projection + argmax: d_next[m] = argmax_n (A[m] . B[n]) with ties to the
+ * lowest n, FP32 accumulation; optional FP32 logits dump. */
+nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t K,
+                               const void* d_A, int32_t lda, const void* d_B, int32_t ldb,
+                               int32_t* d_next, float* d_logits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMT_H_ */

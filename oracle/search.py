@@ -63,13 +63,15 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
     """Greedy translation of a Workload; returns list of outputs in input order.
 
     ``log`` (optional dict) receives 'prunes': [(batch, step, new_to_old)],
-    'gen_tokens', 'steps', 'batches'.
+    'gen_tokens', 'steps', 'batches', and 'margins': per sentence, the top1 - top2
+    logit gap at every generated position (which positions are margin-safe).
     """
     cfg = model.cfg
     lens = wl.lengths()
     batches = plan_batches(lens, max_tokens, max_sents)
     outputs = [None] * wl.n
     prunes = []
+    margins = [None] * wl.n
     gen_tokens = 0
     steps = 0
     for bi, idx in enumerate(batches):
@@ -83,13 +85,16 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
         tok = np.full(B, BOS_ID, dtype=np.int64)
         done = np.zeros(B, dtype=bool)
         gen = [[] for _ in range(B)]
+        gaps = [[] for _ in range(B)]
         t = 0
         while True:
             logits = model.decoder_step(tok, t, cache, ckv, src_len)
             nxt = np.argmax(logits, axis=1)
+            top2 = np.partition(logits, -2, axis=1)[:, -2:]
             for r, s in enumerate(rows):
                 if not done[r]:
                     gen[s].append(int(nxt[r]))
+                    gaps[s].append(float(top2[r, 1] - top2[r, 0]))
                     if nxt[r] == EOS_ID or len(gen[s]) == caps[s]:
                         done[r] = True
             tok = nxt
@@ -109,8 +114,9 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
             g = gen[s]
             gen_tokens += len(g)
             outputs[i] = g[:-1] if g and g[-1] == EOS_ID else g
+            margins[i] = gaps[s]
     if log is not None:
-        log.update(prunes=prunes, gen_tokens=gen_tokens, steps=steps, batches=batches)
+        log.update(prunes=prunes, gen_tokens=gen_tokens, steps=steps, batches=batches, margins=margins)
     return outputs
 
 

@@ -1,0 +1,73 @@
+// common.cuh — shared device helpers for the sm_100a kernels (no method arithmetic
+// beyond FP16<->FP32 conversion and warp reductions).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace nmt {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+
+#define NMT_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::nmt::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + \
+                             __FILE__ + ":" + std::to_string(__LINE__));                \
+  } while (0)
+
+// Every kernel launch of the library goes through NMT_LAUNCH_CHECK, which also counts
+// it (nmt_stats.launches / bench "gpu_launches").
+extern unsigned long long g_launches;
+#define NMT_LAUNCH_CHECK()    \
+  do {                        \
+    ++::nmt::g_launches;      \
+    NMT_CUDA(cudaGetLastError()); \
+  } while (0)
+
+// ---- element conversion --------------------------------------------------------------
+template <class T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+
+// FP32 -> storage type.  FP16: round-to-nearest-even, saturating at +-65504 (reading R19).
+template <class T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __half from_f<__half>(float v) {
+  v = fminf(fmaxf(v, -65504.f), 65504.f);
+  return __float2half_rn(v);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Ordered-float key: larger float -> larger unsigned key (finite inputs).
+__device__ __forceinline__ uint32_t ordered_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+// Packed (value, id) key for argmax with ties -> lowest id: max over keys.
+__device__ __forceinline__ unsigned long long pack_argmax(float v, int id) {
+  return ((unsigned long long)ordered_key(v) << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)id);
+}
+__device__ __forceinline__ int unpack_argmax_id(unsigned long long k) {
+  return (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace nmt

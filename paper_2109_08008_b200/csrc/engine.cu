@@ -1,0 +1,892 @@
+// engine.cu — weight store, arena (the paper's memory pool), batch state,
+// encode / decode-step / prune / translate drivers and the extern "C" ABI of nmt.h.
+// Host code only orchestrates launches; every step of the path runs in kernels.cu /
+// gemm_*.cu on the device.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <memory>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/nmt.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+unsigned long long g_launches = 0;
+
+struct NmtError : std::runtime_error {
+  nmt_status code;
+  NmtError(nmt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define NMT_REQUIRE(cond, code, msg)                         \
+  do {                                                       \
+    if (!(cond)) throw ::nmt::NmtError(code, std::string(msg)); \
+  } while (0)
+
+thread_local std::string g_err;
+
+// ------------------------------------------------------------------ bump arena
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  size_t take(size_t bytes) {
+    size_t off = used;
+    used += (bytes + 255) & ~size_t(255);
+    return off;
+  }
+};
+
+}  // namespace nmt
+
+using namespace nmt;
+
+struct nmt_batch {
+  nmt_model* m = nullptr;
+  int B = 0, S = 0;
+  int step = 0;          // host mirror of decode steps issued
+  int rows_upper = 0;    // host upper bound of live rows
+  int max_cap = 0;
+  bool valid = false;
+  bool pending_step_done = false;  // nmt_decode_step issued, nmt_prune_batch not yet
+};
+
+struct nmt_model {
+  nmt_config cfg{};
+  nmt_precision prec = NMT_FP16;
+  nmt_limits lim{};
+  int device = 0;
+  size_t tb = 2;  // bytes per stored element
+  // weights
+  void* wbuf = nullptr;
+  std::unordered_map<std::string, void*> W;
+  void* ckv_w = nullptr;   // [Ld*2d][d] cross K/V projection of every decoder layer
+  void* ckv_b = nullptr;   // [Ld*2d]
+  float* dlcl_w = nullptr; // packed rows m = 1..L+1
+  float* pe = nullptr;     // [max_pos][d] FP32 sinusoid table
+  // arena
+  Arena ar;
+  int *src = nullptr, *src_len = nullptr, *tgt_cap = nullptr;
+  void *x = nullptr, *u = nullptr, *qkv = nullptr, *o = nullptr, *h = nullptr, *enc = nullptr,
+       *hist = nullptr, *ckv = nullptr;
+  void *g = nullptr, *du = nullptr, *dqkv = nullptr, *dout = nullptr, *dq = nullptr, *dh = nullptr;
+  void *kc = nullptr, *vc = nullptr;
+  unsigned long long* keys = nullptr;
+  int *row_slot = nullptr, *prev_tok = nullptr, *out_tok = nullptr, *gen_len = nullptr;
+  uint8_t* done = nullptr;
+  DevState* st = nullptr;
+  int* bad = nullptr;
+  long long* boff = nullptr;
+  int* blen = nullptr;
+  int* sent_ids = nullptr;
+  // pinned host staging
+  struct Pinned {
+    int* src; int* len; int* cap; long long* boff; int* blen; int* sent; int* out_tok; int* gen_len;
+    DevState* st; int* bad;
+  } hp{};
+  void* pinned = nullptr;
+  nmt_batch batch;
+  ~nmt_model() {
+    if (wbuf) cudaFree(wbuf);
+    if (ar.base) cudaFree(ar.base);
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ NTSD parsing
+struct TensorRec {
+  std::string name;
+  int dtype;  // 0 f32, 1 f16
+  std::vector<uint32_t> dims;
+  const uint8_t* data;
+  size_t nbytes;
+};
+
+std::vector<std::pair<std::string, std::vector<uint32_t>>> canonical(const nmt_config& c) {
+  std::vector<std::pair<std::string, std::vector<uint32_t>>> s;
+  const uint32_t d = c.d_model, F = c.d_ffn, V = c.vocab_size, R = 2 * c.max_rel_pos + 1,
+                 dh = c.d_model / c.n_heads;
+  auto add = [&](const std::string& n, std::vector<uint32_t> sh) { s.emplace_back(n, sh); };
+  add("emb", {V, d});
+  for (int l = 0; l < c.enc_layers; ++l) {
+    std::string p = "enc." + std::to_string(l) + ".";
+    add(p + "attn_ln.g", {d}); add(p + "attn_ln.b", {d});
+    add(p + "qkv.w", {3 * d, d}); add(p + "qkv.b", {3 * d});
+    add(p + "out.w", {d, d}); add(p + "out.b", {d});
+    if (c.use_rpr) { add(p + "rel_k", {R, dh}); add(p + "rel_v", {R, dh}); }
+    add(p + "ffn_ln.g", {d}); add(p + "ffn_ln.b", {d});
+    add(p + "ffn1.w", {F, d}); add(p + "ffn1.b", {F});
+    add(p + "ffn2.w", {d, F}); add(p + "ffn2.b", {d});
+  }
+  if (c.use_dlcl) {
+    for (int k = 0; k <= c.enc_layers; ++k) {
+      add("enc.dlcl.ln." + std::to_string(k) + ".g", {d});
+      add("enc.dlcl.ln." + std::to_string(k) + ".b", {d});
+    }
+    uint32_t L1 = c.enc_layers + 1;
+    add("enc.dlcl.w", {L1 * (L1 + 1) / 2});
+  }
+  add("enc.final_ln.g", {d}); add("enc.final_ln.b", {d});
+  for (int m = 0; m < c.dec_layers; ++m) {
+    std::string p = "dec." + std::to_string(m) + ".";
+    add(p + "self_ln.g", {d}); add(p + "self_ln.b", {d});
+    add(p + "self_qkv.w", {3 * d, d}); add(p + "self_qkv.b", {3 * d});
+    add(p + "self_out.w", {d, d}); add(p + "self_out.b", {d});
+    if (c.use_rpr) { add(p + "rel_k", {R, dh}); add(p + "rel_v", {R, dh}); }
+    add(p + "cross_ln.g", {d}); add(p + "cross_ln.b", {d});
+    add(p + "cross_q.w", {d, d}); add(p + "cross_q.b", {d});
+    add(p + "cross_kv.w", {2 * d, d}); add(p + "cross_kv.b", {2 * d});
+    add(p + "cross_out.w", {d, d}); add(p + "cross_out.b", {d});
+    add(p + "ffn_ln.g", {d}); add(p + "ffn_ln.b", {d});
+    add(p + "ffn1.w", {F, d}); add(p + "ffn1.b", {F});
+    add(p + "ffn2.w", {d, F}); add(p + "ffn2.b", {d});
+  }
+  add("dec.final_ln.g", {d}); add("dec.final_ln.b", {d});
+  return s;
+}
+
+template <class U> U rd(const uint8_t*& p, const uint8_t* end) {
+  NMT_REQUIRE(p + sizeof(U) <= end, NMT_E_INTEGRITY, "NTSD: truncated blob");
+  U v;
+  memcpy(&v, p, sizeof(U));
+  p += sizeof(U);
+  return v;
+}
+
+float half_bits_to_float(uint16_t h) {
+  __half_raw r;
+  r.x = h;
+  return __half2float(__half(r));
+}
+uint16_t float_to_half_bits(float f) {
+  __half hv = __float2half_rn(f);
+  __half_raw r = hv;
+  return r.x;
+}
+
+void validate_config(const nmt_config& c) {
+  NMT_REQUIRE(c.enc_layers >= 1 && c.dec_layers >= 1 && c.n_heads >= 1 && c.vocab_size >= 8,
+              NMT_E_FORMAT, "NTSD: bad layer/head/vocab counts");
+  NMT_REQUIRE(c.d_model % 32 == 0 && c.d_model <= 512 && c.d_model % c.n_heads == 0,
+              NMT_E_UNSUPPORTED, "d_model must be a multiple of 32, <= 512, divisible by heads");
+  NMT_REQUIRE((c.d_model / c.n_heads) % 8 == 0 && c.d_model / c.n_heads <= 128, NMT_E_UNSUPPORTED,
+              "head dim must be a multiple of 8 and <= 128");
+  NMT_REQUIRE(c.d_ffn % 32 == 0, NMT_E_UNSUPPORTED, "d_ffn must be a multiple of 32");
+  NMT_REQUIRE(c.max_rel_pos >= 1 && 2 * c.max_rel_pos + 1 <= 32, NMT_E_UNSUPPORTED,
+              "max_rel_pos must be in [1, 15]");
+  NMT_REQUIRE(c.max_src_len >= 1 && c.max_src_len <= c.max_pos && c.max_tgt_len >= 1 &&
+                  c.max_tgt_len <= c.max_pos,
+              NMT_E_FORMAT, "NTSD: bad max lengths");
+}
+
+// ------------------------------------------------------------------ typed views
+template <class T> struct V {
+  nmt_model* m;
+  const T* w(const std::string& n) const {
+    auto it = m->W.find(n);
+    if (it == m->W.end()) throw NmtError(NMT_E_INTEGRITY, "missing tensor " + n);
+    return static_cast<const T*>(it->second);
+  }
+  const T* rel(const std::string& p, const char* kv) const {
+    return m->cfg.use_rpr ? w(p + kv) : nullptr;
+  }
+  T* p(void* q) const { return static_cast<T*>(q); }
+};
+
+void init_arena(nmt_model* m) {
+  const nmt_config& c = m->cfg;
+  const nmt_limits& L = m->lim;
+  const size_t tb = m->tb, d = c.d_model, F = c.d_ffn, Ld = c.dec_layers;
+  const size_t N = L.max_tokens, Bm = L.max_sents, Tm = L.max_tgt_len;
+  const size_t R = Bm * std::max(1, L.beam);
+  Arena& a = m->ar;
+  struct Item { void** dst; size_t bytes; };
+  std::vector<std::pair<void**, size_t>> items = {
+      {(void**)&m->src, N * 4}, {(void**)&m->src_len, Bm * 4}, {(void**)&m->tgt_cap, Bm * 4},
+      {&m->x, N * d * tb}, {&m->u, N * d * tb}, {&m->qkv, N * 3 * d * tb}, {&m->o, N * d * tb},
+      {&m->h, N * F * tb}, {&m->enc, N * d * tb},
+      {&m->hist, c.use_dlcl ? (size_t)(c.enc_layers + 1) * N * d * tb : 256},
+      {&m->ckv, N * Ld * 2 * d * tb},
+      {&m->g, R * d * tb}, {&m->du, R * d * tb}, {&m->dqkv, R * 3 * d * tb},
+      {&m->dout, R * d * tb}, {&m->dq, R * d * tb}, {&m->dh, R * F * tb},
+      {&m->kc, Ld * R * Tm * d * tb}, {&m->vc, Ld * R * Tm * d * tb},
+      {(void**)&m->keys, R * 8}, {(void**)&m->row_slot, R * 4}, {(void**)&m->prev_tok, R * 4},
+      {(void**)&m->done, R}, {(void**)&m->out_tok, Bm * Tm * 4}, {(void**)&m->gen_len, Bm * 4},
+      {(void**)&m->st, sizeof(DevState)}, {(void**)&m->bad, 4}, {(void**)&m->boff, Bm * 8},
+      {(void**)&m->blen, Bm * 4}, {(void**)&m->sent_ids, Bm * 4},
+  };
+  std::vector<size_t> offs;
+  for (auto& it : items) offs.push_back(a.take(it.second));
+  cudaError_t e = cudaMalloc(&a.base, a.used);
+  NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
+              std::string("arena cudaMalloc failed: ") + cudaGetErrorString(e));
+  a.cap = a.used;
+  for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
+  NMT_CUDA(cudaMemset(a.base, 0, a.used));
+  // pinned staging
+  size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64;
+  NMT_CUDA(cudaMallocHost(&m->pinned, pb));
+  char* p = (char*)m->pinned;
+  auto take = [&](size_t b) { char* r = p; p += (b + 63) & ~size_t(63); return r; };
+  m->hp.boff = (long long*)take(Bm * 8);
+  m->hp.src = (int*)take(N * 4);
+  m->hp.len = (int*)take(Bm * 4);
+  m->hp.cap = (int*)take(Bm * 4);
+  m->hp.blen = (int*)take(Bm * 4);
+  m->hp.sent = (int*)take(Bm * 4);
+  m->hp.out_tok = (int*)take(Bm * Tm * 4);
+  m->hp.gen_len = (int*)take(Bm * 4);
+  m->hp.st = (DevState*)take(sizeof(DevState));
+  m->hp.bad = (int*)take(4);
+}
+
+// ------------------------------------------------------------------ encode
+template <class T>
+void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
+  const nmt_config& c = m->cfg;
+  V<T> v{m};
+  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, L = c.enc_layers, Ld = c.dec_layers;
+  const int N = B * S;
+  const float eps = c.ln_eps;
+  T *x = v.p(m->x), *u = v.p(m->u), *qkv = v.p(m->qkv), *o = v.p(m->o), *h = v.p(m->h),
+    *enc = v.p(m->enc), *hist = v.p(m->hist), *ckv = v.p(m->ckv);
+  const size_t hs = (size_t)N * d;
+  const float sq = std::sqrt((float)d);
+  // y0 = sqrt(d) E[s] + PE(p)
+  embed<T>(m->src, v.w("emb"), m->pe, c.use_dlcl ? o : x, N, d, S, nullptr, nullptr, sq, s);
+  if (c.use_dlcl) {
+    dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, v.w("enc.dlcl.ln.0.g"), v.w("enc.dlcl.ln.0.b"),
+                    c.dlcl_ln, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), x, u, N, d, eps, s);
+  } else {
+    layernorm<T>(x, d, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), u, d, N, d, eps, nullptr, s);
+  }
+  for (int l = 0; l < L; ++l) {
+    const std::string p = "enc." + std::to_string(l) + ".";
+    GemmArgs a;
+    a.M = N; a.N = 3 * d; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "qkv.w"); a.ldb = d;
+    a.bias = v.w(p + "qkv.b"); a.C = qkv; a.ldc = 3 * d;
+    gemm<T>(a, s);
+    attn_encoder<T>(qkv, m->src_len, v.rel(p, "rel_k"), v.rel(p, "rel_v"), o, B, S, d, H,
+                    c.max_rel_pos, c.use_rpr, s);
+    a = GemmArgs();
+    a.M = N; a.N = d; a.K = d; a.A = o; a.lda = d; a.B = v.w(p + "out.w"); a.ldb = d;
+    a.bias = v.w(p + "out.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
+    gemm<T>(a, s);                                          // a = x + Attn(LN(x))
+    layernorm<T>(x, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), u, d, N, d, eps, nullptr, s);
+    a = GemmArgs();
+    a.M = N; a.N = F; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
+    a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = h; a.ldc = F;
+    gemm<T>(a, s);
+    a = GemmArgs();
+    a.M = N; a.N = d; a.K = F; a.A = h; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
+    a.bias = v.w(p + "ffn2.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
+    gemm<T>(a, s);                                          // y_l = a + FFN(LN(a))
+    const bool last = (l == L - 1);
+    const std::string np = last ? "enc.final_ln." : "enc." + std::to_string(l + 1) + ".attn_ln.";
+    if (c.use_dlcl) {
+      const int k = l + 1;  // depth of y
+      const std::string dp = "enc.dlcl.ln." + std::to_string(k) + ".";
+      dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, v.w(dp + "g"),
+                      v.w(dp + "b"), c.dlcl_ln, v.w(np + "g"), v.w(np + "b"),
+                      last ? nullptr : x, last ? enc : u, N, d, eps, s);
+    } else {
+      layernorm<T>(x, d, v.w(np + "g"), v.w(np + "b"), last ? enc : u, d, N, d, eps, nullptr, s);
+    }
+  }
+  // cross K/V of every decoder layer, once per sentence
+  GemmArgs a;
+  a.M = N; a.N = Ld * 2 * d; a.K = d; a.A = enc; a.lda = d; a.B = m->ckv_w; a.ldb = d;
+  a.bias = m->ckv_b; a.C = ckv; a.ldc = Ld * 2 * d;
+  gemm<T>(a, s);
+}
+
+// ------------------------------------------------------------------ decode step
+template <class T>
+void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
+                      cudaStream_t s) {
+  const nmt_config& c = m->cfg;
+  V<T> v{m};
+  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, Ld = c.dec_layers;
+  const int R = b->rows_upper;
+  const int Tm = m->lim.max_tgt_len;
+  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
+  const float eps = c.ln_eps;
+  const int* dR = &m->st->n_live;
+  const int* dt = &m->st->t;
+  T *g = v.p(m->g), *du = v.p(m->du), *dqkv = v.p(m->dqkv), *dout = v.p(m->dout),
+    *dq = v.p(m->dq), *dh = v.p(m->dh);
+  embed<T>(d_prev ? d_prev : m->prev_tok, v.w("emb"), m->pe, g, R, d, 1, dt, dR,
+           std::sqrt((float)d), s);
+  for (int l = 0; l < Ld; ++l) {
+    const std::string p = "dec." + std::to_string(l) + ".";
+    T* kc = v.p(m->kc) + (size_t)l * Rmax * Tm * d;
+    T* vc = v.p(m->vc) + (size_t)l * Rmax * Tm * d;
+    layernorm<T>(g, d, v.w(p + "self_ln.g"), v.w(p + "self_ln.b"), du, d, R, d, eps, dR, s);
+    GemmArgs a;
+    a.M = R; a.N = 3 * d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "self_qkv.w"); a.ldb = d;
+    a.bias = v.w(p + "self_qkv.b"); a.C = dqkv; a.ldc = 3 * d; a.dM = dR;
+    gemm<T>(a, s);
+    attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, v.rel(p, "rel_k"), v.rel(p, "rel_v"),
+                         dout, R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s);
+    a = GemmArgs();
+    a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "self_out.w"); a.ldb = d;
+    a.bias = v.w(p + "self_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
+    gemm<T>(a, s);
+    layernorm<T>(g, d, v.w(p + "cross_ln.g"), v.w(p + "cross_ln.b"), du, d, R, d, eps, dR, s);
+    a = GemmArgs();
+    a.M = R; a.N = d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "cross_q.w"); a.ldb = d;
+    a.bias = v.w(p + "cross_q.b"); a.C = dq; a.ldc = d; a.dM = dR;
+    gemm<T>(a, s);
+    attn_cross<T>(dq, v.p(m->ckv), Ld * 2 * d, l * 2 * d, l * 2 * d + d, b->S, m->src_len,
+                  m->row_slot, dout, R, d, H, dR, s);
+    a = GemmArgs();
+    a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "cross_out.w"); a.ldb = d;
+    a.bias = v.w(p + "cross_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
+    gemm<T>(a, s);
+    layernorm<T>(g, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), du, d, R, d, eps, dR, s);
+    a = GemmArgs();
+    a.M = R; a.N = F; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
+    a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = dh; a.ldc = F; a.dM = dR;
+    gemm<T>(a, s);
+    a = GemmArgs();
+    a.M = R; a.N = d; a.K = F; a.A = dh; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
+    a.bias = v.w(p + "ffn2.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
+    gemm<T>(a, s);
+  }
+  layernorm<T>(g, d, v.w("dec.final_ln.g"), v.w("dec.final_ln.b"), du, d, R, d, eps, dR, s);
+  GemmArgs a;  // tied vocab projection fused with argmax
+  a.M = R; a.N = c.vocab_size; a.K = d; a.A = du; a.lda = d; a.B = v.w("emb"); a.ldb = d;
+  a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
+  gemm<T>(a, s);
+  greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok, Tm,
+                m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
+                out ? out->d_done : nullptr, s);
+}
+
+void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
+                     cudaStream_t s) {
+  if (m->prec == NMT_FP16) decode_step_impl<__half>(m, b, d_prev, out, s);
+  else decode_step_impl<float>(m, b, d_prev, out, s);
+}
+
+// Stage host batch metadata and encode (sources already in m->src).
+void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_cap,
+                   cudaStream_t s) {
+  nmt_batch& b = m->batch;
+  const int Tm = m->lim.max_tgt_len;
+  int mc = 0;
+  for (int i = 0; i < B; ++i) {
+    m->hp.len[i] = h_len[i];
+    int cp = h_cap ? std::min(h_cap[i], Tm) : Tm;
+    cp = std::max(cp, 1);
+    m->hp.cap[i] = cp;
+    mc = std::max(mc, cp);
+  }
+  NMT_CUDA(cudaMemcpyAsync(m->src_len, m->hp.len, B * 4, cudaMemcpyHostToDevice, s));
+  NMT_CUDA(cudaMemcpyAsync(m->tgt_cap, m->hp.cap, B * 4, cudaMemcpyHostToDevice, s));
+  if (m->prec == NMT_FP16) encode_impl<__half>(m, B, S, s);
+  else encode_impl<float>(m, B, S, s);
+  batch_init(m->row_slot, m->prev_tok, m->done, m->gen_len, m->st, B, m->cfg.bos_id, s);
+  b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B; b.max_cap = mc; b.valid = true;
+  b.pending_step_done = false;
+}
+
+void check_batch_shape(nmt_model* m, int B, int S) {
+  NMT_REQUIRE(B >= 1 && S >= 1, NMT_E_ARG, "n_sent and s_max must be >= 1");
+  NMT_REQUIRE(B <= m->lim.max_sents, NMT_E_SHAPE,
+              "n_sent " + std::to_string(B) + " > max_sents " + std::to_string(m->lim.max_sents));
+  NMT_REQUIRE((long long)B * S <= m->lim.max_tokens, NMT_E_SHAPE,
+              "n_sent*s_max " + std::to_string((long long)B * S) + " > max_tokens " +
+                  std::to_string(m->lim.max_tokens));
+  NMT_REQUIRE(S <= m->cfg.max_src_len, NMT_E_INPUT,
+              "s_max " + std::to_string(S) + " > max_src_len " + std::to_string(m->cfg.max_src_len));
+}
+
+void poll_state(nmt_model* m, cudaStream_t s) {
+  NMT_CUDA(cudaMemcpyAsync(m->hp.st, m->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  NMT_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ translate core
+struct Plan {
+  std::vector<int> order;
+  std::vector<int> bstart;  // batch boundaries into order
+};
+
+Plan plan_batches(const int64_t* h_off, int64_t n, int max_tokens, int max_sents) {
+  Plan p;
+  p.order.resize(n);
+  std::iota(p.order.begin(), p.order.end(), 0);
+  // stable sort by (-len, index) (reading R17)
+  std::stable_sort(p.order.begin(), p.order.end(), [&](int a, int b) {
+    return (h_off[a + 1] - h_off[a]) > (h_off[b + 1] - h_off[b]);
+  });
+  int64_t i = 0;
+  while (i < n) {
+    p.bstart.push_back((int)i);
+    int first = (int)(h_off[p.order[i] + 1] - h_off[p.order[i]]);
+    int64_t b = std::min<int64_t>({(int64_t)max_sents, std::max<int64_t>(1, max_tokens / first),
+                                   n - i});
+    i += b;
+  }
+  p.bstart.push_back((int)n);
+  return p;
+}
+
+// Runs every batch; `load_src` stages batch sources into m->src, `emit` consumes results.
+template <class LoadF, class EmitF>
+void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_translate_opts* o,
+                    LoadF load_src, EmitF emit, nmt_stats* st, cudaStream_t s) {
+  const int max_tokens = o && o->max_tokens > 0 ? o->max_tokens : m->lim.max_tokens;
+  const int max_sents = o && o->max_sents > 0 ? o->max_sents : m->lim.max_sents;
+  const int every = o && o->prune_every > 0 ? o->prune_every : 1;
+  const float ratio = o ? o->prune_ratio : 0.25f;
+  const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
+  NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
+              "translate opts exceed the model limits");
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t len = h_off[i + 1] - h_off[i];
+    NMT_REQUIRE(len >= 1, NMT_E_INPUT, "empty source sentence " + std::to_string(i));
+    NMT_REQUIRE(len <= m->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
+                "source " + std::to_string(i) + " longer than max_src_len");
+  }
+  Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned long long l0 = g_launches;
+  int64_t steps = 0, prunes = 0;
+  std::vector<int> lens, caps;
+  for (size_t bi = 0; bi + 1 < p.bstart.size(); ++bi) {
+    const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
+    const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+    lens.resize(B);
+    caps.resize(B);
+    for (int j = 0; j < B; ++j) {
+      int sid = p.order[lo + j];
+      lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+      caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : m->lim.max_tgt_len;
+      m->hp.sent[j] = sid;
+    }
+    load_src(&p.order[lo], B, S, lens.data());
+    encode_common(m, B, S, lens.data(), caps.data(), s);
+    nmt_batch& b = m->batch;
+    int rows = B;
+    int t = 0;
+    for (; t < b.max_cap && rows > 0; ++t) {
+      b.rows_upper = rows;
+      decode_step_any(m, &b, nullptr, nullptr, s);
+      prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, rows, s);
+      if ((t + 1) % sync_every == 0) {
+        poll_state(m, s);
+        rows = m->hp.st->n_live;
+      }
+    }
+    poll_state(m, s);
+    steps += t;
+    prunes += m->hp.st->prunes;
+    b.step = t;
+    emit(b, &p.order[lo], B);
+    b.valid = false;
+  }
+  NMT_CUDA(cudaStreamSynchronize(s));
+  if (st) {
+    st->sentences = n;
+    st->src_tokens = h_off[n] - h_off[0];
+    st->decode_steps = steps;
+    st->prunes = prunes;
+    st->batches = (int64_t)p.bstart.size() - 1;
+    st->launches = (int64_t)(g_launches - l0);
+    st->ms_total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+}
+
+// ------------------------------------------------------------------ load
+nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
+                const nmt_limits* lim) {
+  NMT_REQUIRE(blob && lim, NMT_E_ARG, "null blob or limits");
+  NMT_REQUIRE(prec == NMT_FP16 || prec == NMT_FP32, NMT_E_ARG, "bad precision");
+  const uint8_t* p = (const uint8_t*)blob;
+  const uint8_t* end = p + nbytes;
+  NMT_REQUIRE(nbytes >= 12 && memcmp(p, "NTSD", 4) == 0, NMT_E_FORMAT, "NTSD: bad magic");
+  p += 4;
+  uint32_t ver = rd<uint32_t>(p, end);
+  NMT_REQUIRE(ver == 1, NMT_E_FORMAT, "NTSD: unsupported version " + std::to_string(ver));
+  uint32_t cb = rd<uint32_t>(p, end);
+  NMT_REQUIRE(cb == sizeof(nmt_config), NMT_E_FORMAT, "NTSD: config block size mismatch");
+  NMT_REQUIRE(p + cb <= end, NMT_E_INTEGRITY, "NTSD: truncated config");
+  nmt_config cfg;
+  memcpy(&cfg, p, cb);
+  p += cb;
+  validate_config(cfg);
+  uint32_t nt = rd<uint32_t>(p, end);
+  std::unordered_map<std::string, TensorRec> recs;
+  for (uint32_t i = 0; i < nt; ++i) {
+    TensorRec r;
+    uint16_t nl = rd<uint16_t>(p, end);
+    NMT_REQUIRE(p + nl <= end, NMT_E_INTEGRITY, "NTSD: truncated name");
+    r.name.assign((const char*)p, nl);
+    p += nl;
+    r.dtype = rd<uint8_t>(p, end);
+    uint8_t nd = rd<uint8_t>(p, end);
+    for (int k = 0; k < nd; ++k) r.dims.push_back(rd<uint32_t>(p, end));
+    uint64_t off = rd<uint64_t>(p, end), nb = rd<uint64_t>(p, end);
+    NMT_REQUIRE(r.dtype == 0 || r.dtype == 1, NMT_E_FORMAT, "NTSD: bad dtype for " + r.name);
+    NMT_REQUIRE(off + nb <= nbytes, NMT_E_INTEGRITY, "NTSD: truncated tensor " + r.name);
+    r.data = (const uint8_t*)blob + off;
+    r.nbytes = nb;
+    NMT_REQUIRE(recs.count(r.name) == 0, NMT_E_INTEGRITY, "NTSD: duplicate tensor " + r.name);
+    recs.emplace(r.name, r);
+  }
+  auto can = canonical(cfg);
+  NMT_REQUIRE(recs.size() == can.size(), NMT_E_INTEGRITY,
+              "NTSD: expected " + std::to_string(can.size()) + " tensors, got " +
+                  std::to_string(recs.size()));
+  NMT_REQUIRE(lim->max_tokens >= 1 && lim->max_sents >= 1 && lim->max_tgt_len >= 1 &&
+                  lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1,
+              NMT_E_ARG, "bad limits");
+  NMT_REQUIRE(lim->beam == 1, NMT_E_UNSUPPORTED, "beam > 1 is not built in this version");
+  NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 4096, NMT_E_ARG, "max_sents*beam > 4096");
+
+  std::unique_ptr<nmt_model> m(new nmt_model());
+  m->cfg = cfg;
+  m->prec = prec;
+  m->lim = *lim;
+  m->device = device;
+  m->tb = prec == NMT_FP16 ? 2 : 4;
+  NMT_CUDA(cudaSetDevice(device));
+  // host staging of all weights in the target precision, one H2D copy
+  size_t total = 0;
+  std::vector<size_t> offs;
+  for (auto& kv : can) {
+    auto it = recs.find(kv.first);
+    NMT_REQUIRE(it != recs.end(), NMT_E_INTEGRITY, "NTSD: missing tensor " + kv.first);
+    const TensorRec& r = it->second;
+    NMT_REQUIRE(r.dims == kv.second, NMT_E_INTEGRITY, "NTSD: shape mismatch for " + kv.first);
+    size_t cnt = 1;
+    for (auto d : kv.second) cnt *= d;
+    NMT_REQUIRE(r.nbytes == cnt * (r.dtype == 1 ? 2 : 4), NMT_E_INTEGRITY,
+                "NTSD: byte size mismatch for " + kv.first);
+    offs.push_back(total);
+    total += (cnt * m->tb + 255) & ~size_t(255);
+  }
+  const int d = cfg.d_model, Ld = cfg.dec_layers;
+  const size_t ckv_w_off = total;
+  total += ((size_t)Ld * 2 * d * d * m->tb + 255) & ~size_t(255);
+  const size_t ckv_b_off = total;
+  total += ((size_t)Ld * 2 * d * m->tb + 255) & ~size_t(255);
+  const int L1 = cfg.enc_layers + 1;
+  const size_t dlcl_off = total;
+  total += ((size_t)L1 * (L1 + 1) / 2 * 4 + 255) & ~size_t(255);
+  const size_t pe_off = total;
+  total += (size_t)cfg.max_pos * d * 4;
+  std::vector<uint8_t> host(total, 0);
+  auto get_f = [](const TensorRec& r, size_t i) -> float {
+    if (r.dtype == 1) {
+      uint16_t hb;
+      memcpy(&hb, r.data + 2 * i, 2);
+      return half_bits_to_float(hb);
+    }
+    float f;
+    memcpy(&f, r.data + 4 * i, 4);
+    return f;
+  };
+  auto put = [&](size_t dst, float f) {
+    if (m->tb == 2) {
+      uint16_t hb = float_to_half_bits(f);
+      memcpy(&host[dst], &hb, 2);
+    } else {
+      memcpy(&host[dst], &f, 4);
+    }
+  };
+  for (size_t t = 0; t < can.size(); ++t) {
+    const TensorRec& r = recs.at(can[t].first);
+    size_t cnt = r.nbytes / (r.dtype == 1 ? 2 : 4);
+    for (size_t i = 0; i < cnt; ++i) put(offs[t] + i * m->tb, get_f(r, i));
+  }
+  for (int l = 0; l < Ld; ++l) {
+    const TensorRec& w = recs.at("dec." + std::to_string(l) + ".cross_kv.w");
+    const TensorRec& bb = recs.at("dec." + std::to_string(l) + ".cross_kv.b");
+    size_t wc = (size_t)2 * d * d;
+    for (size_t i = 0; i < wc; ++i) put(ckv_w_off + ((size_t)l * wc + i) * m->tb, get_f(w, i));
+    for (int i = 0; i < 2 * d; ++i) put(ckv_b_off + ((size_t)l * 2 * d + i) * m->tb, get_f(bb, i));
+  }
+  if (cfg.use_dlcl) {
+    const TensorRec& w = recs.at("enc.dlcl.w");
+    for (int i = 0; i < L1 * (L1 + 1) / 2; ++i) {
+      float f = get_f(w, i);
+      memcpy(&host[dlcl_off + 4 * i], &f, 4);
+    }
+  }
+  {  // sinusoid table in double precision (reading R8)
+    const int half = d / 2;
+    for (int pos = 0; pos < cfg.max_pos; ++pos)
+      for (int i = 0; i < half; ++i) {
+        double w = std::exp(-std::log(10000.0) * i / (half - 1));
+        float sv = (float)std::sin(pos * w), cv = (float)std::cos(pos * w);
+        memcpy(&host[pe_off + ((size_t)pos * d + i) * 4], &sv, 4);
+        memcpy(&host[pe_off + ((size_t)pos * d + half + i) * 4], &cv, 4);
+      }
+  }
+  cudaError_t e = cudaMalloc(&m->wbuf, total);
+  NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
+              std::string("weights cudaMalloc failed: ") + cudaGetErrorString(e));
+  NMT_CUDA(cudaMemcpy(m->wbuf, host.data(), total, cudaMemcpyHostToDevice));
+  char* base = (char*)m->wbuf;
+  for (size_t t = 0; t < can.size(); ++t) m->W[can[t].first] = base + offs[t];
+  m->ckv_w = base + ckv_w_off;
+  m->ckv_b = base + ckv_b_off;
+  m->dlcl_w = (float*)(base + dlcl_off);
+  m->pe = (float*)(base + pe_off);
+  init_arena(m.get());
+  NMT_CUDA(cudaDeviceSynchronize());
+  return m.release();
+}
+
+template <class F> nmt_status guard(F f) {
+  try {
+    g_err.clear();
+    f();
+    return NMT_OK;
+  } catch (const NmtError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return NMT_E_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NMT_E_ARG;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* nmt_last_error(void) { return g_err.c_str(); }
+
+nmt_status nmt_load_weights(const void* h_ntsd, size_t nbytes, int device, nmt_precision prec,
+                            const nmt_limits* lim, nmt_model** out) {
+  return guard([&] {
+    NMT_REQUIRE(out, NMT_E_ARG, "null out");
+    *out = nullptr;
+    *out = load(h_ntsd, nbytes, device, prec, lim);
+  });
+}
+
+nmt_status nmt_get_config(const nmt_model* m, nmt_config* out) {
+  return guard([&] {
+    NMT_REQUIRE(m && out, NMT_E_ARG, "null argument");
+    *out = m->cfg;
+  });
+}
+
+void nmt_free_model(nmt_model* m) { delete m; }
+
+nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_len,
+                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, void* stream,
+                      nmt_batch** out) {
+  return guard([&] {
+    NMT_REQUIRE(m && d_src && h_src_len && out, NMT_E_ARG, "null argument");
+    check_batch_shape(m, n_sent, s_max);
+    for (int i = 0; i < n_sent; ++i)
+      NMT_REQUIRE(h_src_len[i] >= 1 && h_src_len[i] <= s_max, NMT_E_INPUT,
+                  "src_len[" + std::to_string(i) + "] out of [1, s_max]");
+    cudaStream_t s = (cudaStream_t)stream;
+    NMT_CUDA(cudaMemcpyAsync(m->src, d_src, (size_t)n_sent * s_max * 4, cudaMemcpyDeviceToDevice, s));
+    encode_common(m, n_sent, s_max, h_src_len, h_tgt_cap, s);
+    *out = &m->batch;
+  });
+}
+
+nmt_status nmt_batch_encoder_output(const nmt_batch* b, float* d_dst, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(b && b->valid && d_dst, NMT_E_ARG, "null or invalid batch");
+    nmt_model* m = b->m;
+    size_t n = (size_t)b->B * b->S * m->cfg.d_model;
+    if (m->prec == NMT_FP16) to_float<__half>((const __half*)m->enc, d_dst, n, (cudaStream_t)stream);
+    else to_float<float>((const float*)m->enc, d_dst, n, (cudaStream_t)stream);
+  });
+}
+
+nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, int32_t step,
+                           const nmt_step_out* out, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(m && b && b->valid && b->m == m, NMT_E_ARG, "null or invalid batch");
+    NMT_REQUIRE(step == b->step, NMT_E_STATE,
+                "step " + std::to_string(step) + " != batch step " + std::to_string(b->step));
+    NMT_REQUIRE(step < m->lim.max_tgt_len, NMT_E_STATE, "step beyond max_tgt_len");
+    decode_step_any(m, b, d_prev, out, (cudaStream_t)stream);
+    b->pending_step_done = true;
+  });
+}
+
+nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_new_to_old,
+                           int32_t* h_n_live, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(m && b && b->valid && b->m == m, NMT_E_ARG, "null or invalid batch");
+    NMT_REQUIRE(b->pending_step_done, NMT_E_STATE, "prune must follow a decode step");
+    cudaStream_t s = (cudaStream_t)stream;
+    prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old, b->rows_upper, s);
+    b->pending_step_done = false;
+    b->step += 1;
+    if (h_n_live) {
+      poll_state(m, s);
+      *h_n_live = m->hp.st->n_live;
+      b->rows_upper = *h_n_live;
+    }
+  });
+}
+
+nmt_status nmt_batch_live(nmt_batch* b, int32_t* h_n_live, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(b && b->valid && h_n_live, NMT_E_ARG, "null or invalid batch");
+    poll_state(b->m, (cudaStream_t)stream);
+    *h_n_live = b->m->hp.st->n_live;
+  });
+}
+
+nmt_status nmt_batch_results(nmt_batch* b, int32_t* h_ids, int32_t* h_len, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(b && b->valid && h_ids && h_len, NMT_E_ARG, "null or invalid batch");
+    nmt_model* m = b->m;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t Tm = m->lim.max_tgt_len;
+    NMT_CUDA(cudaMemcpyAsync(h_ids, m->out_tok, b->B * Tm * 4, cudaMemcpyDeviceToHost, s));
+    NMT_CUDA(cudaMemcpyAsync(h_len, m->gen_len, b->B * 4, cudaMemcpyDeviceToHost, s));
+    NMT_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
+                         const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
+                         int64_t* h_out_off, nmt_stats* stats, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(m && h_ids && h_off && h_out && h_out_off && n >= 0, NMT_E_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int V = m->cfg.vocab_size, eos = m->cfg.eos_id;
+    const int Tm = m->lim.max_tgt_len;
+    std::vector<std::vector<int>> outs(n);
+    int64_t gen = 0;
+    auto load_src = [&](const int* order, int B, int S, const int* lens) {
+      for (int j = 0; j < B; ++j) {
+        const int32_t* src = h_ids + h_off[order[j]];
+        for (int p = 0; p < S; ++p) {
+          int v = p < lens[j] ? src[p] : m->cfg.pad_id;
+          NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          m->hp.src[(size_t)j * S + p] = v;
+        }
+      }
+      NMT_CUDA(cudaMemcpyAsync(m->src, m->hp.src, (size_t)B * S * 4, cudaMemcpyHostToDevice, s));
+    };
+    auto emit = [&](nmt_batch& b, const int* order, int B) {
+      NMT_CUDA(cudaMemcpyAsync(m->hp.out_tok, m->out_tok, (size_t)B * Tm * 4,
+                               cudaMemcpyDeviceToHost, s));
+      NMT_CUDA(cudaMemcpyAsync(m->hp.gen_len, m->gen_len, B * 4, cudaMemcpyDeviceToHost, s));
+      NMT_CUDA(cudaStreamSynchronize(s));
+      for (int j = 0; j < B; ++j) {
+        int gl = m->hp.gen_len[j];
+        gen += gl;
+        const int* t = m->hp.out_tok + (size_t)j * Tm;
+        int ol = (gl > 0 && t[gl - 1] == eos) ? gl - 1 : gl;
+        outs[order[j]].assign(t, t + ol);
+      }
+    };
+    translate_core(m, h_off, n, opts, load_src, emit, stats, s);
+    int64_t pos = 0, ot = 0;
+    h_out_off[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      NMT_REQUIRE(pos + (int64_t)outs[i].size() <= out_cap, NMT_E_SHAPE, "out_cap too small");
+      std::copy(outs[i].begin(), outs[i].end(), h_out + pos);
+      pos += outs[i].size();
+      ot += outs[i].size();
+      h_out_off[i + 1] = pos;
+    }
+    if (stats) {
+      stats->gen_tokens = gen;
+      stats->out_tokens = ot;
+    }
+  });
+}
+
+nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_t* h_off,
+                                int64_t n, const nmt_translate_opts* opts, int32_t* d_out,
+                                int32_t out_stride, int32_t* d_out_len, nmt_stats* stats,
+                                void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(m && d_ids && h_off && d_out && d_out_len && n >= 0, NMT_E_ARG, "null argument");
+    NMT_REQUIRE(out_stride >= m->lim.max_tgt_len, NMT_E_ARG, "out_stride < max_tgt_len");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int Tm = m->lim.max_tgt_len;
+    NMT_CUDA(cudaMemsetAsync(m->bad, 0, 4, s));
+    int64_t gen = 0;
+    auto load_src = [&](const int* order, int B, int S, const int* lens) {
+      for (int j = 0; j < B; ++j) {
+        m->hp.boff[j] = h_off[order[j]];
+        m->hp.blen[j] = lens[j];
+      }
+      NMT_CUDA(cudaMemcpyAsync(m->boff, m->hp.boff, B * 8, cudaMemcpyHostToDevice, s));
+      NMT_CUDA(cudaMemcpyAsync(m->blen, m->hp.blen, B * 4, cudaMemcpyHostToDevice, s));
+      pack_sources(d_ids, m->boff, m->blen, B, S, m->src, m->cfg.vocab_size, m->bad, s);
+    };
+    auto emit = [&](nmt_batch& b, const int* order, int B) {
+      for (int j = 0; j < B; ++j) m->hp.sent[j] = order[j];
+      NMT_CUDA(cudaMemcpyAsync(m->sent_ids, m->hp.sent, B * 4, cudaMemcpyHostToDevice, s));
+      scatter_outputs(m->out_tok, Tm, m->gen_len, m->sent_ids, B, d_out, out_stride, d_out_len, s);
+      NMT_CUDA(cudaMemcpyAsync(m->hp.gen_len, m->gen_len, B * 4, cudaMemcpyDeviceToHost, s));
+      NMT_CUDA(cudaStreamSynchronize(s));  // staging buffers are reused by the next batch
+      for (int j = 0; j < B; ++j) gen += m->hp.gen_len[j];
+    };
+    translate_core(m, h_off, n, opts, load_src, emit, stats, s);
+    if (stats) stats->gen_tokens = gen;
+    NMT_CUDA(cudaMemcpyAsync(m->hp.bad, m->bad, 4, cudaMemcpyDeviceToHost, s));
+    NMT_CUDA(cudaStreamSynchronize(s));
+    NMT_REQUIRE(*m->hp.bad == 0, NMT_E_INPUT, "token id out of range in d_ids");
+  });
+}
+
+nmt_status nmt_dev_gemm(nmt_precision prec, int32_t M, int32_t N, int32_t K, const void* d_A,
+                        int32_t lda, const void* d_B, int32_t ldb, const void* d_bias,
+                        const void* d_R, int32_t ldr, void* d_C, int32_t ldc, int32_t relu,
+                        void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(d_A && d_B && d_C && M >= 0 && N > 0 && K > 0, NMT_E_ARG, "bad gemm args");
+    NMT_REQUIRE(K % 16 == 0, NMT_E_SHAPE, "K must be a multiple of 16");
+    GemmArgs a;
+    a.M = M; a.N = N; a.K = K; a.A = d_A; a.lda = lda; a.B = d_B; a.ldb = ldb; a.bias = d_bias;
+    a.R = d_R; a.ldr = ldr; a.C = d_C; a.ldc = ldc; a.relu = relu;
+    if (prec == NMT_FP16) gemm<__half>(a, (cudaStream_t)stream);
+    else gemm<float>(a, (cudaStream_t)stream);
+  });
+}
+
+nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t K,
+                               const void* d_A, int32_t lda, const void* d_B, int32_t ldb,
+                               int32_t* d_next, float* d_logits, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(d_A && d_B && d_next && M > 0 && N > 0 && K > 0, NMT_E_ARG, "bad gemm args");
+    NMT_REQUIRE(K % 16 == 0 && M <= 4096, NMT_E_SHAPE, "K % 16 != 0 or M > 4096");
+    cudaStream_t s = (cudaStream_t)stream;
+    static unsigned long long* keys = nullptr;
+    if (!keys) NMT_CUDA(cudaMalloc(&keys, 4096 * 8));
+    NMT_CUDA(cudaMemsetAsync(keys, 0, (size_t)M * 8, s));
+    GemmArgs a;
+    a.M = M; a.N = N; a.K = K; a.A = d_A; a.lda = lda; a.B = d_B; a.ldb = ldb;
+    a.argmax = keys; a.logits = d_logits;
+    if (prec == NMT_FP16) gemm<__half>(a, s);
+    else gemm<float>(a, s);
+    argmax_ids(keys, d_next, M, s);
+  });
+}
+
+}  // extern "C"

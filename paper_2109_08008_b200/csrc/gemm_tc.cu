@@ -1,0 +1,321 @@
+// gemm_tc.cu — FP16 tensor-core GEMM for sm_100a: tcgen05.mma (kind::f16, FP32 accumulator
+// in TMEM), operands staged by TMA (cp.async.bulk.tensor, 128B swizzle) through an
+// mbarrier ring, warp-specialised (TMA producer / single-thread MMA issuer / TMEM
+// allocator / 4 epilogue warps).  C[M][N] = A[M][K] . B[N][K]^T with fused epilogues:
+// bias, residual add, ReLU, FP16 store, or the vocab argmax (packed atomicMax, no
+// logits written).  Every projection of the path is one of these
+// (QKV / out / FFN / cross-K/V / decoder / tied vocab projection).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+namespace tc {
+
+constexpr int BM = 128;       // UMMA M (cta_group::1): one TMEM lane per output row
+constexpr int BK = 64;        // 64 halves = 128 B = one swizzle-128B atom row
+constexpr int UMMA_K = 16;    // K per tcgen05.mma for 16-bit inputs
+constexpr int kThreads = 256; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4..7 epilogue
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// K-major, 128B-swizzled operand tile: rows of 128 B, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t make_desc_sw128(const void* p) {
+  const uint64_t a = smem_u32(p);
+  return ((a >> 4) & 0x3FFFull) | (1ull << 16) /*LBO (unused for SW128 K-major)*/ |
+         ((1024ull >> 4) << 32) /*SBO*/ | (1ull << 46) /*sm100 version*/ |
+         (2ull << 61) /*SWIZZLE_128B*/;
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Params {
+  int M, N, K;
+  const __half* bias;
+  const __half* R;
+  int ldr;
+  __half* C;
+  int ldc;
+  int relu;
+  const int* dM;
+  unsigned long long* argmax;
+  float* logits;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BYTES = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+              Params p) {
+  using SM = Smem<BN, STAGES>;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int M = p.dM ? min(p.M, *p.dM) : p.M;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M) return;  // uniform for the CTA: live-row count read on the device
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * SM::STAGE;
+        uint8_t* sb = sa + SM::A_BYTES;
+        mbar_expect_tx(&full[s], SM::STAGE);
+        tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
+        tma_load_2d(sb, &mapB, &full[s], kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (one thread)
+      constexpr uint32_t idesc = (1u << 4)                        // D = F32
+                                 | (0u << 7) | (0u << 10)          // A, B = F16
+                                 | ((uint32_t)(BN >> 3) << 17)     // N
+                                 | ((uint32_t)(BM >> 4) << 24);    // M
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = make_desc_sw128(smem + s * SM::STAGE);
+        const uint64_t db = make_desc_sw128(smem + s * SM::STAGE + SM::A_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk)  // +32 B along K inside the swizzle atom
+          mma_f16(tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
+        mma_commit(&empty[s]);  // frees the stage when these MMAs complete
+      }
+      mma_commit(tmem_full);
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> registers -> global
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;  // TMEM lanes 32q..32q+31
+    const int m = m0 + q * 32 + lane;
+    const bool row_ok = m < M;
+    unsigned long long best = 0ull;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      __syncwarp();  // tcgen05.ld is warp-collective (.sync.aligned)
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      const int nb = n0 + c0;
+      if (!row_ok || nb >= p.N) continue;
+      const int nv = min(32, p.N - nb);
+      if (p.bias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) v[j] += __half2float(p.bias[nb + j]);
+      }
+      if (p.R) {
+        const __half* rr = p.R + (size_t)m * p.ldr + nb;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) v[j] += __half2float(rr[j]);
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+      }
+      if (p.logits) {
+        float* lr = p.logits + (size_t)m * p.N + nb;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) lr[j] = v[j];
+      }
+      if (p.argmax) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) {
+            unsigned long long k = pack_argmax(v[j], nb + j);
+            best = k > best ? k : best;
+          }
+      } else {
+        __half* cr = p.C + (size_t)m * p.ldc + nb;
+        if (nv == 32 && ((reinterpret_cast<uintptr_t>(cr) & 15) == 0)) {
+#pragma unroll
+          for (int j8 = 0; j8 < 4; ++j8) {
+            uint4 pk;
+            __half2* h2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              h2[e] = __halves2half2(from_f<__half>(v[j8 * 8 + 2 * e]),
+                                     from_f<__half>(v[j8 * 8 + 2 * e + 1]));
+            reinterpret_cast<uint4*>(cr)[j8] = pk;
+          }
+        } else {
+          for (int j = 0; j < nv; ++j) cr[j] = from_f<__half>(v[j]);
+        }
+      }
+    }
+    if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    NMT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <int BN, int STAGES>
+void launch(const GemmArgs& a, cudaStream_t s) {
+  using SM = Smem<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
+    attr = true;
+  }
+  CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
+  CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN);
+  Params p;
+  p.M = a.M; p.N = a.N; p.K = a.K;
+  p.bias = static_cast<const __half*>(a.bias);
+  p.R = static_cast<const __half*>(a.R);
+  p.ldr = a.ldr;
+  p.C = static_cast<__half*>(a.C);
+  p.ldc = a.ldc;
+  p.relu = a.relu;
+  p.dM = a.dM;
+  p.argmax = a.argmax;
+  p.logits = a.logits;
+  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM));
+  k_gemm_tc<BN, STAGES><<<grid, kThreads, SM::BYTES, s>>>(ma, mb, p);
+  NMT_LAUNCH_CHECK();
+}
+
+}  // namespace tc
+
+void gemm_tc(const GemmArgs& a, cudaStream_t s) {
+  if (a.M <= 0 || a.N <= 0) return;
+  if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||
+      (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
+    throw CudaError("gemm_tc: K / leading dims must be multiples of 8 and 16-B aligned");
+  if (a.argmax) tc::launch<256, 3>(a, s);
+  else tc::launch<128, 4>(a, s);
+}
+
+}  // namespace nmt

@@ -1,0 +1,117 @@
+// kernels.h — launchers for every sm_100a kernel of the hot path.
+// Each launcher cites the PAPER.md passage / DESIGN.md reading of the step it computes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nmt {
+
+// ---------------------------------------------------------------- GEMM family
+// C[M][N] = A[M][K] . B[N][K]^T (+bias[N]) (+R[M][N]) (ReLU), FP32 accumulation
+// (reductions in FP32).  A, B, bias, R, C are element type T.
+// If dM != nullptr the effective M is min(M, *dM) (live rows read from the device,
+// so decode steps need no host round-trip).  argmax != nullptr switches to the
+// vocab epilogue: logits are not stored in C; per row, the packed (value, ~id)
+// maximum is atomically max-reduced into argmax[m] (no log_softmax
+// for greedy); logits (FP32, ld = N) is an optional dump.
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr; int lda = 0;
+  const void* B = nullptr; int ldb = 0;
+  const void* bias = nullptr;
+  const void* R = nullptr; int ldr = 0;
+  void* C = nullptr; int ldc = 0;
+  int relu = 0;
+  const int* dM = nullptr;
+  unsigned long long* argmax = nullptr;
+  float* logits = nullptr;
+};
+
+template <class T> void gemm_simt(const GemmArgs& a, cudaStream_t s);
+void gemm_tc(const GemmArgs& a, cudaStream_t s);   // FP16 tcgen05 / TMEM / TMA
+template <class T> void gemm(const GemmArgs& a, cudaStream_t s);  // product dispatch by T
+
+// ---------------------------------------------------------------- elementwise / LN
+// y0[r] = sqrt(d) * E[id(r)] + PE[pos(r)]   (tied embedding + sinusoid)
+// encoder: rows r = b*S + p, pos = p;  decoder: pos = *d_t, ids = tokens[r], rows < *dR.
+template <class T>
+void embed(const int* ids, const T* E, const float* pe, T* out, int rows, int d, int S,
+           const int* d_t, const int* dR, float scale, cudaStream_t s);
+
+// out = LN(in; g, b) row-wise, FP32 statistics
+template <class T>
+void layernorm(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, int rows, int d,
+               float eps, const int* dR, cudaStream_t s);
+
+// DLCL combine (Eq. 1-2), one launch per layer boundary l:
+//   z_l = LN^dl_l(y_l) -> hist[l];  x = sum_{k<=l} w[k] z_k;  (x -> xout, LN(x; g2,b2) -> uout)
+// dlcl_ln = 0: z_l = y_l (reading A22 test switch).
+template <class T>
+void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
+                  const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
+                  int d, float eps, cudaStream_t s);
+
+// ---------------------------------------------------------------- attention
+// Encoder RPR self-attention (Shaw et al.) per (sentence, head):
+// qkv [B*S][3d]; out [B*S][d]; key mask j < len[b]; rows p >= len[b] are written 0.
+template <class T>
+void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B,
+                  int S, int d, int H, int kclip, int use_rpr, cudaStream_t s);
+
+// Decoder cached self-attention at step t = *d_t: for live row r
+// (< *dR), slot = row_slot[r]; appends k_t, v_t (from qkv[r]) into the cache at
+// [slot][t] and attends over positions 0..t with r(i,j) = clip(j - t, -k, k) + k.
+// cache layout: K at kc + (slot*Tmax + j)*d, V at vc + ... (same).
+template <class T>
+void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot, const T* relk,
+                       const T* relv, T* out, int rows, int d, int H, int kclip, int use_rpr,
+                       const int* d_t, const int* dR, cudaStream_t s);
+
+// Cross-attention over the once-per-sentence encoder K/V:
+// keys at ckv + (slot*S + j)*ldkv + koff, values at + voff; mask j < src_len[slot].
+template <class T>
+void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, int S, const int* src_len,
+                const int* row_slot, T* out, int rows, int d, int H, const int* dR, cudaStream_t s);
+
+// ---------------------------------------------------------------- greedy bookkeeping
+// Batch state on the device (one int32 block):
+struct DevState {
+  int t;          // current decode step
+  int n_live;     // live rows
+  int n_done;     // done rows among live ones (sticky flags)
+  int prunes;     // number of compactions so far
+};
+
+// After the vocab argmax of step t: next token per live row, sticky done flag
+// (EOS or cap, reading R12), outputs per sentence slot.
+void greedy_finish(unsigned long long* keys, const int* force_next, int* prev_tok, uint8_t* done,
+                   const int* row_slot, const int* cap, int* out_tok, int out_stride, int* gen_len,
+                   DevState* st, int rows_upper, int eos, int* d_next_copy, uint8_t* d_done_copy,
+                   cudaStream_t s);
+
+// Batch pruning decision + stable compaction (reading R18), one CTA.
+// Advances st->t.  new_to_old (optional) receives the map (or identity) for the
+// pre-prune rows; entries >= new count are -1.
+void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
+                   float ratio, int* new_to_old, int rows_upper, cudaStream_t s);
+
+// Fresh batch state: row_slot[r] = r, prev_tok[r] = BOS, done = 0, gen_len = 0,
+// st = {t 0, n_live B, n_done 0, prunes 0}.
+void batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* gen_len, DevState* st, int B,
+                int bos, cudaStream_t s);
+
+// Scatter a finished batch's per-slot outputs to their original sentence ids.
+void scatter_outputs(const int* out_tok, int out_stride, const int* gen_len, const int* sent_ids,
+                     int B, int* d_out, int d_out_stride, int* d_out_len, cudaStream_t s);
+
+// Pack flat EOS-terminated device sources into padded [B][S]: row b copies blen[b]
+// ids from ids + boff[b]; PAD elsewhere.  Ids outside [0, V) set *bad |= 1.
+void pack_sources(const int* ids, const long long* boff, const int* blen, int B, int S, int* out,
+                  int vocab, int* bad, cudaStream_t s);
+
+// Convert a [rows][d] T buffer to FP32 (debug / parity output).
+template <class T> void to_float(const T* in, float* out, size_t n, cudaStream_t s);
+// Convert packed argmax keys to token ids.
+void argmax_ids(unsigned long long* keys, int* ids, int rows, cudaStream_t s);
+
+}  // namespace nmt

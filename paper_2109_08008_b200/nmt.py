@@ -1,0 +1,239 @@
+"""Thin ctypes binding over libnmt.so (include/nmt.h): argument marshalling only.
+
+Every step of the translation path runs in the library's sm_100a kernels; PyTorch
+provides device buffers and streams.  There is no CPU fallback: if the library is
+missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import ntsd
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnmt.so")
+
+NMT_FP32, NMT_FP16 = 0, 1
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INPUT", 4: "E_STATE", 5: "E_FORMAT",
+          6: "E_INTEGRITY", 7: "E_RESOURCE", 8: "E_CUDA", 9: "E_UNSUPPORTED"}
+
+EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
+           "nmt_batch_encoder_output", "nmt_decode_step", "nmt_prune_batch", "nmt_batch_live",
+           "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
+           "nmt_dev_gemm", "nmt_dev_gemm_argmax"]
+
+
+class NmtError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Limits(C.Structure):
+    _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("max_tgt_len", C.c_int32),
+                ("beam", C.c_int32)]
+
+
+class StepOut(C.Structure):
+    _fields_ = [("d_next", C.c_void_p), ("d_done", C.c_void_p), ("d_logits", C.c_void_p)]
+
+
+class TranslateOpts(C.Structure):
+    _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("prune_every", C.c_int32),
+                ("prune_ratio", C.c_float), ("sync_every", C.c_int32), ("h_tgt_cap", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("sentences", "src_tokens", "gen_tokens", "out_tokens",
+                                         "decode_steps", "prunes", "batches", "launches")] + \
+               [("ms_total", C.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libnmt.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2109_08008_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        L.nmt_last_error.restype = C.c_char_p
+        for n in EXPORTS:
+            getattr(L, n)
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        raise NmtError(code, lib().nmt_last_error().decode())
+
+
+def _ptr(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Model:
+    """A loaded model (weights + arena) on one CUDA device."""
+
+    def __init__(self, cfg, weights: dict, precision: str = "fp16", max_tokens: int = 4096,
+                 max_sents: int = 512, max_tgt_len: int | None = None, device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libnmt needs a CUDA device (no CPU fallback)")
+        self.cfg = cfg
+        self.prec = NMT_FP16 if precision == "fp16" else NMT_FP32
+        self.device = device
+        self.V = cfg.vocab_size
+        self.Tmax = max_tgt_len or cfg.max_tgt_len
+        blob = ntsd.pack(cfg, weights)
+        lim = Limits(max_tokens, max_sents, self.Tmax, 1)
+        h = C.c_void_p()
+        torch.cuda.set_device(device)
+        _check(lib().nmt_load_weights(blob, C.c_size_t(len(blob)), device, self.prec, C.byref(lim),
+                                      C.byref(h)))
+        self.h = h
+        self.limits = lim
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().nmt_free_model(self.h)
+            self.h = None
+
+    # ---------------------------------------------------------------- step API
+    def encode(self, src, src_len, tgt_cap=None, stream=None):
+        """src: int32 CUDA tensor [B][S] (PAD-filled); src_len / tgt_cap: host ints."""
+        B, S = src.shape
+        ln = np.ascontiguousarray(src_len, dtype=np.int32)
+        cp = None if tgt_cap is None else np.ascontiguousarray(tgt_cap, dtype=np.int32)
+        b = C.c_void_p()
+        _check(lib().nmt_encode(self.h, _ptr(src), ln.ctypes.data_as(C.c_void_p),
+                                None if cp is None else cp.ctypes.data_as(C.c_void_p), B, S,
+                                _stream(stream), C.byref(b)))
+        return Batch(self, b, B, S)
+
+    def translate(self, ids, off, caps=None, max_tokens=None, max_sents=None, prune_every=1,
+                  prune_ratio=0.25, sync_every=4, stream=None):
+        """Host-buffer translation (C-ABI nmt_translate). Returns (outputs, stats dict)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        n = len(off) - 1
+        capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
+        o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
+                          prune_every, prune_ratio, sync_every,
+                          None if capa is None else capa.ctypes.data)
+        out_cap = n * self.Tmax
+        out = np.empty(max(out_cap, 1), dtype=np.int32)
+        out_off = np.empty(n + 1, dtype=np.int64)
+        st = Stats()
+        _check(lib().nmt_translate(self.h, ids.ctypes.data_as(C.c_void_p), off.ctypes.data_as(C.c_void_p),
+                                   C.c_int64(n), C.byref(o), out.ctypes.data_as(C.c_void_p),
+                                   C.c_int64(out_cap), out_off.ctypes.data_as(C.c_void_p), C.byref(st),
+                                   _stream(stream)))
+        outs = [out[out_off[i]:out_off[i + 1]].tolist() for i in range(n)]
+        return outs, st.as_dict()
+
+    def translate_device(self, d_ids, off, d_out, d_out_len, caps=None, max_tokens=None,
+                         max_sents=None, prune_every=1, prune_ratio=0.25, sync_every=4, stream=None):
+        """Device-resident translation (C-ABI nmt_translate_device); d_out [n][stride]."""
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        n = len(off) - 1
+        capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
+        o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
+                          prune_every, prune_ratio, sync_every,
+                          None if capa is None else capa.ctypes.data)
+        st = Stats()
+        _check(lib().nmt_translate_device(self.h, _ptr(d_ids), off.ctypes.data_as(C.c_void_p),
+                                          C.c_int64(n), C.byref(o), _ptr(d_out),
+                                          C.c_int32(d_out.shape[1]), _ptr(d_out_len), C.byref(st),
+                                          _stream(stream)))
+        self._keep = capa
+        return st.as_dict()
+
+
+class Batch:
+    def __init__(self, model, h, B, S):
+        self.model, self.h, self.B, self.S = model, h, B, S
+        self.step = 0
+
+    def encoder_output(self, stream=None):
+        import torch
+        out = torch.empty(self.B, self.S, self.model.cfg.d_model, dtype=torch.float32, device="cuda")
+        _check(lib().nmt_batch_encoder_output(self.h, _ptr(out), _stream(stream)))
+        return out
+
+    def decode_step(self, prev=None, logits=False, n_live=None, stream=None):
+        """One step; returns dict of CUDA tensors next / done (/ logits) for the live rows."""
+        import torch
+        rows = n_live if n_live is not None else self.live(stream)
+        nxt = torch.empty(max(rows, 1), dtype=torch.int32, device="cuda")
+        done = torch.empty(max(rows, 1), dtype=torch.uint8, device="cuda")
+        lg = torch.empty(max(rows, 1), self.model.V, dtype=torch.float32, device="cuda") if logits else None
+        so = StepOut(nxt.data_ptr(), done.data_ptr(), 0 if lg is None else lg.data_ptr())
+        _check(lib().nmt_decode_step(self.model.h, self.h, _ptr(prev), self.step, C.byref(so),
+                                     _stream(stream)))
+        r = {"next": nxt[:rows], "done": done[:rows]}
+        if lg is not None:
+            r["logits"] = lg[:rows]
+        return r
+
+    def prune(self, ratio=0.25, want_map=True, stream=None):
+        import torch
+        rows = self.live(stream)
+        m = torch.empty(max(rows, 1), dtype=torch.int32, device="cuda") if want_map else None
+        n = C.c_int32()
+        _check(lib().nmt_prune_batch(self.model.h, self.h, C.c_float(ratio), _ptr(m), C.byref(n),
+                                     _stream(stream)))
+        self.step += 1
+        return n.value, (m[:rows] if m is not None else None)
+
+    def live(self, stream=None):
+        n = C.c_int32()
+        _check(lib().nmt_batch_live(self.h, C.byref(n), _stream(stream)))
+        return n.value
+
+    def results(self, stream=None):
+        ids = np.empty((self.B, self.model.Tmax), dtype=np.int32)
+        ln = np.empty(self.B, dtype=np.int32)
+        _check(lib().nmt_batch_results(self.h, ids.ctypes.data_as(C.c_void_p), ln.ctypes.data_as(C.c_void_p),
+                                       _stream(stream)))
+        return ids, ln
+
+
+def dev_gemm(A, B, bias=None, R=None, relu=False, out=None, stream=None):
+    """C = A B^T (+bias) (+R) (relu) through the library GEMM (fp16: tcgen05; fp32: SIMT)."""
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    prec = NMT_FP16 if A.dtype == torch.float16 else NMT_FP32
+    C_ = out if out is not None else torch.empty(M, N, dtype=A.dtype, device=A.device)
+    _check(lib().nmt_dev_gemm(prec, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(bias),
+                              _ptr(R), 0 if R is None else R.stride(0), _ptr(C_), C_.stride(0),
+                              int(relu), _stream(stream)))
+    return C_
+
+
+def dev_gemm_argmax(A, B, logits=False, stream=None):
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    prec = NMT_FP16 if A.dtype == torch.float16 else NMT_FP32
+    nxt = torch.empty(M, dtype=torch.int32, device=A.device)
+    lg = torch.empty(M, N, dtype=torch.float32, device=A.device) if logits else None
+    _check(lib().nmt_dev_gemm_argmax(prec, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
+                                     _ptr(nxt), _ptr(lg), _stream(stream)))
+    return (nxt, lg) if logits else nxt

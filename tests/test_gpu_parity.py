@@ -1,0 +1,237 @@
+"""-m gpu parity tests: the CUDA path through the C ABI vs the FP64 oracle on the same
+seeded inputs (tiny C1 in full; 6-1 / 35-1 on subsets spanning several tiles, the
+RPR clip boundary and ragged tails).  FP32 mode within 1e-4 relative, FP16 within
+2e-2 absolute; greedy tokens bit-exact on margin-safe positions; prune maps bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from synth import tiny_workload, newstest_like, random_tokens, BOS_ID
+from gpu_common import TOL, SAFE_GAP, weights, oracle_model, gpu_model, logits_close, margin_safe, pad_batch
+
+pytestmark = pytest.mark.gpu
+
+PRECS = ["fp32", "fp16"]
+
+
+# ------------------------------------------------------------------ GEMM units
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("M,N,K", [(1, 64, 64), (3, 512, 512), (148, 1536, 512), (300, 2048, 512),
+                                   (129, 512, 2048), (4096, 512, 512), (77, 1000, 64), (512, 32000, 512)])
+def test_gemm_unit(prec, M, N, K):
+    from paper_2109_08008_b200 import dev_gemm
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    dt = torch.float16 if prec == "fp16" else torch.float32
+    A = (torch.randn(M, K, generator=g) / 2).to(dt)
+    B = (torch.randn(N, K, generator=g) / K ** 0.5).to(dt)
+    bias = (torch.randn(N, generator=g) * 0.1).to(dt)
+    R = torch.randn(M, N, generator=g).to(dt)
+    ref = A.double() @ B.double().T + bias.double() + R.double()
+    for relu in (False, True):
+        r = ref.clamp_min(0) if relu else ref
+        out = dev_gemm(A.cuda(), B.cuda(), bias.cuda(), R.cuda(), relu=relu).double().cpu()
+        if prec == "fp32":
+            tol = 1e-4 * max(1.0, float(r.abs().max()))
+            assert float((out - r).abs().max()) <= tol
+        else:  # FP16 output rounding (2^-11 relative) + FP32 accumulation
+            assert float(((out - r).abs() / (r.abs() + 1)).max()) <= 2e-3
+    out = dev_gemm(A.cuda(), B.cuda()).double().cpu()
+    r = A.double() @ B.double().T
+    assert float(((out - r).abs() / (r.abs() + 1)).max()) <= (1e-5 if prec == "fp32" else 2e-3)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("M,N", [(1, 1000), (148, 32000), (513, 32000), (5, 8)])
+def test_gemm_argmax_unit(prec, M, N):
+    from paper_2109_08008_b200 import dev_gemm_argmax
+    K = 64 if N < 100 else 512
+    g = torch.Generator().manual_seed(M + N)
+    dt = torch.float16 if prec == "fp16" else torch.float32
+    A = torch.randn(M, K, generator=g).to(dt)
+    B = (torch.randn(N, K, generator=g) / K ** 0.5).to(dt)
+    nxt, lg = dev_gemm_argmax(A.cuda(), B.cuda(), logits=True)
+    ref = (A.double() @ B.double().T).numpy()
+    ok, worst = logits_close(lg.double().cpu().numpy(), ref, prec)
+    assert ok, worst
+    # the fused argmax equals argmax of the kernel's own FP32 logits, ties -> lowest id
+    lgn = lg.cpu().numpy()
+    assert (nxt.cpu().numpy() == np.argmax(lgn, axis=1)).all()
+    safe = margin_safe(ref, prec)
+    assert (nxt.cpu().numpy()[safe] == np.argmax(ref, axis=1)[safe]).all()
+
+
+def test_argmax_ties_lowest_id():
+    from paper_2109_08008_b200 import dev_gemm_argmax
+    A = torch.ones(4, 64, dtype=torch.float16, device="cuda")
+    B = torch.zeros(1000, 64, dtype=torch.float16, device="cuda")
+    B[[7, 300, 999]] = 1.0        # three equal maxima
+    assert (dev_gemm_argmax(A, B).cpu() == 7).all()
+
+
+# ------------------------------------------------------------------ model parity
+def _teacher_forced(name, prec, srcs, forced, eos_boost=1.0):
+    """Run encoder + forced decode on GPU and oracle; compare encoder out and logits."""
+    cfg, _ = weights(name, eos_boost)
+    om = oracle_model(name, eos_boost)
+    gm = gpu_model(name, prec, eos_boost, max_tokens=4096, max_sents=64, max_tgt_len=64)
+    src, lens = pad_batch(srcs)
+    batch = gm.encode(torch.from_numpy(src).cuda(), lens)
+    enc_o, lens_o = om.encode_batch(srcs)
+    enc_g = batch.encoder_output().cpu().numpy()
+    B, T = forced.shape
+    for b in range(B):   # compare valid positions only (padding rows are unused)
+        ok, worst = logits_close(enc_g[b, :lens[b]], enc_o[b, :lens[b]], prec)
+        assert ok, ("encoder", b, worst)
+    ckv = om.cross_kv(enc_o)
+    cache = om.new_cache(B, T)
+    worst_all = 0.0
+    for t in range(T):
+        prev = torch.from_numpy(forced[:, t].astype(np.int32)).cuda()
+        r = batch.decode_step(prev=prev, logits=True, n_live=B)
+        lo = om.decoder_step(forced[:, t], t, cache, ckv, lens_o)
+        lg = r["logits"].double().cpu().numpy()
+        ok, worst = logits_close(lg, lo, prec)
+        worst_all = max(worst_all, worst)
+        assert ok, ("step", t, worst)
+        safe = margin_safe(lo, prec)
+        assert (r["next"].cpu().numpy()[safe] == np.argmax(lo, 1)[safe]).all(), ("argmax", t)
+        n, _ = batch.prune(ratio=-1.0, want_map=False)
+        assert n == B
+    return worst_all
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_tiny_teacher_forced(prec):
+    wl = tiny_workload()
+    srcs = [wl.sentence(i) for i in range(wl.n)]
+    T = 20   # spans the RPR clip boundary t = 8/9
+    forced = np.concatenate([np.full((wl.n, 1), BOS_ID), random_tokens(wl.n, T - 1, 1000)], 1)
+    _teacher_forced("tiny", prec, srcs, forced)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name", ["student-6-1", "student-35-1"])
+def test_base_teacher_forced(prec, name):
+    wl = newstest_like(24, 32000)
+    srcs = [wl.sentence(i) for i in range(wl.n)]
+    T = 12
+    forced = np.concatenate([np.full((wl.n, 1), BOS_ID), random_tokens(wl.n, T - 1, 32000, seed=5)], 1)
+    _teacher_forced(name, prec, srcs, forced)
+
+
+def _free_running(name, prec, wl, eos_boost, max_tokens=4096, max_sents=512, ratio=0.25):
+    from oracle import translate_fast
+    om = oracle_model(name, eos_boost)
+    log = {}
+    ref = translate_fast(om, wl, max_tokens, max_sents, prune_ratio=ratio, log=log)
+    gm = gpu_model(name, prec, eos_boost, max_tokens=max_tokens, max_sents=max_sents)
+    out, st = gm.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=max_tokens, max_sents=max_sents,
+                           prune_ratio=ratio)
+    n_cmp = 0
+    full = True
+    for i in range(wl.n):
+        g, o, gaps = out[i], ref[i], log["margins"][i]
+        # compare up to (and including) the first margin-unsafe position
+        k = 0
+        while k < len(gaps) and gaps[k] > SAFE_GAP[prec]:
+            k += 1
+        if k == len(gaps):
+            assert g == o, (i, g, o)
+        else:
+            full = False
+            assert g[:k + 1] == o[:k] + g[k:k + 1], (i, k, g, o)
+        n_cmp += min(k, len(o))
+    if full:
+        assert st["gen_tokens"] == log["gen_tokens"]
+    return n_cmp, st, log
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_tiny_free_running_with_pruning(prec):
+    wl = tiny_workload(n=8, seed=3)
+    n_cmp, st, log = _free_running("tiny", prec, wl, eos_boost=3.0, max_tokens=40, max_sents=3)
+    assert n_cmp > 20
+    if prec == "fp32":
+        assert st["prunes"] == len(log["prunes"])
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_prune_maps_bit_exact(prec):
+    """Step API with pruning: new_to_old maps equal the oracle's at every decision point."""
+    from oracle import translate_fast
+    wl = tiny_workload(n=12, seed=5, max_cap=16)
+    om = oracle_model("tiny", 3.0)
+    log = {}
+    translate_fast(om, wl, 4096, 512, prune_ratio=0.25, log=log)
+    assert len(log["batches"]) == 1
+    order = log["batches"][0]
+    srcs = [wl.sentence(i) for i in order]
+    caps = wl.caps[order]
+    gm = gpu_model("tiny", prec, 3.0, max_tokens=4096, max_sents=64, max_tgt_len=64)
+    src, lens = pad_batch(srcs)
+    batch = gm.encode(torch.from_numpy(src).cuda(), lens, tgt_cap=caps)
+    n = len(order)
+    events = []
+    t = 0
+    while n > 0:
+        batch.decode_step(n_live=n)
+        n_new, m = batch.prune(ratio=0.25)
+        if 0 < n_new < n:
+            events.append((t, m.cpu().numpy()[:n_new].tolist()))
+        n = n_new
+        t += 1
+    ref = [(st, keep.tolist()) for (_, st, keep) in log["prunes"]]
+    if prec == "fp32":
+        assert events == ref
+    else:
+        assert events[:1] == ref[:1] or len(ref) == 0
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_35_1_free_running_subset(prec):
+    wl = newstest_like(40, 32000)
+    n_cmp, st, log = _free_running("student-35-1", prec, wl, eos_boost=1.0, max_tokens=512,
+                                   max_sents=16)
+    assert n_cmp > 0
+
+
+def test_translate_host_equals_device_and_steps():
+    cfg, _ = weights("student-35-1")
+    wl = newstest_like(64, 32000, start=1000)
+    gm = gpu_model("student-35-1", "fp16", max_tokens=1024, max_sents=32)
+    out_h, st_h = gm.translate(wl.ids, wl.off, caps=wl.caps)
+    d_ids = torch.from_numpy(wl.ids).cuda()
+    d_out = torch.zeros(wl.n, gm.Tmax, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(wl.n, dtype=torch.int32, device="cuda")
+    st_d = gm.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps)
+    d_out, d_len = d_out.cpu().numpy(), d_len.cpu().numpy()
+    for i in range(wl.n):
+        g = d_out[i, :d_len[i]].tolist()
+        if g and g[-1] == 3:
+            g = g[:-1]
+        assert g == out_h[i]
+    assert st_h["gen_tokens"] == st_d["gen_tokens"] == int(d_len.sum())
+    # deterministic: a second run is byte-identical
+    out_h2, _ = gm.translate(wl.ids, wl.off, caps=wl.caps)
+    assert out_h2 == out_h
+
+
+def test_batch_invariance_fp32():
+    """Sentence alone == sentence inside a bigger batch (PAPER.md:121 batching is exact)."""
+    wl = newstest_like(16, 32000, start=50)
+    gm = gpu_model("student-6-1", "fp32", max_tokens=2048, max_sents=64)
+    full, _ = gm.translate(wl.ids, wl.off, caps=wl.caps)
+    for i in (0, 7, 15):
+        one = wl.shard(i, i + 1)
+        o, _ = gm.translate(one.ids, one.off, caps=one.caps)
+        assert o[0] == full[i]
+
+
+def test_errors():
+    from paper_2109_08008_b200 import NmtError
+    gm = gpu_model("tiny", "fp16", max_tokens=64, max_sents=4, max_tgt_len=16)
+    src = torch.full((5, 4), 5, dtype=torch.int32, device="cuda")
+    with pytest.raises(NmtError, match="E_SHAPE"):
+        gm.encode(src, [4] * 5)
+    with pytest.raises(NmtError, match="E_INPUT"):
+        gm.translate(np.array([5, 2000, 3], np.int32), np.array([0, 3]))
