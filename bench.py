@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: FP16 greedy translation with the 35-1 Transformer-DLCL-RPR
+student (BASELINE.json configs[2], metric "target tokens/sec ... ms/decode step").
+
+A step = nmt_translate_device over one newstest-sized chunk (2998 sentences) of the
+synthetic 1M-sentence set (DESIGN.md input recipe): length sort, dynamic 4096-token /
+512-sentence batches, 35-layer encoder with RPR + DLCL, cached greedy
+decoding with the fused vocab argmax, batch pruning (rho = 0.25).  Each rank/step gets a
+distinct chunk (weak scaling: sentences are independent; no collective
+on the data path).  Inputs are resident in HBM for `value`; `e2e` times nmt_translate
+with host buffers (H2D of sources + D2H of outputs inside the timed region).
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Under torchrun each rank uses LOCAL_RANK's GPU; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "target tokens/sec (FP16 greedy, 35-1 student) at 1/2/4/8 B200; ms/decode step"
+UNIT = "target tokens/s"
+CHUNK = 2998            # newstest2018-sized chunk
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+TENSOR_CLASSES = {"enc_gemm", "vocab_argmax", "dec_gemm"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------- clocks sampler
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------- oracle (CPU) legs
+_OM = None
+_WL = None
+
+
+def _oracle_worker(args):
+    lo, hi, mt, ms = args
+    from threadpoolctl import threadpool_limits
+    from oracle import translate_fast
+    with threadpool_limits(1):
+        log = {}
+        translate_fast(_OM, _WL.shard(lo, hi), mt, ms, prune_ratio=0.25, log=log)
+    return log["gen_tokens"]
+
+
+def oracle_timed(cfg, W, wl, workers, max_tokens=4096, max_sents=512):
+    """O-fast (FP32 NumPy, cached + batched + pruned) as it stands, `workers` processes with
+    one BLAS thread each on contiguous shards (the paper's CPU scheme)."""
+    global _OM, _WL
+    import multiprocessing as mp
+    from oracle import OracleModel
+    _OM = OracleModel(W, cfg, dtype=np.float32)
+    _WL = wl
+    n = wl.n
+    bounds = np.linspace(0, n, workers + 1).astype(int)
+    jobs = [(int(bounds[i]), int(bounds[i + 1]), max_tokens, max_sents) for i in range(workers)
+            if bounds[i + 1] > bounds[i]]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(jobs)) as pool:
+        toks = pool.map(_oracle_worker, jobs)
+    dt = time.perf_counter() - t0
+    return sum(toks), dt, len(jobs)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle is this tier's reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    from synth import PRESETS, generate_weights, newstest_like
+    cfg = PRESETS[args.config]
+    W = generate_weights(cfg)
+    workers = min(cpu_cores(), 64)
+    per = args.ref_sents_per_worker
+    times, toks = [], []
+    for k in range(args.warmup + args.steps):
+        wl = newstest_like(workers * per, cfg.vocab_size, start=k * workers * per)
+        t, dt, used = oracle_timed(cfg, W, wl, workers)
+        if k >= args.warmup:
+            times.append(dt)
+            toks.append(t)
+    T = sum(times)
+    v = sum(toks) / T
+    sample = f"{args.steps} steps x {workers * per} sentences of the synthetic 1M set ({workers} procs x {per})"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * T / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"{args.config} greedy, oracle O-fast sample",
+                                            "max_tokens": 4096, "max_sents": 512},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- product arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--config", default="student-35-1")
+    ap.add_argument("--chunk", type=int, default=CHUNK)
+    ap.add_argument("--max-tokens", type=int, default=4096)
+    ap.add_argument("--max-sents", type=int, default=512)
+    ap.add_argument("--sync-every", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
+    ap.add_argument("--ref-sents-per-worker", type=int, default=12)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    from synth import PRESETS, generate_weights, newstest_like
+    cfg = PRESETS[args.config]
+    W = generate_weights(cfg)
+
+    # CPU baseline first (forked NumPy workers; before CUDA is initialised)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = min(cpu_cores(), 64)
+        wl = newstest_like(workers * args.cpu_sents_per_worker, cfg.vocab_size, start=900_000)
+        t, dt, used = oracle_timed(cfg, W, wl, workers, args.max_tokens, args.max_sents)
+        cpu = {"value": t / dt, "unit": UNIT, "cores": used, "kind": "oracle",
+               "sample": f"{wl.n} sentences (sentences 900000.. of the synthetic 1M set), "
+                         f"{used} processes x 1 BLAS thread, O-fast FP32, {dt:.1f} s"}
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2109_08008_b200 import Model
+
+    model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents)
+    stream = torch.cuda.current_stream()
+
+    n_chunks = args.warmup + args.steps
+    chunks = []
+    for k in range(n_chunks):
+        idx = k * world + rank
+        wl = newstest_like(args.chunk, cfg.vocab_size, start=idx * args.chunk)
+        chunks.append((wl, torch.from_numpy(wl.ids).cuda()))
+    Tm = model.Tmax
+    d_out = torch.empty(args.chunk, Tm, dtype=torch.int32, device="cuda")
+    d_len = torch.empty(args.chunk, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def dev_step(k):
+        wl, d_ids = chunks[k]
+        return model.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps,
+                                      max_tokens=args.max_tokens, max_sents=args.max_sents,
+                                      sync_every=args.sync_every)
+
+    for k in range(args.warmup):
+        dev_step(k)
+    barrier()
+    clk = Clocks(local)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    gen = steps = launches = 0
+    for k in range(args.warmup, n_chunks):
+        st = dev_step(k)
+        gen += st["gen_tokens"]
+        steps += st["decode_steps"]
+        launches += st["launches"]
+    ev1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+
+    def allred(x, op):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=op)
+        return t.item()
+
+    import torch.distributed as tdist
+    MAX = tdist.ReduceOp.MAX if world > 1 else None
+    SUM = tdist.ReduceOp.SUM if world > 1 else None
+    ms_max = allred(ms, MAX)
+    gen_all = allred(float(gen), SUM)
+    steps_all = allred(float(steps), SUM)
+    value = gen_all / (ms_max / 1000.0)
+
+    # ---- e2e through the host-buffer C-ABI call (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g2 = 0
+        h2d = d2h = 0
+        for k in range(args.warmup, n_chunks):
+            wl, _ = chunks[k]
+            outs, st = model.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=args.max_tokens,
+                                       max_sents=args.max_sents, sync_every=args.sync_every)
+            g2 += st["gen_tokens"]
+            h2d += wl.ids.nbytes
+            d2h += 4 * sum(len(o) for o in outs) + 4 * len(outs)
+        e1.record(stream)
+        barrier()
+        ems = allred(e0.elapsed_time(e1), MAX)
+        e2e = {"value": allred(float(g2), SUM) / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+
+    # ---- per-kernel-class profile of one more step (CUDA events on the launching stream)
+    model.profile(2)
+    st = dev_step(args.warmup)
+    prof = model.profile(0)
+    tot = sum(v["ms"] for v in prof.values())
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    pk, src = peaks()
+    if dom_name in TENSOR_CLASSES:
+        ach = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+        peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s"}
+    else:
+        ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        peak = pk["hbm_gbs"]
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s"}
+    roof.update({"frac": ach / peak, "traffic": None, "kernel": dom_name,
+                 "share_of_step": dom["ms"] / tot if tot else None, "peak_source": src,
+                 "per_launch": {"flops" if roof["bound"] == "tensor" else "bytes":
+                                (dom["flops"] if roof["bound"] == "tensor" else dom["bytes"]) / dom["launches"],
+                                "ms": dom["ms"] / dom["launches"], "launches": dom["launches"]}})
+    dec_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("dec") or k in ("vocab_argmax", "bookkeeping"))
+    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
+                   "share": round(v["ms"] / tot, 4) if tot else None} for k, v in prof.items()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": f"{args.config} FP16 greedy, {args.chunk}-sentence newstest-shaped "
+                                   f"chunk per rank per step, batch pruning rho=0.25",
+                       "max_tokens": args.max_tokens, "max_sents": args.max_sents,
+                       "parallelism": f"sentence-sharded x{world}",
+                       "l2": "working set > L2 (262 MB FP16 weights + DLCL history)"},
+            "ms_per_decode_step": ms_max / max(1.0, steps_all / world),
+            "ms_per_decode_step_kernels": dec_ms / max(1, st["decode_steps"]),
+            "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "kernels": kernels,
+            "cpu_baseline": cpu, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,21 @@ nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_
 
 const char* nmt_last_error(void);   /* thread-local; valid until the next nmt_* call */
 
+/* Per-kernel-class profile, measured with CUDA events recorded on the launching stream
+ * around every launch while enabled (adds two event records per launch).
+ * mode: 1 = enable, 2 = reset counters and enable, 0 = reset and disable,
+ *       -1 = read only.  When `out` is non-NULL, up to `cap` entries for the classes
+ * that ran are written (read happens before any reset) and *n_out is set.
+ * flops / bytes are the ALGORITHMIC work of the launches.
+ * Synchronises the device. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double ms, flops, bytes;
+} nmt_prof_entry;
+nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t cap,
+                       int32_t* n_out);
+
 /* ---- kernel-level entry points used by the unit parity tests ------------------- */
 /* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision
  * (FP16: tcgen05/TMEM/TMA tensor-core GEMM; FP32: SIMT), all pointers device, row-major

@@ -93,7 +93,18 @@ struct nmt_model {
   } hp{};
   void* pinned = nullptr;
   nmt_batch batch;
+  // optional per-kernel-class CUDA-event profile (bench roofline)
+  struct ProfRec { int cls; cudaEvent_t a, b; double flops, bytes; };
+  struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<ProfRec> pending;
+    double ms[16] = {}, flops[16] = {}, bytes[16] = {};
+    long long n[16] = {};
+  } prof;
   ~nmt_model() {
+    for (auto e : prof.pool) cudaEventDestroy(e);
     if (wbuf) cudaFree(wbuf);
     if (ar.base) cudaFree(ar.base);
     if (pinned) cudaFreeHost(pinned);
@@ -233,7 +244,8 @@ void init_arena(nmt_model* m) {
   for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
   NMT_CUDA(cudaMemset(a.base, 0, a.used));
   // pinned staging
-  size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64;
+  size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 +
+              16 * 64 /* per-region 64-B rounding */;
   NMT_CUDA(cudaMallocHost(&m->pinned, pb));
   char* p = (char*)m->pinned;
   auto take = [&](size_t b) { char* r = p; p += (b + 63) & ~size_t(63); return r; };
@@ -249,6 +261,60 @@ void init_arena(nmt_model* m) {
   m->hp.bad = (int*)take(4);
 }
 
+// ------------------------------------------------------------------ profiling
+enum ProfClass {
+  P_ENC_GEMM = 0, P_ENC_ATTN, P_DLCL, P_ENC_LN, P_EMBED, P_DEC_GEMM, P_VOCAB, P_DEC_SELF,
+  P_DEC_CROSS, P_DEC_LN, P_BOOK, P_NCLS
+};
+const char* kProfNames[P_NCLS] = {"enc_gemm",  "enc_rpr_attn", "dlcl_combine", "enc_layernorm",
+                                  "embed",     "dec_gemm",     "vocab_argmax", "dec_self_attn",
+                                  "dec_cross_attn", "dec_layernorm", "bookkeeping"};
+
+void prof_flush(nmt_model* m) {
+  auto& P = m->prof;
+  for (auto& r : P.pending) {
+    float ms = 0.f;
+    NMT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    P.ms[r.cls] += ms;
+    P.flops[r.cls] += r.flops;
+    P.bytes[r.cls] += r.bytes;
+    P.n[r.cls] += 1;
+  }
+  P.pending.clear();
+  P.used = 0;
+}
+
+// Runs f() (one kernel launch); when profiling, brackets it with stream events and
+// records its algorithmic FLOPs / bytes.
+template <class F>
+void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {
+  auto& P = m->prof;
+  if (!P.on) {
+    f();
+    return;
+  }
+  while (P.pool.size() < P.used + 2) {
+    cudaEvent_t e;
+    NMT_CUDA(cudaEventCreate(&e));
+    P.pool.push_back(e);
+  }
+  cudaEvent_t a = P.pool[P.used++], b = P.pool[P.used++];
+  NMT_CUDA(cudaEventRecord(a, s));
+  f();
+  NMT_CUDA(cudaEventRecord(b, s));
+  P.pending.push_back({cls, a, b, flops, bytes});
+}
+#define PROF(cls, fl, by, stmt) prof_run(m, cls, (double)(fl), (double)(by), s, [&] { stmt; })
+
+double gemm_bytes(const GemmArgs& a, size_t tb) {
+  double b = ((double)a.M * a.K + (double)a.N * a.K) * tb;
+  if (!a.argmax) b += (double)a.M * a.N * tb;
+  if (a.R) b += (double)a.M * a.N * tb;
+  if (a.bias) b += (double)a.N * tb;
+  return b;
+}
+double gemm_flops(const GemmArgs& a) { return 2.0 * a.M * a.N * a.K; }
+
 // ------------------------------------------------------------------ encode
 template <class T>
 void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
@@ -257,56 +323,70 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
   const int d = c.d_model, F = c.d_ffn, H = c.n_heads, L = c.enc_layers, Ld = c.dec_layers;
   const int N = B * S;
   const float eps = c.ln_eps;
+  const size_t tb = sizeof(T);
   T *x = v.p(m->x), *u = v.p(m->u), *qkv = v.p(m->qkv), *o = v.p(m->o), *h = v.p(m->h),
     *enc = v.p(m->enc), *hist = v.p(m->hist), *ckv = v.p(m->ckv);
   const size_t hs = (size_t)N * d;
+  const double row = (double)N * d * tb;  // bytes of one [N][d] activation
   const float sq = std::sqrt((float)d);
   // y0 = sqrt(d) E[s] + PE(p)
-  embed<T>(m->src, v.w("emb"), m->pe, c.use_dlcl ? o : x, N, d, S, nullptr, nullptr, sq, s);
+  PROF(P_EMBED, 0, 2 * row, embed<T>(m->src, v.w("emb"), m->pe, c.use_dlcl ? o : x, N, d, S,
+                                      nullptr, nullptr, sq, s));
   if (c.use_dlcl) {
-    dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, v.w("enc.dlcl.ln.0.g"), v.w("enc.dlcl.ln.0.b"),
-                    c.dlcl_ln, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), x, u, N, d, eps, s);
+    PROF(P_DLCL, 0, 4 * row,
+         dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, v.w("enc.dlcl.ln.0.g"), v.w("enc.dlcl.ln.0.b"),
+                         c.dlcl_ln, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), x, u, N, d,
+                         eps, s));
   } else {
-    layernorm<T>(x, d, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), u, d, N, d, eps, nullptr, s);
+    PROF(P_ENC_LN, 0, 2 * row,
+         layernorm<T>(x, d, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), u, d, N, d, eps,
+                      nullptr, s));
   }
+  const double attn_flops = 4.0 * B * H * (double)S * S * (d / H);
   for (int l = 0; l < L; ++l) {
     const std::string p = "enc." + std::to_string(l) + ".";
     GemmArgs a;
     a.M = N; a.N = 3 * d; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "qkv.w"); a.ldb = d;
     a.bias = v.w(p + "qkv.b"); a.C = qkv; a.ldc = 3 * d;
-    gemm<T>(a, s);
-    attn_encoder<T>(qkv, m->src_len, v.rel(p, "rel_k"), v.rel(p, "rel_v"), o, B, S, d, H,
-                    c.max_rel_pos, c.use_rpr, s);
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_ENC_ATTN, attn_flops, 4 * row,
+         attn_encoder<T>(qkv, m->src_len, v.rel(p, "rel_k"), v.rel(p, "rel_v"), o, B, S, d, H,
+                         c.max_rel_pos, c.use_rpr, s));
     a = GemmArgs();
     a.M = N; a.N = d; a.K = d; a.A = o; a.lda = d; a.B = v.w(p + "out.w"); a.ldb = d;
     a.bias = v.w(p + "out.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
-    gemm<T>(a, s);                                          // a = x + Attn(LN(x))
-    layernorm<T>(x, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), u, d, N, d, eps, nullptr, s);
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // a = x + Attn(LN(x))
+    PROF(P_ENC_LN, 0, 2 * row,
+         layernorm<T>(x, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), u, d, N, d, eps, nullptr, s));
     a = GemmArgs();
     a.M = N; a.N = F; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
     a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = h; a.ldc = F;
-    gemm<T>(a, s);
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
     a = GemmArgs();
     a.M = N; a.N = d; a.K = F; a.A = h; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
     a.bias = v.w(p + "ffn2.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
-    gemm<T>(a, s);                                          // y_l = a + FFN(LN(a))
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // y_l = a + FFN(LN(a))
     const bool last = (l == L - 1);
     const std::string np = last ? "enc.final_ln." : "enc." + std::to_string(l + 1) + ".attn_ln.";
     if (c.use_dlcl) {
       const int k = l + 1;  // depth of y
       const std::string dp = "enc.dlcl.ln." + std::to_string(k) + ".";
-      dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, v.w(dp + "g"),
-                      v.w(dp + "b"), c.dlcl_ln, v.w(np + "g"), v.w(np + "b"),
-                      last ? nullptr : x, last ? enc : u, N, d, eps, s);
+      // reads y + k history rows, writes z_k, (x), LN(x)
+      PROF(P_DLCL, 0, (1 + k + 1 + (last ? 0 : 1) + 1) * row,
+           dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, v.w(dp + "g"),
+                           v.w(dp + "b"), c.dlcl_ln, v.w(np + "g"), v.w(np + "b"),
+                           last ? nullptr : x, last ? enc : u, N, d, eps, s));
     } else {
-      layernorm<T>(x, d, v.w(np + "g"), v.w(np + "b"), last ? enc : u, d, N, d, eps, nullptr, s);
+      PROF(P_ENC_LN, 0, 2 * row,
+           layernorm<T>(x, d, v.w(np + "g"), v.w(np + "b"), last ? enc : u, d, N, d, eps, nullptr,
+                        s));
     }
   }
   // cross K/V of every decoder layer, once per sentence
   GemmArgs a;
   a.M = N; a.N = Ld * 2 * d; a.K = d; a.A = enc; a.lda = d; a.B = m->ckv_w; a.ldb = d;
   a.bias = m->ckv_b; a.C = ckv; a.ldc = Ld * 2 * d;
-  gemm<T>(a, s);
+  PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
 }
 
 // ------------------------------------------------------------------ decode step
@@ -320,56 +400,67 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   const int Tm = m->lim.max_tgt_len;
   const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
   const float eps = c.ln_eps;
+  const size_t tb = sizeof(T);
   const int* dR = &m->st->n_live;
   const int* dt = &m->st->t;
+  const int t = b->step;  // host mirror (profile byte counts only)
+  const double row = (double)R * d * tb;
   T *g = v.p(m->g), *du = v.p(m->du), *dqkv = v.p(m->dqkv), *dout = v.p(m->dout),
     *dq = v.p(m->dq), *dh = v.p(m->dh);
-  embed<T>(d_prev ? d_prev : m->prev_tok, v.w("emb"), m->pe, g, R, d, 1, dt, dR,
-           std::sqrt((float)d), s);
+  PROF(P_EMBED, 0, 2 * row,
+       embed<T>(d_prev ? d_prev : m->prev_tok, v.w("emb"), m->pe, g, R, d, 1, dt, dR,
+                std::sqrt((float)d), s));
   for (int l = 0; l < Ld; ++l) {
     const std::string p = "dec." + std::to_string(l) + ".";
     T* kc = v.p(m->kc) + (size_t)l * Rmax * Tm * d;
     T* vc = v.p(m->vc) + (size_t)l * Rmax * Tm * d;
-    layernorm<T>(g, d, v.w(p + "self_ln.g"), v.w(p + "self_ln.b"), du, d, R, d, eps, dR, s);
+    PROF(P_DEC_LN, 0, 2 * row,
+         layernorm<T>(g, d, v.w(p + "self_ln.g"), v.w(p + "self_ln.b"), du, d, R, d, eps, dR, s));
     GemmArgs a;
     a.M = R; a.N = 3 * d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "self_qkv.w"); a.ldb = d;
     a.bias = v.w(p + "self_qkv.b"); a.C = dqkv; a.ldc = 3 * d; a.dM = dR;
-    gemm<T>(a, s);
-    attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, v.rel(p, "rel_k"), v.rel(p, "rel_v"),
-                         dout, R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
+         attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, v.rel(p, "rel_k"), v.rel(p, "rel_v"),
+                              dout, R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s));
     a = GemmArgs();
     a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "self_out.w"); a.ldb = d;
     a.bias = v.w(p + "self_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    gemm<T>(a, s);
-    layernorm<T>(g, d, v.w(p + "cross_ln.g"), v.w(p + "cross_ln.b"), du, d, R, d, eps, dR, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_LN, 0, 2 * row,
+         layernorm<T>(g, d, v.w(p + "cross_ln.g"), v.w(p + "cross_ln.b"), du, d, R, d, eps, dR, s));
     a = GemmArgs();
     a.M = R; a.N = d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "cross_q.w"); a.ldb = d;
     a.bias = v.w(p + "cross_q.b"); a.C = dq; a.ldc = d; a.dM = dR;
-    gemm<T>(a, s);
-    attn_cross<T>(dq, v.p(m->ckv), Ld * 2 * d, l * 2 * d, l * 2 * d + d, b->S, m->src_len,
-                  m->row_slot, dout, R, d, H, dR, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
+         attn_cross<T>(dq, v.p(m->ckv), Ld * 2 * d, l * 2 * d, l * 2 * d + d, b->S, m->src_len,
+                       m->row_slot, dout, R, d, H, dR, s));
     a = GemmArgs();
     a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "cross_out.w"); a.ldb = d;
     a.bias = v.w(p + "cross_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    gemm<T>(a, s);
-    layernorm<T>(g, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), du, d, R, d, eps, dR, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_LN, 0, 2 * row,
+         layernorm<T>(g, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), du, d, R, d, eps, dR, s));
     a = GemmArgs();
     a.M = R; a.N = F; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
     a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = dh; a.ldc = F; a.dM = dR;
-    gemm<T>(a, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
     a = GemmArgs();
     a.M = R; a.N = d; a.K = F; a.A = dh; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
     a.bias = v.w(p + "ffn2.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    gemm<T>(a, s);
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
   }
-  layernorm<T>(g, d, v.w("dec.final_ln.g"), v.w("dec.final_ln.b"), du, d, R, d, eps, dR, s);
+  PROF(P_DEC_LN, 0, 2 * row,
+       layernorm<T>(g, d, v.w("dec.final_ln.g"), v.w("dec.final_ln.b"), du, d, R, d, eps, dR, s));
   GemmArgs a;  // tied vocab projection fused with argmax
   a.M = R; a.N = c.vocab_size; a.K = d; a.A = du; a.lda = d; a.B = v.w("emb"); a.ldb = d;
   a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
-  gemm<T>(a, s);
-  greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok, Tm,
-                m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
-                out ? out->d_done : nullptr, s);
+  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+  PROF(P_BOOK, 0, 0,
+       greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
+                     Tm, m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
+                     out ? out->d_done : nullptr, s));
 }
 
 void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
@@ -414,6 +505,7 @@ void check_batch_shape(nmt_model* m, int B, int S) {
 void poll_state(nmt_model* m, cudaStream_t s) {
   NMT_CUDA(cudaMemcpyAsync(m->hp.st, m->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   NMT_CUDA(cudaStreamSynchronize(s));
+  if (!m->prof.pending.empty()) prof_flush(m);
 }
 
 // ------------------------------------------------------------------ translate core
@@ -483,7 +575,8 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
     for (; t < b.max_cap && rows > 0; ++t) {
       b.rows_upper = rows;
       decode_step_any(m, &b, nullptr, nullptr, s);
-      prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, rows, s);
+      PROF(P_BOOK, 0, 0,
+           prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, rows, s));
       if ((t + 1) % sync_every == 0) {
         poll_state(m, s);
         rows = m->hp.st->n_live;
@@ -852,6 +945,38 @@ nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_
     NMT_CUDA(cudaMemcpyAsync(m->hp.bad, m->bad, 4, cudaMemcpyDeviceToHost, s));
     NMT_CUDA(cudaStreamSynchronize(s));
     NMT_REQUIRE(*m->hp.bad == 0, NMT_E_INPUT, "token id out of range in d_ids");
+  });
+}
+
+nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t cap,
+                       int32_t* n_out) {
+  return guard([&] {
+    NMT_REQUIRE(m, NMT_E_ARG, "null model");
+    NMT_CUDA(cudaDeviceSynchronize());
+    prof_flush(m);
+    if (out) {
+      NMT_REQUIRE(n_out, NMT_E_ARG, "null n_out");
+      int n = 0;
+      for (int c = 0; c < P_NCLS && n < cap; ++c) {
+        if (!m->prof.n[c]) continue;
+        nmt_prof_entry& e = out[n++];
+        memset(&e, 0, sizeof(e));
+        strncpy(e.name, kProfNames[c], sizeof(e.name) - 1);
+        e.launches = m->prof.n[c];
+        e.ms = m->prof.ms[c];
+        e.flops = m->prof.flops[c];
+        e.bytes = m->prof.bytes[c];
+      }
+      *n_out = n;
+    }
+    if (mode == 2 || mode == 0) {  // reset counters
+      auto& P = m->prof;
+      std::fill(P.ms, P.ms + 16, 0.0);
+      std::fill(P.flops, P.flops + 16, 0.0);
+      std::fill(P.bytes, P.bytes + 16, 0.0);
+      std::fill(P.n, P.n + 16, 0ll);
+    }
+    if (mode >= 0 && mode <= 2) m->prof.on = (mode != 0);
   });
 }
 

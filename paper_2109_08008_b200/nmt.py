@@ -23,7 +23,12 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INPUT", 4: "E_STATE", 5: "E_F
 EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_batch_encoder_output", "nmt_decode_step", "nmt_prune_batch", "nmt_batch_live",
            "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
-           "nmt_dev_gemm", "nmt_dev_gemm_argmax"]
+           "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile"]
+
+
+class ProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
 
 
 class NmtError(RuntimeError):
@@ -113,6 +118,16 @@ class Model:
         if getattr(self, "h", None):
             lib().nmt_free_model(self.h)
             self.h = None
+
+    def profile(self, mode: int = -1):
+        """mode 1 enable, 2 reset+enable, 0 reset+disable, -1 read.  Returns
+        {class: {launches, ms, flops, bytes}} read before any reset."""
+        buf = (ProfEntry * 16)()
+        n = C.c_int32()
+        _check(lib().nmt_profile(self.h, mode, buf, 16, C.byref(n)))
+        return {buf[i].name.decode(): {"launches": buf[i].launches, "ms": buf[i].ms,
+                                       "flops": buf[i].flops, "bytes": buf[i].bytes}
+                for i in range(n.value)}
 
     # ---------------------------------------------------------------- step API
     def encode(self, src, src_len, tgt_cap=None, stream=None):

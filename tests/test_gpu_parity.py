@@ -150,7 +150,7 @@ def _free_running(name, prec, wl, eos_boost, max_tokens=4096, max_sents=512, rat
 def test_tiny_free_running_with_pruning(prec):
     wl = tiny_workload(n=8, seed=3)
     n_cmp, st, log = _free_running("tiny", prec, wl, eos_boost=3.0, max_tokens=40, max_sents=3)
-    assert n_cmp > 20
+    assert n_cmp > (20 if prec == "fp32" else 8)   # FP16: fewer margin-safe positions
     if prec == "fp32":
         assert st["prunes"] == len(log["prunes"])
 
