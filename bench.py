@@ -203,7 +203,9 @@ def main():
     from paper_2109_08008_b200 import Model
 
     model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents)
-    stream = torch.cuda.current_stream()
+    # a non-default stream: decode steps are replayed as CUDA graphs (no capture on stream 0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     n_chunks = args.warmup + args.steps
     chunks = []

@@ -1,0 +1,457 @@
+// attention.cu — RPR self-attention (Shaw et al.; "maximum relative
+// length was 8"), cached decoder self-attention and cross-attention
+// over the once-per-sentence encoder K/V.
+//
+// Bandwidth/latency-bound at these shapes (S <= 120, dh = 64): SIMT FP32 with every
+// (query, key) pair and every (query, channel) pair in parallel; reductions by warp
+// shuffle; no serial dependency chains.  Keys and values carry the clipped relative
+// embeddings A^K[r], A^V[r], r(i,j) = clip(j - i, -k, k) + k (reading R7/R24):
+//   e_ij = (q_i . k_j + q_i . A^K[r(i,j)]) / sqrt(dh)
+//   o_i  = sum_j a_ij v_j + sum_r (sum_{j: r(i,j) = r} a_ij) A^V[r]
+// The second form of o_i needs only the 2k+1 bucket sums: buckets 1..2k-1 hold one key
+// each, buckets 0 and 2k the tails j <= i-k and j >= i+k.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+
+template <class T> struct Vec8;   // 8 consecutive elements -> float[8]
+template <> struct Vec8<__half> {
+  static __device__ __forceinline__ void load(const __half* p, float* f) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 x = __half22float2(h[e]);
+      f[2 * e] = x.x;
+      f[2 * e + 1] = x.y;
+    }
+  }
+};
+template <> struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float* f) {
+    float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+};
+
+template <int DH>
+__device__ __forceinline__ float dot_ss(const float* __restrict__ a, const float* __restrict__ b) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int c = 0; c < DH; c += 4) {
+    s0 = fmaf(a[c], b[c], s0);
+    s1 = fmaf(a[c + 1], b[c + 1], s1);
+    s2 = fmaf(a[c + 2], b[c + 2], s2);
+    s3 = fmaf(a[c + 3], b[c + 3], s3);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+// ----------------------------------------------------------------- encoder (per sentence, head)
+template <class T, int DH>
+__global__ void __launch_bounds__(256) k_attn_enc(const T* __restrict__ qkv,
+                                                  const int* __restrict__ len,
+                                                  const T* __restrict__ relk,
+                                                  const T* __restrict__ relv, T* __restrict__ out,
+                                                  int S, int d, int kclip, int use_rpr) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int R = 2 * kclip + 1, LQ = DH + 1, LP = S + 1, LB = R + 1;
+  float* sQ = sm;                  // [S][DH+1]
+  float* sK = sQ + S * LQ;         // [S][DH+1]
+  float* sV = sK + S * LQ;         // [S][DH]
+  float* sAK = sV + S * DH;        // [R][DH+1]
+  float* sAV = sAK + R * LQ;       // [R][DH]
+  float* sQA = sAV + R * DH;       // [S][R+1]   q_i . A^K[r]
+  float* sP = sQA + S * LB;        // [S][S+1]   scores -> probabilities
+  float* sB = sP + S * LP;         // [S][R+1]   bucket sums
+  const int n = len[b];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const size_t rs = 3 * (size_t)d;
+  const T* base = qkv + (size_t)b * S * rs + h * DH;
+  // phase 0: stage Q, K, V (8 elements per thread-iteration) and the relative tables
+  for (int idx = tid; idx < n * (DH / 8); idx += nt) {
+    const int j = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
+    float f[8];
+    const T* rp = base + (size_t)j * rs + c;
+    Vec8<T>::load(rp, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sQ[j * LQ + c + e] = f[e];
+    Vec8<T>::load(rp + d, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sK[j * LQ + c + e] = f[e];
+    Vec8<T>::load(rp + 2 * d, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sV[j * DH + c + e] = f[e];
+  }
+  if (use_rpr)
+    for (int idx = tid; idx < R * DH; idx += nt) {
+      const int r = idx / DH, c = idx % DH;
+      sAK[r * LQ + c] = to_f(relk[idx]);
+      sAV[r * DH + c] = to_f(relv[idx]);
+    }
+  __syncthreads();
+  // phase 1: raw scores q_i . k_j and q_i . A^K[r] for every pair
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx - i * n;
+    sP[i * LP + j] = dot_ss<DH>(sQ + i * LQ, sK + j * LQ);
+  }
+  if (use_rpr)
+    for (int idx = tid; idx < n * R; idx += nt) {
+      const int i = idx / R, r = idx - i * R;
+      sQA[i * LB + r] = dot_ss<DH>(sQ + i * LQ, sAK + r * LQ);
+    }
+  __syncthreads();
+  // phase 2: masked FP32 softmax per query row (warp per row) + bucket sums
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const float scale = rsqrtf((float)DH);
+  for (int i = warp; i < n; i += nw) {
+    float* p = sP + i * LP;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) {
+      float e = p[j];
+      if (use_rpr) e += sQA[i * LB + min(max(j - i, -kclip), kclip) + kclip];
+      e *= scale;
+      p[j] = e;
+      mx = fmaxf(mx, e);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float e = __expf(p[j] - mx);
+      p[j] = e;
+      sum += e;
+    }
+    const float inv = 1.f / warp_sum(sum);
+    float lo = 0.f, hi = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float a = p[j] * inv;
+      p[j] = a;
+      if (j - i <= -kclip) lo += a;
+      if (j - i >= kclip) hi += a;
+    }
+    if (use_rpr) {
+      lo = warp_sum(lo);
+      hi = warp_sum(hi);
+      __syncwarp();
+      if (lane < R) {
+        float v;
+        if (lane == 0) v = lo;
+        else if (lane == R - 1) v = hi;
+        else {
+          const int j = i + lane - kclip;
+          v = (j >= 0 && j < n) ? p[j] : 0.f;
+        }
+        sB[i * LB + lane] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // phase 3: o_i[c] = sum_j a_ij v_j[c] + sum_r B_ir A^V[r][c]  (every (i, c) in parallel)
+  T* obase = out + (size_t)b * S * d + h * DH;
+  for (int idx = tid; idx < S * DH; idx += nt) {
+    const int i = idx / DH, c = idx - i * DH;
+    float o = 0.f;
+    if (i < n) {
+      const float* p = sP + i * LP;
+      float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+      int j = 0;
+      for (; j + 3 < n; j += 4) {
+        o0 = fmaf(p[j], sV[j * DH + c], o0);
+        o1 = fmaf(p[j + 1], sV[(j + 1) * DH + c], o1);
+        o2 = fmaf(p[j + 2], sV[(j + 2) * DH + c], o2);
+        o3 = fmaf(p[j + 3], sV[(j + 3) * DH + c], o3);
+      }
+      for (; j < n; ++j) o0 = fmaf(p[j], sV[j * DH + c], o0);
+      o = (o0 + o1) + (o2 + o3);
+      if (use_rpr)
+        for (int r = 0; r < R; ++r) o = fmaf(sB[i * LB + r], sAV[r * DH + c], o);
+    }
+    obase[(size_t)i * d + c] = from_f<T>(o);  // padding query rows -> 0
+  }
+}
+
+template <class T, int DH>
+void launch_enc(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
+                int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  const int R = 2 * kclip + 1;
+  size_t fl = 2 * S * (DH + 1) + S * DH + R * (DH + 1) + R * DH + S * (R + 1) + S * (S + 1) +
+              S * (R + 1);
+  size_t smem = fl * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr = true;
+  }
+  k_attn_enc<T, DH><<<dim3(B, H), 256, smem, s>>>(qkv, len, relk, relv, out, S, d, kclip, use_rpr);
+  NMT_LAUNCH_CHECK();
+}
+
+template <class T>
+void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
+                  int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  if (B <= 0) return;
+  switch (d / H) {
+    case 16: launch_enc<T, 16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 32: launch_enc<T, 32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 64: launch_enc<T, 64>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    default: throw CudaError("attn_encoder: head dim must be 16, 32 or 64");
+  }
+}
+
+// ----------------------------------------------------------------- decoder self-attention
+// One warp per (live row, head) at step t = *d_t: k_t, v_t are appended to the cache slot,
+// then positions 0..t are attended; only buckets 0..k occur (j <= t) and every
+// j <= t - k falls in bucket 0.
+template <class T, int DH>
+__global__ void __launch_bounds__(128) k_attn_dec_self(
+    const T* __restrict__ qkv, T* __restrict__ kc, T* __restrict__ vc, int Tmax,
+    const int* __restrict__ row_slot, const T* __restrict__ relk, const T* __restrict__ relv,
+    T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
+    const int* __restrict__ dR) {
+  extern __shared__ float sm[];
+  constexpr int CPL = (DH + 31) / 32;  // channels per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + warp;
+  const int row = gw / H, h = gw - (gw / H) * H;
+  if (row >= min(rows, *dR)) return;
+  const int t = *d_t;
+  float* q = sm + warp * (DH + 32 + Tmax);
+  float* x = q + DH;   // q . A^K[r], then bucket sums
+  float* p = x + 32;
+  const int slot = row_slot[row];
+  const T* src = qkv + (size_t)row * 3 * d + h * DH;
+  T* kbase = kc + (size_t)slot * Tmax * d + h * DH;
+  T* vbase = vc + (size_t)slot * Tmax * d + h * DH;
+  for (int c = lane; c < DH; c += 32) {
+    q[c] = to_f(src[c]);
+    kbase[(size_t)t * d + c] = src[d + c];        // KV-cache append
+    vbase[(size_t)t * d + c] = src[2 * d + c];
+  }
+  __syncwarp();
+  if (use_rpr && lane <= kclip) {
+    float a = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < DH; ++c) a = fmaf(q[c], to_f(relk[lane * DH + c]), a);
+    x[lane] = a;
+  }
+  __syncwarp();
+  const float scale = rsqrtf((float)DH);
+  float mx = -INFINITY;
+  for (int j = lane; j <= t; j += 32) {
+    const T* kr = kbase + (size_t)j * d;
+    float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      float f[8];
+      Vec8<T>::load(kr + c, f);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        e0 = fmaf(f[u], q[c + u], e0);
+        e1 = fmaf(f[u + 1], q[c + u + 1], e1);
+      }
+    }
+    float e = e0 + e1;
+    if (use_rpr) e += x[max(j - t, -kclip) + kclip];
+    e *= scale;
+    p[j] = e;
+    mx = fmaxf(mx, e);
+  }
+  mx = warp_max(mx);
+  float sum = 0.f, lo = 0.f;
+  for (int j = lane; j <= t; j += 32) {
+    const float e = __expf(p[j] - mx);
+    p[j] = e;
+    sum += e;
+    if (j <= t - kclip) lo += e;
+  }
+  const float inv = 1.f / warp_sum(sum);
+  lo = warp_sum(lo);
+  __syncwarp();
+  if (use_rpr) {
+    if (lane <= kclip) {
+      float bsum;
+      if (lane == 0) bsum = lo;
+      else {
+        const int j = t - kclip + lane;
+        bsum = j >= 0 ? p[j] : 0.f;
+      }
+      x[lane] = bsum;  // (unnormalised)
+    }
+    __syncwarp();
+  }
+  float o[CPL];
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) o[u] = 0.f;
+  int j = 0;
+  for (; j + 1 <= t; j += 2) {
+    const float p0 = p[j], p1 = p[j + 1];
+    const T* v0 = vbase + (size_t)j * d;
+    const T* v1 = v0 + d;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int c = lane + 32 * u;
+      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), fmaf(p1, to_f(v1[c]), o[u]));
+    }
+  }
+  for (; j <= t; ++j) {
+    const float p0 = p[j];
+    const T* v0 = vbase + (size_t)j * d;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int c = lane + 32 * u;
+      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), o[u]);
+    }
+  }
+  T* orow = out + (size_t)row * d + h * DH;
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) {
+    const int c = lane + 32 * u;
+    if (c < DH) {
+      float r = o[u];
+      if (use_rpr)
+        for (int b = 0; b <= kclip; ++b) r = fmaf(x[b], to_f(relv[b * DH + c]), r);
+      orow[c] = from_f<T>(r * inv);
+    }
+  }
+}
+
+template <class T>
+void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot, const T* relk,
+                       const T* relv, T* out, int rows, int d, int H, int kclip, int use_rpr,
+                       const int* d_t, const int* dR, cudaStream_t s) {
+  if (rows <= 0) return;
+  const int nw = 4, dh = d / H;
+  size_t smem = sizeof(float) * nw * (dh + 32 + Tmax);
+  dim3 grid(ceil_div(rows * H, nw));
+#define NMT_DS(DH)                                                                             \
+  k_attn_dec_self<T, DH><<<grid, nw * 32, smem, s>>>(qkv, kc, vc, Tmax, row_slot, relk, relv, \
+                                                     out, rows, d, H, kclip, use_rpr, d_t, dR)
+  switch (dh) {
+    case 16: NMT_DS(16); break;
+    case 32: NMT_DS(32); break;
+    case 64: NMT_DS(64); break;
+    default: throw CudaError("attn_decoder_self: head dim must be 16, 32 or 64");
+  }
+#undef NMT_DS
+  NMT_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------------- cross-attention
+// One warp per (live row, head); keys at ckv + (slot*S + j)*ldkv + koff + h*dh, values at
+// + voff; mask j < src_len[slot].  S = *dS (device) so a captured step graph serves every
+// batch; Smax sizes shared memory.
+template <class T, int DH>
+__global__ void __launch_bounds__(128) k_attn_cross(
+    const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv, int koff, int voff,
+    const int* __restrict__ dS, int Smax, const int* __restrict__ src_len,
+    const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,
+    const int* __restrict__ dR) {
+  extern __shared__ float sm[];
+  constexpr int CPL = (DH + 31) / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + warp;
+  const int row = gw / H, h = gw - (gw / H) * H;
+  if (row >= min(rows, *dR)) return;
+  const int S = *dS;
+  float* q = sm + warp * (DH + Smax);
+  float* p = q + DH;
+  const int slot = row_slot[row];
+  const int n = src_len[slot];
+  for (int c = lane; c < DH; c += 32) q[c] = to_f(qb[(size_t)row * d + h * DH + c]);
+  __syncwarp();
+  const float scale = rsqrtf((float)DH);
+  const T* base = ckv + (size_t)slot * S * ldkv + h * DH;
+  float mx = -INFINITY;
+  for (int j = lane; j < n; j += 32) {
+    const T* kr = base + (size_t)j * ldkv + koff;
+    float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      float f[8];
+      Vec8<T>::load(kr + c, f);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        e0 = fmaf(f[u], q[c + u], e0);
+        e1 = fmaf(f[u + 1], q[c + u + 1], e1);
+      }
+    }
+    const float e = (e0 + e1) * scale;
+    p[j] = e;
+    mx = fmaxf(mx, e);
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int j = lane; j < n; j += 32) {
+    const float e = __expf(p[j] - mx);
+    p[j] = e;
+    sum += e;
+  }
+  const float inv = 1.f / warp_sum(sum);
+  __syncwarp();
+  float o[CPL];
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) o[u] = 0.f;
+  int j = 0;
+  for (; j + 1 < n; j += 2) {
+    const float p0 = p[j], p1 = p[j + 1];
+    const T* v0 = base + (size_t)j * ldkv + voff;
+    const T* v1 = v0 + ldkv;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int c = lane + 32 * u;
+      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), fmaf(p1, to_f(v1[c]), o[u]));
+    }
+  }
+  for (; j < n; ++j) {
+    const float p0 = p[j];
+    const T* v0 = base + (size_t)j * ldkv + voff;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int c = lane + 32 * u;
+      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), o[u]);
+    }
+  }
+  T* orow = out + (size_t)row * d + h * DH;
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) {
+    const int c = lane + 32 * u;
+    if (c < DH) orow[c] = from_f<T>(o[u] * inv);
+  }
+}
+
+template <class T>
+void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const int* dS, int Smax,
+                const int* src_len, const int* row_slot, T* out, int rows, int d, int H,
+                const int* dR, cudaStream_t s) {
+  if (rows <= 0) return;
+  const int nw = 4, dh = d / H;
+  size_t smem = sizeof(float) * nw * (dh + Smax);
+  dim3 grid(ceil_div(rows * H, nw));
+#define NMT_CS(DH)                                                                          \
+  k_attn_cross<T, DH><<<grid, nw * 32, smem, s>>>(q, ckv, ldkv, koff, voff, dS, Smax, src_len, \
+                                                  row_slot, out, rows, d, H, dR)
+  switch (dh) {
+    case 16: NMT_CS(16); break;
+    case 32: NMT_CS(32); break;
+    case 64: NMT_CS(64); break;
+    default: throw CudaError("attn_cross: head dim must be 16, 32 or 64");
+  }
+#undef NMT_CS
+  NMT_LAUNCH_CHECK();
+}
+
+#define NMT_INST_ATT(T)                                                                         \
+  template void attn_encoder<T>(const T*, const int*, const T*, const T*, T*, int, int, int,    \
+                                int, int, int, cudaStream_t);                                   \
+  template void attn_decoder_self<T>(const T*, T*, T*, int, const int*, const T*, const T*, T*, \
+                                     int, int, int, int, int, const int*, const int*,           \
+                                     cudaStream_t);                                             \
+  template void attn_cross<T>(const T*, const T*, int, int, int, const int*, int, const int*,   \
+                              const int*, T*, int, int, int, const int*, cudaStream_t);
+NMT_INST_ATT(float)
+NMT_INST_ATT(__half)
+
+}  // namespace nmt

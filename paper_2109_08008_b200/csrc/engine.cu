@@ -1,115 +1,24 @@
-// engine.cu — weight store, arena (the paper's memory pool), batch state,
-// encode / decode-step / prune / translate drivers and the extern "C" ABI of nmt.h.
-// Host code only orchestrates launches; every step of the path runs in kernels.cu /
-// gemm_*.cu on the device.
+// engine.cu — NTSD loader, arena (the paper's memory pool), batch planning
+// (PAPER.md:121, :138, :154), translate drivers with device-side pruning and CUDA-graph
+// decode steps, and the extern "C" ABI of include/nmt.h.  Host code only plans and
+// orchestrates; every step of the path runs in kernels on the device.
 #include <cuda_fp16.h>
-#include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
-#include <memory>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <numeric>
-#include <string>
-#include <unordered_map>
-#include <vector>
 
-#include "../../include/nmt.h"
-#include "common.cuh"
-#include "kernels.h"
+#include "engine.h"
 
 namespace nmt {
 unsigned long long g_launches = 0;
-
-struct NmtError : std::runtime_error {
-  nmt_status code;
-  NmtError(nmt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-#define NMT_REQUIRE(cond, code, msg)                         \
-  do {                                                       \
-    if (!(cond)) throw ::nmt::NmtError(code, std::string(msg)); \
-  } while (0)
-
 thread_local std::string g_err;
-
-// ------------------------------------------------------------------ bump arena
-struct Arena {
-  char* base = nullptr;
-  size_t cap = 0, used = 0;
-  size_t take(size_t bytes) {
-    size_t off = used;
-    used += (bytes + 255) & ~size_t(255);
-    return off;
-  }
-};
-
 }  // namespace nmt
 
 using namespace nmt;
-
-struct nmt_batch {
-  nmt_model* m = nullptr;
-  int B = 0, S = 0;
-  int step = 0;          // host mirror of decode steps issued
-  int rows_upper = 0;    // host upper bound of live rows
-  int max_cap = 0;
-  bool valid = false;
-  bool pending_step_done = false;  // nmt_decode_step issued, nmt_prune_batch not yet
-};
-
-struct nmt_model {
-  nmt_config cfg{};
-  nmt_precision prec = NMT_FP16;
-  nmt_limits lim{};
-  int device = 0;
-  size_t tb = 2;  // bytes per stored element
-  // weights
-  void* wbuf = nullptr;
-  std::unordered_map<std::string, void*> W;
-  void* ckv_w = nullptr;   // [Ld*2d][d] cross K/V projection of every decoder layer
-  void* ckv_b = nullptr;   // [Ld*2d]
-  float* dlcl_w = nullptr; // packed rows m = 1..L+1
-  float* pe = nullptr;     // [max_pos][d] FP32 sinusoid table
-  // arena
-  Arena ar;
-  int *src = nullptr, *src_len = nullptr, *tgt_cap = nullptr;
-  void *x = nullptr, *u = nullptr, *qkv = nullptr, *o = nullptr, *h = nullptr, *enc = nullptr,
-       *hist = nullptr, *ckv = nullptr;
-  void *g = nullptr, *du = nullptr, *dqkv = nullptr, *dout = nullptr, *dq = nullptr, *dh = nullptr;
-  void *kc = nullptr, *vc = nullptr;
-  unsigned long long* keys = nullptr;
-  int *row_slot = nullptr, *prev_tok = nullptr, *out_tok = nullptr, *gen_len = nullptr;
-  uint8_t* done = nullptr;
-  DevState* st = nullptr;
-  int* bad = nullptr;
-  long long* boff = nullptr;
-  int* blen = nullptr;
-  int* sent_ids = nullptr;
-  // pinned host staging
-  struct Pinned {
-    int* src; int* len; int* cap; long long* boff; int* blen; int* sent; int* out_tok; int* gen_len;
-    DevState* st; int* bad;
-  } hp{};
-  void* pinned = nullptr;
-  nmt_batch batch;
-  // optional per-kernel-class CUDA-event profile (bench roofline)
-  struct ProfRec { int cls; cudaEvent_t a, b; double flops, bytes; };
-  struct Prof {
-    bool on = false;
-    std::vector<cudaEvent_t> pool;
-    size_t used = 0;
-    std::vector<ProfRec> pending;
-    double ms[16] = {}, flops[16] = {}, bytes[16] = {};
-    long long n[16] = {};
-  } prof;
-  ~nmt_model() {
-    for (auto e : prof.pool) cudaEventDestroy(e);
-    if (wbuf) cudaFree(wbuf);
-    if (ar.base) cudaFree(ar.base);
-    if (pinned) cudaFreeHost(pinned);
-  }
-};
 
 namespace {
 
@@ -189,30 +98,17 @@ void validate_config(const nmt_config& c) {
               NMT_E_FORMAT, "NTSD: bad layer/head/vocab counts");
   NMT_REQUIRE(c.d_model % 32 == 0 && c.d_model <= 512 && c.d_model % c.n_heads == 0,
               NMT_E_UNSUPPORTED, "d_model must be a multiple of 32, <= 512, divisible by heads");
-  NMT_REQUIRE((c.d_model / c.n_heads) % 8 == 0 && c.d_model / c.n_heads <= 128, NMT_E_UNSUPPORTED,
-              "head dim must be a multiple of 8 and <= 128");
+  const int dh = c.d_model / c.n_heads;
+  NMT_REQUIRE(dh == 16 || dh == 32 || dh == 64, NMT_E_UNSUPPORTED, "head dim must be 16, 32 or 64");
   NMT_REQUIRE(c.d_ffn % 32 == 0, NMT_E_UNSUPPORTED, "d_ffn must be a multiple of 32");
   NMT_REQUIRE(c.max_rel_pos >= 1 && 2 * c.max_rel_pos + 1 <= 32, NMT_E_UNSUPPORTED,
               "max_rel_pos must be in [1, 15]");
-  NMT_REQUIRE(c.max_src_len >= 1 && c.max_src_len <= c.max_pos && c.max_tgt_len >= 1 &&
-                  c.max_tgt_len <= c.max_pos,
-              NMT_E_FORMAT, "NTSD: bad max lengths");
+  NMT_REQUIRE(c.max_src_len >= 1 && c.max_src_len <= 120 && c.max_src_len <= c.max_pos &&
+                  c.max_tgt_len >= 1 && c.max_tgt_len <= c.max_pos,
+              NMT_E_FORMAT, "NTSD: bad max lengths (max_src_len <= 120)");
 }
 
-// ------------------------------------------------------------------ typed views
-template <class T> struct V {
-  nmt_model* m;
-  const T* w(const std::string& n) const {
-    auto it = m->W.find(n);
-    if (it == m->W.end()) throw NmtError(NMT_E_INTEGRITY, "missing tensor " + n);
-    return static_cast<const T*>(it->second);
-  }
-  const T* rel(const std::string& p, const char* kv) const {
-    return m->cfg.use_rpr ? w(p + kv) : nullptr;
-  }
-  T* p(void* q) const { return static_cast<T*>(q); }
-};
-
+// ------------------------------------------------------------------ arena
 void init_arena(nmt_model* m) {
   const nmt_config& c = m->cfg;
   const nmt_limits& L = m->lim;
@@ -220,11 +116,10 @@ void init_arena(nmt_model* m) {
   const size_t N = L.max_tokens, Bm = L.max_sents, Tm = L.max_tgt_len;
   const size_t R = Bm * std::max(1, L.beam);
   Arena& a = m->ar;
-  struct Item { void** dst; size_t bytes; };
   std::vector<std::pair<void**, size_t>> items = {
       {(void**)&m->src, N * 4}, {(void**)&m->src_len, Bm * 4}, {(void**)&m->tgt_cap, Bm * 4},
       {&m->x, N * d * tb}, {&m->u, N * d * tb}, {&m->qkv, N * 3 * d * tb}, {&m->o, N * d * tb},
-      {&m->h, N * F * tb}, {&m->enc, N * d * tb},
+      {&m->h, N * F * tb}, {&m->enc_out, N * d * tb},
       {&m->hist, c.use_dlcl ? (size_t)(c.enc_layers + 1) * N * d * tb : 256},
       {&m->ckv, N * Ld * 2 * d * tb},
       {&m->g, R * d * tb}, {&m->du, R * d * tb}, {&m->dqkv, R * 3 * d * tb},
@@ -243,9 +138,8 @@ void init_arena(nmt_model* m) {
   a.cap = a.used;
   for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
   NMT_CUDA(cudaMemset(a.base, 0, a.used));
-  // pinned staging
-  size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 +
-              16 * 64 /* per-region 64-B rounding */;
+  // pinned host staging (each region rounded to 64 B)
+  size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 + 16 * 64;
   NMT_CUDA(cudaMallocHost(&m->pinned, pb));
   char* p = (char*)m->pinned;
   auto take = [&](size_t b) { char* r = p; p += (b + 63) & ~size_t(63); return r; };
@@ -261,348 +155,55 @@ void init_arena(nmt_model* m) {
   m->hp.bad = (int*)take(4);
 }
 
-// ------------------------------------------------------------------ profiling
-enum ProfClass {
-  P_ENC_GEMM = 0, P_ENC_ATTN, P_DLCL, P_ENC_LN, P_EMBED, P_DEC_GEMM, P_VOCAB, P_DEC_SELF,
-  P_DEC_CROSS, P_DEC_LN, P_BOOK, P_NCLS
-};
-const char* kProfNames[P_NCLS] = {"enc_gemm",  "enc_rpr_attn", "dlcl_combine", "enc_layernorm",
-                                  "embed",     "dec_gemm",     "vocab_argmax", "dec_self_attn",
-                                  "dec_cross_attn", "dec_layernorm", "bookkeeping"};
-
-void prof_flush(nmt_model* m) {
-  auto& P = m->prof;
-  for (auto& r : P.pending) {
-    float ms = 0.f;
-    NMT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-    P.ms[r.cls] += ms;
-    P.flops[r.cls] += r.flops;
-    P.bytes[r.cls] += r.bytes;
-    P.n[r.cls] += 1;
-  }
-  P.pending.clear();
-  P.used = 0;
-}
-
-// Runs f() (one kernel launch); when profiling, brackets it with stream events and
-// records its algorithmic FLOPs / bytes.
-template <class F>
-void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {
-  auto& P = m->prof;
-  if (!P.on) {
-    f();
-    return;
-  }
-  while (P.pool.size() < P.used + 2) {
-    cudaEvent_t e;
-    NMT_CUDA(cudaEventCreate(&e));
-    P.pool.push_back(e);
-  }
-  cudaEvent_t a = P.pool[P.used++], b = P.pool[P.used++];
-  NMT_CUDA(cudaEventRecord(a, s));
-  f();
-  NMT_CUDA(cudaEventRecord(b, s));
-  P.pending.push_back({cls, a, b, flops, bytes});
-}
-#define PROF(cls, fl, by, stmt) prof_run(m, cls, (double)(fl), (double)(by), s, [&] { stmt; })
-
-double gemm_bytes(const GemmArgs& a, size_t tb) {
-  double b = ((double)a.M * a.K + (double)a.N * a.K) * tb;
-  if (!a.argmax) b += (double)a.M * a.N * tb;
-  if (a.R) b += (double)a.M * a.N * tb;
-  if (a.bias) b += (double)a.N * tb;
-  return b;
-}
-double gemm_flops(const GemmArgs& a) { return 2.0 * a.M * a.N * a.K; }
-
-// ------------------------------------------------------------------ encode
-template <class T>
-void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
+void bind_weights(nmt_model* m) {
   const nmt_config& c = m->cfg;
-  V<T> v{m};
-  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, L = c.enc_layers, Ld = c.dec_layers;
-  const int N = B * S;
-  const float eps = c.ln_eps;
-  const size_t tb = sizeof(T);
-  T *x = v.p(m->x), *u = v.p(m->u), *qkv = v.p(m->qkv), *o = v.p(m->o), *h = v.p(m->h),
-    *enc = v.p(m->enc), *hist = v.p(m->hist), *ckv = v.p(m->ckv);
-  const size_t hs = (size_t)N * d;
-  const double row = (double)N * d * tb;  // bytes of one [N][d] activation
-  const float sq = std::sqrt((float)d);
-  // y0 = sqrt(d) E[s] + PE(p)
-  PROF(P_EMBED, 0, 2 * row, embed<T>(m->src, v.w("emb"), m->pe, c.use_dlcl ? o : x, N, d, S,
-                                      nullptr, nullptr, sq, s));
+  auto W = [&](const std::string& n) -> const void* {
+    auto it = m->W.find(n);
+    NMT_REQUIRE(it != m->W.end(), NMT_E_INTEGRITY, "missing tensor " + n);
+    return it->second;
+  };
+  m->emb = W("emb");
+  m->enc_fg = W("enc.final_ln.g");
+  m->enc_fb = W("enc.final_ln.b");
+  m->dec_fg = W("dec.final_ln.g");
+  m->dec_fb = W("dec.final_ln.b");
   if (c.use_dlcl) {
-    PROF(P_DLCL, 0, 4 * row,
-         dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, v.w("enc.dlcl.ln.0.g"), v.w("enc.dlcl.ln.0.b"),
-                         c.dlcl_ln, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), x, u, N, d,
-                         eps, s));
-  } else {
-    PROF(P_ENC_LN, 0, 2 * row,
-         layernorm<T>(x, d, v.w("enc.0.attn_ln.g"), v.w("enc.0.attn_ln.b"), u, d, N, d, eps,
-                      nullptr, s));
+    m->dl0_g = W("enc.dlcl.ln.0.g");
+    m->dl0_b = W("enc.dlcl.ln.0.b");
   }
-  const double attn_flops = 4.0 * B * H * (double)S * S * (d / H);
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < c.enc_layers; ++l) {
     const std::string p = "enc." + std::to_string(l) + ".";
-    GemmArgs a;
-    a.M = N; a.N = 3 * d; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "qkv.w"); a.ldb = d;
-    a.bias = v.w(p + "qkv.b"); a.C = qkv; a.ldc = 3 * d;
-    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    PROF(P_ENC_ATTN, attn_flops, 4 * row,
-         attn_encoder<T>(qkv, m->src_len, v.rel(p, "rel_k"), v.rel(p, "rel_v"), o, B, S, d, H,
-                         c.max_rel_pos, c.use_rpr, s));
-    a = GemmArgs();
-    a.M = N; a.N = d; a.K = d; a.A = o; a.lda = d; a.B = v.w(p + "out.w"); a.ldb = d;
-    a.bias = v.w(p + "out.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
-    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // a = x + Attn(LN(x))
-    PROF(P_ENC_LN, 0, 2 * row,
-         layernorm<T>(x, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), u, d, N, d, eps, nullptr, s));
-    a = GemmArgs();
-    a.M = N; a.N = F; a.K = d; a.A = u; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
-    a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = h; a.ldc = F;
-    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    a = GemmArgs();
-    a.M = N; a.N = d; a.K = F; a.A = h; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
-    a.bias = v.w(p + "ffn2.b"); a.R = x; a.ldr = d; a.C = x; a.ldc = d;
-    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // y_l = a + FFN(LN(a))
-    const bool last = (l == L - 1);
-    const std::string np = last ? "enc.final_ln." : "enc." + std::to_string(l + 1) + ".attn_ln.";
+    EncW e{};
+    e.attn_g = W(p + "attn_ln.g"); e.attn_b = W(p + "attn_ln.b");
+    e.qkv_w = W(p + "qkv.w"); e.qkv_b = W(p + "qkv.b");
+    e.out_w = W(p + "out.w"); e.out_b = W(p + "out.b");
+    e.relk = c.use_rpr ? W(p + "rel_k") : nullptr;
+    e.relv = c.use_rpr ? W(p + "rel_v") : nullptr;
+    e.ffn_g = W(p + "ffn_ln.g"); e.ffn_b = W(p + "ffn_ln.b");
+    e.w1 = W(p + "ffn1.w"); e.b1 = W(p + "ffn1.b"); e.w2 = W(p + "ffn2.w"); e.b2 = W(p + "ffn2.b");
     if (c.use_dlcl) {
-      const int k = l + 1;  // depth of y
-      const std::string dp = "enc.dlcl.ln." + std::to_string(k) + ".";
-      // reads y + k history rows, writes z_k, (x), LN(x)
-      PROF(P_DLCL, 0, (1 + k + 1 + (last ? 0 : 1) + 1) * row,
-           dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, v.w(dp + "g"),
-                           v.w(dp + "b"), c.dlcl_ln, v.w(np + "g"), v.w(np + "b"),
-                           last ? nullptr : x, last ? enc : u, N, d, eps, s));
-    } else {
-      PROF(P_ENC_LN, 0, 2 * row,
-           layernorm<T>(x, d, v.w(np + "g"), v.w(np + "b"), last ? enc : u, d, N, d, eps, nullptr,
-                        s));
+      e.dl_g = W("enc.dlcl.ln." + std::to_string(l + 1) + ".g");
+      e.dl_b = W("enc.dlcl.ln." + std::to_string(l + 1) + ".b");
     }
+    m->enc.push_back(e);
   }
-  // cross K/V of every decoder layer, once per sentence
-  GemmArgs a;
-  a.M = N; a.N = Ld * 2 * d; a.K = d; a.A = enc; a.lda = d; a.B = m->ckv_w; a.ldb = d;
-  a.bias = m->ckv_b; a.C = ckv; a.ldc = Ld * 2 * d;
-  PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-}
-
-// ------------------------------------------------------------------ decode step
-template <class T>
-void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
-                      cudaStream_t s) {
-  const nmt_config& c = m->cfg;
-  V<T> v{m};
-  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, Ld = c.dec_layers;
-  const int R = b->rows_upper;
-  const int Tm = m->lim.max_tgt_len;
-  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
-  const float eps = c.ln_eps;
-  const size_t tb = sizeof(T);
-  const int* dR = &m->st->n_live;
-  const int* dt = &m->st->t;
-  const int t = b->step;  // host mirror (profile byte counts only)
-  const double row = (double)R * d * tb;
-  T *g = v.p(m->g), *du = v.p(m->du), *dqkv = v.p(m->dqkv), *dout = v.p(m->dout),
-    *dq = v.p(m->dq), *dh = v.p(m->dh);
-  PROF(P_EMBED, 0, 2 * row,
-       embed<T>(d_prev ? d_prev : m->prev_tok, v.w("emb"), m->pe, g, R, d, 1, dt, dR,
-                std::sqrt((float)d), s));
-  for (int l = 0; l < Ld; ++l) {
+  for (int l = 0; l < c.dec_layers; ++l) {
     const std::string p = "dec." + std::to_string(l) + ".";
-    T* kc = v.p(m->kc) + (size_t)l * Rmax * Tm * d;
-    T* vc = v.p(m->vc) + (size_t)l * Rmax * Tm * d;
-    PROF(P_DEC_LN, 0, 2 * row,
-         layernorm<T>(g, d, v.w(p + "self_ln.g"), v.w(p + "self_ln.b"), du, d, R, d, eps, dR, s));
-    GemmArgs a;
-    a.M = R; a.N = 3 * d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "self_qkv.w"); a.ldb = d;
-    a.bias = v.w(p + "self_qkv.b"); a.C = dqkv; a.ldc = 3 * d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
-         attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, v.rel(p, "rel_k"), v.rel(p, "rel_v"),
-                              dout, R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s));
-    a = GemmArgs();
-    a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "self_out.w"); a.ldb = d;
-    a.bias = v.w(p + "self_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    PROF(P_DEC_LN, 0, 2 * row,
-         layernorm<T>(g, d, v.w(p + "cross_ln.g"), v.w(p + "cross_ln.b"), du, d, R, d, eps, dR, s));
-    a = GemmArgs();
-    a.M = R; a.N = d; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "cross_q.w"); a.ldb = d;
-    a.bias = v.w(p + "cross_q.b"); a.C = dq; a.ldc = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
-         attn_cross<T>(dq, v.p(m->ckv), Ld * 2 * d, l * 2 * d, l * 2 * d + d, b->S, m->src_len,
-                       m->row_slot, dout, R, d, H, dR, s));
-    a = GemmArgs();
-    a.M = R; a.N = d; a.K = d; a.A = dout; a.lda = d; a.B = v.w(p + "cross_out.w"); a.ldb = d;
-    a.bias = v.w(p + "cross_out.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    PROF(P_DEC_LN, 0, 2 * row,
-         layernorm<T>(g, d, v.w(p + "ffn_ln.g"), v.w(p + "ffn_ln.b"), du, d, R, d, eps, dR, s));
-    a = GemmArgs();
-    a.M = R; a.N = F; a.K = d; a.A = du; a.lda = d; a.B = v.w(p + "ffn1.w"); a.ldb = d;
-    a.bias = v.w(p + "ffn1.b"); a.relu = 1; a.C = dh; a.ldc = F; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    a = GemmArgs();
-    a.M = R; a.N = d; a.K = F; a.A = dh; a.lda = F; a.B = v.w(p + "ffn2.w"); a.ldb = F;
-    a.bias = v.w(p + "ffn2.b"); a.R = g; a.ldr = d; a.C = g; a.ldc = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-  }
-  PROF(P_DEC_LN, 0, 2 * row,
-       layernorm<T>(g, d, v.w("dec.final_ln.g"), v.w("dec.final_ln.b"), du, d, R, d, eps, dR, s));
-  GemmArgs a;  // tied vocab projection fused with argmax
-  a.M = R; a.N = c.vocab_size; a.K = d; a.A = du; a.lda = d; a.B = v.w("emb"); a.ldb = d;
-  a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
-  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-  PROF(P_BOOK, 0, 0,
-       greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
-                     Tm, m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
-                     out ? out->d_done : nullptr, s));
-}
-
-void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
-                     cudaStream_t s) {
-  if (m->prec == NMT_FP16) decode_step_impl<__half>(m, b, d_prev, out, s);
-  else decode_step_impl<float>(m, b, d_prev, out, s);
-}
-
-// Stage host batch metadata and encode (sources already in m->src).
-void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_cap,
-                   cudaStream_t s) {
-  nmt_batch& b = m->batch;
-  const int Tm = m->lim.max_tgt_len;
-  int mc = 0;
-  for (int i = 0; i < B; ++i) {
-    m->hp.len[i] = h_len[i];
-    int cp = h_cap ? std::min(h_cap[i], Tm) : Tm;
-    cp = std::max(cp, 1);
-    m->hp.cap[i] = cp;
-    mc = std::max(mc, cp);
-  }
-  NMT_CUDA(cudaMemcpyAsync(m->src_len, m->hp.len, B * 4, cudaMemcpyHostToDevice, s));
-  NMT_CUDA(cudaMemcpyAsync(m->tgt_cap, m->hp.cap, B * 4, cudaMemcpyHostToDevice, s));
-  if (m->prec == NMT_FP16) encode_impl<__half>(m, B, S, s);
-  else encode_impl<float>(m, B, S, s);
-  batch_init(m->row_slot, m->prev_tok, m->done, m->gen_len, m->st, B, m->cfg.bos_id, s);
-  b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B; b.max_cap = mc; b.valid = true;
-  b.pending_step_done = false;
-}
-
-void check_batch_shape(nmt_model* m, int B, int S) {
-  NMT_REQUIRE(B >= 1 && S >= 1, NMT_E_ARG, "n_sent and s_max must be >= 1");
-  NMT_REQUIRE(B <= m->lim.max_sents, NMT_E_SHAPE,
-              "n_sent " + std::to_string(B) + " > max_sents " + std::to_string(m->lim.max_sents));
-  NMT_REQUIRE((long long)B * S <= m->lim.max_tokens, NMT_E_SHAPE,
-              "n_sent*s_max " + std::to_string((long long)B * S) + " > max_tokens " +
-                  std::to_string(m->lim.max_tokens));
-  NMT_REQUIRE(S <= m->cfg.max_src_len, NMT_E_INPUT,
-              "s_max " + std::to_string(S) + " > max_src_len " + std::to_string(m->cfg.max_src_len));
-}
-
-void poll_state(nmt_model* m, cudaStream_t s) {
-  NMT_CUDA(cudaMemcpyAsync(m->hp.st, m->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-  NMT_CUDA(cudaStreamSynchronize(s));
-  if (!m->prof.pending.empty()) prof_flush(m);
-}
-
-// ------------------------------------------------------------------ translate core
-struct Plan {
-  std::vector<int> order;
-  std::vector<int> bstart;  // batch boundaries into order
-};
-
-Plan plan_batches(const int64_t* h_off, int64_t n, int max_tokens, int max_sents) {
-  Plan p;
-  p.order.resize(n);
-  std::iota(p.order.begin(), p.order.end(), 0);
-  // stable sort by (-len, index) (reading R17)
-  std::stable_sort(p.order.begin(), p.order.end(), [&](int a, int b) {
-    return (h_off[a + 1] - h_off[a]) > (h_off[b + 1] - h_off[b]);
-  });
-  int64_t i = 0;
-  while (i < n) {
-    p.bstart.push_back((int)i);
-    int first = (int)(h_off[p.order[i] + 1] - h_off[p.order[i]]);
-    int64_t b = std::min<int64_t>({(int64_t)max_sents, std::max<int64_t>(1, max_tokens / first),
-                                   n - i});
-    i += b;
-  }
-  p.bstart.push_back((int)n);
-  return p;
-}
-
-// Runs every batch; `load_src` stages batch sources into m->src, `emit` consumes results.
-template <class LoadF, class EmitF>
-void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_translate_opts* o,
-                    LoadF load_src, EmitF emit, nmt_stats* st, cudaStream_t s) {
-  const int max_tokens = o && o->max_tokens > 0 ? o->max_tokens : m->lim.max_tokens;
-  const int max_sents = o && o->max_sents > 0 ? o->max_sents : m->lim.max_sents;
-  const int every = o && o->prune_every > 0 ? o->prune_every : 1;
-  const float ratio = o ? o->prune_ratio : 0.25f;
-  const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
-  NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
-              "translate opts exceed the model limits");
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t len = h_off[i + 1] - h_off[i];
-    NMT_REQUIRE(len >= 1, NMT_E_INPUT, "empty source sentence " + std::to_string(i));
-    NMT_REQUIRE(len <= m->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
-                "source " + std::to_string(i) + " longer than max_src_len");
-  }
-  Plan p = plan_batches(h_off, n, max_tokens, max_sents);
-  auto t0 = std::chrono::steady_clock::now();
-  unsigned long long l0 = g_launches;
-  int64_t steps = 0, prunes = 0;
-  std::vector<int> lens, caps;
-  for (size_t bi = 0; bi + 1 < p.bstart.size(); ++bi) {
-    const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
-    const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
-    lens.resize(B);
-    caps.resize(B);
-    for (int j = 0; j < B; ++j) {
-      int sid = p.order[lo + j];
-      lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
-      caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : m->lim.max_tgt_len;
-      m->hp.sent[j] = sid;
-    }
-    load_src(&p.order[lo], B, S, lens.data());
-    encode_common(m, B, S, lens.data(), caps.data(), s);
-    nmt_batch& b = m->batch;
-    int rows = B;
-    int t = 0;
-    for (; t < b.max_cap && rows > 0; ++t) {
-      b.rows_upper = rows;
-      decode_step_any(m, &b, nullptr, nullptr, s);
-      PROF(P_BOOK, 0, 0,
-           prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, rows, s));
-      if ((t + 1) % sync_every == 0) {
-        poll_state(m, s);
-        rows = m->hp.st->n_live;
-      }
-    }
-    poll_state(m, s);
-    steps += t;
-    prunes += m->hp.st->prunes;
-    b.step = t;
-    emit(b, &p.order[lo], B);
-    b.valid = false;
-  }
-  NMT_CUDA(cudaStreamSynchronize(s));
-  if (st) {
-    st->sentences = n;
-    st->src_tokens = h_off[n] - h_off[0];
-    st->decode_steps = steps;
-    st->prunes = prunes;
-    st->batches = (int64_t)p.bstart.size() - 1;
-    st->launches = (int64_t)(g_launches - l0);
-    st->ms_total =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    DecW e{};
+    e.self_g = W(p + "self_ln.g"); e.self_b = W(p + "self_ln.b");
+    e.qkv_w = W(p + "self_qkv.w"); e.qkv_b = W(p + "self_qkv.b");
+    e.so_w = W(p + "self_out.w"); e.so_b = W(p + "self_out.b");
+    e.relk = c.use_rpr ? W(p + "rel_k") : nullptr;
+    e.relv = c.use_rpr ? W(p + "rel_v") : nullptr;
+    e.cross_g = W(p + "cross_ln.g"); e.cross_b = W(p + "cross_ln.b");
+    e.cq_w = W(p + "cross_q.w"); e.cq_b = W(p + "cross_q.b");
+    e.co_w = W(p + "cross_out.w"); e.co_b = W(p + "cross_out.b");
+    e.ffn_g = W(p + "ffn_ln.g"); e.ffn_b = W(p + "ffn_ln.b");
+    e.w1 = W(p + "ffn1.w"); e.b1 = W(p + "ffn1.b"); e.w2 = W(p + "ffn2.w"); e.b2 = W(p + "ffn2.b");
+    m->dec.push_back(e);
   }
 }
 
-// ------------------------------------------------------------------ load
 nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
                 const nmt_limits* lim) {
   NMT_REQUIRE(blob && lim, NMT_E_ARG, "null blob or limits");
@@ -656,7 +257,6 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->device = device;
   m->tb = prec == NMT_FP16 ? 2 : 4;
   NMT_CUDA(cudaSetDevice(device));
-  // host staging of all weights in the target precision, one H2D copy
   size_t total = 0;
   std::vector<size_t> offs;
   for (auto& kv : can) {
@@ -665,7 +265,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
     const TensorRec& r = it->second;
     NMT_REQUIRE(r.dims == kv.second, NMT_E_INTEGRITY, "NTSD: shape mismatch for " + kv.first);
     size_t cnt = 1;
-    for (auto d : kv.second) cnt *= d;
+    for (auto dd : kv.second) cnt *= dd;
     NMT_REQUIRE(r.nbytes == cnt * (r.dtype == 1 ? 2 : 4), NMT_E_INTEGRITY,
                 "NTSD: byte size mismatch for " + kv.first);
     offs.push_back(total);
@@ -702,8 +302,9 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   };
   for (size_t t = 0; t < can.size(); ++t) {
     const TensorRec& r = recs.at(can[t].first);
-    size_t cnt = r.nbytes / (r.dtype == 1 ? 2 : 4);
-    for (size_t i = 0; i < cnt; ++i) put(offs[t] + i * m->tb, get_f(r, i));
+    const size_t cnt = r.nbytes / (r.dtype == 1 ? 2 : 4);
+    if (r.dtype == 1 && m->tb == 2) memcpy(&host[offs[t]], r.data, r.nbytes);  // FP16 -> FP16
+    else for (size_t i = 0; i < cnt; ++i) put(offs[t] + i * m->tb, get_f(r, i));
   }
   for (int l = 0; l < Ld; ++l) {
     const TensorRec& w = recs.at("dec." + std::to_string(l) + ".cross_kv.w");
@@ -719,7 +320,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
       memcpy(&host[dlcl_off + 4 * i], &f, 4);
     }
   }
-  {  // sinusoid table in double precision (reading R8)
+  {  // sinusoid table in double precision, stored FP32 (reading R8)
     const int half = d / 2;
     for (int pos = 0; pos < cfg.max_pos; ++pos)
       for (int i = 0; i < half; ++i) {
@@ -739,9 +340,184 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->ckv_b = base + ckv_b_off;
   m->dlcl_w = (float*)(base + dlcl_off);
   m->pe = (float*)(base + pe_off);
+  bind_weights(m.get());
   init_arena(m.get());
   NMT_CUDA(cudaDeviceSynchronize());
   return m.release();
+}
+
+// ------------------------------------------------------------------ batches
+void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_cap,
+                   cudaStream_t s) {
+  nmt_batch& b = m->batch;
+  const int Tm = m->lim.max_tgt_len;
+  int mc = 0;
+  for (int i = 0; i < B; ++i) {
+    m->hp.len[i] = h_len[i];
+    int cp = h_cap ? std::min(h_cap[i], Tm) : Tm;
+    cp = std::max(cp, 1);
+    m->hp.cap[i] = cp;
+    mc = std::max(mc, cp);
+  }
+  NMT_CUDA(cudaMemcpyAsync(m->src_len, m->hp.len, B * 4, cudaMemcpyHostToDevice, s));
+  NMT_CUDA(cudaMemcpyAsync(m->tgt_cap, m->hp.cap, B * 4, cudaMemcpyHostToDevice, s));
+  encode_any(m, B, S, s);
+  PROF(P_BOOK, 0, 0,
+       batch_init(m->row_slot, m->prev_tok, m->done, m->gen_len, m->st, B, S, m->cfg.bos_id, s));
+  b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B; b.max_cap = mc; b.valid = true;
+  b.pending_step_done = false;
+}
+
+void check_batch_shape(nmt_model* m, int B, int S) {
+  NMT_REQUIRE(B >= 1 && S >= 1, NMT_E_ARG, "n_sent and s_max must be >= 1");
+  NMT_REQUIRE(B <= m->lim.max_sents, NMT_E_SHAPE,
+              "n_sent " + std::to_string(B) + " > max_sents " + std::to_string(m->lim.max_sents));
+  NMT_REQUIRE((long long)B * S <= m->lim.max_tokens, NMT_E_SHAPE,
+              "n_sent*s_max " + std::to_string((long long)B * S) + " > max_tokens " +
+                  std::to_string(m->lim.max_tokens));
+  NMT_REQUIRE(S <= m->cfg.max_src_len, NMT_E_INPUT,
+              "s_max " + std::to_string(S) + " > max_src_len " + std::to_string(m->cfg.max_src_len));
+}
+
+void poll_state(nmt_model* m, cudaStream_t s) {
+  NMT_CUDA(cudaMemcpyAsync(m->hp.st, m->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  NMT_CUDA(cudaStreamSynchronize(s));
+  if (!m->prof.pending.empty()) prof_flush(m);
+}
+
+// One greedy step + pruning decision for `rows` live rows.  After one eager step the
+// pair is captured once per (rows bucket, cadence, ratio) into a CUDA graph and
+// replayed: every kernel reads t, the live count and S from device memory, so a graph
+// serves every step of every batch (no per-step host round trip).
+void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio,
+                    cudaStream_t s) {
+  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
+  const int bucket = std::min(Rmax, (rows + 31) & ~31);
+  auto eager = [&] {
+    decode_step_any(m, &b, nullptr, nullptr, s);
+    PROF(P_BOOK, 0, 0,
+         prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, b.rows_upper,
+                       s));
+  };
+  if (m->prof.on || !m->eager_done || s == nullptr) {
+    b.rows_upper = rows;
+    eager();
+    m->eager_done = true;
+    return;
+  }
+  unsigned rb;
+  memcpy(&rb, &ratio, 4);
+  auto key = std::make_tuple(bucket, every, rb);
+  auto it = m->graphs.find(key);
+  if (it == m->graphs.end()) {
+    b.rows_upper = bucket;
+    cudaGraph_t g;
+    NMT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      eager();
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      throw;
+    }
+    NMT_CUDA(cudaStreamEndCapture(s, &g));
+    cudaGraphExec_t ex;
+    NMT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    NMT_CUDA(cudaGraphDestroy(g));
+    it = m->graphs.emplace(key, ex).first;
+  }
+  NMT_CUDA(cudaGraphLaunch(it->second, s));
+  g_launches += 1;
+}
+
+// ------------------------------------------------------------------ translate core
+struct Plan {
+  std::vector<int> order;
+  std::vector<int> bstart;  // batch boundaries into order
+};
+
+// Dynamic batching over length-sorted input, reading R17:
+// stable sort by (-len, index); b = min(max_sents, floor(max_tokens / len_first), rest).
+Plan plan_batches(const int64_t* h_off, int64_t n, int max_tokens, int max_sents) {
+  Plan p;
+  p.order.resize(n);
+  std::iota(p.order.begin(), p.order.end(), 0);
+  std::stable_sort(p.order.begin(), p.order.end(), [&](int a, int b) {
+    return (h_off[a + 1] - h_off[a]) > (h_off[b + 1] - h_off[b]);
+  });
+  int64_t i = 0;
+  while (i < n) {
+    p.bstart.push_back((int)i);
+    int first = (int)(h_off[p.order[i] + 1] - h_off[p.order[i]]);
+    int64_t b = std::min<int64_t>({(int64_t)max_sents, std::max<int64_t>(1, max_tokens / first),
+                                   n - i});
+    i += b;
+  }
+  p.bstart.push_back((int)n);
+  return p;
+}
+
+template <class LoadF, class EmitF>
+void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_translate_opts* o,
+                    LoadF load_src, EmitF emit, nmt_stats* st, cudaStream_t s) {
+  const int max_tokens = o && o->max_tokens > 0 ? o->max_tokens : m->lim.max_tokens;
+  const int max_sents = o && o->max_sents > 0 ? o->max_sents : m->lim.max_sents;
+  const int every = o && o->prune_every > 0 ? o->prune_every : 1;
+  const float ratio = o ? o->prune_ratio : 0.25f;
+  const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
+  NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
+              "translate opts exceed the model limits");
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t len = h_off[i + 1] - h_off[i];
+    NMT_REQUIRE(len >= 1, NMT_E_INPUT, "empty source sentence " + std::to_string(i));
+    NMT_REQUIRE(len <= m->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
+                "source " + std::to_string(i) + " longer than max_src_len");
+  }
+  Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned long long l0 = g_launches;
+  int64_t steps = 0, prunes = 0;
+  std::vector<int> lens, caps;
+  for (size_t bi = 0; bi + 1 < p.bstart.size(); ++bi) {
+    const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
+    const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+    lens.resize(B);
+    caps.resize(B);
+    for (int j = 0; j < B; ++j) {
+      int sid = p.order[lo + j];
+      lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+      caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : m->lim.max_tgt_len;
+    }
+    load_src(&p.order[lo], B, S, lens.data());
+    encode_common(m, B, S, lens.data(), caps.data(), s);
+    nmt_batch& b = m->batch;
+    int rows = B;
+    int t = 0;
+    // the live count is polled every `sync_every` steps (lagged upper bound for grids)
+    for (; t < b.max_cap && rows > 0; ++t) {
+      step_and_prune(m, b, rows, every, ratio, s);
+      if ((t + 1) % sync_every == 0) {
+        poll_state(m, s);
+        rows = m->hp.st->n_live;
+      }
+    }
+    poll_state(m, s);
+    steps += t;
+    prunes += m->hp.st->prunes;
+    b.step = t;
+    emit(b, &p.order[lo], B);
+    b.valid = false;
+  }
+  NMT_CUDA(cudaStreamSynchronize(s));
+  if (st) {
+    st->sentences = n;
+    st->src_tokens = h_off[n] - h_off[0];
+    st->decode_steps = steps;
+    st->prunes = prunes;
+    st->batches = (int64_t)p.bstart.size() - 1;
+    st->launches = (int64_t)(g_launches - l0);
+    st->ms_total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
 }
 
 template <class F> nmt_status guard(F f) {
@@ -807,8 +583,10 @@ nmt_status nmt_batch_encoder_output(const nmt_batch* b, float* d_dst, void* stre
     NMT_REQUIRE(b && b->valid && d_dst, NMT_E_ARG, "null or invalid batch");
     nmt_model* m = b->m;
     size_t n = (size_t)b->B * b->S * m->cfg.d_model;
-    if (m->prec == NMT_FP16) to_float<__half>((const __half*)m->enc, d_dst, n, (cudaStream_t)stream);
-    else to_float<float>((const float*)m->enc, d_dst, n, (cudaStream_t)stream);
+    if (m->prec == NMT_FP16)
+      to_float<__half>((const __half*)m->enc_out, d_dst, n, (cudaStream_t)stream);
+    else
+      to_float<float>((const float*)m->enc_out, d_dst, n, (cudaStream_t)stream);
   });
 }
 
@@ -816,6 +594,7 @@ nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, in
                            const nmt_step_out* out, void* stream) {
   return guard([&] {
     NMT_REQUIRE(m && b && b->valid && b->m == m, NMT_E_ARG, "null or invalid batch");
+    NMT_REQUIRE(!b->pending_step_done, NMT_E_STATE, "decode_step called twice without prune");
     NMT_REQUIRE(step == b->step, NMT_E_STATE,
                 "step " + std::to_string(step) + " != batch step " + std::to_string(b->step));
     NMT_REQUIRE(step < m->lim.max_tgt_len, NMT_E_STATE, "step beyond max_tgt_len");
@@ -830,7 +609,8 @@ nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_n
     NMT_REQUIRE(m && b && b->valid && b->m == m, NMT_E_ARG, "null or invalid batch");
     NMT_REQUIRE(b->pending_step_done, NMT_E_STATE, "prune must follow a decode step");
     cudaStream_t s = (cudaStream_t)stream;
-    prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old, b->rows_upper, s);
+    prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old, b->rows_upper,
+                  s);
     b->pending_step_done = false;
     b->step += 1;
     if (h_n_live) {
@@ -896,18 +676,17 @@ nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_of
       }
     };
     translate_core(m, h_off, n, opts, load_src, emit, stats, s);
-    int64_t pos = 0, ot = 0;
+    int64_t pos = 0;
     h_out_off[0] = 0;
     for (int64_t i = 0; i < n; ++i) {
       NMT_REQUIRE(pos + (int64_t)outs[i].size() <= out_cap, NMT_E_SHAPE, "out_cap too small");
       std::copy(outs[i].begin(), outs[i].end(), h_out + pos);
       pos += outs[i].size();
-      ot += outs[i].size();
       h_out_off[i + 1] = pos;
     }
     if (stats) {
       stats->gen_tokens = gen;
-      stats->out_tokens = ot;
+      stats->out_tokens = pos;
     }
   });
 }
@@ -1002,7 +781,7 @@ nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t
     NMT_REQUIRE(d_A && d_B && d_next && M > 0 && N > 0 && K > 0, NMT_E_ARG, "bad gemm args");
     NMT_REQUIRE(K % 16 == 0 && M <= 4096, NMT_E_SHAPE, "K % 16 != 0 or M > 4096");
     cudaStream_t s = (cudaStream_t)stream;
-    static unsigned long long* keys = nullptr;
+    static unsigned long long* keys = nullptr;  // test hook scratch (not on the product path)
     if (!keys) NMT_CUDA(cudaMalloc(&keys, 4096 * 8));
     NMT_CUDA(cudaMemsetAsync(keys, 0, (size_t)M * 8, s));
     GemmArgs a;

@@ -1,0 +1,156 @@
+// engine.h — internal state of libnmt: model (weights + arena, the paper's memory pool,
+// PAPER.md:143), batch, profiler, decode-step graph cache.  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/nmt.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+
+struct NmtError : std::runtime_error {
+  nmt_status code;
+  NmtError(nmt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define NMT_REQUIRE(cond, code, msg)                             \
+  do {                                                           \
+    if (!(cond)) throw ::nmt::NmtError(code, std::string(msg)); \
+  } while (0)
+
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  size_t take(size_t bytes) {
+    size_t off = used;
+    used += (bytes + 255) & ~size_t(255);
+    return off;
+  }
+};
+
+// Device pointers of one encoder layer l (0-based; the paper's layer l+1).
+struct EncW {
+  const void *attn_g, *attn_b, *qkv_w, *qkv_b, *out_w, *out_b, *relk, *relv, *ffn_g, *ffn_b, *w1,
+      *b1, *w2, *b2;
+  const void *dl_g, *dl_b;  // LN^dl_{l+1} (applied to y_{l+1}), DLCL only
+};
+struct DecW {
+  const void *self_g, *self_b, *qkv_w, *qkv_b, *so_w, *so_b, *relk, *relv, *cross_g, *cross_b,
+      *cq_w, *cq_b, *co_w, *co_b, *ffn_g, *ffn_b, *w1, *b1, *w2, *b2;
+};
+
+enum ProfClass {
+  P_ENC_GEMM = 0, P_ENC_ATTN, P_DLCL, P_ENC_LN, P_EMBED, P_DEC_GEMM, P_VOCAB, P_DEC_SELF,
+  P_DEC_CROSS, P_DEC_LN, P_BOOK, P_NCLS
+};
+extern const char* kProfNames[P_NCLS];
+
+}  // namespace nmt
+
+struct nmt_batch {
+  nmt_model* m = nullptr;
+  int B = 0, S = 0;
+  int step = 0;          // host mirror of decode steps issued
+  int rows_upper = 0;    // host upper bound of live rows (grid sizing)
+  int max_cap = 0;
+  bool valid = false;
+  bool pending_step_done = false;  // nmt_decode_step issued, nmt_prune_batch not yet
+};
+
+struct nmt_model {
+  nmt_config cfg{};
+  nmt_precision prec = NMT_FP16;
+  nmt_limits lim{};
+  int device = 0;
+  size_t tb = 2;  // bytes per stored element
+  // weights
+  void* wbuf = nullptr;
+  std::unordered_map<std::string, void*> W;
+  std::vector<nmt::EncW> enc;
+  std::vector<nmt::DecW> dec;
+  const void *emb = nullptr, *dl0_g = nullptr, *dl0_b = nullptr, *enc_fg = nullptr,
+             *enc_fb = nullptr, *dec_fg = nullptr, *dec_fb = nullptr;
+  void* ckv_w = nullptr;   // [Ld*2d][d] cross K/V projection of every decoder layer
+  void* ckv_b = nullptr;   // [Ld*2d]
+  float* dlcl_w = nullptr; // packed rows m = 1..L+1 (row m at offset m(m-1)/2)
+  float* pe = nullptr;     // [max_pos][d] FP32 sinusoid table
+  // arena
+  nmt::Arena ar;
+  int *src = nullptr, *src_len = nullptr, *tgt_cap = nullptr;
+  void *x = nullptr, *u = nullptr, *qkv = nullptr, *o = nullptr, *h = nullptr, *enc_out = nullptr,
+       *hist = nullptr, *ckv = nullptr;
+  void *g = nullptr, *du = nullptr, *dqkv = nullptr, *dout = nullptr, *dq = nullptr, *dh = nullptr;
+  void *kc = nullptr, *vc = nullptr;
+  unsigned long long* keys = nullptr;
+  int *row_slot = nullptr, *prev_tok = nullptr, *out_tok = nullptr, *gen_len = nullptr;
+  uint8_t* done = nullptr;
+  nmt::DevState* st = nullptr;
+  int* bad = nullptr;
+  long long* boff = nullptr;
+  int* blen = nullptr;
+  int* sent_ids = nullptr;
+  // pinned host staging
+  struct Pinned {
+    int* src; int* len; int* cap; long long* boff; int* blen; int* sent; int* out_tok; int* gen_len;
+    nmt::DevState* st; int* bad;
+  } hp{};
+  void* pinned = nullptr;
+  nmt_batch batch;
+  // per-kernel-class CUDA-event profile (bench roofline)
+  struct ProfRec { int cls; cudaEvent_t a, b; double flops, bytes; };
+  struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<ProfRec> pending;
+    double ms[16] = {}, flops[16] = {}, bytes[16] = {};
+    long long n[16] = {};
+  } prof;
+  // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits)
+  std::map<std::tuple<int, int, unsigned>, cudaGraphExec_t> graphs;
+  bool eager_done = false;  // one eager step ran (kernel attributes set) before capture
+  ~nmt_model() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto e : prof.pool) cudaEventDestroy(e);
+    if (wbuf) cudaFree(wbuf);
+    if (ar.base) cudaFree(ar.base);
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+namespace nmt {
+// forward.cu
+void encode_any(nmt_model* m, int B, int S, cudaStream_t s);
+void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
+                     cudaStream_t s);
+void prof_flush(nmt_model* m);
+template <class F>
+void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {
+  auto& P = m->prof;
+  if (!P.on) {
+    f();
+    return;
+  }
+  while (P.pool.size() < P.used + 2) {
+    cudaEvent_t e;
+    NMT_CUDA(cudaEventCreate(&e));
+    P.pool.push_back(e);
+  }
+  cudaEvent_t a = P.pool[P.used++], b = P.pool[P.used++];
+  NMT_CUDA(cudaEventRecord(a, s));
+  f();
+  NMT_CUDA(cudaEventRecord(b, s));
+  P.pending.push_back({cls, a, b, flops, bytes});
+}
+// Runs one launch; when profiling, brackets it with stream events and records its
+// ALGORITHMIC FLOPs / bytes.
+#define PROF(cls, fl, by, stmt) \
+  ::nmt::prof_run(m, cls, (double)(fl), (double)(by), s, [&] { stmt; })
+}  // namespace nmt

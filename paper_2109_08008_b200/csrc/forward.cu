@@ -1,0 +1,207 @@
+// forward.cu — launch sequences of the encoder (once per batch) and of one greedy decode
+// step.  Every arithmetic step runs in the kernels of kernels.cu / attention.cu / gemm_*.cu.
+//
+// Encoder (Eq. 1-2):
+//   y0 = sqrt(d) E[s] + PE;  z0 = LN^dl_0(y0);  x1 = W1_0 z0;  u = LN^a_1(x1)      [embed, dlcl]
+//   per layer l: QKV = u Wqkv^T + b                                                [gemm]
+//                o = RPRAttn(QKV)                                                   [attn]
+//                x = x + o Wo^T + bo         (residual in the GEMM epilogue)       [gemm]
+//                u = LN^f(x);  h = relu(u W1^T + b1);  x = x + h W2^T + b2          [ln, gemm x2]
+//                z_l = LN^dl_l(x); x = sum_k W^{(l+1)}_k z_k; u = LN^a_{l+1}(x)     [dlcl]
+//   enc = LN^enc(sum_k W^{(L+1)}_k z_k);  [CK|CV]_m = enc Wkv_m^T + b for all m     [dlcl, gemm]
+// Decode step t, rows = live batch rows:
+//   g = sqrt(d) E[w_t] + PE(t), u = LN^s(g)                                         [embed_dec_ln]
+//   qkv = u Wqkv^T + b; cached RPR self-attn (appends k_t, v_t); g += o Wso^T + b     [gemm, attn, gemm]
+//   q = LN^c(g) Wq^T + b; cross-attn over cached CK/CV; g += o Wco^T + b              [ln, gemm, attn, gemm]
+//   g += relu(LN^f(g) W1^T + b1) W2^T + b2                                            [ln, gemm x2]
+//   next = argmax_v LN^dec(g) . E[v]   (fused vocab GEMM + argmax)                    [ln, gemm]
+//   sticky done flags, outputs per slot                                               [finish]
+#include <cmath>
+
+#include "engine.h"
+
+namespace nmt {
+
+const char* kProfNames[P_NCLS] = {"enc_gemm",  "enc_rpr_attn", "dlcl_combine", "enc_layernorm",
+                                  "embed",     "dec_gemm",     "vocab_argmax", "dec_self_attn",
+                                  "dec_cross_attn", "dec_layernorm", "bookkeeping"};
+
+void prof_flush(nmt_model* m) {
+  auto& P = m->prof;
+  for (auto& r : P.pending) {
+    float ms = 0.f;
+    NMT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    P.ms[r.cls] += ms;
+    P.flops[r.cls] += r.flops;
+    P.bytes[r.cls] += r.bytes;
+    P.n[r.cls] += 1;
+  }
+  P.pending.clear();
+  P.used = 0;
+}
+
+namespace {
+
+double gemm_bytes(const GemmArgs& a, size_t tb) {
+  double b = ((double)a.M * a.K + (double)a.N * a.K) * tb;
+  if (!a.argmax) b += (double)a.M * a.N * tb;
+  if (a.R) b += (double)a.M * a.N * tb;
+  if (a.bias) b += (double)a.N * tb;
+  return b;
+}
+double gemm_flops(const GemmArgs& a) { return 2.0 * a.M * a.N * a.K; }
+
+GemmArgs mk(int M, int N, int K, const void* A, int lda, const void* B, int ldb, const void* bias,
+            void* C, int ldc) {
+  GemmArgs a;
+  a.M = M; a.N = N; a.K = K; a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.bias = bias;
+  a.C = C; a.ldc = ldc;
+  return a;
+}
+
+template <class T> const T* cT(const void* p) { return static_cast<const T*>(p); }
+
+template <class T>
+void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
+  const nmt_config& c = m->cfg;
+  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, L = c.enc_layers, Ld = c.dec_layers;
+  const int N = B * S;
+  const float eps = c.ln_eps;
+  const size_t tb = sizeof(T);
+  T *x = (T*)m->x, *u = (T*)m->u, *qkv = (T*)m->qkv, *o = (T*)m->o, *h = (T*)m->h,
+    *enc = (T*)m->enc_out, *hist = (T*)m->hist, *ckv = (T*)m->ckv;
+  const size_t hs = (size_t)N * d;
+  const double row = (double)N * d * tb;  // bytes of one [N][d] activation
+  const float sq = std::sqrt((float)d);
+  PROF(P_EMBED, 0, 2 * row,
+       embed<T>(m->src, cT<T>(m->emb), m->pe, c.use_dlcl ? o : x, N, d, S, nullptr, nullptr, sq, s));
+  const EncW& w0 = m->enc[0];
+  if (c.use_dlcl) {
+    PROF(P_DLCL, 0, 4 * row,
+         dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, cT<T>(m->dl0_g), cT<T>(m->dl0_b), c.dlcl_ln,
+                         cT<T>(w0.attn_g), cT<T>(w0.attn_b), x, u, N, d, eps, s));
+  } else {
+    PROF(P_ENC_LN, 0, 2 * row,
+         layernorm<T>(x, d, cT<T>(w0.attn_g), cT<T>(w0.attn_b), u, d, N, d, eps, nullptr, s));
+  }
+  const double attn_flops = 4.0 * B * H * (double)S * S * (d / H);
+  for (int l = 0; l < L; ++l) {
+    const EncW& w = m->enc[l];
+    GemmArgs a = mk(N, 3 * d, d, u, d, w.qkv_w, d, w.qkv_b, qkv, 3 * d);
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_ENC_ATTN, attn_flops, 4 * row,
+         attn_encoder<T>(qkv, m->src_len, cT<T>(w.relk), cT<T>(w.relv), o, B, S, d, H,
+                         c.max_rel_pos, c.use_rpr, s));
+    a = mk(N, d, d, o, d, w.out_w, d, w.out_b, x, d);
+    a.R = x; a.ldr = d;
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // a = x + Attn(LN(x))
+    PROF(P_ENC_LN, 0, 2 * row,
+         layernorm<T>(x, d, cT<T>(w.ffn_g), cT<T>(w.ffn_b), u, d, N, d, eps, nullptr, s));
+    a = mk(N, F, d, u, d, w.w1, d, w.b1, h, F);
+    a.relu = 1;
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    a = mk(N, d, F, h, F, w.w2, F, w.b2, x, d);
+    a.R = x; a.ldr = d;
+    PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));  // y_l = a + FFN(LN(a))
+    const bool last = (l == L - 1);
+    const T* ng = last ? cT<T>(m->enc_fg) : cT<T>(m->enc[l + 1].attn_g);
+    const T* nb = last ? cT<T>(m->enc_fb) : cT<T>(m->enc[l + 1].attn_b);
+    if (c.use_dlcl) {
+      const int k = l + 1;  // depth of y
+      PROF(P_DLCL, 0, (1 + k + 1 + (last ? 0 : 1) + 1) * row,
+           dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, cT<T>(w.dl_g),
+                           cT<T>(w.dl_b), c.dlcl_ln, ng, nb, last ? nullptr : x,
+                           last ? enc : u, N, d, eps, s));
+    } else {
+      PROF(P_ENC_LN, 0, 2 * row,
+           layernorm<T>(x, d, ng, nb, last ? enc : u, d, N, d, eps, nullptr, s));
+    }
+  }
+  // cross K/V of every decoder layer, once per sentence
+  GemmArgs a = mk(N, Ld * 2 * d, d, enc, d, m->ckv_w, d, m->ckv_b, ckv, Ld * 2 * d);
+  PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+}
+
+template <class T>
+void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
+                      cudaStream_t s) {
+  const nmt_config& c = m->cfg;
+  const int d = c.d_model, F = c.d_ffn, H = c.n_heads, Ld = c.dec_layers;
+  const int R = b->rows_upper;
+  const int Tm = m->lim.max_tgt_len;
+  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
+  const float eps = c.ln_eps;
+  const size_t tb = sizeof(T);
+  const int* dR = &m->st->n_live;
+  const int* dt = &m->st->t;
+  const int t = b->step;  // host mirror (profile byte counts only)
+  const double row = (double)R * d * tb;
+  T *g = (T*)m->g, *du = (T*)m->du, *dqkv = (T*)m->dqkv, *dout = (T*)m->dout, *dq = (T*)m->dq,
+    *dh = (T*)m->dh;
+  // g = sqrt(d) E[w_t] + PE(t) fused with the first layer's pre-norm
+  PROF(P_EMBED, 0, 3 * row,
+       embed_dec_ln<T>(d_prev ? d_prev : m->prev_tok, cT<T>(m->emb), m->pe,
+                       cT<T>(m->dec[0].self_g), cT<T>(m->dec[0].self_b), g, du, R, d,
+                       std::sqrt((float)d), eps, dt, dR, s));
+  for (int l = 0; l < Ld; ++l) {
+    const DecW& w = m->dec[l];
+    T* kc = (T*)m->kc + (size_t)l * Rmax * Tm * d;
+    T* vc = (T*)m->vc + (size_t)l * Rmax * Tm * d;
+    if (l > 0)
+      PROF(P_DEC_LN, 0, 2 * row,
+           layernorm<T>(g, d, cT<T>(w.self_g), cT<T>(w.self_b), du, d, R, d, eps, dR, s));
+    GemmArgs a = mk(R, 3 * d, d, du, d, w.qkv_w, d, w.qkv_b, dqkv, 3 * d);
+    a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
+         attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, cT<T>(w.relk), cT<T>(w.relv), dout,
+                              R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s));
+    a = mk(R, d, d, dout, d, w.so_w, d, w.so_b, g, d);
+    a.R = g; a.ldr = d; a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_LN, 0, 2 * row,
+         layernorm<T>(g, d, cT<T>(w.cross_g), cT<T>(w.cross_b), du, d, R, d, eps, dR, s));
+    a = mk(R, d, d, du, d, w.cq_w, d, w.cq_b, dq, d);
+    a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
+         attn_cross<T>(dq, (const T*)m->ckv, Ld * 2 * d, l * 2 * d, l * 2 * d + d, &m->st->S,
+                       c.max_src_len, m->src_len, m->row_slot, dout, R, d, H, dR, s));
+    a = mk(R, d, d, dout, d, w.co_w, d, w.co_b, g, d);
+    a.R = g; a.ldr = d; a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_LN, 0, 2 * row,
+         layernorm<T>(g, d, cT<T>(w.ffn_g), cT<T>(w.ffn_b), du, d, R, d, eps, dR, s));
+    a = mk(R, F, d, du, d, w.w1, d, w.b1, dh, F);
+    a.relu = 1; a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    a = mk(R, d, F, dh, F, w.w2, F, w.b2, g, d);
+    a.R = g; a.ldr = d; a.dM = dR;
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+  }
+  PROF(P_DEC_LN, 0, 2 * row,
+       layernorm<T>(g, d, cT<T>(m->dec_fg), cT<T>(m->dec_fb), du, d, R, d, eps, dR, s));
+  // tied vocab projection fused with argmax: logits never stored
+  GemmArgs a = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
+  a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
+  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+  PROF(P_BOOK, 0, 0,
+       greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
+                     Tm, m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
+                     out ? out->d_done : nullptr, s));
+}
+
+}  // namespace
+
+void encode_any(nmt_model* m, int B, int S, cudaStream_t s) {
+  if (m->prec == NMT_FP16) encode_impl<__half>(m, B, S, s);
+  else encode_impl<float>(m, B, S, s);
+}
+
+void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
+                     cudaStream_t s) {
+  if (m->prec == NMT_FP16) decode_step_impl<__half>(m, b, d_prev, out, s);
+  else decode_step_impl<float>(m, b, d_prev, out, s);
+}
+
+}  // namespace nmt

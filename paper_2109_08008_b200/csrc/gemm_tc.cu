@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -277,7 +278,40 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+struct MapKey {
+  const void* p;
+  int rows, cols, ld, box;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.p);
+    h ^= (size_t)k.rows * 0x9E3779B97F4A7C15ull + ((size_t)k.cols << 20) + ((size_t)k.ld << 40) +
+         (size_t)k.box;
+    return h;
+  }
+};
+
+CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows);
+
+// Tensor maps are pure functions of (pointer, shape, box): cache them (the arena and the
+// weights never move), so a steady-state launch does no host-side encoding.
 CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  static std::mutex mu;
+  MapKey k{ptr, rows, cols, ld, box_rows};
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(k);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 65536) cache.clear();
+  CUtensorMap m = encode_map(ptr, rows, cols, ld, box_rows);
+  cache.emplace(k, m);
+  return m;
+}
+
+CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};

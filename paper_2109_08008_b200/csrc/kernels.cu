@@ -78,6 +78,42 @@ void layernorm(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, in
   NMT_LAUNCH_CHECK();
 }
 
+template <class T>
+__global__ void k_embed_dec_ln(const int* __restrict__ ids, const T* __restrict__ E,
+                               const float* __restrict__ pe, const T* __restrict__ gam,
+                               const T* __restrict__ bet, T* __restrict__ g, T* __restrict__ u,
+                               int rows, int d, float scale, float eps, const int* __restrict__ d_t,
+                               const int* __restrict__ dR) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= min(rows, *dR)) return;
+  const int E_ = d >> 5;
+  const T* e = E + (size_t)ids[row] * d;
+  const float* p = pe + (size_t)(*d_t) * d;
+  float v[kMaxLaneElems];
+#pragma unroll
+  for (int i = 0; i < kMaxLaneElems; ++i)
+    if (i < E_) {
+      const int c = lane + 32 * i;
+      const T gt = from_f<T>(to_f(e[c]) * scale + p[c]);
+      g[(size_t)row * d + c] = gt;
+      v[i] = to_f(gt);
+    }
+  ln_regs(v, E_, d, gam, bet, eps, lane);
+#pragma unroll
+  for (int i = 0; i < kMaxLaneElems; ++i)
+    if (i < E_) u[(size_t)row * d + lane + 32 * i] = from_f<T>(v[i]);
+}
+
+template <class T>
+void embed_dec_ln(const int* ids, const T* E, const float* pe, const T* gam, const T* bet, T* g,
+                  T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
+                  cudaStream_t s) {
+  if (rows <= 0) return;
+  k_embed_dec_ln<T><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows, d, scale,
+                                                      eps, d_t, dR);
+  NMT_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------- DLCL combine
 // Eq. 2: x_{l+1} = sum_{k=0..l} W^{(l+1)}_k LN(y_k).  z_k = LN^dl_k(y_k)
 // is written once into the history when y_k is produced and re-read by every later
@@ -133,304 +169,130 @@ __global__ void k_dlcl(const T* __restrict__ y, T* __restrict__ hist, size_t his
 template <class T>
 void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
+                  int d, float eps, cudaStream_t s);
+
+// Vectorised variant: lane owns E contiguous columns [lane*E, lane*E + E) so every row
+// access is 16-B vector loads/stores (one 1 KB row per warp-instruction pair at d = 512).
+template <class T> struct VecIO;
+template <> struct VecIO<__half> {
+  static constexpr int W = 8;  // elements per 16 B
+  static __device__ __forceinline__ void ld(const __half* p, float* f) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 x = __half22float2(h[e]);
+      f[2 * e] = x.x;
+      f[2 * e + 1] = x.y;
+    }
+  }
+  static __device__ __forceinline__ void st(__half* p, const float* f) {
+    uint4 u;
+    __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __halves2half2(from_f<__half>(f[2 * e]), from_f<__half>(f[2 * e + 1]));
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <> struct VecIO<float> {
+  static constexpr int W = 4;
+  static __device__ __forceinline__ void ld(const float* p, float* f) {
+    float4 v = *reinterpret_cast<const float4*>(p);
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float* f) {
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+};
+
+template <class T, int E>
+__device__ __forceinline__ void ldrow(const T* p, float* v) {
+#pragma unroll
+  for (int i = 0; i < E; i += VecIO<T>::W) VecIO<T>::ld(p + i, v + i);
+}
+template <class T, int E>
+__device__ __forceinline__ void strow(T* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < E; i += VecIO<T>::W) VecIO<T>::st(p + i, v + i);
+}
+template <class T, int E>
+__device__ __forceinline__ void ln_contig(float* v, int d, const T* g, const T* b, float eps,
+                                          int lane) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) s += v[i];
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float t = v[i] - mu;
+    q += t * t;
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + eps);
+  float gv[E], bv[E];
+  ldrow<T, E>(g + lane * E, gv);
+  ldrow<T, E>(b + lane * E, bv);
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i] = (v[i] - mu) * rstd * gv[i] + bv[i];
+}
+
+template <class T, int E>
+__global__ void __launch_bounds__(256) k_dlcl_vec(
+    const T* __restrict__ y, T* __restrict__ hist, size_t hist_stride, int l,
+    const float* __restrict__ w, const T* __restrict__ gdl, const T* __restrict__ bdl, int dlcl_ln,
+    const T* __restrict__ g2, const T* __restrict__ b2, T* __restrict__ xout, T* __restrict__ uout,
+    int rows, float eps) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  constexpr int d = 32 * E;
+  const size_t off = (size_t)row * d + lane * E;
+  float z[E], x[E];
+  ldrow<T, E>(y + off, z);
+  if (dlcl_ln) ln_contig<T, E>(z, d, gdl, bdl, eps, lane);
+  // z_l rounded to storage precision: later combines re-read exactly this value
+  strow<T, E>(hist + (size_t)l * hist_stride + off, z);
+#pragma unroll
+  for (int i = 0; i < E; ++i) z[i] = to_f(from_f<T>(z[i]));
+#pragma unroll
+  for (int i = 0; i < E; ++i) x[i] = 0.f;
+  int k = 0;
+  for (; k + 1 < l; k += 2) {  // two history rows in flight per lane
+    float a[E], b[E];
+    ldrow<T, E>(hist + (size_t)k * hist_stride + off, a);
+    ldrow<T, E>(hist + (size_t)(k + 1) * hist_stride + off, b);
+    const float wa = w[k], wb = w[k + 1];
+#pragma unroll
+    for (int i = 0; i < E; ++i) x[i] = fmaf(wb, b[i], fmaf(wa, a[i], x[i]));
+  }
+  for (; k < l; ++k) {
+    float a[E];
+    ldrow<T, E>(hist + (size_t)k * hist_stride + off, a);
+    const float wa = w[k];
+#pragma unroll
+    for (int i = 0; i < E; ++i) x[i] = fmaf(wa, a[i], x[i]);
+  }
+  const float wl = w[l];
+#pragma unroll
+  for (int i = 0; i < E; ++i) x[i] = fmaf(wl, z[i], x[i]);
+  if (xout) strow<T, E>(xout + off, x);
+  ln_contig<T, E>(x, d, g2, b2, eps, lane);
+  strow<T, E>(uout + off, x);
+}
+
+template <class T>
+void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
+                  const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
                   int d, float eps, cudaStream_t s) {
   if (rows <= 0) return;
-  k_dlcl<T><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, dlcl_ln, g2,
-                                               b2, xout, uout, rows, d, eps);
-  NMT_LAUNCH_CHECK();
-}
-
-// ------------------------------------------------------------------- attention helpers
-template <class T>
-__device__ __forceinline__ float dot_gs(const T* __restrict__ row, const float* __restrict__ q,
-                                        int dh) {
-  float acc = 0.f;
-  for (int c = 0; c < dh; ++c) acc += to_f(row[c]) * q[c];
-  return acc;
-}
-template <>
-__device__ __forceinline__ float dot_gs<__half>(const __half* __restrict__ row,
-                                                const float* __restrict__ q, int dh) {
-  float acc = 0.f;
-  if ((dh & 7) == 0) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(row);
-    for (int c8 = 0; c8 < (dh >> 3); ++c8) {
-      uint4 u = r4[c8];
-      const __half2* h2 = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __half22float2(h2[e]);
-        acc += f.x * q[c8 * 8 + 2 * e] + f.y * q[c8 * 8 + 2 * e + 1];
-      }
-    }
-  } else {
-    for (int c = 0; c < dh; ++c) acc += __half2float(row[c]) * q[c];
-  }
-  return acc;
-}
-
-// ------------------------------------------------------------------- encoder RPR attention
-// grid (B, H), 4 warps; Q, K, V of one (sentence, head) staged in shared memory as FP32.
-//   e_ij = (q_i . k_j + q_i . A^K[r(i,j)]) / sqrt(dh)   masked j >= len
-//   o_i  = sum_j a_ij v_j + sum_r (sum_{j: r(i,j)=r} a_ij) A^V[r]
-template <class T>
-__global__ void k_attn_enc(const T* __restrict__ qkv, const int* __restrict__ len,
-                           const T* __restrict__ relk, const T* __restrict__ relv,
-                           T* __restrict__ out, int S, int d, int H, int kclip, int use_rpr) {
-  extern __shared__ float sm[];
-  const int b = blockIdx.x, h = blockIdx.y;
-  const int dh = d / H, R = 2 * kclip + 1, ld = dh + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  float* sQ = sm;                 // [S][dh+1]
-  float* sK = sQ + S * ld;        // [S][dh+1]
-  float* sV = sK + S * ld;        // [S][dh]
-  float* sAK = sV + S * dh;       // [R][dh]
-  float* sAV = sAK + R * dh;      // [R][dh]
-  float* sP = sAV + R * dh;       // [nw][S]
-  float* sX = sP + nw * S;        // [nw][32]  (qa, then bucket sums)
-  const int n = len[b];
-  const size_t rs = 3 * (size_t)d;
-  for (int idx = threadIdx.x; idx < n * dh; idx += blockDim.x) {
-    int j = idx / dh, c = idx % dh;
-    const T* rp = qkv + ((size_t)b * S + j) * rs + h * dh + c;
-    sQ[j * ld + c] = to_f(rp[0]);
-    sK[j * ld + c] = to_f(rp[d]);
-    sV[j * dh + c] = to_f(rp[2 * d]);
-  }
-  if (use_rpr)
-    for (int idx = threadIdx.x; idx < R * dh; idx += blockDim.x) {
-      sAK[idx] = to_f(relk[idx]);
-      sAV[idx] = to_f(relv[idx]);
-    }
-  __syncthreads();
-  const float scale = rsqrtf((float)dh);
-  float* p = sP + warp * S;
-  float* x = sX + warp * 32;
-  for (int i = warp; i < S; i += nw) {
-    T* orow = out + ((size_t)b * S + i) * d + h * dh;
-    if (i >= n) {  // padding query rows: zero output
-      for (int c = lane; c < dh; c += 32) orow[c] = from_f<T>(0.f);
-      continue;
-    }
-    const float* qi = sQ + i * ld;
-    if (use_rpr) {
-      if (lane < R) {
-        float a = 0.f;
-        for (int c = 0; c < dh; ++c) a += qi[c] * sAK[lane * dh + c];
-        x[lane] = a;
-      }
-      __syncwarp();
-    }
-    float mx = -INFINITY;
-    for (int j = lane; j < n; j += 32) {
-      const float* kj = sK + j * ld;
-      float e = 0.f;
-      for (int c = 0; c < dh; ++c) e += qi[c] * kj[c];
-      if (use_rpr) e += x[min(max(j - i, -kclip), kclip) + kclip];
-      e *= scale;
-      p[j] = e;
-      mx = fmaxf(mx, e);
-    }
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      float e = __expf(p[j] - mx);
-      p[j] = e;
-      sum += e;
-    }
-    const float inv = 1.f / warp_sum(sum);
-    __syncwarp();
-    if (use_rpr) {
-      if (lane < R) {  // bucket sums of the normalised weights
-        float bs = 0.f;
-        int r = lane;
-        if (r == 0) {
-          for (int j = 0; j <= min(i - kclip, n - 1); ++j) bs += p[j];
-        } else if (r == R - 1) {
-          for (int j = max(i + kclip, 0); j < n; ++j) bs += p[j];
-        } else {
-          int j = i + r - kclip;
-          if (j >= 0 && j < n) bs = p[j];
-        }
-        x[lane] = bs * inv;
-      }
-      __syncwarp();
-    }
-    for (int c = lane; c < dh; c += 32) {
-      float o = 0.f;
-      for (int j = 0; j < n; ++j) o += p[j] * sV[j * dh + c];
-      o *= inv;
-      if (use_rpr)
-        for (int r = 0; r < R; ++r) o += x[r] * sAV[r * dh + c];
-      orow[c] = from_f<T>(o);
-    }
-    __syncwarp();
-  }
-}
-
-template <class T>
-void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
-                  int d, int H, int kclip, int use_rpr, cudaStream_t s) {
-  if (B <= 0) return;
-  const int dh = d / H, R = 2 * kclip + 1, nw = 4;
-  size_t smem = sizeof(float) * (2 * S * (dh + 1) + S * dh + 2 * R * dh + nw * S + nw * 32);
-  static bool attr_set[2] = {false, false};
-  bool& set = attr_set[sizeof(T) == 2];
-  if (!set) {
-    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    set = true;
-  }
-  k_attn_enc<T><<<dim3(B, H), nw * 32, smem, s>>>(qkv, len, relk, relv, out, S, d, H, kclip,
-                                                  use_rpr);
-  NMT_LAUNCH_CHECK();
-}
-
-// ------------------------------------------------------------------- decoder self-attention
-// One warp per (live row, head).  Step t: write k_t, v_t to the cache slot, then attend
-// over j = 0..t; only buckets 0..k occur (j <= t) and every j <= t-k shares bucket 0.
-template <class T>
-__global__ void k_attn_dec_self(const T* __restrict__ qkv, T* __restrict__ kc, T* __restrict__ vc,
-                                int Tmax, const int* __restrict__ row_slot,
-                                const T* __restrict__ relk, const T* __restrict__ relv,
-                                T* __restrict__ out, int rows, int d, int H, int kclip,
-                                int use_rpr, const int* __restrict__ d_t,
-                                const int* __restrict__ dR) {
-  extern __shared__ float sm[];
-  const int dh = d / H;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int gw = blockIdx.x * nw + warp;
-  const int row = gw / H, h = gw % H;
-  const int nrows = min(rows, *dR);
-  if (row >= nrows) return;
-  const int t = *d_t;
-  float* q = sm + warp * (dh + 32 + Tmax);
-  float* x = q + dh;
-  float* p = x + 32;
-  const int slot = row_slot[row];
-  const T* src = qkv + (size_t)row * 3 * d + h * dh;
-  T* krow = kc + ((size_t)slot * Tmax + t) * d + h * dh;
-  T* vrow = vc + ((size_t)slot * Tmax + t) * d + h * dh;
-  for (int c = lane; c < dh; c += 32) {
-    q[c] = to_f(src[c]);
-    krow[c] = src[d + c];
-    vrow[c] = src[2 * d + c];
-  }
-  __syncwarp();
-  if (use_rpr && lane <= kclip) {
-    float a = 0.f;
-    for (int c = 0; c < dh; ++c) a += q[c] * to_f(relk[lane * dh + c]);
-    x[lane] = a;
-  }
-  __syncwarp();
-  const float scale = rsqrtf((float)dh);
-  float mx = -INFINITY;
-  const T* kbase = kc + (size_t)slot * Tmax * d + h * dh;
-  for (int j = lane; j <= t; j += 32) {
-    float e = dot_gs<T>(kbase + (size_t)j * d, q, dh);
-    if (use_rpr) e += x[max(j - t, -kclip) + kclip];
-    e *= scale;
-    p[j] = e;
-    mx = fmaxf(mx, e);
-  }
-  mx = warp_max(mx);
-  float sum = 0.f;
-  for (int j = lane; j <= t; j += 32) {
-    float e = __expf(p[j] - mx);
-    p[j] = e;
-    sum += e;
-  }
-  const float inv = 1.f / warp_sum(sum);
-  __syncwarp();
-  if (use_rpr) {
-    float bs = 0.f;
-    if (lane == 0) {
-      for (int j = 0; j <= t - kclip; ++j) bs += p[j];
-    } else if (lane <= kclip) {
-      int j = t - kclip + lane;
-      if (j >= 0) bs = p[j];
-    }
-    __syncwarp();
-    if (lane <= kclip) x[lane] = bs * inv;
-    __syncwarp();
-  }
-  const T* vbase = vc + (size_t)slot * Tmax * d + h * dh;
-  T* orow = out + (size_t)row * d + h * dh;
-  for (int c = lane; c < dh; c += 32) {
-    float o = 0.f;
-    for (int j = 0; j <= t; ++j) o += p[j] * to_f(vbase[(size_t)j * d + c]);
-    o *= inv;
-    if (use_rpr)
-      for (int r = 0; r <= kclip; ++r) o += x[r] * to_f(relv[r * dh + c]);
-    orow[c] = from_f<T>(o);
-  }
-}
-
-template <class T>
-void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot, const T* relk,
-                       const T* relv, T* out, int rows, int d, int H, int kclip, int use_rpr,
-                       const int* d_t, const int* dR, cudaStream_t s) {
-  if (rows <= 0) return;
-  const int nw = 4, dh = d / H;
-  size_t smem = sizeof(float) * nw * (dh + 32 + Tmax);
-  k_attn_dec_self<T><<<ceil_div(rows * H, nw), nw * 32, smem, s>>>(
-      qkv, kc, vc, Tmax, row_slot, relk, relv, out, rows, d, H, kclip, use_rpr, d_t, dR);
-  NMT_LAUNCH_CHECK();
-}
-
-// ------------------------------------------------------------------- cross-attention
-template <class T>
-__global__ void k_attn_cross(const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv,
-                             int koff, int voff, int S, const int* __restrict__ src_len,
-                             const int* __restrict__ row_slot, T* __restrict__ out, int rows,
-                             int d, int H, const int* __restrict__ dR) {
-  extern __shared__ float sm[];
-  const int dh = d / H;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int gw = blockIdx.x * nw + warp;
-  const int row = gw / H, h = gw % H;
-  const int nrows = min(rows, *dR);
-  if (row >= nrows) return;
-  float* q = sm + warp * (dh + S);
-  float* p = q + dh;
-  const int slot = row_slot[row];
-  const int n = src_len[slot];
-  for (int c = lane; c < dh; c += 32) q[c] = to_f(qb[(size_t)row * d + h * dh + c]);
-  __syncwarp();
-  const float scale = rsqrtf((float)dh);
-  const T* base = ckv + (size_t)slot * S * ldkv + h * dh;
-  float mx = -INFINITY;
-  for (int j = lane; j < n; j += 32) {
-    float e = dot_gs<T>(base + (size_t)j * ldkv + koff, q, dh) * scale;
-    p[j] = e;
-    mx = fmaxf(mx, e);
-  }
-  mx = warp_max(mx);
-  float sum = 0.f;
-  for (int j = lane; j < n; j += 32) {
-    float e = __expf(p[j] - mx);
-    p[j] = e;
-    sum += e;
-  }
-  const float inv = 1.f / warp_sum(sum);
-  __syncwarp();
-  T* orow = out + (size_t)row * d + h * dh;
-  for (int c = lane; c < dh; c += 32) {
-    float o = 0.f;
-    for (int j = 0; j < n; ++j) o += p[j] * to_f(base[(size_t)j * ldkv + voff + c]);
-    orow[c] = from_f<T>(o * inv);
-  }
-}
-
-template <class T>
-void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, int S, const int* src_len,
-                const int* row_slot, T* out, int rows, int d, int H, const int* dR, cudaStream_t s) {
-  if (rows <= 0) return;
-  const int nw = 4, dh = d / H;
-  size_t smem = sizeof(float) * nw * (dh + S);
-  k_attn_cross<T><<<ceil_div(rows * H, nw), nw * 32, smem, s>>>(q, ckv, ldkv, koff, voff, S,
-                                                                 src_len, row_slot, out, rows, d,
-                                                                 H, dR);
+  if (d == 512)
+    k_dlcl_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl,
+                                                         dlcl_ln, g2, b2, xout, uout, rows, eps);
+  else if (d == 256)
+    k_dlcl_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl,
+                                                        dlcl_ln, g2, b2, xout, uout, rows, eps);
+  else
+    k_dlcl<T><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, dlcl_ln, g2,
+                                                 b2, xout, uout, rows, d, eps);
   NMT_LAUNCH_CHECK();
 }
 
@@ -564,7 +426,7 @@ void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, in
 }
 
 __global__ void k_batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* gen_len,
-                             DevState* st, int B, int bos) {
+                             DevState* st, int B, int S, int bos) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < B) {
     row_slot[r] = r;
@@ -577,13 +439,14 @@ __global__ void k_batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* g
     st->n_live = B;
     st->n_done = 0;
     st->prunes = 0;
+    st->S = S;
   }
 }
 
 void batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* gen_len, DevState* st, int B,
-                int bos, cudaStream_t s) {
+                int S, int bos, cudaStream_t s) {
   k_batch_init<<<ceil_div(B > 0 ? B : 1, 128), 128, 0, s>>>(row_slot, prev_tok, done, gen_len, st,
-                                                            B, bos);
+                                                            B, S, bos);
   NMT_LAUNCH_CHECK();
 }
 
@@ -661,14 +524,9 @@ void argmax_ids(unsigned long long* keys, int* ids, int rows, cudaStream_t s) {
                              const int*, cudaStream_t);                                         \
   template void dlcl_combine<T>(const T*, T*, size_t, int, const float*, const T*, const T*,    \
                                 int, const T*, const T*, T*, T*, int, int, float, cudaStream_t); \
-  template void attn_encoder<T>(const T*, const int*, const T*, const T*, T*, int, int, int,    \
-                                int, int, int, cudaStream_t);                                   \
-  template void attn_decoder_self<T>(const T*, T*, T*, int, const int*, const T*, const T*, T*, \
-                                     int, int, int, int, int, const int*, const int*,           \
-                                     cudaStream_t);                                             \
-  template void attn_cross<T>(const T*, const T*, int, int, int, int, const int*, const int*,   \
-                              T*, int, int, int, const int*, cudaStream_t);                     \
-  template void to_float<T>(const T*, float*, size_t, cudaStream_t);
+  template void to_float<T>(const T*, float*, size_t, cudaStream_t);                          \
+  template void embed_dec_ln<T>(const int*, const T*, const float*, const T*, const T*, T*, T*, \
+                                int, int, float, float, const int*, const int*, cudaStream_t);
 NMT_INST(float)
 NMT_INST(__half)
 

@@ -68,10 +68,19 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
                        const int* d_t, const int* dR, cudaStream_t s);
 
 // Cross-attention over the once-per-sentence encoder K/V:
-// keys at ckv + (slot*S + j)*ldkv + koff, values at + voff; mask j < src_len[slot].
+// keys at ckv + (slot*S + j)*ldkv + koff, values at + voff; mask j < src_len[slot];
+// S = *dS read on the device (graph-replayable), Smax sizes shared memory.
 template <class T>
-void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, int S, const int* src_len,
-                const int* row_slot, T* out, int rows, int d, int H, const int* dR, cudaStream_t s);
+void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const int* dS, int Smax,
+                const int* src_len, const int* row_slot, T* out, int rows, int d, int H,
+                const int* dR, cudaStream_t s);
+
+// Decoder input + first pre-norm, fused (one warp per live row):
+//   g = sqrt(d) E[w_r] + PE(t),  u = LN(g; gam, bet)     (t = *d_t)
+template <class T>
+void embed_dec_ln(const int* ids, const T* E, const float* pe, const T* gam, const T* bet, T* g,
+                  T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
+                  cudaStream_t s);
 
 // ---------------------------------------------------------------- greedy bookkeeping
 // Batch state on the device (one int32 block):
@@ -80,6 +89,7 @@ struct DevState {
   int n_live;     // live rows
   int n_done;     // done rows among live ones (sticky flags)
   int prunes;     // number of compactions so far
+  int S;          // padded source length of the batch (cross-attention stride)
 };
 
 // After the vocab argmax of step t: next token per live row, sticky done flag
@@ -98,7 +108,7 @@ void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, in
 // Fresh batch state: row_slot[r] = r, prev_tok[r] = BOS, done = 0, gen_len = 0,
 // st = {t 0, n_live B, n_done 0, prunes 0}.
 void batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* gen_len, DevState* st, int B,
-                int bos, cudaStream_t s);
+                int S, int bos, cudaStream_t s);
 
 // Scatter a finished batch's per-slot outputs to their original sentence ids.
 void scatter_outputs(const int* out_tok, int out_stride, const int* gen_len, const int* sent_ids,

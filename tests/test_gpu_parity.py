@@ -203,7 +203,10 @@ def test_translate_host_equals_device_and_steps():
     d_ids = torch.from_numpy(wl.ids).cuda()
     d_out = torch.zeros(wl.n, gm.Tmax, dtype=torch.int32, device="cuda")
     d_len = torch.zeros(wl.n, dtype=torch.int32, device="cuda")
-    st_d = gm.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps)
+    side = torch.cuda.Stream()      # non-default stream: CUDA-graph decode steps
+    with torch.cuda.stream(side):
+        st_d = gm.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps)
+    torch.cuda.synchronize()
     d_out, d_len = d_out.cpu().numpy(), d_len.cpu().numpy()
     for i in range(wl.n):
         g = d_out[i, :d_len[i]].tolist()
@@ -211,9 +214,11 @@ def test_translate_host_equals_device_and_steps():
             g = g[:-1]
         assert g == out_h[i]
     assert st_h["gen_tokens"] == st_d["gen_tokens"] == int(d_len.sum())
-    # deterministic: a second run is byte-identical
-    out_h2, _ = gm.translate(wl.ids, wl.off, caps=wl.caps)
+    # deterministic: a second run (graph replay on a side stream) is byte-identical
+    with torch.cuda.stream(side):
+        out_h2, st2 = gm.translate(wl.ids, wl.off, caps=wl.caps)
     assert out_h2 == out_h
+    assert st2["launches"] < st_h["launches"]   # graphs: one launch per decode step
 
 
 def test_batch_invariance_fp32():
