@@ -116,6 +116,18 @@ void init_arena(nmt_model* m) {
   const size_t N = L.max_tokens, Bm = L.max_sents, Tm = L.max_tgt_len;
   const size_t R = Bm * std::max(1, L.beam);
   Arena& a = m->ar;
+  // split-K workspace: max over the decode GEMM shapes of m_tiles * n_tiles * splits * 128*64
+  size_t ws_floats = 0;
+  {
+    const int shapes[5][2] = {{3 * (int)d, (int)d}, {(int)d, (int)d}, {(int)F, (int)d},
+                              {(int)d, (int)F}, {(int)d, (int)d}};
+    const size_t mt = (R + 127) / 128;
+    for (auto& sh : shapes) {
+      const size_t nt = (sh[0] + 63) / 64, sp = decode_splits(sh[0], sh[1]);
+      if (sp > 1) ws_floats = std::max(ws_floats, mt * nt * sp * 128 * 64);
+    }
+  }
+  const size_t cnt_ints = ((R + 127) / 128) * ((std::max(3 * d, F) + 63) / 64);
   std::vector<std::pair<void**, size_t>> items = {
       {(void**)&m->src, N * 4}, {(void**)&m->src_len, Bm * 4}, {(void**)&m->tgt_cap, Bm * 4},
       {&m->x, N * d * tb}, {&m->u, N * d * tb}, {&m->qkv, N * 3 * d * tb}, {&m->o, N * d * tb},
@@ -129,6 +141,8 @@ void init_arena(nmt_model* m) {
       {(void**)&m->done, R}, {(void**)&m->out_tok, Bm * Tm * 4}, {(void**)&m->gen_len, Bm * 4},
       {(void**)&m->st, sizeof(DevState)}, {(void**)&m->bad, 4}, {(void**)&m->boff, Bm * 8},
       {(void**)&m->blen, Bm * 4}, {(void**)&m->sent_ids, Bm * 4},
+      {(void**)&m->gemm_ws, std::max<size_t>(ws_floats * 4, 256)},
+      {(void**)&m->gemm_cnt, std::max<size_t>(cnt_ints * 4, 256)},
   };
   std::vector<size_t> offs;
   for (auto& it : items) offs.push_back(a.take(it.second));
@@ -771,6 +785,34 @@ nmt_status nmt_dev_gemm(nmt_precision prec, int32_t M, int32_t N, int32_t K, con
     a.R = d_R; a.ldr = ldr; a.C = d_C; a.ldc = ldc; a.relu = relu;
     if (prec == NMT_FP16) gemm<__half>(a, (cudaStream_t)stream);
     else gemm<float>(a, (cudaStream_t)stream);
+  });
+}
+
+nmt_status nmt_dev_gemm_decode(int32_t M, int32_t N, int32_t K, const void* d_A, int32_t lda,
+                               const void* d_B, int32_t ldb, const void* d_bias, const void* d_R,
+                               int32_t ldr, void* d_C, int32_t ldc, int32_t relu, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(d_A && d_B && d_C && M > 0 && M <= 4096 && N > 0 && K > 0, NMT_E_ARG,
+                "bad gemm args");
+    NMT_REQUIRE(K % 16 == 0, NMT_E_SHAPE, "K must be a multiple of 16");
+    static float* ws = nullptr;   // test hook scratch (not on the product path)
+    static int* cnt = nullptr;
+    const int sp = decode_splits(N, K);
+    const size_t need = (size_t)((M + 127) / 128) * ((N + 63) / 64) * sp * 128 * 64;
+    static size_t have = 0;
+    if (need > have) {
+      if (ws) cudaFree(ws);
+      if (cnt) cudaFree(cnt);
+      NMT_CUDA(cudaMalloc(&ws, need * 4));
+      NMT_CUDA(cudaMalloc(&cnt, 65536 * 4));
+      NMT_CUDA(cudaMemset(cnt, 0, 65536 * 4));
+      have = need;
+    }
+    GemmArgs a;
+    a.M = M; a.N = N; a.K = K; a.A = d_A; a.lda = lda; a.B = d_B; a.ldb = ldb; a.bias = d_bias;
+    a.R = d_R; a.ldr = ldr; a.C = d_C; a.ldc = ldc; a.relu = relu;
+    a.tile_n = 64; a.splits = sp; a.ws = ws; a.counters = cnt;
+    gemm<__half>(a, (cudaStream_t)stream);
   });
 }
 

@@ -96,6 +96,8 @@ struct nmt_model {
   long long* boff = nullptr;
   int* blen = nullptr;
   int* sent_ids = nullptr;
+  float* gemm_ws = nullptr;   // split-K partials of the decode GEMMs
+  int* gemm_cnt = nullptr;    // split-K arrival counters (self-resetting)
   // pinned host staging
   struct Pinned {
     int* src; int* len; int* cap; long long* boff; int* blen; int* sent; int* out_tok; int* gen_len;

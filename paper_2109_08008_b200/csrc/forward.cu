@@ -61,6 +61,16 @@ GemmArgs mk(int M, int N, int K, const void* A, int lda, const void* B, int ldb,
 
 template <class T> const T* cT(const void* p) { return static_cast<const T*>(p); }
 
+// Decode-size GEMM (rows = live batch rows): 64-wide output tiles and a fixed split-K
+// factor that depends on the weight shape only (batch invariance), see gemm_tc.cu.
+GemmArgs dec_cfg(nmt_model* m, GemmArgs a) {
+  a.tile_n = 64;
+  a.splits = decode_splits(a.N, a.K);
+  a.ws = m->gemm_ws;
+  a.counters = m->gemm_cnt;
+  return a;
+}
+
 template <class T>
 void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
   const nmt_config& c = m->cfg;
@@ -152,32 +162,32 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
            layernorm<T>(g, d, cT<T>(w.self_g), cT<T>(w.self_b), du, d, R, d, eps, dR, s));
     GemmArgs a = mk(R, 3 * d, d, du, d, w.qkv_w, d, w.qkv_b, dqkv, 3 * d);
     a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
          attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, cT<T>(w.relk), cT<T>(w.relv), dout,
                               R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s));
     a = mk(R, d, d, dout, d, w.so_w, d, w.so_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_LN, 0, 2 * row,
          layernorm<T>(g, d, cT<T>(w.cross_g), cT<T>(w.cross_b), du, d, R, d, eps, dR, s));
     a = mk(R, d, d, du, d, w.cq_w, d, w.cq_b, dq, d);
     a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
          attn_cross<T>(dq, (const T*)m->ckv, Ld * 2 * d, l * 2 * d, l * 2 * d + d, &m->st->S,
                        c.max_src_len, m->src_len, m->row_slot, dout, R, d, H, dR, s));
     a = mk(R, d, d, dout, d, w.co_w, d, w.co_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_LN, 0, 2 * row,
          layernorm<T>(g, d, cT<T>(w.ffn_g), cT<T>(w.ffn_b), du, d, R, d, eps, dR, s));
     a = mk(R, F, d, du, d, w.w1, d, w.b1, dh, F);
     a.relu = 1; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     a = mk(R, d, F, dh, F, w.w2, F, w.b2, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
-    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
   }
   PROF(P_DEC_LN, 0, 2 * row,
        layernorm<T>(g, d, cT<T>(m->dec_fg), cT<T>(m->dec_fb), du, d, R, d, eps, dR, s));

@@ -1,10 +1,19 @@
 // gemm_tc.cu — FP16 tensor-core GEMM for sm_100a: tcgen05.mma (kind::f16, FP32 accumulator
 // in TMEM), operands staged by TMA (cp.async.bulk.tensor, 128B swizzle) through an
-// mbarrier ring, warp-specialised (TMA producer / single-thread MMA issuer / TMEM
-// allocator / 4 epilogue warps).  C[M][N] = A[M][K] . B[N][K]^T with fused epilogues:
-// bias, residual add, ReLU, FP16 store, or the vocab argmax (packed atomicMax, no
-// logits written).  Every projection of the path is one of these
-// (QKV / out / FFN / cross-K/V / decoder / tied vocab projection).
+// mbarrier ring.  Persistent and warp-specialised:
+//   warp 0     TMA producer (one elected thread)
+//   warp 1     MMA issuer (one thread), double-buffered TMEM accumulators so the
+//              epilogue of unit i overlaps the main loop of unit i+1
+//   warp 2     TMEM allocator
+//   warps 4..7 epilogue: TMEM -> registers (tcgen05.ld) -> fused bias / residual / ReLU /
+//              FP16 store, or the vocab argmax (packed atomicMax; logits never stored,
+//              PAPER.md:143)
+// C[M][N] = A[M][K] . B[N][K]^T.  Every projection of the path is one of these (QKV / out /
+// FFN / cross-K/V / decoder / tied vocab projection).
+// Optional deterministic split-K (decode GEMMs have few rows and few output tiles): every
+// split writes an FP32 partial; the last split to arrive for a tile (atomic counter) sums
+// the partials in split order 0..S-1 and runs the epilogue, so results do not depend on
+// which CTA finishes last nor on the number of rows (batch invariance).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -20,7 +29,7 @@ namespace tc {
 constexpr int BM = 128;       // UMMA M (cta_group::1): one TMEM lane per output row
 constexpr int BK = 64;        // 64 halves = 128 B = one swizzle-128B atom row
 constexpr int UMMA_K = 16;    // K per tcgen05.mma for 16-bit inputs
-constexpr int kThreads = 256; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4..7 epilogue
+constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -32,6 +41,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -96,6 +108,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// Plain (coherent) load: the residual may alias the output (in-place x += f(x)).
+__device__ __forceinline__ void load8h(const __half* p, float* f) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 x = __half22float2(h[e]);
+    f[2 * e] = x.x;
+    f[2 * e + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 struct Params {
   int M, N, K;
@@ -108,6 +132,9 @@ struct Params {
   const int* dM;
   unsigned long long* argmax;
   float* logits;
+  int splits;         // split-K factor (kb_total % splits == 0)
+  float* ws;          // split-K partials [tile][split][BM][BN]
+  int* counters;      // split-K arrival counters [tile] (self-resetting)
 };
 
 template <int BN, int STAGES>
@@ -118,32 +145,115 @@ struct Smem {
   static constexpr int BYTES = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
+// Epilogue for 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators).
+__device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float* v,
+                                           unsigned long long& best) {
+  const int nv = min(32, p.N - nb);
+  const bool full = nv == 32;
+  if (p.bias) {
+    if (full) {
+#pragma unroll
+      for (int j8 = 0; j8 < 4; ++j8) {
+        float f[8];
+        load8h(p.bias + nb + j8 * 8, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[j8 * 8 + e] += f[e];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) v[j] += __half2float(p.bias[nb + j]);
+    }
+  }
+  if (p.R) {
+    const __half* rr = p.R + (size_t)m * p.ldr + nb;
+    if (full && ((reinterpret_cast<uintptr_t>(rr) & 15) == 0)) {
+#pragma unroll
+      for (int j8 = 0; j8 < 4; ++j8) {
+        float f[8];
+        load8h(rr + j8 * 8, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[j8 * 8 + e] += f[e];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) v[j] += __half2float(rr[j]);
+    }
+  }
+  if (p.relu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  if (p.logits) {
+    float* lr = p.logits + (size_t)m * p.N + nb;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) lr[j] = v[j];
+  }
+  if (p.argmax) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) {
+        const unsigned long long k = pack_argmax(v[j], nb + j);
+        best = k > best ? k : best;
+      }
+    return;
+  }
+  __half* cr = p.C + (size_t)m * p.ldc + nb;
+  if (full && ((reinterpret_cast<uintptr_t>(cr) & 15) == 0)) {
+#pragma unroll
+    for (int j8 = 0; j8 < 4; ++j8) {
+      uint4 pk;
+      __half2* h2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __halves2half2(from_f<__half>(v[j8 * 8 + 2 * e]), from_f<__half>(v[j8 * 8 + 2 * e + 1]));
+      reinterpret_cast<uint4*>(cr)[j8] = pk;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) cr[j] = from_f<__half>(v[j]);
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               Params p) {
   using SM = Smem<BN, STAGES>;
-  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                 : 2 * BN <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;       // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int M = p.dM ? min(p.M, *p.dM) : p.M;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= M) return;  // uniform for the CTA: live-row count read on the device
+  const int num_m = (M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
+  const int S = p.splits;
+  const int units = num_m * num_n * S;
+  const int kb_total = (p.K + BK - 1) / BK;
+  const int kps = kb_total / S;
+  if ((int)blockIdx.x >= units) return;  // uniform: nothing for this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -161,15 +271,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * SM::STAGE;
-        uint8_t* sb = sa + SM::A_BYTES;
-        mbar_expect_tx(&full[s], SM::STAGE);
-        tma_load_2d(sa, &mapA, &full[s], kb * BK, m0);
-        tma_load_2d(sb, &mapB, &full[s], kb * BK, n0);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int s = u % S, rest = u / S;
+        const int m0 = (rest % num_m) * BM, n0 = (rest / num_m) * BN;
+        for (int kb = s * kps; kb < (s + 1) * kps; ++kb, ++it) {
+          const int st = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* sa = smem + st * SM::STAGE;
+          mbar_expect_tx(&full[st], SM::STAGE);
+          tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
+          tma_load_2d(sa + SM::A_BYTES, &mapB, &full[st], kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -178,82 +292,111 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  | (0u << 7) | (0u << 10)          // A, B = F16
                                  | ((uint32_t)(BN >> 3) << 17)     // N
                                  | ((uint32_t)(BM >> 4) << 24);    // M
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, local = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+        const int s = u % S;
+        const int acc = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);   // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = make_desc_sw128(smem + s * SM::STAGE);
-        const uint64_t db = make_desc_sw128(smem + s * SM::STAGE + SM::A_BYTES);
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int kb = s * kps, first = 1; kb < (s + 1) * kps; ++kb, ++it, first = 0) {
+          const int st = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = make_desc_sw128(smem + st * SM::STAGE);
+          const uint64_t db = make_desc_sw128(smem + st * SM::STAGE + SM::A_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / UMMA_K; ++kk)  // +32 B along K inside the swizzle atom
-          mma_f16(tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
-        mma_commit(&empty[s]);  // frees the stage when these MMAs complete
-      }
-      mma_commit(tmem_full);
-    }
-  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> registers -> global
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;  // TMEM lanes 32q..32q+31
-    const int m = m0 + q * 32 + lane;
-    const bool row_ok = m < M;
-    unsigned long long best = 0ull;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      __syncwarp();  // tcgen05.ld is warp-collective (.sync.aligned)
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-      const int nb = n0 + c0;
-      if (!row_ok || nb >= p.N) continue;
-      const int nv = min(32, p.N - nb);
-      if (p.bias) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) v[j] += __half2float(p.bias[nb + j]);
-      }
-      if (p.R) {
-        const __half* rr = p.R + (size_t)m * p.ldr + nb;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) v[j] += __half2float(rr[j]);
-      }
-      if (p.relu) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-      }
-      if (p.logits) {
-        float* lr = p.logits + (size_t)m * p.N + nb;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) lr[j] = v[j];
-      }
-      if (p.argmax) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) {
-            unsigned long long k = pack_argmax(v[j], nb + j);
-            best = k > best ? k : best;
-          }
-      } else {
-        __half* cr = p.C + (size_t)m * p.ldc + nb;
-        if (nv == 32 && ((reinterpret_cast<uintptr_t>(cr) & 15) == 0)) {
-#pragma unroll
-          for (int j8 = 0; j8 < 4; ++j8) {
-            uint4 pk;
-            __half2* h2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              h2[e] = __halves2half2(from_f<__half>(v[j8 * 8 + 2 * e]),
-                                     from_f<__half>(v[j8 * 8 + 2 * e + 1]));
-            reinterpret_cast<uint4*>(cr)[j8] = pk;
-          }
-        } else {
-          for (int j = 0; j < nv; ++j) cr[j] = from_f<__half>(v[j]);
+          for (int kk = 0; kk < BK / UMMA_K; ++kk)  // +32 B along K inside the swizzle atom
+            mma_f16(d, da + 2 * kk, db + 2 * kk, idesc, (first == 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[st]);  // frees the stage when these MMAs complete
         }
+        mma_commit(&tfull[acc]);
       }
     }
-    if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
+  } else if (warp >= 4) {  // ---------------- epilogue
+    const int q = warp & 3;  // TMEM lanes 32q..32q+31
+    int local = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+      const int s = u % S, rest = u / S, tile = rest;
+      const int m0 = (rest % num_m) * BM, n0 = (rest / num_m) * BN;
+      const int acc = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int r = q * 32 + lane;
+      const int m = m0 + r;
+      const bool row_ok = m < M;
+      const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      if (S == 1) {
+        unsigned long long best = 0ull;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          if (c0 + 32 >= BN) {  // accumulator fully read: hand it back to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          if (row_ok && n0 + c0 < p.N) epilogue32(p, m, n0 + c0, v, best);
+        }
+        if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
+      } else {
+        // split-K: FP32 partial -> workspace, last arrival reduces in split order
+        float* wsp = p.ws + ((size_t)tile * S + s) * BM * BN + (size_t)r * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          if (c0 + 32 >= BN) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(wsp + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          }
+        }
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) {
+          const int old = atomicAdd(p.counters + tile, 1);
+          const int last = (old == S - 1);
+          if (last) p.counters[tile] = 0;  // self-reset for the next launch / graph replay
+          *s_flag = last;
+        }
+        epi_bar();
+        if (*s_flag) {
+          __threadfence();
+          unsigned long long best = 0ull;
+          const float* w0 = p.ws + (size_t)tile * S * BM * BN + (size_t)r * BN;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            if (!row_ok || n0 + c0 >= p.N) continue;
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            for (int sp = 0; sp < S; ++sp) {
+              const float* src = w0 + (size_t)sp * BM * BN + c0;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
+                v[j] += f.x; v[j + 1] += f.y; v[j + 2] += f.z; v[j + 3] += f.w;
+              }
+            }
+            epilogue32(p, m, n0 + c0, v, best);
+          }
+          if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
+        }
+        epi_bar();  // s_flag reused by the next unit
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -294,7 +437,19 @@ struct MapKeyHash {
   }
 };
 
-CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows);
+CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
 
 // Tensor maps are pure functions of (pointer, shape, box): cache them (the arena and the
 // weights never move), so a steady-state launch does no host-side encoding.
@@ -311,18 +466,14 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows) 
   return m;
 }
 
-CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
-  CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
-                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
-  return m;
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    NMT_CUDA(cudaGetDevice(&dev));
+    NMT_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
 }
 
 template <int BN, int STAGES>
@@ -334,6 +485,10 @@ void launch(const GemmArgs& a, cudaStream_t s) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     attr = true;
   }
+  const int splits = a.splits > 0 ? a.splits : 1;
+  const int kb_total = (a.K + BK - 1) / BK;
+  if (kb_total % splits) throw CudaError("gemm_tc: K blocks not divisible by splits");
+  if (splits > 1 && (!a.ws || !a.counters)) throw CudaError("gemm_tc: split-K needs workspace");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN);
   Params p;
@@ -347,20 +502,36 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.dM = a.dM;
   p.argmax = a.argmax;
   p.logits = a.logits;
-  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM));
+  p.splits = splits;
+  p.ws = a.ws;
+  p.counters = a.counters;
+  const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN) * splits;
+  const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
   k_gemm_tc<BN, STAGES><<<grid, kThreads, SM::BYTES, s>>>(ma, mb, p);
   NMT_LAUNCH_CHECK();
 }
 
 }  // namespace tc
 
+int decode_splits(int N, int K) {
+  const int kb = (K + tc::BK - 1) / tc::BK, n_tiles = (N + 63) / 64;
+  int sp = 1;
+  while (sp * 2 <= 8 && kb % (sp * 2) == 0 && kb / (sp * 2) >= 2 && n_tiles * sp < 64) sp *= 2;
+  return sp;
+}
+
 void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
   if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||
       (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
     throw CudaError("gemm_tc: K / leading dims must be multiples of 8 and 16-B aligned");
-  if (a.argmax) tc::launch<256, 3>(a, s);
-  else tc::launch<128, 4>(a, s);
+  if (a.argmax) {
+    tc::launch<256, 3>(a, s);
+  } else if (a.tile_n == 64) {
+    tc::launch<64, 4>(a, s);
+  } else {
+    tc::launch<128, 4>(a, s);
+  }
 }
 
 }  // namespace nmt

@@ -25,7 +25,17 @@ struct GemmArgs {
   const int* dM = nullptr;
   unsigned long long* argmax = nullptr;
   float* logits = nullptr;
+  // tcgen05 path only: output tile width (128, or 64 for decode-size GEMMs) and a
+  // deterministic split-K factor with its FP32 workspace / self-resetting counters.
+  int tile_n = 128;
+  int splits = 1;
+  float* ws = nullptr;
+  int* counters = nullptr;
 };
+
+// Split-K factor for a decode-size GEMM of shape (N, K) with 64-wide tiles: a function of
+// the weight shape only (never of the live-row count), so results are batch invariant.
+int decode_splits(int N, int K);
 
 template <class T> void gemm_simt(const GemmArgs& a, cudaStream_t s);
 void gemm_tc(const GemmArgs& a, cudaStream_t s);   // FP16 tcgen05 / TMEM / TMA

@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INPUT", 4: "E_STATE", 5: "E_F
 EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_batch_encoder_output", "nmt_decode_step", "nmt_prune_batch", "nmt_batch_live",
            "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
-           "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile"]
+           "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode"]
 
 
 class ProfEntry(C.Structure):
@@ -239,6 +239,18 @@ def dev_gemm(A, B, bias=None, R=None, relu=False, out=None, stream=None):
     _check(lib().nmt_dev_gemm(prec, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(bias),
                               _ptr(R), 0 if R is None else R.stride(0), _ptr(C_), C_.stride(0),
                               int(relu), _stream(stream)))
+    return C_
+
+
+def dev_gemm_decode(A, B, bias=None, R=None, relu=False, out=None, stream=None):
+    """FP16 GEMM in the decode-step configuration (64-wide tiles, deterministic split-K)."""
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    C_ = out if out is not None else torch.empty(M, N, dtype=A.dtype, device=A.device)
+    _check(lib().nmt_dev_gemm_decode(M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(bias),
+                                     _ptr(R), 0 if R is None else R.stride(0), _ptr(C_), C_.stride(0),
+                                     int(relu), _stream(stream)))
     return C_
 
 

@@ -40,6 +40,29 @@ def test_gemm_unit(prec, M, N, K):
     assert float(((out - r).abs() / (r.abs() + 1)).max()) <= (1e-5 if prec == "fp32" else 2e-3)
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 1536, 512), (148, 512, 512), (148, 2048, 512), (300, 512, 2048),
+                                   (512, 1536, 512), (37, 64, 64), (9, 256, 64)])
+def test_gemm_decode_splitk_unit(M, N, K):
+    """Decode configuration: 64-wide tiles + deterministic split-K (last CTA reduces)."""
+    from paper_2109_08008_b200 import dev_gemm_decode, dev_gemm
+    g = torch.Generator().manual_seed(M + 3 * N + K)
+    A = (torch.randn(M, K, generator=g) / 2).half()
+    B = (torch.randn(N, K, generator=g) / K ** 0.5).half()
+    bias = (torch.randn(N, generator=g) * 0.1).half()
+    R = torch.randn(M, N, generator=g).half()
+    ref = A.double() @ B.double().T + bias.double() + R.double()
+    for relu in (False, True):
+        r = ref.clamp_min(0) if relu else ref
+        out = dev_gemm_decode(A.cuda(), B.cuda(), bias.cuda(), R.cuda(), relu=relu)
+        assert float(((out.double().cpu() - r).abs() / (r.abs() + 1)).max()) <= 2e-3
+        again = dev_gemm_decode(A.cuda(), B.cuda(), bias.cuda(), R.cuda(), relu=relu)
+        assert torch.equal(out, again)                      # deterministic reduction order
+    # rows are independent of the other rows (batch invariance of the split policy)
+    full = dev_gemm_decode(A.cuda(), B.cuda(), bias.cuda(), R.cuda())
+    part = dev_gemm_decode(A[: max(1, M // 3)].cuda(), B.cuda(), bias.cuda(), R[: max(1, M // 3)].cuda())
+    assert torch.equal(full[: max(1, M // 3)], part)
+
+
 @pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("M,N", [(1, 1000), (148, 32000), (513, 32000), (5, 8)])
 def test_gemm_argmax_unit(prec, M, N):
