@@ -92,10 +92,42 @@ __global__ void __launch_bounds__(256) k_attn_enc(const T* __restrict__ qkv,
       sAV[r * DH + c] = to_f(relv[idx]);
     }
   __syncthreads();
-  // phase 1: raw scores q_i . k_j and q_i . A^K[r] for every pair
-  for (int idx = tid; idx < n * n; idx += nt) {
-    const int i = idx / n, j = idx - i * n;
-    sP[i * LP + j] = dot_ss<DH>(sQ + i * LQ, sK + j * LQ);
+  // phase 1: raw scores q_i . k_j for every pair, 4x4 register tiles (rows i = ib + r*n4,
+  // cols j = jb + s*n4 so a warp's K rows are consecutive -> conflict-free) and
+  // q_i . A^K[r] for every (i, r)
+  const int n4 = (n + 3) >> 2;
+  for (int idx = tid; idx < n4 * n4; idx += nt) {
+    const int ib = idx / n4, jb = idx - ib * n4;
+    const float* qa[4];
+    const float* kb[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      qa[r] = sQ + min(ib + r * n4, n - 1) * LQ;
+      kb[r] = sK + min(jb + r * n4, n - 1) * LQ;
+    }
+    float acc[4][4] = {};
+#pragma unroll 8
+    for (int c = 0; c < DH; ++c) {
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        a[r] = qa[r][c];
+        b[r] = kb[r][c];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) acc[r][s2] = fmaf(a[r], b[s2], acc[r][s2]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = ib + r * n4;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        const int j = jb + s2 * n4;
+        if (i < n && j < n) sP[i * LP + j] = acc[r][s2];
+      }
+    }
   }
   if (use_rpr)
     for (int idx = tid; idx < n * R; idx += nt) {
@@ -148,27 +180,54 @@ __global__ void __launch_bounds__(256) k_attn_enc(const T* __restrict__ qkv,
     }
   }
   __syncthreads();
-  // phase 3: o_i[c] = sum_j a_ij v_j[c] + sum_r B_ir A^V[r][c]  (every (i, c) in parallel)
+  // phase 3: o_i[c] = sum_j a_ij v_j[c] + sum_r B_ir A^V[r][c]; 4 rows x 4 channels per
+  // thread (rows i = ib + r*n4, channels c = cb + k*DH/4: a warp reads consecutive V columns)
   T* obase = out + (size_t)b * S * d + h * DH;
-  for (int idx = tid; idx < S * DH; idx += nt) {
-    const int i = idx / DH, c = idx - i * DH;
-    float o = 0.f;
-    if (i < n) {
-      const float* p = sP + i * LP;
-      float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-      int j = 0;
-      for (; j + 3 < n; j += 4) {
-        o0 = fmaf(p[j], sV[j * DH + c], o0);
-        o1 = fmaf(p[j + 1], sV[(j + 1) * DH + c], o1);
-        o2 = fmaf(p[j + 2], sV[(j + 2) * DH + c], o2);
-        o3 = fmaf(p[j + 3], sV[(j + 3) * DH + c], o3);
-      }
-      for (; j < n; ++j) o0 = fmaf(p[j], sV[j * DH + c], o0);
-      o = (o0 + o1) + (o2 + o3);
-      if (use_rpr)
-        for (int r = 0; r < R; ++r) o = fmaf(sB[i * LB + r], sAV[r * DH + c], o);
+  constexpr int CQ = DH / 4;
+  for (int idx = tid; idx < n4 * CQ; idx += nt) {
+    const int ib = idx / CQ, cb = idx - ib * CQ;
+    const float* pr[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) pr[r] = sP + min(ib + r * n4, n - 1) * LP;
+    float acc[4][4] = {};
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+      float pv[4], vv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pv[r] = pr[r][j];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) vv[k] = sV[j * DH + cb + k * CQ];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[r][k] = fmaf(pv[r], vv[k], acc[r][k]);
     }
-    obase[(size_t)i * d + c] = from_f<T>(o);  // padding query rows -> 0
+    if (use_rpr) {
+      for (int rr = 0; rr < R; ++rr) {
+        float bv[4], av[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) bv[r] = sB[min(ib + r * n4, n - 1) * LB + rr];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) av[k] = sAV[rr * DH + cb + k * CQ];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[r][k] = fmaf(bv[r], av[k], acc[r][k]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = ib + r * n4;
+      if (i < n) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) obase[(size_t)i * d + cb + k * CQ] = from_f<T>(acc[r][k]);
+      }
+    }
+  }
+  // padding query rows -> 0 (finite inputs for the following GEMM / LN)
+  for (int idx = n * DH + tid; idx < S * DH; idx += nt) {
+    const int i = idx / DH, c = idx - i * DH;
+    obase[(size_t)i * d + c] = from_f<T>(0.f);
   }
 }
 

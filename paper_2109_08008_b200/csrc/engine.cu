@@ -262,7 +262,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
                   lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1,
               NMT_E_ARG, "bad limits");
   NMT_REQUIRE(lim->beam == 1, NMT_E_UNSUPPORTED, "beam > 1 is not built in this version");
-  NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 4096, NMT_E_ARG, "max_sents*beam > 4096");
+  NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 16384, NMT_E_ARG, "max_sents*beam > 16384");
 
   std::unique_ptr<nmt_model> m(new nmt_model());
   m->cfg = cfg;

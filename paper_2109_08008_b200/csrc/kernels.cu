@@ -360,13 +360,12 @@ __device__ int block_excl_scan(int v, int* total) {
   return warp_tot[warp] + incl - v;
 }
 
-constexpr int kPruneMaxRows = 4096;
+constexpr int kPrunePer = 16;                   // rows per thread held in registers
+constexpr int kPruneMaxRows = 1024 * kPrunePer;  // 16384
 
 __global__ void __launch_bounds__(1024) k_prune(DevState* st, int* row_slot, int* prev_tok,
                                                 uint8_t* done, int every, float ratio,
                                                 int* new_to_old) {
-  __shared__ int s_slot[kPruneMaxRows];
-  __shared__ int s_tok[kPruneMaxRows];
   __shared__ int s_total;
   const int n = st->n_live, nd = st->n_done, t = st->t;
   bool all_done = (n > 0 && nd == n);
@@ -384,23 +383,34 @@ __global__ void __launch_bounds__(1024) k_prune(DevState* st, int* row_slot, int
     if (threadIdx.x == 0) st->t = t + 1;
     return;
   }
-  // each thread owns a contiguous chunk of rows
+  // each thread owns a contiguous chunk of <= kPrunePer rows, read into registers before
+  // the scan's barrier so the stable in-place compaction cannot overwrite unread rows
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int lo = threadIdx.x * per, hi = min(n, lo + per);
+  int r_slot[kPrunePer], r_tok[kPrunePer];
+  unsigned keepmask = 0;
   int keep = 0;
-  for (int i = lo; i < hi; ++i) {
-    s_slot[i] = row_slot[i];
-    s_tok[i] = prev_tok[i];
-    keep += done[i] ? 0 : 1;
+#pragma unroll
+  for (int k = 0; k < kPrunePer; ++k) {
+    const int i = lo + k;
+    if (i < hi) {
+      r_slot[k] = row_slot[i];
+      r_tok[k] = prev_tok[i];
+      if (!done[i]) {
+        keepmask |= 1u << k;
+        ++keep;
+      }
+    }
   }
   int base = block_excl_scan(keep, &s_total);
   __syncthreads();
   int o = base;
-  for (int i = lo; i < hi; ++i) {
-    if (!done[i]) {
-      row_slot[o] = s_slot[i];
-      prev_tok[o] = s_tok[i];
-      if (new_to_old) new_to_old[o] = i;
+#pragma unroll
+  for (int k = 0; k < kPrunePer; ++k) {
+    if (keepmask & (1u << k)) {
+      row_slot[o] = r_slot[k];
+      prev_tok[o] = r_tok[k];
+      if (new_to_old) new_to_old[o] = lo + k;
       ++o;
     }
   }
