@@ -248,10 +248,273 @@ void launch_enc(const T* qkv, const int* len, const T* relk, const T* relv, T* o
   NMT_LAUNCH_CHECK();
 }
 
+// ----------------------------------------------------------------- encoder, FP16 tensor cores
+// Same computation for the FP16 path with warp-level mma.sync (m16n8k16, FP16 in / FP32
+// accumulate): S = Q K^T and O = P V on tensor cores, the RPR terms q . A^K[r] and
+// sum_r B_ir A^V[r] in FP32 SIMT.  Scores, softmax and bucket sums stay in registers
+// (FP32); P is rounded to FP16 only as the A operand of P V (within the FP16-mode
+// tolerance).  One CTA per (sentence, head), 4 warps, each owning 16-query blocks.
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int DH, int NT>  // NT = number of 8-wide key tiles (Sp = 8*NT, multiple of 16)
+__global__ void __launch_bounds__(128) k_attn_enc_mma(const __half* __restrict__ qkv,
+                                                      const int* __restrict__ len,
+                                                      const __half* __restrict__ relk,
+                                                      const __half* __restrict__ relv,
+                                                      __half* __restrict__ out, int S, int d,
+                                                      int kclip, int use_rpr) {
+  constexpr int SP = NT * 8, LDH = DH + 8;  // padded row (16-B multiple, conflict-free ldmatrix)
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __half* sQ = reinterpret_cast<__half*>(smraw);   // [SP][LDH]
+  __half* sK = sQ + SP * LDH;                       // [SP][LDH]
+  __half* sV = sK + SP * LDH;                       // [SP][LDH]
+  float* sAK = reinterpret_cast<float*>(sV + SP * LDH);  // [R][DH]
+  float* sAV = sAK + 32 * DH;                             // [R][DH]
+  float* sQA = sAV + 32 * DH;                             // [SP][R+1]
+  float* sB = sQA + SP * 33;                              // [SP][R+1]
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int R = 2 * kclip + 1, LB = 33;
+  const int n = len[b];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t rs = 3 * (size_t)d;
+  const __half* base = qkv + (size_t)b * S * rs + h * DH;
+  // stage Q, K, V (zero rows >= n) and the relative tables
+  for (int idx = tid; idx < SP * (DH / 8); idx += 128) {
+    const int j = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
+    uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
+    if (j < n) {
+      const __half* rp = base + (size_t)j * rs + c;
+      q = *reinterpret_cast<const uint4*>(rp);
+      k = *reinterpret_cast<const uint4*>(rp + d);
+      v = *reinterpret_cast<const uint4*>(rp + 2 * d);
+    }
+    *reinterpret_cast<uint4*>(sQ + j * LDH + c) = q;
+    *reinterpret_cast<uint4*>(sK + j * LDH + c) = k;
+    *reinterpret_cast<uint4*>(sV + j * LDH + c) = v;
+  }
+  if (use_rpr) {
+    for (int idx = tid; idx < R * DH; idx += 128) {
+      sAK[idx] = __half2float(relk[idx]);
+      sAV[idx] = __half2float(relv[idx]);
+    }
+    for (int idx = tid; idx < SP * LB; idx += 128) sB[idx] = 0.f;
+  }
+  __syncthreads();
+  if (use_rpr)  // q_i . A^K[r] (FP32 SIMT)
+    for (int idx = tid; idx < n * R; idx += 128) {
+      const int i = idx / R, r = idx - i * R;
+      float a = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < DH; ++c) a = fmaf(__half2float(sQ[i * LDH + c]), sAK[r * DH + c], a);
+      sQA[i * LB + r] = a;
+    }
+  __syncthreads();
+  const float scale = rsqrtf((float)DH);
+  const int g = lane >> 2, tig = lane & 3;
+  const int nblk = (n + 15) >> 4;
+  for (int mb = warp; mb < nblk; mb += 4) {
+    const int m0 = mb * 16;
+    // ---- S = Q K^T for rows m0..m0+15, all SP key columns
+    float sc[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+#pragma unroll
+    for (int k0 = 0; k0 < DH; k0 += 16) {
+      uint32_t af[4];
+      {
+        const int mi = lane >> 3, rr = lane & 7;
+        ldsm_x4(af, sQ + (m0 + rr + (mi & 1) * 8) * LDH + k0 + (mi >> 1) * 8);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; t += 2) {
+        uint32_t bf[4];  // matrices (t, k0) (t, k0+8) (t+1, k0) (t+1, k0+8)
+        const int mi = lane >> 3, rr = lane & 7;
+        ldsm_x4(bf, sK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
+        mma16816(sc[t], af, bf[0], bf[1]);
+        mma16816(sc[t + 1], af, bf[2], bf[3]);
+      }
+    }
+    // ---- RPR key term, mask, scale, softmax (rows r0 = m0+g, r1 = m0+g+8)
+    const int r0 = m0 + g, r1 = r0 + 8;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = e < 2 ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
+        float v = sc[t][e];
+        if (j < n && i < n) {
+          if (use_rpr) v += sQA[i * LB + min(max(j - i, -kclip), kclip) + kclip];
+          v *= scale;
+        } else {
+          v = -INFINITY;
+        }
+        sc[t][e] = v;
+        if (e < 2) mx0 = fmaxf(mx0, v);
+        else mx1 = fmaxf(mx1, v);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
+    if (mx1 == -INFINITY) mx1 = 0.f;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = __expf(sc[t][e] - (e < 2 ? mx0 : mx1));
+        sc[t][e] = v;
+        if (e < 2) s0 += v;
+        else s1 += v;
+      }
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    const float inv0 = s0 > 0.f ? 1.f / s0 : 0.f, inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
+    float lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool top = e < 2;
+        const int i = top ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
+        const float p = sc[t][e] * (top ? inv0 : inv1);
+        sc[t][e] = p;
+        if (use_rpr && i < n && j < n) {
+          const int dj = j - i;
+          if (dj <= -kclip) { if (top) lo0 += p; else lo1 += p; }
+          else if (dj >= kclip) { if (top) hi0 += p; else hi1 += p; }
+          else sB[i * LB + dj + kclip] = p;  // unique writer per (i, middle bucket)
+        }
+      }
+    if (use_rpr) {
+      lo0 += __shfl_xor_sync(0xffffffffu, lo0, 1); lo0 += __shfl_xor_sync(0xffffffffu, lo0, 2);
+      hi0 += __shfl_xor_sync(0xffffffffu, hi0, 1); hi0 += __shfl_xor_sync(0xffffffffu, hi0, 2);
+      lo1 += __shfl_xor_sync(0xffffffffu, lo1, 1); lo1 += __shfl_xor_sync(0xffffffffu, lo1, 2);
+      hi1 += __shfl_xor_sync(0xffffffffu, hi1, 1); hi1 += __shfl_xor_sync(0xffffffffu, hi1, 2);
+      if (tig == 0) {
+        if (r0 < n) { sB[r0 * LB] = lo0; sB[r0 * LB + R - 1] = hi0; }
+        if (r1 < n) { sB[r1 * LB] = lo1; sB[r1 * LB + R - 1] = hi1; }
+      }
+    }
+    // ---- O = P V (P from registers as FP16 A fragments)
+    float oc[DH / 8][4];
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NT / 2; ++kk) {
+      uint32_t af[4];
+      af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
+      af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
+      af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+      af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 16) {
+        uint32_t bf[4];  // .trans: (j0,c0) (j0+8,c0) (j0,c0+8) (j0+8,c0+8)
+        const int mi = lane >> 3, rr = lane & 7;
+        ldsm_x4_t(bf, sV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+        mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+        mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+      }
+    }
+    __syncwarp();
+    // ---- + sum_r B_ir A^V[r][c], store (rows >= n written as 0)
+    __half* orow0 = out + ((size_t)b * S + r0) * d + h * DH;
+    __half* orow1 = out + ((size_t)b * S + r1) * d + h * DH;
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) {
+      const int c = t * 8 + 2 * tig;
+      float o00 = oc[t][0], o01 = oc[t][1], o10 = oc[t][2], o11 = oc[t][3];
+      if (use_rpr) {
+        for (int r = 0; r < R; ++r) {
+          const float b0 = r0 < n ? sB[r0 * LB + r] : 0.f, b1 = r1 < n ? sB[r1 * LB + r] : 0.f;
+          const float a0 = sAV[r * DH + c], a1 = sAV[r * DH + c + 1];
+          o00 = fmaf(b0, a0, o00); o01 = fmaf(b0, a1, o01);
+          o10 = fmaf(b1, a0, o10); o11 = fmaf(b1, a1, o11);
+        }
+      }
+      if (r0 < S)
+        *reinterpret_cast<__half2*>(orow0 + c) =
+            r0 < n ? __floats2half2_rn(o00, o01) : __floats2half2_rn(0.f, 0.f);
+      if (r1 < S)
+        *reinterpret_cast<__half2*>(orow1 + c) =
+            r1 < n ? __floats2half2_rn(o10, o11) : __floats2half2_rn(0.f, 0.f);
+    }
+  }
+  // query rows beyond the last 16-block are padding: zero them
+  for (int idx = nblk * 16 * DH + tid; idx < S * DH; idx += 128) {
+    const int i = idx / DH, c = idx - i * DH;
+    out[((size_t)b * S + i) * d + h * DH + c] = __float2half(0.f);
+  }
+}
+
+template <int DH>
+void launch_enc_mma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                    __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  const int sp = (S + 15) / 16 * 16;
+  auto smem_for = [](int SP) {
+    return (size_t)3 * SP * (DH + 8) * 2 + 2 * 32 * DH * 4 + 2 * SP * 33 * 4;
+  };
+#define NMT_EM(NTV)                                                                          \
+  {                                                                                          \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_mma<DH, NTV>,                                \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      attr = true;                                                                           \
+    }                                                                                        \
+    k_attn_enc_mma<DH, NTV><<<dim3(B, H), 128, smem_for(NTV * 8), s>>>(qkv, len, relk, relv, \
+                                                                      out, S, d, kclip,       \
+                                                                      use_rpr);               \
+  }
+  if (sp <= 16) NMT_EM(2)
+  else if (sp <= 32) NMT_EM(4)
+  else if (sp <= 48) NMT_EM(6)
+  else if (sp <= 64) NMT_EM(8)
+  else if (sp <= 80) NMT_EM(10)
+  else if (sp <= 96) NMT_EM(12)
+  else if (sp <= 112) NMT_EM(14)
+  else if (sp <= 128) NMT_EM(16)
+  else throw CudaError("attn_encoder: S > 128");
+#undef NMT_EM
+  NMT_LAUNCH_CHECK();
+}
+
 template <class T>
 void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
                   int d, int H, int kclip, int use_rpr, cudaStream_t s) {
   if (B <= 0) return;
+  if constexpr (sizeof(T) == 2) {  // FP16 mode: tensor-core attention
+    switch (d / H) {
+      case 16: launch_enc_mma<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
+      case 32: launch_enc_mma<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
+      case 64: launch_enc_mma<64>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
+      default: throw CudaError("attn_encoder: head dim must be 16, 32 or 64");
+    }
+  }
   switch (d / H) {
     case 16: launch_enc<T, 16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
     case 32: launch_enc<T, 32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
