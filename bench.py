@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--max-tokens", type=int, default=16384)
     ap.add_argument("--max-sents", type=int, default=2048)
     ap.add_argument("--sync-every", type=int, default=4)
+    ap.add_argument("--workers", type=int, default=2,
+                    help="concurrent batch workers per GPU (own arena + stream, shared weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
     ap.add_argument("--ref-sents-per-worker", type=int, default=12)
@@ -226,11 +228,12 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def dev_step(k):
+    def dev_step(k, workers=None):
         wl, d_ids = chunks[k]
         return model.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps,
                                       max_tokens=args.max_tokens, max_sents=args.max_sents,
-                                      sync_every=args.sync_every)
+                                      sync_every=args.sync_every,
+                                      workers=args.workers if workers is None else workers)
 
     for k in range(args.warmup):
         dev_step(k)
@@ -277,7 +280,8 @@ def main():
         for k in range(args.warmup, n_chunks):
             wl, _ = chunks[k]
             outs, st = model.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=args.max_tokens,
-                                       max_sents=args.max_sents, sync_every=args.sync_every)
+                                       max_sents=args.max_sents, sync_every=args.sync_every,
+                                       workers=args.workers)
             g2 += st["gen_tokens"]
             h2d += wl.ids.nbytes
             d2h += 4 * sum(len(o) for o in outs) + 4 * len(outs)
@@ -289,7 +293,7 @@ def main():
 
     # ---- per-kernel-class profile of one more step (CUDA events on the launching stream)
     model.profile(2)
-    st = dev_step(args.warmup)
+    st = dev_step(args.warmup, workers=1)  # per-class events need one stream
     prof = model.profile(0)
     tot = sum(v["ms"] for v in prof.values())
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])

@@ -134,6 +134,8 @@ typedef struct {
   float prune_ratio;     /* rho (0.25); < 0 = never prune                        */
   int32_t sync_every;    /* host polls the live count every k steps (>= 1)       */
   const int32_t* h_tgt_cap; /* optional [n] per-sentence caps (synthetic workloads) */
+  int32_t n_workers;     /* concurrent batch workers (own arena + stream each, shared
+                            weights); 0/1 = one.  Outputs do not depend on it.     */
 } nmt_translate_opts;
 
 typedef struct {

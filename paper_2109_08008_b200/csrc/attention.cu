@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(128) k_attn_enc_mma(const __half* __restrict__
   __half* sK = sQ + SP * LDH;                       // [SP][LDH]
   __half* sV = sK + SP * LDH;                       // [SP][LDH]
   float* sAK = reinterpret_cast<float*>(sV + SP * LDH);  // [R][DH]
-  float* sAV = sAK + 32 * DH;                             // [R][DH]
+  float* sAV = sAK + 32 * (DH + 1);                       // [R][DH]  (sAK rows padded: DH+1)
   float* sQA = sAV + 32 * DH;                             // [SP][R+1]
   float* sB = sQA + SP * 33;                              // [SP][R+1]
   const int b = blockIdx.x, h = blockIdx.y;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(128) k_attn_enc_mma(const __half* __restrict__
   }
   if (use_rpr) {
     for (int idx = tid; idx < R * DH; idx += 128) {
-      sAK[idx] = __half2float(relk[idx]);
+      sAK[(idx / DH) * (DH + 1) + idx % DH] = __half2float(relk[idx]);
       sAV[idx] = __half2float(relv[idx]);
     }
     for (int idx = tid; idx < SP * LB; idx += 128) sB[idx] = 0.f;
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(128) k_attn_enc_mma(const __half* __restrict__
       const int i = idx / R, r = idx - i * R;
       float a = 0.f;
 #pragma unroll 8
-      for (int c = 0; c < DH; ++c) a = fmaf(__half2float(sQ[i * LDH + c]), sAK[r * DH + c], a);
+      for (int c = 0; c < DH; ++c) a = fmaf(__half2float(sQ[i * LDH + c]), sAK[r * (DH + 1) + c], a);
       sQA[i * LB + r] = a;
     }
   __syncthreads();
@@ -476,7 +476,7 @@ void launch_enc_mma(const __half* qkv, const int* len, const __half* relk, const
                     __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
   const int sp = (S + 15) / 16 * 16;
   auto smem_for = [](int SP) {
-    return (size_t)3 * SP * (DH + 8) * 2 + 2 * 32 * DH * 4 + 2 * SP * 33 * 4;
+    return (size_t)3 * SP * (DH + 8) * 2 + 32 * (2 * DH + 1) * 4 + 2 * SP * 33 * 4;
   };
 #define NMT_EM(NTV)                                                                          \
   {                                                                                          \

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -24,7 +25,7 @@ struct CudaError : std::runtime_error {
 
 // Every kernel launch of the library goes through NMT_LAUNCH_CHECK, which also counts
 // it (nmt_stats.launches / bench "gpu_launches").
-extern unsigned long long g_launches;
+extern std::atomic<unsigned long long> g_launches;
 #define NMT_LAUNCH_CHECK()    \
   do {                        \
     ++::nmt::g_launches;      \

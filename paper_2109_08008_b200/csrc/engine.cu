@@ -10,11 +10,13 @@
 #include <cstring>
 #include <memory>
 #include <numeric>
+#include <mutex>
+#include <thread>
 
 #include "engine.h"
 
 namespace nmt {
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
 thread_local std::string g_err;
 }  // namespace nmt
 
@@ -470,6 +472,24 @@ Plan plan_batches(const int64_t* h_off, int64_t n, int max_tokens, int max_sents
   return p;
 }
 
+nmt_model* clone_worker(nmt_model* m) {
+  std::unique_ptr<nmt_model> c(new nmt_model());
+  c->cfg = m->cfg; c->prec = m->prec; c->lim = m->lim; c->device = m->device; c->tb = m->tb;
+  c->wbuf = m->wbuf; c->owns_weights = false;
+  c->W = m->W; c->enc = m->enc; c->dec = m->dec;
+  c->emb = m->emb; c->dl0_g = m->dl0_g; c->dl0_b = m->dl0_b; c->enc_fg = m->enc_fg;
+  c->enc_fb = m->enc_fb; c->dec_fg = m->dec_fg; c->dec_fb = m->dec_fb;
+  c->ckv_w = m->ckv_w; c->ckv_b = m->ckv_b; c->dlcl_w = m->dlcl_w; c->pe = m->pe;
+  init_arena(c.get());
+  NMT_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  return c.release();
+}
+
+// Whole-set driver.  Batches (length-sorted plan) are taken from a shared counter by
+// `n_workers` workers, each a (model-or-clone, stream) pair on its own host thread; worker 0
+// is the model itself on the caller's stream.  load_src(wm, stream, order, B, S, lens)
+// stages the batch sources into wm->src; emit(wm, stream, order, B) consumes the results
+// and returns the batch's generated-token count.
 template <class LoadF, class EmitF>
 void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_translate_opts* o,
                     LoadF load_src, EmitF emit, nmt_stats* st, cudaStream_t s) {
@@ -478,6 +498,7 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   const int every = o && o->prune_every > 0 ? o->prune_every : 1;
   const float ratio = o ? o->prune_ratio : 0.25f;
   const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
+  const int W = o && o->n_workers > 1 ? std::min(o->n_workers, 8) : 1;
   NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
               "translate opts exceed the model limits");
   for (int64_t i = 0; i < n; ++i) {
@@ -486,48 +507,95 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
     NMT_REQUIRE(len <= m->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
                 "source " + std::to_string(i) + " longer than max_src_len");
   }
+  while ((int)m->workers.size() < W - 1) m->workers.push_back(clone_worker(m));
   Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+  const int nb = (int)p.bstart.size() - 1;
   auto t0 = std::chrono::steady_clock::now();
   unsigned long long l0 = g_launches;
-  int64_t steps = 0, prunes = 0;
-  std::vector<int> lens, caps;
-  for (size_t bi = 0; bi + 1 < p.bstart.size(); ++bi) {
-    const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
-    const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
-    lens.resize(B);
-    caps.resize(B);
-    for (int j = 0; j < B; ++j) {
-      int sid = p.order[lo + j];
-      lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
-      caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : m->lim.max_tgt_len;
-    }
-    load_src(&p.order[lo], B, S, lens.data());
-    encode_common(m, B, S, lens.data(), caps.data(), s);
-    nmt_batch& b = m->batch;
-    int rows = B;
-    int t = 0;
-    // the live count is polled every `sync_every` steps (lagged upper bound for grids)
-    for (; t < b.max_cap && rows > 0; ++t) {
-      step_and_prune(m, b, rows, every, ratio, s);
-      if ((t + 1) % sync_every == 0) {
-        poll_state(m, s);
-        rows = m->hp.st->n_live;
+  std::atomic<int> next{0};
+  std::atomic<int64_t> steps{0}, prunes{0}, gen{0};
+  std::atomic<bool> failed{false};
+
+  auto run = [&](nmt_model* wm, cudaStream_t ws) {
+    std::vector<int> lens, caps;
+    for (;;) {
+      const int bi = next++;
+      if (bi >= nb || failed) break;
+      const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
+      const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+      lens.resize(B);
+      caps.resize(B);
+      for (int j = 0; j < B; ++j) {
+        int sid = p.order[lo + j];
+        lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+        caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : wm->lim.max_tgt_len;
       }
+      load_src(wm, ws, &p.order[lo], B, S, lens.data());
+      encode_common(wm, B, S, lens.data(), caps.data(), ws);
+      nmt_batch& b = wm->batch;
+      int rows = B;
+      int t = 0;
+      // the live count is polled every `sync_every` steps (lagged upper bound for grids)
+      for (; t < b.max_cap && rows > 0; ++t) {
+        step_and_prune(wm, b, rows, every, ratio, ws);
+        if ((t + 1) % sync_every == 0) {
+          poll_state(wm, ws);
+          rows = wm->hp.st->n_live;
+        }
+      }
+      poll_state(wm, ws);
+      steps += t;
+      prunes += wm->hp.st->prunes;
+      b.step = t;
+      gen += emit(wm, ws, &p.order[lo], B);
+      b.valid = false;
     }
-    poll_state(m, s);
-    steps += t;
-    prunes += m->hp.st->prunes;
-    b.step = t;
-    emit(b, &p.order[lo], B);
-    b.valid = false;
+  };
+
+  if (W == 1) {
+    run(m, s);
+  } else {
+    cudaEvent_t ev;
+    NMT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    NMT_CUDA(cudaEventRecord(ev, s));  // workers start after prior work on the caller stream
+    for (int w = 0; w < W - 1; ++w) NMT_CUDA(cudaStreamWaitEvent(m->workers[w]->own_stream, ev, 0));
+    std::mutex emu;
+    std::string emsg;
+    nmt_status ecode = NMT_OK;
+    auto guarded = [&](nmt_model* wm, cudaStream_t ws) {
+      try {
+        NMT_CUDA(cudaSetDevice(m->device));
+        run(wm, ws);
+      } catch (const NmtError& e) {
+        std::lock_guard<std::mutex> g(emu);
+        if (ecode == NMT_OK) { ecode = e.code; emsg = e.what(); }
+        failed = true;
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> g(emu);
+        if (ecode == NMT_OK) { ecode = NMT_E_CUDA; emsg = e.what(); }
+        failed = true;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int w = 0; w < W - 1; ++w)
+      th.emplace_back(guarded, m->workers[w], m->workers[w]->own_stream);
+    guarded(m, s);
+    for (auto& t : th) t.join();
+    for (int w = 0; w < W - 1; ++w) {
+      NMT_CUDA(cudaEventRecord(ev, m->workers[w]->own_stream));
+      NMT_CUDA(cudaStreamWaitEvent(s, ev, 0));  // caller stream orders after every worker
+    }
+    NMT_CUDA(cudaEventDestroy(ev));
+    if (ecode != NMT_OK) throw NmtError(ecode, emsg);
   }
   NMT_CUDA(cudaStreamSynchronize(s));
   if (st) {
     st->sentences = n;
     st->src_tokens = h_off[n] - h_off[0];
+    st->gen_tokens = gen;
     st->decode_steps = steps;
     st->prunes = prunes;
-    st->batches = (int64_t)p.bstart.size() - 1;
+    st->batches = nb;
     st->launches = (int64_t)(g_launches - l0);
     st->ms_total =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -664,30 +732,32 @@ nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_of
     const int V = m->cfg.vocab_size, eos = m->cfg.eos_id;
     const int Tm = m->lim.max_tgt_len;
     std::vector<std::vector<int>> outs(n);
-    int64_t gen = 0;
-    auto load_src = [&](const int* order, int B, int S, const int* lens) {
+    auto load_src = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B, int S,
+                        const int* lens) {
       for (int j = 0; j < B; ++j) {
         const int32_t* src = h_ids + h_off[order[j]];
         for (int p = 0; p < S; ++p) {
-          int v = p < lens[j] ? src[p] : m->cfg.pad_id;
+          int v = p < lens[j] ? src[p] : wm->cfg.pad_id;
           NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
-          m->hp.src[(size_t)j * S + p] = v;
+          wm->hp.src[(size_t)j * S + p] = v;
         }
       }
-      NMT_CUDA(cudaMemcpyAsync(m->src, m->hp.src, (size_t)B * S * 4, cudaMemcpyHostToDevice, s));
+      NMT_CUDA(cudaMemcpyAsync(wm->src, wm->hp.src, (size_t)B * S * 4, cudaMemcpyHostToDevice, ws));
     };
-    auto emit = [&](nmt_batch& b, const int* order, int B) {
-      NMT_CUDA(cudaMemcpyAsync(m->hp.out_tok, m->out_tok, (size_t)B * Tm * 4,
-                               cudaMemcpyDeviceToHost, s));
-      NMT_CUDA(cudaMemcpyAsync(m->hp.gen_len, m->gen_len, B * 4, cudaMemcpyDeviceToHost, s));
-      NMT_CUDA(cudaStreamSynchronize(s));
+    auto emit = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B) -> int64_t {
+      NMT_CUDA(cudaMemcpyAsync(wm->hp.out_tok, wm->out_tok, (size_t)B * Tm * 4,
+                               cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaMemcpyAsync(wm->hp.gen_len, wm->gen_len, B * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaStreamSynchronize(ws));
+      int64_t g = 0;
       for (int j = 0; j < B; ++j) {
-        int gl = m->hp.gen_len[j];
-        gen += gl;
-        const int* t = m->hp.out_tok + (size_t)j * Tm;
+        int gl = wm->hp.gen_len[j];
+        g += gl;
+        const int* t = wm->hp.out_tok + (size_t)j * Tm;
         int ol = (gl > 0 && t[gl - 1] == eos) ? gl - 1 : gl;
         outs[order[j]].assign(t, t + ol);
       }
+      return g;
     };
     translate_core(m, h_off, n, opts, load_src, emit, stats, s);
     int64_t pos = 0;
@@ -698,10 +768,7 @@ nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_of
       pos += outs[i].size();
       h_out_off[i + 1] = pos;
     }
-    if (stats) {
-      stats->gen_tokens = gen;
-      stats->out_tokens = pos;
-    }
+    if (stats) stats->out_tokens = pos;
   });
 }
 
@@ -715,29 +782,36 @@ nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_
     cudaStream_t s = (cudaStream_t)stream;
     const int Tm = m->lim.max_tgt_len;
     NMT_CUDA(cudaMemsetAsync(m->bad, 0, 4, s));
-    int64_t gen = 0;
-    auto load_src = [&](const int* order, int B, int S, const int* lens) {
+    for (auto* w : m->workers) NMT_CUDA(cudaMemsetAsync(w->bad, 0, 4, s));
+    auto load_src = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B, int S,
+                        const int* lens) {
       for (int j = 0; j < B; ++j) {
-        m->hp.boff[j] = h_off[order[j]];
-        m->hp.blen[j] = lens[j];
+        wm->hp.boff[j] = h_off[order[j]];
+        wm->hp.blen[j] = lens[j];
       }
-      NMT_CUDA(cudaMemcpyAsync(m->boff, m->hp.boff, B * 8, cudaMemcpyHostToDevice, s));
-      NMT_CUDA(cudaMemcpyAsync(m->blen, m->hp.blen, B * 4, cudaMemcpyHostToDevice, s));
-      pack_sources(d_ids, m->boff, m->blen, B, S, m->src, m->cfg.vocab_size, m->bad, s);
+      NMT_CUDA(cudaMemcpyAsync(wm->boff, wm->hp.boff, B * 8, cudaMemcpyHostToDevice, ws));
+      NMT_CUDA(cudaMemcpyAsync(wm->blen, wm->hp.blen, B * 4, cudaMemcpyHostToDevice, ws));
+      pack_sources(d_ids, wm->boff, wm->blen, B, S, wm->src, wm->cfg.vocab_size, wm->bad, ws);
     };
-    auto emit = [&](nmt_batch& b, const int* order, int B) {
-      for (int j = 0; j < B; ++j) m->hp.sent[j] = order[j];
-      NMT_CUDA(cudaMemcpyAsync(m->sent_ids, m->hp.sent, B * 4, cudaMemcpyHostToDevice, s));
-      scatter_outputs(m->out_tok, Tm, m->gen_len, m->sent_ids, B, d_out, out_stride, d_out_len, s);
-      NMT_CUDA(cudaMemcpyAsync(m->hp.gen_len, m->gen_len, B * 4, cudaMemcpyDeviceToHost, s));
-      NMT_CUDA(cudaStreamSynchronize(s));  // staging buffers are reused by the next batch
-      for (int j = 0; j < B; ++j) gen += m->hp.gen_len[j];
+    auto emit = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B) -> int64_t {
+      for (int j = 0; j < B; ++j) wm->hp.sent[j] = order[j];
+      NMT_CUDA(cudaMemcpyAsync(wm->sent_ids, wm->hp.sent, B * 4, cudaMemcpyHostToDevice, ws));
+      scatter_outputs(wm->out_tok, Tm, wm->gen_len, wm->sent_ids, B, d_out, out_stride, d_out_len,
+                      ws);
+      NMT_CUDA(cudaMemcpyAsync(wm->hp.gen_len, wm->gen_len, B * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaStreamSynchronize(ws));  // staging buffers are reused by the next batch
+      int64_t g = 0;
+      for (int j = 0; j < B; ++j) g += wm->hp.gen_len[j];
+      return g;
     };
     translate_core(m, h_off, n, opts, load_src, emit, stats, s);
-    if (stats) stats->gen_tokens = gen;
-    NMT_CUDA(cudaMemcpyAsync(m->hp.bad, m->bad, 4, cudaMemcpyDeviceToHost, s));
-    NMT_CUDA(cudaStreamSynchronize(s));
-    NMT_REQUIRE(*m->hp.bad == 0, NMT_E_INPUT, "token id out of range in d_ids");
+    int bad = 0;
+    for (nmt_model* wm : [&] { std::vector<nmt_model*> v{m}; for (auto* w : m->workers) v.push_back(w); return v; }()) {
+      NMT_CUDA(cudaMemcpyAsync(wm->hp.bad, wm->bad, 4, cudaMemcpyDeviceToHost, s));
+      NMT_CUDA(cudaStreamSynchronize(s));
+      bad |= *wm->hp.bad;
+    }
+    NMT_REQUIRE(bad == 0, NMT_E_INPUT, "token id out of range in d_ids");
   });
 }
 

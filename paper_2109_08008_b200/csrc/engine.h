@@ -118,10 +118,18 @@ struct nmt_model {
   // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits)
   std::map<std::tuple<int, int, unsigned>, cudaGraphExec_t> graphs;
   bool eager_done = false;  // one eager step ran (kernel attributes set) before capture
+  // Concurrent batch workers (the GPU analog of the paper's parallel decoding processes,
+  // PAPER.md:129-131): clones sharing this model's weights, each with its own arena,
+  // stream, batch state and graphs.  Created lazily by nmt_translate*(n_workers > 1).
+  bool owns_weights = true;
+  std::vector<nmt_model*> workers;
+  cudaStream_t own_stream = nullptr;
   ~nmt_model() {
+    for (auto* w : workers) delete w;
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto e : prof.pool) cudaEventDestroy(e);
-    if (wbuf) cudaFree(wbuf);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (wbuf && owns_weights) cudaFree(wbuf);
     if (ar.base) cudaFree(ar.base);
     if (pinned) cudaFreeHost(pinned);
   }

@@ -48,7 +48,8 @@ class StepOut(C.Structure):
 
 class TranslateOpts(C.Structure):
     _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("prune_every", C.c_int32),
-                ("prune_ratio", C.c_float), ("sync_every", C.c_int32), ("h_tgt_cap", C.c_void_p)]
+                ("prune_ratio", C.c_float), ("sync_every", C.c_int32), ("h_tgt_cap", C.c_void_p),
+                ("n_workers", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -142,7 +143,7 @@ class Model:
         return Batch(self, b, B, S)
 
     def translate(self, ids, off, caps=None, max_tokens=None, max_sents=None, prune_every=1,
-                  prune_ratio=0.25, sync_every=4, stream=None):
+                  prune_ratio=0.25, sync_every=4, workers=1, stream=None):
         """Host-buffer translation (C-ABI nmt_translate). Returns (outputs, stats dict)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         off = np.ascontiguousarray(off, dtype=np.int64)
@@ -150,7 +151,7 @@ class Model:
         capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
         o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
                           prune_every, prune_ratio, sync_every,
-                          None if capa is None else capa.ctypes.data)
+                          None if capa is None else capa.ctypes.data, workers)
         out_cap = n * self.Tmax
         out = np.empty(max(out_cap, 1), dtype=np.int32)
         out_off = np.empty(n + 1, dtype=np.int64)
@@ -163,14 +164,15 @@ class Model:
         return outs, st.as_dict()
 
     def translate_device(self, d_ids, off, d_out, d_out_len, caps=None, max_tokens=None,
-                         max_sents=None, prune_every=1, prune_ratio=0.25, sync_every=4, stream=None):
+                         max_sents=None, prune_every=1, prune_ratio=0.25, sync_every=4, workers=1,
+                         stream=None):
         """Device-resident translation (C-ABI nmt_translate_device); d_out [n][stride]."""
         off = np.ascontiguousarray(off, dtype=np.int64)
         n = len(off) - 1
         capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
         o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
                           prune_every, prune_ratio, sync_every,
-                          None if capa is None else capa.ctypes.data)
+                          None if capa is None else capa.ctypes.data, workers)
         st = Stats()
         _check(lib().nmt_translate_device(self.h, _ptr(d_ids), off.ctypes.data_as(C.c_void_p),
                                           C.c_int64(n), C.byref(o), _ptr(d_out),

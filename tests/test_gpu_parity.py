@@ -244,6 +244,30 @@ def test_translate_host_equals_device_and_steps():
     assert st2["launches"] < st_h["launches"]   # graphs: one launch per decode step
 
 
+def test_concurrent_workers_identical():
+    """n_workers concurrent batch workers (own arena + stream, shared weights) give the
+    same outputs as one worker, on host and device paths."""
+    wl = newstest_like(300, 32000, start=2000)
+    gm = gpu_model("student-6-1", "fp16", max_tokens=1024, max_sents=64)
+    ref, st1 = gm.translate(wl.ids, wl.off, caps=wl.caps)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for w in (2, 3):
+            out, st = gm.translate(wl.ids, wl.off, caps=wl.caps, workers=w)
+            assert out == ref
+            assert st["gen_tokens"] == st1["gen_tokens"] and st["batches"] == st1["batches"]
+        d_ids = torch.from_numpy(wl.ids).cuda()
+        d_out = torch.zeros(wl.n, gm.Tmax, dtype=torch.int32, device="cuda")
+        d_len = torch.zeros(wl.n, dtype=torch.int32, device="cuda")
+        st = gm.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, workers=3)
+    torch.cuda.synchronize()
+    d_out, d_len = d_out.cpu().numpy(), d_len.cpu().numpy()
+    for i in range(wl.n):
+        g = d_out[i, :d_len[i]].tolist()
+        assert (g[:-1] if g and g[-1] == 3 else g) == ref[i]
+    assert st["gen_tokens"] == st1["gen_tokens"]
+
+
 def test_batch_invariance_fp32():
     """Sentence alone == sentence inside a bigger batch (PAPER.md:121 batching is exact)."""
     wl = newstest_like(16, 32000, start=50)
