@@ -206,6 +206,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2109_08008_b200 import Model
+    from paper_2109_08008_b200.dist import chunk_index
 
     model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents)
     # a non-default stream: decode steps are replayed as CUDA graphs (no capture on stream 0)
@@ -215,7 +216,7 @@ def main():
     n_chunks = args.warmup + args.steps
     chunks = []
     for k in range(n_chunks):
-        idx = k * world + rank
+        idx = chunk_index(k, rank, world)   # disjoint chunks per (step, rank): weak scaling
         wl = newstest_like(args.chunk, cfg.vocab_size, start=idx * args.chunk)
         chunks.append((wl, torch.from_numpy(wl.ids).cuda()))
     Tm = model.Tmax
@@ -254,19 +255,9 @@ def main():
     clocks = clk.stop()
     ms = ev0.elapsed_time(ev1)
 
-    def allred(x, op):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=op)
-        return t.item()
-
-    import torch.distributed as tdist
-    MAX = tdist.ReduceOp.MAX if world > 1 else None
-    SUM = tdist.ReduceOp.SUM if world > 1 else None
-    ms_max = allred(ms, MAX)
-    gen_all = allred(float(gen), SUM)
-    steps_all = allred(float(steps), SUM)
+    from paper_2109_08008_b200.dist import reduce_timing
+    ms_max, gen_all = reduce_timing(ms, float(gen), device="cuda")   # max over ranks / sum
+    _, steps_all = reduce_timing(ms, float(steps), device="cuda")
     value = gen_all / (ms_max / 1000.0)
 
     # ---- e2e through the host-buffer C-ABI call (H2D + D2H inside the timed region)
@@ -287,8 +278,8 @@ def main():
             d2h += 4 * sum(len(o) for o in outs) + 4 * len(outs)
         e1.record(stream)
         barrier()
-        ems = allred(e0.elapsed_time(e1), MAX)
-        e2e = {"value": allred(float(g2), SUM) / (ems / 1000.0), "unit": UNIT,
+        ems, g2_all = reduce_timing(e0.elapsed_time(e1), float(g2), device="cuda")
+        e2e = {"value": g2_all / (ems / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
     # ---- per-kernel-class profile of one more step (CUDA events on the launching stream)
