@@ -407,6 +407,204 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ cluster split-K
+// Decode-size GEMMs (rows = live batch rows <= a few hundred): one 128 x 64 output tile is
+// computed by a thread-block CLUSTER of S CTAs, CTA s accumulating k-blocks
+// [s*kps, (s+1)*kps) in its own TMEM.  Partials are exchanged through distributed shared
+// memory (no global round trip, no atomics): after a cluster barrier, CTA c reduces rows
+// [c*128/S, (c+1)*128/S) by reading the S partials in split order 0..S-1 (deterministic,
+// independent of the row count) and applies the fused epilogue.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(const float* local_addr, uint32_t rank) {
+  uint32_t a = smem_u32(local_addr), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ra)
+               : "memory");
+  return v;
+}
+
+// Epilogue for 16 consecutive columns (n0 % 16 == 0 assumed for the vector paths).
+__device__ __forceinline__ void epilogue16(const Params& p, int m, int nb, float* v) {
+  const int nv = min(16, p.N - nb);
+  const bool full = nv == 16;
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nv) v[j] += __half2float(p.bias[nb + j]);
+  }
+  if (p.R) {
+    const __half* rr = p.R + (size_t)m * p.ldr + nb;
+    if (full && ((reinterpret_cast<uintptr_t>(rr) & 15) == 0)) {
+      float f[8];
+      load8h(rr, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] += f[e];
+      load8h(rr + 8, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[8 + e] += f[e];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) v[j] += __half2float(rr[j]);
+    }
+  }
+  if (p.relu) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  __half* cr = p.C + (size_t)m * p.ldc + nb;
+  if (full && ((reinterpret_cast<uintptr_t>(cr) & 15) == 0)) {
+#pragma unroll
+    for (int j8 = 0; j8 < 2; ++j8) {
+      uint4 pk;
+      __half2* h2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __halves2half2(from_f<__half>(v[j8 * 8 + 2 * e]), from_f<__half>(v[j8 * 8 + 2 * e + 1]));
+      reinterpret_cast<uint4*>(cr)[j8] = pk;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nv) cr[j] = from_f<__half>(v[j]);
+  }
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tc_cluster(const __grid_constant__ CUtensorMap mapA,
+                      const __grid_constant__ CUtensorMap mapB, Params p) {
+  constexpr int BN = 64;
+  using SM = Smem<BN, STAGES>;
+  constexpr int LDP = BN + 4;  // padded FP32 partial row (conflict-light float4 stores)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  float* part = reinterpret_cast<float*>(smem + STAGES * SM::STAGE);      // [BM][LDP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(part + BM * LDP);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int S = p.splits;
+  const int s = (int)cluster_ctarank();          // split index == rank in the cluster
+  const int tile = blockIdx.x / S;
+  const int num_m = (p.M + BM - 1) / BM;         // grid sized by the host upper bound
+  const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+  const int Meff = p.dM ? min(p.M, *p.dM) : p.M;
+  const bool live = m0 < Meff;                   // uniform across the cluster
+  const int kb_total = (p.K + BK - 1) / BK;
+  const int kps = kb_total / S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (live) {
+    if (warp == 0 && lane == 0) {
+      for (int st = 0; st < STAGES; ++st) {
+        mbar_init(&full[st], 1);
+        mbar_init(&empty[st], 1);
+      }
+      mbar_init(tfull, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    }
+    if (warp == 2) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(64));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int i = 0; i < kps; ++i) {
+          const int kb = s * kps + i, st = i % STAGES;
+          const uint32_t ph = (i / STAGES) & 1;
+          mbar_wait(&empty[st], ph ^ 1);
+          uint8_t* sa = smem + st * SM::STAGE;
+          mbar_expect_tx(&full[st], SM::STAGE);
+          tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
+          tma_load_2d(sa + SM::A_BYTES, &mapB, &full[st], kb * BK, n0);
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+        for (int i = 0; i < kps; ++i) {
+          const int st = i % STAGES;
+          const uint32_t ph = (i / STAGES) & 1;
+          mbar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = make_desc_sw128(smem + st * SM::STAGE);
+          const uint64_t db = make_desc_sw128(smem + st * SM::STAGE + SM::A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk)
+            mma_f16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[st]);
+        }
+        mma_commit(tfull);
+      }
+    } else if (warp >= 4) {  // TMEM -> FP32 partial in this CTA's shared memory
+      mbar_wait(tfull, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int q = warp & 3, r = q * 32 + lane;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        __syncwarp();
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(part + r * LDP + c0 + j) =
+              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  cluster_sync_all();  // every split's partial is in its shared memory
+  if (live) {
+    // CTA s reduces rows [s*BM/S, (s+1)*BM/S) of the tile: (row, 16-column group) per item
+    const int rows = BM / S;
+    for (int it = threadIdx.x; it < rows * (BN / 16); it += kThreads) {
+      const int rr = s * rows + it / (BN / 16), cg = (it % (BN / 16)) * 16;
+      const int m = m0 + rr, nb = n0 + cg;
+      if (m >= Meff || nb >= p.N) continue;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int sp = 0; sp < S; ++sp) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const float4 f = ld_dsmem_f4(part + rr * LDP + cg + j, (uint32_t)sp);
+          v[j] += f.x; v[j + 1] += f.y; v[j + 2] += f.z; v[j + 3] += f.w;
+        }
+      }
+      epilogue16(p, m, nb, v);
+    }
+  }
+  cluster_sync_all();  // keep shared memory alive until every CTA has read it
+  if (live && warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot),
+                 "r"(64));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -511,6 +709,49 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   NMT_LAUNCH_CHECK();
 }
 
+void launch_cluster(const GemmArgs& a, cudaStream_t s) {
+  constexpr int STAGES = 4;
+  using SM = Smem<64, STAGES>;
+  const int bytes = SM::BYTES + BM * (64 + 4) * 4;
+  static bool attr = false;
+  if (!attr) {
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc_cluster<STAGES>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc_cluster<STAGES>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  const int S = a.splits;
+  if (((a.K + BK - 1) / BK) % S || BM % S) throw CudaError("gemm_tc: bad cluster split");
+  CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
+  CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, 64);
+  Params p{};
+  p.M = a.M; p.N = a.N; p.K = a.K;
+  p.bias = static_cast<const __half*>(a.bias);
+  p.R = static_cast<const __half*>(a.R);
+  p.ldr = a.ldr;
+  p.C = static_cast<__half*>(a.C);
+  p.ldc = a.ldc;
+  p.relu = a.relu;
+  p.dM = a.dM;
+  p.splits = S;
+  const int tiles = ceil_div(a.M, BM) * ceil_div(a.N, 64);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles * S);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc_cluster<STAGES>, ma, mb, p));
+  NMT_LAUNCH_CHECK();
+}
+
 }  // namespace tc
 
 int decode_splits(int N, int K) {
@@ -527,6 +768,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     throw CudaError("gemm_tc: K / leading dims must be multiples of 8 and 16-B aligned");
   if (a.argmax) {
     tc::launch<256, 3>(a, s);
+  } else if (a.tile_n == 64 && a.splits > 1) {
+    tc::launch_cluster(a, s);   // split-K reduced through distributed shared memory
   } else if (a.tile_n == 64) {
     tc::launch<64, 4>(a, s);
   } else {
