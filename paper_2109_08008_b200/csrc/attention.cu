@@ -507,13 +507,11 @@ template <class T>
 void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
                   int d, int H, int kclip, int use_rpr, cudaStream_t s) {
   if (B <= 0) return;
-  if constexpr (sizeof(T) == 2) {  // FP16 mode: tensor-core attention
-    switch (d / H) {
-      case 16: launch_enc_mma<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
-      case 32: launch_enc_mma<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
-      case 64: launch_enc_mma<64>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); return;
-      default: throw CudaError("attn_encoder: head dim must be 16, 32 or 64");
-    }
+  if constexpr (sizeof(T) == 2) {  // FP16 mode: all contractions on tensor cores
+    attn_encoder_tc(reinterpret_cast<const __half*>(qkv), len,
+                    reinterpret_cast<const __half*>(relk), reinterpret_cast<const __half*>(relv),
+                    reinterpret_cast<__half*>(out), B, S, d, H, kclip, use_rpr, s);
+    return;
   }
   switch (d / H) {
     case 16: launch_enc<T, 16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
@@ -521,6 +519,37 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
     case 64: launch_enc<T, 64>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
     default: throw CudaError("attn_encoder: head dim must be 16, 32 or 64");
   }
+}
+
+// o[0..8) = sum_{j < n} p[j] * V[j][c0 .. c0+8) for this lane's 8-channel group (lanes
+// 0..DH/8-1 hold the result).  G = DH/8 lanes share a value row (one 16-B load each), a
+// warp covers 32/G rows per iteration; the row groups are combined by xor-shuffles.
+template <class T, int DH>
+__device__ __forceinline__ void pv_accumulate(const float* __restrict__ p,
+                                              const T* __restrict__ vbase, int stride, int n,
+                                              int lane, float* o) {
+  constexpr int G = DH / 8, KP = 32 / G;
+  const int sub = lane % G, kq = lane / G;
+  float a[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) a[e] = 0.f;
+#pragma unroll 2
+  for (int j0 = 0; j0 < n; j0 += KP) {
+    const int j = j0 + kq;
+    if (j < n) {
+      float v[8];
+      Vec8<T>::load(vbase + (size_t)j * stride + sub * 8, v);
+      const float pj = p[j];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = fmaf(pj, v[e], a[e]);
+    }
+  }
+#pragma unroll
+  for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] += __shfl_xor_sync(0xffffffffu, a[e], off);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) o[e] = a[e];
 }
 
 // ----------------------------------------------------------------- decoder self-attention
@@ -604,39 +633,21 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     }
     __syncwarp();
   }
-  float o[CPL];
+  float o[8];
+  pv_accumulate<T, DH>(p, vbase, d, t + 1, lane, o);
+  constexpr int G = DH / 8;
+  if (lane < G) {
+    const int c0 = lane * 8;
+    if (use_rpr)
+      for (int b = 0; b <= kclip; ++b) {
+        float rv[8];
+        Vec8<T>::load(relv + b * DH + c0, rv);
 #pragma unroll
-  for (int u = 0; u < CPL; ++u) o[u] = 0.f;
-  int j = 0;
-  for (; j + 1 <= t; j += 2) {
-    const float p0 = p[j], p1 = p[j + 1];
-    const T* v0 = vbase + (size_t)j * d;
-    const T* v1 = v0 + d;
+        for (int e = 0; e < 8; ++e) o[e] = fmaf(x[b], rv[e], o[e]);
+      }
+    T* orow = out + (size_t)row * d + h * DH + c0;
 #pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int c = lane + 32 * u;
-      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), fmaf(p1, to_f(v1[c]), o[u]));
-    }
-  }
-  for (; j <= t; ++j) {
-    const float p0 = p[j];
-    const T* v0 = vbase + (size_t)j * d;
-#pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int c = lane + 32 * u;
-      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), o[u]);
-    }
-  }
-  T* orow = out + (size_t)row * d + h * DH;
-#pragma unroll
-  for (int u = 0; u < CPL; ++u) {
-    const int c = lane + 32 * u;
-    if (c < DH) {
-      float r = o[u];
-      if (use_rpr)
-        for (int b = 0; b <= kclip; ++b) r = fmaf(x[b], to_f(relv[b * DH + c]), r);
-      orow[c] = from_f<T>(r * inv);
-    }
+    for (int e = 0; e < 8; ++e) orow[e] = from_f<T>(o[e] * inv);
   }
 }
 
@@ -713,34 +724,13 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   }
   const float inv = 1.f / warp_sum(sum);
   __syncwarp();
-  float o[CPL];
+  float o[8];
+  pv_accumulate<T, DH>(p, base + voff, ldkv, n, lane, o);
+  constexpr int G = DH / 8;
+  if (lane < G) {
+    T* orow = out + (size_t)row * d + h * DH + lane * 8;
 #pragma unroll
-  for (int u = 0; u < CPL; ++u) o[u] = 0.f;
-  int j = 0;
-  for (; j + 1 < n; j += 2) {
-    const float p0 = p[j], p1 = p[j + 1];
-    const T* v0 = base + (size_t)j * ldkv + voff;
-    const T* v1 = v0 + ldkv;
-#pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int c = lane + 32 * u;
-      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), fmaf(p1, to_f(v1[c]), o[u]));
-    }
-  }
-  for (; j < n; ++j) {
-    const float p0 = p[j];
-    const T* v0 = base + (size_t)j * ldkv + voff;
-#pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int c = lane + 32 * u;
-      if (c < DH) o[u] = fmaf(p0, to_f(v0[c]), o[u]);
-    }
-  }
-  T* orow = out + (size_t)row * d + h * DH;
-#pragma unroll
-  for (int u = 0; u < CPL; ++u) {
-    const int c = lane + 32 * u;
-    if (c < DH) orow[c] = from_f<T>(o[u] * inv);
+    for (int e = 0; e < 8; ++e) orow[e] = from_f<T>(o[e] * inv);
   }
 }
 

@@ -1,0 +1,309 @@
+// attention_tc.cu — encoder RPR self-attention for the FP16 path, every contraction on the
+// tensor cores (warp-level mma.sync m16n8k16, FP16 in / FP32 accumulate):
+//   S   = Q K^T                      (keys)
+//   QA  = Q A^K^T                    (q_i . A^K[r], the relative-key term, 17 -> 32 cols)
+//   O   = P V + B A^V                (values + relative-value term; B = bucket sums)
+// with r(i,j) = clip(j - i, -k, k) + k (Shaw et al.; clip 8).
+// Scores, masking and the softmax stay in FP32 registers; P and the bucket sums B are
+// rounded to FP16 only as MMA operands (FP16-mode tolerance).  One CTA per
+// (sentence, head), 4 warps each owning 16-query blocks; Q/K/V staged with cp.async.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+namespace {
+
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// 16-byte async global->shared copy; src_bytes = 0 zero-fills (padding rows)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
+constexpr int RP = 32;   // relative buckets padded to 32 (2k+1 <= 31)
+constexpr int QLD = 33;  // FP32 row stride of q . A^K
+
+template <int DH, int NT>
+struct EncSmem {
+  static constexpr int SP = NT * 8, LDH = DH + 8, LDB = RP + 8;
+  static constexpr int Q = 0, K = Q + SP * LDH * 2, V = K + SP * LDH * 2, AK = V + SP * LDH * 2,
+                       AV = AK + RP * LDH * 2, QA = AV + RP * LDH * 2, B = QA + SP * QLD * 4,
+                       BYTES = B + SP * LDB * 2;
+};
+
+template <int DH, int NT>  // NT = 8-wide key tiles (SP = 8*NT, multiple of 16)
+__global__ void __launch_bounds__(128) k_attn_enc_tc(const __half* __restrict__ qkv,
+                                                     const int* __restrict__ len,
+                                                     const __half* __restrict__ relk,
+                                                     const __half* __restrict__ relv,
+                                                     __half* __restrict__ out, int S, int d,
+                                                     int kclip, int use_rpr) {
+  using L = EncSmem<DH, NT>;
+  constexpr int SP = L::SP, LDH = L::LDH, LDB = L::LDB;
+  extern __shared__ __align__(16) uint8_t sm[];
+  __half* sQ = reinterpret_cast<__half*>(sm + L::Q);
+  __half* sK = reinterpret_cast<__half*>(sm + L::K);
+  __half* sV = reinterpret_cast<__half*>(sm + L::V);
+  __half* sAK = reinterpret_cast<__half*>(sm + L::AK);   // [RP][LDH], rows >= R zero
+  __half* sAV = reinterpret_cast<__half*>(sm + L::AV);   // [RP][LDH], rows >= R zero
+  float* sQA = reinterpret_cast<float*>(sm + L::QA);     // [SP][QLD]
+  __half* sB = reinterpret_cast<__half*>(sm + L::B);     // [SP][LDB] bucket sums (FP16)
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int R = 2 * kclip + 1;
+  const int n = len[b];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t rs = 3 * (size_t)d;
+  const __half* base = qkv + (size_t)b * S * rs + h * DH;
+  // ---- stage Q, K, V asynchronously (rows >= n zero-filled) + relative tables
+  for (int idx = tid; idx < SP * (DH / 8); idx += 128) {
+    const int j = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
+    const bool ok = j < n;
+    const __half* rp = base + (size_t)(ok ? j : 0) * rs + c;
+    cp_async16(sQ + j * LDH + c, rp, ok ? 16 : 0);
+    cp_async16(sK + j * LDH + c, rp + d, ok ? 16 : 0);
+    cp_async16(sV + j * LDH + c, rp + 2 * d, ok ? 16 : 0);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int idx = tid; idx < RP * DH; idx += 128) {
+    const int r = idx / DH, c = idx % DH;
+    const bool ok = use_rpr && r < R;
+    sAK[r * LDH + c] = ok ? relk[r * DH + c] : __float2half(0.f);
+    sAV[r * LDH + c] = ok ? relv[r * DH + c] : __float2half(0.f);
+  }
+  for (int idx = tid; idx < SP * LDB / 2; idx += 128) reinterpret_cast<uint32_t*>(sB)[idx] = 0u;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+
+  const float scale = rsqrtf((float)DH);
+  const int g = lane >> 2, tig = lane & 3, mi = lane >> 3, rr = lane & 7;
+  const int nblk = (n + 15) >> 4;
+  for (int mb = warp; mb < nblk; mb += 4) {
+    const int m0 = mb * 16;
+    // ---- S = Q K^T and QA = Q A^K^T
+    float sc[NT][4], qa[RP / 8][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+#pragma unroll
+    for (int t = 0; t < RP / 8; ++t) qa[t][0] = qa[t][1] = qa[t][2] = qa[t][3] = 0.f;
+#pragma unroll
+    for (int k0 = 0; k0 < DH; k0 += 16) {
+      uint32_t af[4];
+      ldsm_x4(af, sQ + (m0 + rr + (mi & 1) * 8) * LDH + k0 + (mi >> 1) * 8);
+#pragma unroll
+      for (int t = 0; t < NT; t += 2) {
+        uint32_t bf[4];  // (t, k0) (t, k0+8) (t+1, k0) (t+1, k0+8)
+        ldsm_x4(bf, sK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
+        mma16816(sc[t], af, bf[0], bf[1]);
+        mma16816(sc[t + 1], af, bf[2], bf[3]);
+      }
+      if (use_rpr) {
+#pragma unroll
+        for (int t = 0; t < RP / 8; t += 2) {
+          uint32_t bf[4];
+          ldsm_x4(bf, sAK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
+          mma16816(qa[t], af, bf[0], bf[1]);
+          mma16816(qa[t + 1], af, bf[2], bf[3]);
+        }
+      }
+    }
+    const int r0 = m0 + g, r1 = r0 + 8;
+    if (use_rpr) {  // this warp's 16 rows of q . A^K -> shared (indexed by bucket below)
+#pragma unroll
+      for (int t = 0; t < RP / 8; ++t) {
+        const int c = t * 8 + 2 * tig;
+        sQA[r0 * QLD + c] = qa[t][0];
+        sQA[r0 * QLD + c + 1] = qa[t][1];
+        sQA[r1 * QLD + c] = qa[t][2];
+        sQA[r1 * QLD + c + 1] = qa[t][3];
+      }
+      __syncwarp();
+    }
+    // ---- relative-key term, mask, scale, FP32 softmax (rows r0, r1; quad reductions)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = e < 2 ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
+        float v = sc[t][e];
+        if (j < n && i < n) {
+          if (use_rpr) v += sQA[i * QLD + min(max(j - i, -kclip), kclip) + kclip];
+          v *= scale;
+        } else {
+          v = -INFINITY;
+        }
+        sc[t][e] = v;
+        if (e < 2) mx0 = fmaxf(mx0, v);
+        else mx1 = fmaxf(mx1, v);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
+    if (mx1 == -INFINITY) mx1 = 0.f;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = __expf(sc[t][e] - (e < 2 ? mx0 : mx1));
+        sc[t][e] = v;
+        if (e < 2) s0 += v;
+        else s1 += v;
+      }
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    const float inv0 = s0 > 0.f ? 1.f / s0 : 0.f, inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
+    float lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool top = e < 2;
+        const int i = top ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
+        const float p = sc[t][e] * (top ? inv0 : inv1);
+        sc[t][e] = p;
+        if (use_rpr && i < n && j < n) {
+          const int dj = j - i;
+          if (dj <= -kclip) { if (top) lo0 += p; else lo1 += p; }
+          else if (dj >= kclip) { if (top) hi0 += p; else hi1 += p; }
+          else sB[i * LDB + dj + kclip] = __float2half(p);  // unique writer per (i, bucket)
+        }
+      }
+    if (use_rpr) {
+      lo0 += __shfl_xor_sync(0xffffffffu, lo0, 1); lo0 += __shfl_xor_sync(0xffffffffu, lo0, 2);
+      hi0 += __shfl_xor_sync(0xffffffffu, hi0, 1); hi0 += __shfl_xor_sync(0xffffffffu, hi0, 2);
+      lo1 += __shfl_xor_sync(0xffffffffu, lo1, 1); lo1 += __shfl_xor_sync(0xffffffffu, lo1, 2);
+      hi1 += __shfl_xor_sync(0xffffffffu, hi1, 1); hi1 += __shfl_xor_sync(0xffffffffu, hi1, 2);
+      if (tig == 0) {
+        if (r0 < n) { sB[r0 * LDB] = __float2half(lo0); sB[r0 * LDB + R - 1] = __float2half(hi0); }
+        if (r1 < n) { sB[r1 * LDB] = __float2half(lo1); sB[r1 * LDB + R - 1] = __float2half(hi1); }
+      }
+      __syncwarp();
+    }
+    // ---- O = P V (+ B A^V): P from registers as FP16 A fragments, B via ldmatrix
+    float oc[DH / 8][4];
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NT / 2; ++kk) {
+      uint32_t af[4];
+      af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
+      af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
+      af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+      af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 16) {
+        uint32_t bf[4];  // .trans: (j0,c0) (j0+8,c0) (j0,c0+8) (j0+8,c0+8)
+        ldsm_x4_t(bf, sV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+        mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+        mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+      }
+    }
+    if (use_rpr) {
+#pragma unroll
+      for (int kk = 0; kk < RP / 16; ++kk) {
+        uint32_t af[4];
+        ldsm_x4(af, sB + (m0 + rr + (mi & 1) * 8) * LDB + kk * 16 + (mi >> 1) * 8);
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 16) {
+          uint32_t bf[4];
+          ldsm_x4_t(bf, sAV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+          mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+          mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+        }
+      }
+    }
+    // ---- store (query rows >= n written as 0)
+    __half* orow0 = out + ((size_t)b * S + r0) * d + h * DH;
+    __half* orow1 = out + ((size_t)b * S + r1) * d + h * DH;
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) {
+      const int c = t * 8 + 2 * tig;
+      if (r0 < S)
+        *reinterpret_cast<__half2*>(orow0 + c) =
+            r0 < n ? __floats2half2_rn(oc[t][0], oc[t][1]) : __floats2half2_rn(0.f, 0.f);
+      if (r1 < S)
+        *reinterpret_cast<__half2*>(orow1 + c) =
+            r1 < n ? __floats2half2_rn(oc[t][2], oc[t][3]) : __floats2half2_rn(0.f, 0.f);
+    }
+  }
+  // query rows beyond the last 16-block are padding: zero them
+  for (int idx = nblk * 16 * (DH / 8) + tid; idx < S * (DH / 8); idx += 128) {
+    const int i = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
+    *reinterpret_cast<uint4*>(out + ((size_t)b * S + i) * d + h * DH + c) = make_uint4(0, 0, 0, 0);
+  }
+}
+
+template <int DH, int NT>
+void launch_nt(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+               __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  using L = EncSmem<DH, NT>;
+  static bool attr = false;
+  if (!attr) {
+    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tc<DH, NT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    attr = true;
+  }
+  k_attn_enc_tc<DH, NT><<<dim3(B, H), 128, L::BYTES, s>>>(qkv, len, relk, relv, out, S, d, kclip,
+                                                         use_rpr);
+}
+
+template <int DH>
+void launch_dh(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+               __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  const int sp = (S + 15) / 16 * 16;
+  switch (sp) {
+    case 16: launch_nt<DH, 2>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 32: launch_nt<DH, 4>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 48: launch_nt<DH, 6>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 64: launch_nt<DH, 8>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 80: launch_nt<DH, 10>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 96: launch_nt<DH, 12>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 112: launch_nt<DH, 14>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 128: launch_nt<DH, 16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    default: throw CudaError("attn_encoder: S > 128");
+  }
+}
+
+}  // namespace
+
+void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                     __half* out, int B, int S, int d, int H, int kclip, int use_rpr,
+                     cudaStream_t s) {
+  if (2 * kclip + 1 > RP - 1) throw CudaError("attn_encoder_tc: 2k+1 must be < 32");
+  switch (d / H) {
+    case 16: launch_dh<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 32: launch_dh<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 64: launch_dh<64>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    default: throw CudaError("attn_encoder_tc: head dim must be 16, 32 or 64");
+  }
+  NMT_LAUNCH_CHECK();
+}
+
+}  // namespace nmt

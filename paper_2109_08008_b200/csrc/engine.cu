@@ -410,10 +410,11 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
   const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
   const int bucket = std::min(Rmax, (rows + 31) & ~31);
   auto eager = [&] {
-    decode_step_any(m, &b, nullptr, nullptr, s);
+    decode_step_any(m, &b, nullptr, nullptr, s, /*finish=*/false);
     PROF(P_BOOK, 0, 0,
-         prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr, b.rows_upper,
-                       s));
+         finish_prune(m->keys, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
+                      m->lim.max_tgt_len, m->gen_len, m->st, m->cfg.eos_id, every, ratio,
+                      b.rows_upper, s));
   };
   if (m->prof.on || !m->eager_done || s == nullptr) {
     b.rows_upper = rows;

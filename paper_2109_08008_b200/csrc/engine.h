@@ -138,8 +138,9 @@ struct nmt_model {
 namespace nmt {
 // forward.cu
 void encode_any(nmt_model* m, int B, int S, cudaStream_t s);
+// finish = false leaves the greedy bookkeeping to a following finish_prune launch.
 void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
-                     cudaStream_t s);
+                     cudaStream_t s, bool finish = true);
 void prof_flush(nmt_model* m);
 template <class F>
 void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {

@@ -134,7 +134,7 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
 
 template <class T>
 void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool finish) {
   const nmt_config& c = m->cfg;
   const int d = c.d_model, F = c.d_ffn, H = c.n_heads, Ld = c.dec_layers;
   const int R = b->rows_upper;
@@ -195,10 +195,11 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   GemmArgs a = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
   a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
   PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-  PROF(P_BOOK, 0, 0,
-       greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
-                     Tm, m->gen_len, m->st, R, c.eos_id, out ? out->d_next : nullptr,
-                     out ? out->d_done : nullptr, s));
+  if (finish)
+    PROF(P_BOOK, 0, 0,
+         greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap,
+                       m->out_tok, Tm, m->gen_len, m->st, R, c.eos_id,
+                       out ? out->d_next : nullptr, out ? out->d_done : nullptr, s));
 }
 
 }  // namespace
@@ -209,9 +210,9 @@ void encode_any(nmt_model* m, int B, int S, cudaStream_t s) {
 }
 
 void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
-                     cudaStream_t s) {
-  if (m->prec == NMT_FP16) decode_step_impl<__half>(m, b, d_prev, out, s);
-  else decode_step_impl<float>(m, b, d_prev, out, s);
+                     cudaStream_t s, bool finish) {
+  if (m->prec == NMT_FP16) decode_step_impl<__half>(m, b, d_prev, out, s, finish);
+  else decode_step_impl<float>(m, b, d_prev, out, s, finish);
 }
 
 }  // namespace nmt

@@ -71,9 +71,14 @@ __global__ void k_layernorm(const T* __restrict__ in, int ldi, const T* __restri
 }
 
 template <class T>
+bool layernorm_vec(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, int rows, int d,
+                   float eps, const int* dR, cudaStream_t s);
+
+template <class T>
 void layernorm(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, int rows, int d,
                float eps, const int* dR, cudaStream_t s) {
   if (rows <= 0) return;
+  if (layernorm_vec<T>(in, ldi, g, b, out, ldo, rows, d, eps, dR, s)) return;  // d = 256 / 512
   k_layernorm<T><<<ceil_div(rows, 8), 256, 0, s>>>(in, ldi, g, b, out, ldo, rows, d, eps, dR);
   NMT_LAUNCH_CHECK();
 }
@@ -105,10 +110,16 @@ __global__ void k_embed_dec_ln(const int* __restrict__ ids, const T* __restrict_
 }
 
 template <class T>
+bool embed_dec_ln_vec(const int* ids, const T* E, const float* pe, const T* gam, const T* bet, T* g,
+                      T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
+                      cudaStream_t s);
+
+template <class T>
 void embed_dec_ln(const int* ids, const T* E, const float* pe, const T* gam, const T* bet, T* g,
                   T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
                   cudaStream_t s) {
   if (rows <= 0) return;
+  if (embed_dec_ln_vec<T>(ids, E, pe, gam, bet, g, u, rows, d, scale, eps, d_t, dR, s)) return;
   k_embed_dec_ln<T><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows, d, scale,
                                                       eps, d_t, dR);
   NMT_LAUNCH_CHECK();
@@ -296,6 +307,77 @@ void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w
   NMT_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------------- vectorised row kernels
+// One warp per row, lane owns E contiguous columns: 16-B loads/stores (d = 32*E).
+template <class T, int E>
+__global__ void __launch_bounds__(256) k_layernorm_vec(const T* __restrict__ in, int ldi,
+                                                       const T* __restrict__ g,
+                                                       const T* __restrict__ b,
+                                                       T* __restrict__ out, int ldo, int rows,
+                                                       float eps, const int* __restrict__ dR) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nrows = dR ? min(rows, *dR) : rows;
+  if (row >= nrows) return;
+  float v[E];
+  ldrow<T, E>(in + (size_t)row * ldi + lane * E, v);
+  ln_contig<T, E>(v, 32 * E, g, b, eps, lane);
+  strow<T, E>(out + (size_t)row * ldo + lane * E, v);
+}
+
+template <class T>
+bool layernorm_vec(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, int rows, int d,
+                   float eps, const int* dR, cudaStream_t s) {
+  const bool al = (ldi % 8 == 0) && (ldo % 8 == 0);
+  if (d == 512 && al)
+    k_layernorm_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(in, ldi, g, b, out, ldo, rows, eps, dR);
+  else if (d == 256 && al)
+    k_layernorm_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(in, ldi, g, b, out, ldo, rows, eps, dR);
+  else
+    return false;
+  NMT_LAUNCH_CHECK();
+  return true;
+}
+
+template <class T, int E>
+__global__ void __launch_bounds__(256) k_embed_dec_ln_vec(
+    const int* __restrict__ ids, const T* __restrict__ Em, const float* __restrict__ pe,
+    const T* __restrict__ gam, const T* __restrict__ bet, T* __restrict__ g, T* __restrict__ u,
+    int rows, float scale, float eps, const int* __restrict__ d_t, const int* __restrict__ dR) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= min(rows, *dR)) return;
+  constexpr int d = 32 * E;
+  float v[E];
+  ldrow<T, E>(Em + (size_t)ids[row] * d + lane * E, v);
+  const float* p = pe + (size_t)(*d_t) * d + lane * E;
+#pragma unroll
+  for (int i = 0; i < E; i += 4) {
+    const float4 q = *reinterpret_cast<const float4*>(p + i);
+    v[i] = to_f(from_f<T>(v[i] * scale + q.x));
+    v[i + 1] = to_f(from_f<T>(v[i + 1] * scale + q.y));
+    v[i + 2] = to_f(from_f<T>(v[i + 2] * scale + q.z));
+    v[i + 3] = to_f(from_f<T>(v[i + 3] * scale + q.w));
+  }
+  strow<T, E>(g + (size_t)row * d + lane * E, v);   // g (residual stream) in storage precision
+  ln_contig<T, E>(v, d, gam, bet, eps, lane);
+  strow<T, E>(u + (size_t)row * d + lane * E, v);
+}
+
+template <class T>
+bool embed_dec_ln_vec(const int* ids, const T* E, const float* pe, const T* gam, const T* bet, T* g,
+                      T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
+                      cudaStream_t s) {
+  if (d == 512)
+    k_embed_dec_ln_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows,
+                                                                scale, eps, d_t, dR);
+  else if (d == 256)
+    k_embed_dec_ln_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows,
+                                                               scale, eps, d_t, dR);
+  else
+    return false;
+  NMT_LAUNCH_CHECK();
+  return true;
+}
+
 // ------------------------------------------------------------------- greedy bookkeeping
 __global__ void k_greedy_finish(unsigned long long* __restrict__ keys, int* __restrict__ prev_tok,
                                 uint8_t* __restrict__ done, const int* __restrict__ row_slot,
@@ -363,9 +445,60 @@ __device__ int block_excl_scan(int v, int* total) {
 constexpr int kPrunePer = 16;                   // rows per thread held in registers
 constexpr int kPruneMaxRows = 1024 * kPrunePer;  // 16384
 
+__device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
+                           float ratio, int* new_to_old);
+
 __global__ void __launch_bounds__(1024) k_prune(DevState* st, int* row_slot, int* prev_tok,
                                                 uint8_t* done, int every, float ratio,
                                                 int* new_to_old) {
+  prune_body(st, row_slot, prev_tok, done, every, ratio, new_to_old);
+}
+
+// Greedy finish (k_greedy_finish) + pruning decision/compaction (k_prune) in one CTA: the
+// decode step's bookkeeping tail as a single launch.
+__global__ void __launch_bounds__(1024) k_finish_prune(
+    unsigned long long* __restrict__ keys, int* __restrict__ prev_tok, uint8_t* __restrict__ done,
+    int* __restrict__ row_slot, const int* __restrict__ cap, int* __restrict__ out_tok,
+    int out_stride, int* __restrict__ gen_len, DevState* st, int eos, int every, float ratio) {
+  __shared__ int s_new;
+  if (threadIdx.x == 0) s_new = 0;
+  __syncthreads();
+  const int n = st->n_live, t = st->t;
+  int cnt = 0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const unsigned long long k = keys[r];
+    keys[r] = 0ull;
+    const int tok = unpack_argmax_id(k);
+    prev_tok[r] = tok;
+    if (!done[r]) {
+      const int slot = row_slot[r];
+      out_tok[(size_t)slot * out_stride + t] = tok;
+      gen_len[slot] = t + 1;
+      if (tok == eos || t + 1 >= cap[slot]) {
+        done[r] = 1;
+        ++cnt;
+      }
+    }
+  }
+  cnt = (int)warp_sum((float)cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_new, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) st->n_done += s_new;
+  __syncthreads();
+  prune_body(st, row_slot, prev_tok, done, every, ratio, nullptr);
+}
+
+void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* row_slot,
+                  const int* cap, int* out_tok, int out_stride, int* gen_len, DevState* st,
+                  int eos, int every, float ratio, int rows_upper, cudaStream_t s) {
+  if (rows_upper > kPruneMaxRows) throw CudaError("finish_prune: too many rows");
+  k_finish_prune<<<1, 1024, 0, s>>>(keys, prev_tok, done, row_slot, cap, out_tok, out_stride,
+                                    gen_len, st, eos, every, ratio);
+  NMT_LAUNCH_CHECK();
+}
+
+__device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
+                           float ratio, int* new_to_old) {
   __shared__ int s_total;
   const int n = st->n_live, nd = st->n_done, t = st->t;
   bool all_done = (n > 0 && nd == n);

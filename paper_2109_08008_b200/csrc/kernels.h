@@ -68,6 +68,11 @@ template <class T>
 void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B,
                   int S, int d, int H, int kclip, int use_rpr, cudaStream_t s);
 
+// FP16 path of attn_encoder: Q K^T, q.A^K and P V + B A^V on tensor cores (attention_tc.cu).
+void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                     __half* out, int B, int S, int d, int H, int kclip, int use_rpr,
+                     cudaStream_t s);
+
 // Decoder cached self-attention at step t = *d_t: for live row r
 // (< *dR), slot = row_slot[r]; appends k_t, v_t (from qkv[r]) into the cache at
 // [slot][t] and attends over positions 0..t with r(i,j) = clip(j - t, -k, k) + k.
@@ -114,6 +119,11 @@ void greedy_finish(unsigned long long* keys, const int* force_next, int* prev_to
 // pre-prune rows; entries >= new count are -1.
 void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
                    float ratio, int* new_to_old, int rows_upper, cudaStream_t s);
+
+// greedy_finish + prune_compact fused into one single-CTA launch (translate loop).
+void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* row_slot,
+                  const int* cap, int* out_tok, int out_stride, int* gen_len, DevState* st,
+                  int eos, int every, float ratio, int rows_upper, cudaStream_t s);
 
 // Fresh batch state: row_slot[r] = r, prev_tok[r] = BOS, done = 0, gen_len = 0,
 // st = {t 0, n_live B, n_done 0, prunes 0}.
