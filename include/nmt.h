@@ -90,8 +90,13 @@ void nmt_free_model(nmt_model* m);
  * Requires n_sent <= max_sents, n_sent*s_max <= max_tokens, s_max <= max_src_len.
  * Only one batch per model may be live; encoding a new one invalidates the previous. */
 nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_len,
-                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, void* stream,
-                      nmt_batch** out);
+                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, int32_t beam,
+                      void* stream, nmt_batch** out);
+/*   beam: 1 = greedy; 2..min(4, limits.beam) = beam search: each
+ *   sentence gets `beam` consecutive live rows; nmt_decode_step then performs a whole beam
+ *   step (log-softmax, top-2K, EOS finalisation, early stop "when any candidate predicts the
+ *   EOS symbol, and there are no candidates with higher scores") and the batch results are
+ *   the best finished hypothesis per sentence.  Teacher forcing (d_prev) is greedy-only. */
 
 /* Copy the batch's encoder output enc [n_sent][s_max][d] as FP32 into d_dst (parity/debug). */
 nmt_status nmt_batch_encoder_output(const nmt_batch* b, float* d_dst, void* stream);
@@ -136,6 +141,7 @@ typedef struct {
   const int32_t* h_tgt_cap; /* optional [n] per-sentence caps (synthetic workloads) */
   int32_t n_workers;     /* concurrent batch workers (own arena + stream each, shared
                             weights); 0/1 = one.  Outputs do not depend on it.     */
+  int32_t beam;          /* 0/1 = greedy; 2..4 = beam search     */
 } nmt_translate_opts;
 
 typedef struct {

@@ -524,10 +524,13 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
 // o[0..8) = sum_{j < n} p[j] * V[j][c0 .. c0+8) for this lane's 8-channel group (lanes
 // 0..DH/8-1 hold the result).  G = DH/8 lanes share a value row (one 16-B load each), a
 // warp covers 32/G rows per iteration; the row groups are combined by xor-shuffles.
+// Row j lives in slot (anc_row && j < t_own ? anc_row[j] : own_slot): beam hypotheses read
+// their ancestors' cached positions through the ancestry table (no K/V copies).
 template <class T, int DH>
 __device__ __forceinline__ void pv_accumulate(const float* __restrict__ p,
-                                              const T* __restrict__ vbase, int stride, int n,
-                                              int lane, float* o) {
+                                              const T* __restrict__ v0, size_t slot_stride,
+                                              int own_slot, const int* __restrict__ anc_row,
+                                              int t_own, int stride, int n, int lane, float* o) {
   constexpr int G = DH / 8, KP = 32 / G;
   const int sub = lane % G, kq = lane / G;
   float a[8];
@@ -538,7 +541,8 @@ __device__ __forceinline__ void pv_accumulate(const float* __restrict__ p,
     const int j = j0 + kq;
     if (j < n) {
       float v[8];
-      Vec8<T>::load(vbase + (size_t)j * stride + sub * 8, v);
+      const int sl = (anc_row && j < t_own) ? anc_row[j] : own_slot;
+      Vec8<T>::load(v0 + (size_t)sl * slot_stride + (size_t)j * stride + sub * 8, v);
       const float pj = p[j];
 #pragma unroll
       for (int e = 0; e < 8; ++e) a[e] = fmaf(pj, v[e], a[e]);
@@ -561,9 +565,8 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     const T* __restrict__ qkv, T* __restrict__ kc, T* __restrict__ vc, int Tmax,
     const int* __restrict__ row_slot, const T* __restrict__ relk, const T* __restrict__ relv,
     T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
-    const int* __restrict__ dR) {
+    const int* __restrict__ dR, const int* __restrict__ anc) {
   extern __shared__ float sm[];
-  constexpr int CPL = (DH + 31) / 32;  // channels per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
@@ -591,8 +594,10 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
   __syncwarp();
   const float scale = rsqrtf((float)DH);
   float mx = -INFINITY;
+  const int* anc_row = anc ? anc + (size_t)slot * Tmax : nullptr;
   for (int j = lane; j <= t; j += 32) {
-    const T* kr = kbase + (size_t)j * d;
+    const int sl = (anc_row && j < t) ? anc_row[j] : slot;
+    const T* kr = kc + ((size_t)sl * Tmax + j) * d + h * DH;
     float e0 = 0.f, e1 = 0.f;
 #pragma unroll
     for (int c = 0; c < DH; c += 8) {
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     __syncwarp();
   }
   float o[8];
-  pv_accumulate<T, DH>(p, vbase, d, t + 1, lane, o);
+  pv_accumulate<T, DH>(p, vc + h * DH, (size_t)Tmax * d, slot, anc_row, t, d, t + 1, lane, o);
   constexpr int G = DH / 8;
   if (lane < G) {
     const int c0 = lane * 8;
@@ -654,14 +659,14 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
 template <class T>
 void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot, const T* relk,
                        const T* relv, T* out, int rows, int d, int H, int kclip, int use_rpr,
-                       const int* d_t, const int* dR, cudaStream_t s) {
+                       const int* d_t, const int* dR, const int* anc, cudaStream_t s) {
   if (rows <= 0) return;
   const int nw = 4, dh = d / H;
   size_t smem = sizeof(float) * nw * (dh + 32 + Tmax);
   dim3 grid(ceil_div(rows * H, nw));
 #define NMT_DS(DH)                                                                             \
   k_attn_dec_self<T, DH><<<grid, nw * 32, smem, s>>>(qkv, kc, vc, Tmax, row_slot, relk, relv, \
-                                                     out, rows, d, H, kclip, use_rpr, d_t, dR)
+                                                     out, rows, d, H, kclip, use_rpr, d_t, dR, anc)
   switch (dh) {
     case 16: NMT_DS(16); break;
     case 32: NMT_DS(32); break;
@@ -681,9 +686,8 @@ __global__ void __launch_bounds__(128) k_attn_cross(
     const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv, int koff, int voff,
     const int* __restrict__ dS, int Smax, const int* __restrict__ src_len,
     const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,
-    const int* __restrict__ dR) {
+    const int* __restrict__ dR, int beam) {
   extern __shared__ float sm[];
-  constexpr int CPL = (DH + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   const int S = *dS;
   float* q = sm + warp * (DH + Smax);
   float* p = q + DH;
-  const int slot = row_slot[row];
+  const int slot = row_slot[row] / beam;  // sentence slot (beam rows share the encoder K/V)
   const int n = src_len[slot];
   for (int c = lane; c < DH; c += 32) q[c] = to_f(qb[(size_t)row * d + h * DH + c]);
   __syncwarp();
@@ -725,7 +729,7 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   const float inv = 1.f / warp_sum(sum);
   __syncwarp();
   float o[8];
-  pv_accumulate<T, DH>(p, base + voff, ldkv, n, lane, o);
+  pv_accumulate<T, DH>(p, base + voff, 0, 0, nullptr, 0, ldkv, n, lane, o);
   constexpr int G = DH / 8;
   if (lane < G) {
     T* orow = out + (size_t)row * d + h * DH + lane * 8;
@@ -737,14 +741,14 @@ __global__ void __launch_bounds__(128) k_attn_cross(
 template <class T>
 void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const int* dS, int Smax,
                 const int* src_len, const int* row_slot, T* out, int rows, int d, int H,
-                const int* dR, cudaStream_t s) {
+                const int* dR, int beam, cudaStream_t s) {
   if (rows <= 0) return;
   const int nw = 4, dh = d / H;
   size_t smem = sizeof(float) * nw * (dh + Smax);
   dim3 grid(ceil_div(rows * H, nw));
 #define NMT_CS(DH)                                                                          \
   k_attn_cross<T, DH><<<grid, nw * 32, smem, s>>>(q, ckv, ldkv, koff, voff, dS, Smax, src_len, \
-                                                  row_slot, out, rows, d, H, dR)
+                                                  row_slot, out, rows, d, H, dR, beam)
   switch (dh) {
     case 16: NMT_CS(16); break;
     case 32: NMT_CS(32); break;
@@ -760,9 +764,9 @@ void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const in
                                 int, int, int, cudaStream_t);                                   \
   template void attn_decoder_self<T>(const T*, T*, T*, int, const int*, const T*, const T*, T*, \
                                      int, int, int, int, int, const int*, const int*,           \
-                                     cudaStream_t);                                             \
+                                     const int*, cudaStream_t);                                 \
   template void attn_cross<T>(const T*, const T*, int, int, int, const int*, int, const int*,   \
-                              const int*, T*, int, int, int, const int*, cudaStream_t);
+                              const int*, T*, int, int, int, const int*, int, cudaStream_t);
 NMT_INST_ATT(float)
 NMT_INST_ATT(__half)
 

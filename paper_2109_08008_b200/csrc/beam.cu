@@ -1,0 +1,306 @@
+// beam.cu — batched beam search on the device ("the search ends when any
+// candidate predicts the EOS symbol, and there are no candidates with higher scores";
+// reading R15/R16: fairseq-style 2K candidates, unnormalised sum of log-probabilities).
+//
+// Layout: the live rows of a batch are grouped per sentence, K consecutive rows each
+// (row r -> sentence group r / K).  Row r owns a physical cache slot row_slot[r]
+// (= sentence_slot*K + k, fixed); beam re-ordering never copies K/V: each slot keeps an
+// ancestry table anc[slot][j] = physical slot holding position j of its hypothesis, and a
+// token history htok[slot][j] (j = 0 is BOS).  The self-attention kernel reads position j
+// < t through anc (CopyBlocks-free beam reorder).
+//
+// Step t: vocab GEMM -> FP32 logits [rows][V];  k_beam_row_topk: per row LSE and the top-2K
+// log-probs (value desc, id asc);  k_beam_select: per sentence the top-2K of the K x 2K
+// candidates ordered by (score desc, slot*V + v asc), EOS candidates ranked < K finalise
+// (best kept, ties -> earliest), the first K non-EOS become the new rows, actives are
+// finalised at the cap, early stop when best finished >= best active.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+
+constexpr int kKB = 8;  // candidates kept per row (= 2 * max beam 4)
+
+// ------------------------------------------------------------------ per-row top-K + LSE
+__device__ __forceinline__ bool cand_better(float a, int ia, float b, int ib) {
+  return a > b || (a == b && ia < ib);
+}
+
+__global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__ logits, int V,
+                                                       int KB, const int* __restrict__ dR,
+                                                       float* __restrict__ cand_v,
+                                                       int* __restrict__ cand_i) {
+  const int row = blockIdx.x;
+  if (row >= *dR) return;
+  const float* x = logits + (size_t)row * V;
+  float tv[kKB];
+  int ti[kKB];
+#pragma unroll
+  for (int k = 0; k < kKB; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
+  float m = -INFINITY, s = 0.f;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float f = x[v];
+    if (f > m) { s = s * __expf(m - f) + 1.f; m = f; }
+    else s += __expf(f - m);
+    if (cand_better(f, v, tv[kKB - 1], ti[kKB - 1])) {  // sorted insertion
+      float cv = f; int ci = v;
+#pragma unroll
+      for (int k = 0; k < kKB; ++k) {
+        if (cand_better(cv, ci, tv[k], ti[k])) {
+          const float t1 = tv[k]; const int t2 = ti[k];
+          tv[k] = cv; ti[k] = ci; cv = t1; ci = t2;
+        }
+      }
+    }
+  }
+  // block LSE
+  __shared__ float sm_m[8], sm_s[8];
+  __shared__ float sv[256 * kKB];
+  __shared__ int si[256 * kKB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    float mm = m;
+    for (int o = 16; o; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+    float ss = (m == -INFINITY) ? 0.f : s * __expf(m - mm);
+    ss = warp_sum(ss);
+    if (lane == 0) { sm_m[warp] = mm; sm_s[warp] = ss; }
+  }
+#pragma unroll
+  for (int k = 0; k < kKB; ++k) {
+    sv[threadIdx.x * kKB + k] = tv[k];
+    si[threadIdx.x * kKB + k] = ti[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float mm = lane < 8 ? sm_m[lane] : -INFINITY;
+    float M = mm;
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float ss = (lane < 8 && mm > -INFINITY) ? sm_s[lane] * __expf(mm - M) : 0.f;
+    ss = warp_sum(ss);
+    const float lse = M + __logf(ss);
+    // merge 256 x KB candidates: each lane scans 8 threads' sorted lists, then KB rounds
+    // of warp argmax (value desc, id asc)
+    int ptr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ptr[q] = 0;
+    for (int k = 0; k < KB; ++k) {
+      float bv = -INFINITY; int bi = 0x7fffffff, bq = -1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int th = lane * 8 + q;
+        if (ptr[q] < kKB) {
+          const float v = sv[th * kKB + ptr[q]];
+          const int id = si[th * kKB + ptr[q]];
+          if (cand_better(v, id, bv, bi)) { bv = v; bi = id; bq = q; }
+        }
+      }
+      float wv = bv; int wi = bi;
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+        if (cand_better(ov, oi, wv, wi)) { wv = ov; wi = oi; }
+      }
+      if (bq >= 0 && bi == wi && bv == wv) ptr[bq]++;  // the owning lane advances
+      if (lane == 0) {
+        cand_v[(size_t)row * KB + k] = wv - lse;        // log_softmax value
+        cand_i[(size_t)row * KB + k] = wi;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ per-sentence select
+// One warp per live sentence group.  Shared staging per warp: the K parents' ancestry and
+// token histories (t+1 ints each), so the in-place rewrite of the group's slots is safe.
+struct SelCand { float v; int k; int tok; };
+
+template <int K>
+__global__ void __launch_bounds__(128) k_beam_select(
+    const float* __restrict__ cand_v, const int* __restrict__ cand_i, float* __restrict__ score,
+    int* __restrict__ prev_tok, uint8_t* __restrict__ done, const int* __restrict__ row_slot,
+    const int* __restrict__ cap, int* __restrict__ anc, int* __restrict__ htok, int Tmax,
+    float* __restrict__ best_score, int* __restrict__ out_tok, int* __restrict__ gen_len,
+    DevState* st, int V, int eos) {
+  extern __shared__ int sm_i[];
+  constexpr int KB = 2 * K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int grp = blockIdx.x * nw + warp;
+  const int n_live = st->n_live;
+  if (grp * K >= n_live) return;
+  const int r0 = grp * K;
+  if (done[r0]) return;  // finished sentence waiting to be pruned
+  const int t = st->t;
+  const int sent = row_slot[r0] / K;
+  int* s_anc = sm_i + warp * 2 * K * (Tmax + 1);
+  int* s_tok = s_anc + K * (Tmax + 1);
+  __shared__ SelCand s_sel[4][2 * K];
+  __shared__ int s_cnt[4];
+  // candidate per lane: row k = lane / KB, rank q = lane % KB
+  float cv = -INFINITY;
+  int ck = 0x7fffffff, ctok = 0, ckey = 0x7fffffff;
+  if (lane < K * KB) {
+    const int k = lane / KB, q = lane % KB;
+    const float sc = score[r0 + k];
+    if (sc > -INFINITY) {
+      cv = sc + cand_v[(size_t)(r0 + k) * KB + q];
+      ctok = cand_i[(size_t)(r0 + k) * KB + q];
+      ck = k;
+      ckey = k * V + ctok;
+    }
+  }
+  // 2K rounds of warp argmax by (score desc, slot*V + v asc)
+  for (int rank = 0; rank < 2 * K; ++rank) {
+    float wv = cv; int wk = ckey;
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int okey = __shfl_xor_sync(0xffffffffu, wk, o);
+      if (cand_better(ov, okey, wv, wk)) { wv = ov; wk = okey; }
+    }
+    if (ckey == wk && cv == wv && wv > -INFINITY) {
+      s_sel[warp][rank] = {cv, ck, ctok};
+      cv = -INFINITY; ckey = 0x7fffffff;
+    } else if (lane == 0 && !(wv > -INFINITY)) {
+      s_sel[warp][rank] = {-INFINITY, -1, 0};
+    }
+    __syncwarp();
+  }
+  // sequential bookkeeping by lane 0 (K tiny)
+  __shared__ int s_fin_k[4], s_fin_tok[4], s_done[4];
+  __shared__ SelCand s_new[4][K];
+  if (lane == 0) {
+    float fin = best_score[sent];
+    int fk = -1, ftok = 0;
+    float fsc = -INFINITY;
+    int n_new = 0;
+    for (int rank = 0; rank < 2 * K; ++rank) {
+      const SelCand c = s_sel[warp][rank];
+      if (!(c.v > -INFINITY)) break;
+      if (c.tok == eos) {
+        if (rank < K && c.v > fin) { fin = c.v; fk = c.k; ftok = c.tok; fsc = c.v; }
+      } else if (n_new < K) {
+        s_new[warp][n_new++] = c;
+      }
+    }
+    const bool at_cap = t + 1 >= cap[sent];
+    if (at_cap)
+      for (int i = 0; i < n_new; ++i)
+        if (s_new[warp][i].v > fin) { fin = s_new[warp][i].v; fk = s_new[warp][i].k; ftok = s_new[warp][i].tok; fsc = fin; }
+    float best_act = -INFINITY;
+    for (int i = 0; i < n_new; ++i) best_act = fmaxf(best_act, s_new[warp][i].v);
+    const bool early = fin > -INFINITY && fin >= best_act;
+    s_done[warp] = at_cap || n_new == 0 || early;
+    s_fin_k[warp] = fk;
+    s_fin_tok[warp] = ftok;
+    s_cnt[warp] = n_new;
+    if (fk >= 0) best_score[sent] = fsc;
+  }
+  __syncwarp();
+  const int fk = s_fin_k[warp], n_new = s_cnt[warp];
+  const bool sdone = s_done[warp];
+  // a new best finished hypothesis: tokens = htok[parent][1..t] + token
+  if (fk >= 0) {
+    const int ps = row_slot[r0 + fk];
+    for (int j = lane; j < t; j += 32) out_tok[(size_t)sent * Tmax + j] = htok[(size_t)ps * Tmax + j + 1];
+    if (lane == 0) {
+      out_tok[(size_t)sent * Tmax + t] = s_fin_tok[warp];
+      gen_len[sent] = t + 1;
+    }
+  }
+  if (sdone) {
+    if (lane < K) done[r0 + lane] = 1;
+    if (lane == 0) atomicAdd(&st->n_done, K);
+    return;
+  }
+  // stage parents' ancestry / history, then rewrite this group's slots in place
+  for (int i = 0; i < n_new; ++i) {
+    const int ps = row_slot[r0 + s_new[warp][i].k];
+    for (int j = lane; j <= t; j += 32) {
+      s_anc[i * (Tmax + 1) + j] = j < t ? anc[(size_t)ps * Tmax + j] : ps;
+      s_tok[i * (Tmax + 1) + j] = htok[(size_t)ps * Tmax + j];
+    }
+  }
+  __syncwarp();
+  for (int i = 0; i < K; ++i) {
+    const int r = r0 + i, slot = row_slot[r];
+    if (i < n_new) {
+      for (int j = lane; j <= t; j += 32) {
+        anc[(size_t)slot * Tmax + j] = s_anc[i * (Tmax + 1) + j];
+        htok[(size_t)slot * Tmax + j] = s_tok[i * (Tmax + 1) + j];
+      }
+      if (lane == 0) {
+        if (t + 1 < Tmax) htok[(size_t)slot * Tmax + t + 1] = s_new[warp][i].tok;
+        prev_tok[r] = s_new[warp][i].tok;
+        score[r] = s_new[warp][i].v;
+      }
+    } else if (lane == 0) {
+      score[r] = -INFINITY;  // fewer than K continuations (tiny vocabularies)
+      prev_tok[r] = eos;
+    }
+  }
+}
+
+void beam_row_topk(const float* logits, int V, int KB, const int* dR, int rows_upper,
+                   float* cand_v, int* cand_i, cudaStream_t s) {
+  if (rows_upper <= 0) return;
+  if (KB > kKB) throw CudaError("beam_row_topk: 2K > 8");
+  k_beam_row_topk<<<rows_upper, 256, 0, s>>>(logits, V, KB, dR, cand_v, cand_i);
+  NMT_LAUNCH_CHECK();
+}
+
+void beam_select(int K, const float* cand_v, const int* cand_i, float* score, int* prev_tok,
+                 uint8_t* done, const int* row_slot, const int* cap, int* anc, int* htok,
+                 int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st, int V,
+                 int eos, int rows_upper, cudaStream_t s) {
+  if (rows_upper <= 0) return;
+  const int groups = (rows_upper + K - 1) / K, nw = 4;
+  const size_t smem = (size_t)nw * 2 * K * (Tmax + 1) * sizeof(int);
+#define NMT_BS(KK)                                                                            \
+  k_beam_select<KK><<<ceil_div(groups, nw), nw * 32, smem, s>>>(                              \
+      cand_v, cand_i, score, prev_tok, done, row_slot, cap, anc, htok, Tmax, best_score,       \
+      out_tok, gen_len, st, V, eos)
+  switch (K) {
+    case 1: NMT_BS(1); break;
+    case 2: NMT_BS(2); break;
+    case 3: NMT_BS(3); break;
+    case 4: NMT_BS(4); break;
+    default: throw CudaError("beam_select: beam must be 1..4");
+  }
+#undef NMT_BS
+  NMT_LAUNCH_CHECK();
+}
+
+__global__ void k_beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok,
+                            int Tmax, float* best_score, int* gen_len, DevState* st, int B, int K,
+                            int S, int bos) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < B * K) {
+    row_slot[r] = r;
+    prev_tok[r] = bos;
+    done[r] = 0;
+    score[r] = (r % K == 0) ? 0.f : -INFINITY;  // t = 0: only the BOS hypothesis is active
+    htok[(size_t)r * Tmax] = bos;
+  }
+  if (r < B) {
+    best_score[r] = -INFINITY;
+    gen_len[r] = 0;
+  }
+  if (r == 0) {
+    st->t = 0;
+    st->n_live = B * K;
+    st->n_done = 0;
+    st->prunes = 0;
+    st->S = S;
+  }
+}
+
+void beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok, int Tmax,
+               float* best_score, int* gen_len, DevState* st, int B, int K, int S, int bos,
+               cudaStream_t s) {
+  const int n = B * K;
+  k_beam_init<<<ceil_div(n > 0 ? n : 1, 128), 128, 0, s>>>(row_slot, prev_tok, done, score, htok,
+                                                           Tmax, best_score, gen_len, st, B, K, S,
+                                                           bos);
+  NMT_LAUNCH_CHECK();
+}
+
+}  // namespace nmt

@@ -145,6 +145,14 @@ void init_arena(nmt_model* m) {
       {(void**)&m->blen, Bm * 4}, {(void**)&m->sent_ids, Bm * 4},
       {(void**)&m->gemm_ws, std::max<size_t>(ws_floats * 4, 256)},
       {(void**)&m->gemm_cnt, std::max<size_t>(cnt_ints * 4, 256)},
+      // beam search: only sized when the limits ask for beam > 1
+      {(void**)&m->bscore, L.beam > 1 ? R * 4 : 256},
+      {(void**)&m->anc, L.beam > 1 ? R * Tm * 4 : 256},
+      {(void**)&m->htok, L.beam > 1 ? R * Tm * 4 : 256},
+      {(void**)&m->best_score, L.beam > 1 ? Bm * 4 : 256},
+      {(void**)&m->blogits, L.beam > 1 ? R * (size_t)c.vocab_size * 4 : 256},
+      {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
+      {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
   };
   std::vector<size_t> offs;
   for (auto& it : items) offs.push_back(a.take(it.second));
@@ -263,7 +271,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   NMT_REQUIRE(lim->max_tokens >= 1 && lim->max_sents >= 1 && lim->max_tgt_len >= 1 &&
                   lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1,
               NMT_E_ARG, "bad limits");
-  NMT_REQUIRE(lim->beam == 1, NMT_E_UNSUPPORTED, "beam > 1 is not built in this version");
+  NMT_REQUIRE(lim->beam <= 4, NMT_E_UNSUPPORTED, "beam > 4 is not built");
   NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 16384, NMT_E_ARG, "max_sents*beam > 16384");
 
   std::unique_ptr<nmt_model> m(new nmt_model());
@@ -364,8 +372,10 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
 
 // ------------------------------------------------------------------ batches
 void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_cap,
-                   cudaStream_t s) {
+                   cudaStream_t s, int K = 1) {
   nmt_batch& b = m->batch;
+  NMT_REQUIRE(K >= 1 && K <= m->lim.beam && K <= 4, NMT_E_ARG,
+              "beam " + std::to_string(K) + " outside [1, min(4, limits.beam)]");
   const int Tm = m->lim.max_tgt_len;
   int mc = 0;
   for (int i = 0; i < B; ++i) {
@@ -378,9 +388,15 @@ void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_ca
   NMT_CUDA(cudaMemcpyAsync(m->src_len, m->hp.len, B * 4, cudaMemcpyHostToDevice, s));
   NMT_CUDA(cudaMemcpyAsync(m->tgt_cap, m->hp.cap, B * 4, cudaMemcpyHostToDevice, s));
   encode_any(m, B, S, s);
-  PROF(P_BOOK, 0, 0,
-       batch_init(m->row_slot, m->prev_tok, m->done, m->gen_len, m->st, B, S, m->cfg.bos_id, s));
-  b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B; b.max_cap = mc; b.valid = true;
+  if (K == 1)
+    PROF(P_BOOK, 0, 0,
+         batch_init(m->row_slot, m->prev_tok, m->done, m->gen_len, m->st, B, S, m->cfg.bos_id, s));
+  else
+    PROF(P_BOOK, 0, 0,
+         beam_init(m->row_slot, m->prev_tok, m->done, m->bscore, m->htok, Tm, m->best_score,
+                   m->gen_len, m->st, B, K, S, m->cfg.bos_id, s));
+  b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B * K; b.max_cap = mc; b.valid = true;
+  b.K = K;
   b.pending_step_done = false;
 }
 
@@ -410,21 +426,28 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
   const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
   const int bucket = std::min(Rmax, (rows + 31) & ~31);
   auto eager = [&] {
-    decode_step_any(m, &b, nullptr, nullptr, s, /*finish=*/false);
-    PROF(P_BOOK, 0, 0,
-         finish_prune(m->keys, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
-                      m->lim.max_tgt_len, m->gen_len, m->st, m->cfg.eos_id, every, ratio,
-                      b.rows_upper, s));
+    if (b.K == 1) {  // greedy: argmax epilogue, then finish + prune in one CTA
+      decode_step_any(m, &b, nullptr, nullptr, s, /*finish=*/false);
+      PROF(P_BOOK, 0, 0,
+           finish_prune(m->keys, m->prev_tok, m->done, m->row_slot, m->tgt_cap, m->out_tok,
+                        m->lim.max_tgt_len, m->gen_len, m->st, m->cfg.eos_id, every, ratio,
+                        b.rows_upper, s));
+    } else {         // beam: logits -> row top-2K -> per-sentence select, then prune
+      decode_step_any(m, &b, nullptr, nullptr, s, /*finish=*/true);
+      PROF(P_BOOK, 0, 0,
+           prune_compact(m->st, m->row_slot, m->prev_tok, m->done, every, ratio, nullptr,
+                         b.rows_upper, s, m->bscore));
+    }
   };
-  if (m->prof.on || !m->eager_done || s == nullptr) {
-    b.rows_upper = rows;
-    eager();
-    m->eager_done = true;
-    return;
-  }
   unsigned rb;
   memcpy(&rb, &ratio, 4);
-  auto key = std::make_tuple(bucket, every, rb);
+  auto key = std::make_tuple(bucket, every, rb, b.K);
+  if (m->prof.on || s == nullptr || !m->eager_keys.count(key)) {
+    b.rows_upper = rows;
+    eager();  // first use of a configuration runs eagerly (sets kernel attributes)
+    m->eager_keys.insert(key);
+    return;
+  }
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {
     b.rows_upper = bucket;
@@ -500,6 +523,7 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   const float ratio = o ? o->prune_ratio : 0.25f;
   const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
   const int W = o && o->n_workers > 1 ? std::min(o->n_workers, 8) : 1;
+  const int K = o && o->beam > 1 ? o->beam : 1;  // beam width; 1 = greedy
   NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
               "translate opts exceed the model limits");
   for (int64_t i = 0; i < n; ++i) {
@@ -532,9 +556,9 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
         caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : wm->lim.max_tgt_len;
       }
       load_src(wm, ws, &p.order[lo], B, S, lens.data());
-      encode_common(wm, B, S, lens.data(), caps.data(), ws);
+      encode_common(wm, B, S, lens.data(), caps.data(), ws, K);
       nmt_batch& b = wm->batch;
-      int rows = B;
+      int rows = B * K;
       int t = 0;
       // the live count is polled every `sync_every` steps (lagged upper bound for grids)
       for (; t < b.max_cap && rows > 0; ++t) {
@@ -646,7 +670,8 @@ nmt_status nmt_get_config(const nmt_model* m, nmt_config* out) {
 void nmt_free_model(nmt_model* m) { delete m; }
 
 nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_len,
-                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, void* stream,
+                      const int32_t* h_tgt_cap, int32_t n_sent, int32_t s_max, int32_t beam,
+                      void* stream,
                       nmt_batch** out) {
   return guard([&] {
     NMT_REQUIRE(m && d_src && h_src_len && out, NMT_E_ARG, "null argument");
@@ -656,7 +681,7 @@ nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_l
                   "src_len[" + std::to_string(i) + "] out of [1, s_max]");
     cudaStream_t s = (cudaStream_t)stream;
     NMT_CUDA(cudaMemcpyAsync(m->src, d_src, (size_t)n_sent * s_max * 4, cudaMemcpyDeviceToDevice, s));
-    encode_common(m, n_sent, s_max, h_src_len, h_tgt_cap, s);
+    encode_common(m, n_sent, s_max, h_src_len, h_tgt_cap, s, beam < 1 ? 1 : beam);
     *out = &m->batch;
   });
 }
@@ -681,6 +706,7 @@ nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, in
     NMT_REQUIRE(step == b->step, NMT_E_STATE,
                 "step " + std::to_string(step) + " != batch step " + std::to_string(b->step));
     NMT_REQUIRE(step < m->lim.max_tgt_len, NMT_E_STATE, "step beyond max_tgt_len");
+    NMT_REQUIRE(!(d_prev && b->K > 1), NMT_E_UNSUPPORTED, "teacher forcing is greedy-only");
     decode_step_any(m, b, d_prev, out, (cudaStream_t)stream);
     b->pending_step_done = true;
   });
@@ -693,7 +719,7 @@ nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_n
     NMT_REQUIRE(b->pending_step_done, NMT_E_STATE, "prune must follow a decode step");
     cudaStream_t s = (cudaStream_t)stream;
     prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old, b->rows_upper,
-                  s);
+                  s, b->K > 1 ? m->bscore : nullptr);
     b->pending_step_done = false;
     b->step += 1;
     if (h_n_live) {

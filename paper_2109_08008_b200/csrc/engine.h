@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -60,6 +61,7 @@ struct nmt_batch {
   int step = 0;          // host mirror of decode steps issued
   int rows_upper = 0;    // host upper bound of live rows (grid sizing)
   int max_cap = 0;
+  int K = 1;             // beam width (1 = greedy)
   bool valid = false;
   bool pending_step_done = false;  // nmt_decode_step issued, nmt_prune_batch not yet
 };
@@ -98,6 +100,14 @@ struct nmt_model {
   int* sent_ids = nullptr;
   float* gemm_ws = nullptr;   // split-K partials of the decode GEMMs
   int* gemm_cnt = nullptr;    // split-K arrival counters (self-resetting)
+  // beam search state (allocated when limits.beam > 1)
+  float* bscore = nullptr;    // [R] cumulative log-prob per live row
+  int* anc = nullptr;         // [R][Tmax] ancestry (slot holding position j)
+  int* htok = nullptr;        // [R][Tmax] token history per slot (j = 0: BOS)
+  float* best_score = nullptr;  // [max_sents] best finished hypothesis score
+  float* blogits = nullptr;   // [R][V] FP32 logits of the step
+  float* cand_v = nullptr;    // [R][2K] top log-probs per row
+  int* cand_i = nullptr;      // [R][2K] their token ids
   // pinned host staging
   struct Pinned {
     int* src; int* len; int* cap; long long* boff; int* blen; int* sent; int* out_tok; int* gen_len;
@@ -116,8 +126,8 @@ struct nmt_model {
     long long n[16] = {};
   } prof;
   // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits)
-  std::map<std::tuple<int, int, unsigned>, cudaGraphExec_t> graphs;
-  bool eager_done = false;  // one eager step ran (kernel attributes set) before capture
+  std::map<std::tuple<int, int, unsigned, int>, cudaGraphExec_t> graphs;
+  std::set<std::tuple<int, int, unsigned, int>> eager_keys;  // configurations run eagerly once
   // Concurrent batch workers (the GPU analog of the paper's parallel decoding processes,
   // PAPER.md:129-131): clones sharing this model's weights, each with its own arena,
   // stream, batch state and graphs.  Created lazily by nmt_translate*(n_workers > 1).

@@ -165,7 +165,8 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
          attn_decoder_self<T>(dqkv, kc, vc, Tm, m->row_slot, cT<T>(w.relk), cT<T>(w.relv), dout,
-                              R, d, H, c.max_rel_pos, c.use_rpr, dt, dR, s));
+                              R, d, H, c.max_rel_pos, c.use_rpr, dt, dR,
+                              b->K > 1 ? m->anc : nullptr, s));
     a = mk(R, d, d, dout, d, w.so_w, d, w.so_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
@@ -176,7 +177,7 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
          attn_cross<T>(dq, (const T*)m->ckv, Ld * 2 * d, l * 2 * d, l * 2 * d + d, &m->st->S,
-                       c.max_src_len, m->src_len, m->row_slot, dout, R, d, H, dR, s));
+                       c.max_src_len, m->src_len, m->row_slot, dout, R, d, H, dR, b->K, s));
     a = mk(R, d, d, dout, d, w.co_w, d, w.co_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
@@ -191,15 +192,33 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   }
   PROF(P_DEC_LN, 0, 2 * row,
        layernorm<T>(g, d, cT<T>(m->dec_fg), cT<T>(m->dec_fb), du, d, R, d, eps, dR, s));
-  // tied vocab projection fused with argmax: logits never stored
-  GemmArgs a = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
-  a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
-  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-  if (finish)
-    PROF(P_BOOK, 0, 0,
-         greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap,
-                       m->out_tok, Tm, m->gen_len, m->st, R, c.eos_id,
-                       out ? out->d_next : nullptr, out ? out->d_done : nullptr, s));
+  if (b->K == 1) {
+    // tied vocab projection fused with argmax: logits never stored
+    GemmArgs a = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
+    a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
+    PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
+    if (finish)
+      PROF(P_BOOK, 0, 0,
+           greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap,
+                         m->out_tok, Tm, m->gen_len, m->st, R, c.eos_id,
+                         out ? out->d_next : nullptr, out ? out->d_done : nullptr, s));
+    return;
+  }
+  // beam: FP32 logits -> per-row LSE + top-2K -> per-sentence select
+  const int K = b->K, V = c.vocab_size;
+  GemmArgs a = mk(R, V, d, du, d, m->emb, d, nullptr, nullptr, 0);
+  a.dM = dR; a.logits = m->blogits;
+  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) + (double)R * V * 4, gemm<T>(a, s));
+  if (out && out->d_logits)
+    NMT_CUDA(cudaMemcpyAsync(out->d_logits, m->blogits, (size_t)R * V * 4,
+                             cudaMemcpyDeviceToDevice, s));
+  if (!finish) return;
+  PROF(P_BOOK, 0, (double)R * V * 4,
+       beam_row_topk(m->blogits, V, 2 * K, dR, R, m->cand_v, m->cand_i, s));
+  PROF(P_BOOK, 0, 0,
+       beam_select(K, m->cand_v, m->cand_i, m->bscore, m->prev_tok, m->done, m->row_slot,
+                   m->tgt_cap, m->anc, m->htok, Tm, m->best_score, m->out_tok, m->gen_len, m->st,
+                   V, c.eos_id, R, s));
 }
 
 }  // namespace

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
         unsigned long long k = pack_argmax(v, n);
         best = k > best ? k : best;
       } else {
-        C[(size_t)m * a.ldc + n] = from_f<T>(v);
+        if (C) C[(size_t)m * a.ldc + n] = from_f<T>(v);  // C == null: logits only (beam)
       }
     }
     if (a.argmax && best) atomicMax(a.argmax + m, best);

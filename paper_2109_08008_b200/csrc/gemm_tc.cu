@@ -187,9 +187,15 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
   }
   if (p.logits) {
     float* lr = p.logits + (size_t)m * p.N + nb;
+    if (full && ((p.N & 3) == 0)) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nv) lr[j] = v[j];
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(lr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) lr[j] = v[j];
+    }
   }
   if (p.argmax) {
 #pragma unroll
@@ -200,6 +206,7 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
       }
     return;
   }
+  if (!p.C) return;  // logits-only (beam search) epilogue
   __half* cr = p.C + (size_t)m * p.ldc + nb;
   if (full && ((reinterpret_cast<uintptr_t>(cr) & 15) == 0)) {
 #pragma unroll

@@ -446,12 +446,12 @@ constexpr int kPrunePer = 16;                   // rows per thread held in regis
 constexpr int kPruneMaxRows = 1024 * kPrunePer;  // 16384
 
 __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
-                           float ratio, int* new_to_old);
+                           float ratio, int* new_to_old, float* score);
 
 __global__ void __launch_bounds__(1024) k_prune(DevState* st, int* row_slot, int* prev_tok,
                                                 uint8_t* done, int every, float ratio,
-                                                int* new_to_old) {
-  prune_body(st, row_slot, prev_tok, done, every, ratio, new_to_old);
+                                                int* new_to_old, float* score) {
+  prune_body(st, row_slot, prev_tok, done, every, ratio, new_to_old, score);
 }
 
 // Greedy finish (k_greedy_finish) + pruning decision/compaction (k_prune) in one CTA: the
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(1024) k_finish_prune(
   __syncthreads();
   if (threadIdx.x == 0) st->n_done += s_new;
   __syncthreads();
-  prune_body(st, row_slot, prev_tok, done, every, ratio, nullptr);
+  prune_body(st, row_slot, prev_tok, done, every, ratio, nullptr, nullptr);
 }
 
 void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* row_slot,
@@ -498,7 +498,7 @@ void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* r
 }
 
 __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
-                           float ratio, int* new_to_old) {
+                           float ratio, int* new_to_old, float* score) {
   __shared__ int s_total;
   const int n = st->n_live, nd = st->n_done, t = st->t;
   bool all_done = (n > 0 && nd == n);
@@ -521,6 +521,7 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int lo = threadIdx.x * per, hi = min(n, lo + per);
   int r_slot[kPrunePer], r_tok[kPrunePer];
+  float r_sc[kPrunePer];
   unsigned keepmask = 0;
   int keep = 0;
 #pragma unroll
@@ -529,6 +530,7 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
     if (i < hi) {
       r_slot[k] = row_slot[i];
       r_tok[k] = prev_tok[i];
+      r_sc[k] = score ? score[i] : 0.f;
       if (!done[i]) {
         keepmask |= 1u << k;
         ++keep;
@@ -543,6 +545,7 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
     if (keepmask & (1u << k)) {
       row_slot[o] = r_slot[k];
       prev_tok[o] = r_tok[k];
+      if (score) score[o] = r_sc[k];
       if (new_to_old) new_to_old[o] = lo + k;
       ++o;
     }
@@ -562,9 +565,9 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
 }
 
 void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
-                   float ratio, int* new_to_old, int rows_upper, cudaStream_t s) {
+                   float ratio, int* new_to_old, int rows_upper, cudaStream_t s, float* score) {
   if (rows_upper > kPruneMaxRows) throw CudaError("prune_compact: too many rows");
-  k_prune<<<1, 1024, 0, s>>>(st, row_slot, prev_tok, done, every, ratio, new_to_old);
+  k_prune<<<1, 1024, 0, s>>>(st, row_slot, prev_tok, done, every, ratio, new_to_old, score);
   NMT_LAUNCH_CHECK();
 }
 

@@ -6,6 +6,8 @@
 
 namespace nmt {
 
+struct DevState;
+
 // ---------------------------------------------------------------- GEMM family
 // C[M][N] = A[M][K] . B[N][K]^T (+bias[N]) (+R[M][N]) (ReLU), FP32 accumulation
 // (reductions in FP32).  A, B, bias, R, C are element type T.
@@ -77,18 +79,35 @@ void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, cons
 // (< *dR), slot = row_slot[r]; appends k_t, v_t (from qkv[r]) into the cache at
 // [slot][t] and attends over positions 0..t with r(i,j) = clip(j - t, -k, k) + k.
 // cache layout: K at kc + (slot*Tmax + j)*d, V at vc + ... (same).
+// anc (beam, optional): [slot][Tmax] ancestry — position j < t of this hypothesis lives in
+// slot anc[slot][j] (beam reorder without K/V copies).
 template <class T>
 void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot, const T* relk,
                        const T* relv, T* out, int rows, int d, int H, int kclip, int use_rpr,
-                       const int* d_t, const int* dR, cudaStream_t s);
+                       const int* d_t, const int* dR, const int* anc, cudaStream_t s);
 
 // Cross-attention over the once-per-sentence encoder K/V:
-// keys at ckv + (slot*S + j)*ldkv + koff, values at + voff; mask j < src_len[slot];
-// S = *dS read on the device (graph-replayable), Smax sizes shared memory.
+// keys at ckv + (sent*S + j)*ldkv + koff, values at + voff, sent = row_slot[r] / beam;
+// mask j < src_len[sent]; S = *dS read on the device (graph-replayable), Smax sizes smem.
 template <class T>
 void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const int* dS, int Smax,
                 const int* src_len, const int* row_slot, T* out, int rows, int d, int H,
-                const int* dR, cudaStream_t s);
+                const int* dR, int beam, cudaStream_t s);
+
+// ---------------------------------------------------------------- beam search (beam.cu)
+// FP32 logits [rows][V] -> per row the top-KB log-probs (value desc, id asc), LSE in FP32.
+void beam_row_topk(const float* logits, int V, int KB, const int* dR, int rows_upper,
+                   float* cand_v, int* cand_i, cudaStream_t s);
+// Per sentence (K consecutive live rows): top-2K candidates, EOS finalisation, early stop
+// (PAPER.md:103), new rows (tokens, scores, ancestry / token histories), winner written to
+// out_tok / gen_len of the sentence slot.
+void beam_select(int K, const float* cand_v, const int* cand_i, float* score, int* prev_tok,
+                 uint8_t* done, const int* row_slot, const int* cap, int* anc, int* htok,
+                 int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st,
+                 int V, int eos, int rows_upper, cudaStream_t s);
+void beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok, int Tmax,
+               float* best_score, int* gen_len, DevState* st, int B, int K, int S, int bos,
+               cudaStream_t s);
 
 // Decoder input + first pre-norm, fused (one warp per live row):
 //   g = sqrt(d) E[w_r] + PE(t),  u = LN(g; gam, bet)     (t = *d_t)
@@ -118,7 +137,8 @@ void greedy_finish(unsigned long long* keys, const int* force_next, int* prev_to
 // Advances st->t.  new_to_old (optional) receives the map (or identity) for the
 // pre-prune rows; entries >= new count are -1.
 void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
-                   float ratio, int* new_to_old, int rows_upper, cudaStream_t s);
+                   float ratio, int* new_to_old, int rows_upper, cudaStream_t s,
+                   float* score = nullptr /* beam: per-row scores compacted alongside */);
 
 // greedy_finish + prune_compact fused into one single-CTA launch (translate loop).
 void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* row_slot,

@@ -49,7 +49,7 @@ class StepOut(C.Structure):
 class TranslateOpts(C.Structure):
     _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("prune_every", C.c_int32),
                 ("prune_ratio", C.c_float), ("sync_every", C.c_int32), ("h_tgt_cap", C.c_void_p),
-                ("n_workers", C.c_int32)]
+                ("n_workers", C.c_int32), ("beam", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -97,7 +97,8 @@ class Model:
     """A loaded model (weights + arena) on one CUDA device."""
 
     def __init__(self, cfg, weights: dict, precision: str = "fp16", max_tokens: int = 4096,
-                 max_sents: int = 512, max_tgt_len: int | None = None, device: int = 0):
+                 max_sents: int = 512, max_tgt_len: int | None = None, device: int = 0,
+                 beam: int = 1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libnmt needs a CUDA device (no CPU fallback)")
@@ -107,7 +108,7 @@ class Model:
         self.V = cfg.vocab_size
         self.Tmax = max_tgt_len or cfg.max_tgt_len
         blob = ntsd.pack(cfg, weights)
-        lim = Limits(max_tokens, max_sents, self.Tmax, 1)
+        lim = Limits(max_tokens, max_sents, self.Tmax, beam)
         h = C.c_void_p()
         torch.cuda.set_device(device)
         _check(lib().nmt_load_weights(blob, C.c_size_t(len(blob)), device, self.prec, C.byref(lim),
@@ -131,19 +132,19 @@ class Model:
                 for i in range(n.value)}
 
     # ---------------------------------------------------------------- step API
-    def encode(self, src, src_len, tgt_cap=None, stream=None):
+    def encode(self, src, src_len, tgt_cap=None, beam=1, stream=None):
         """src: int32 CUDA tensor [B][S] (PAD-filled); src_len / tgt_cap: host ints."""
         B, S = src.shape
         ln = np.ascontiguousarray(src_len, dtype=np.int32)
         cp = None if tgt_cap is None else np.ascontiguousarray(tgt_cap, dtype=np.int32)
         b = C.c_void_p()
         _check(lib().nmt_encode(self.h, _ptr(src), ln.ctypes.data_as(C.c_void_p),
-                                None if cp is None else cp.ctypes.data_as(C.c_void_p), B, S,
+                                None if cp is None else cp.ctypes.data_as(C.c_void_p), B, S, beam,
                                 _stream(stream), C.byref(b)))
         return Batch(self, b, B, S)
 
     def translate(self, ids, off, caps=None, max_tokens=None, max_sents=None, prune_every=1,
-                  prune_ratio=0.25, sync_every=4, workers=1, stream=None):
+                  prune_ratio=0.25, sync_every=4, workers=1, beam=1, stream=None):
         """Host-buffer translation (C-ABI nmt_translate). Returns (outputs, stats dict)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         off = np.ascontiguousarray(off, dtype=np.int64)
@@ -151,7 +152,7 @@ class Model:
         capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
         o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
                           prune_every, prune_ratio, sync_every,
-                          None if capa is None else capa.ctypes.data, workers)
+                          None if capa is None else capa.ctypes.data, workers, beam)
         out_cap = n * self.Tmax
         out = np.empty(max(out_cap, 1), dtype=np.int32)
         out_off = np.empty(n + 1, dtype=np.int64)
@@ -165,6 +166,7 @@ class Model:
 
     def translate_device(self, d_ids, off, d_out, d_out_len, caps=None, max_tokens=None,
                          max_sents=None, prune_every=1, prune_ratio=0.25, sync_every=4, workers=1,
+                         beam=1,
                          stream=None):
         """Device-resident translation (C-ABI nmt_translate_device); d_out [n][stride]."""
         off = np.ascontiguousarray(off, dtype=np.int64)
@@ -172,7 +174,7 @@ class Model:
         capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
         o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
                           prune_every, prune_ratio, sync_every,
-                          None if capa is None else capa.ctypes.data, workers)
+                          None if capa is None else capa.ctypes.data, workers, beam)
         st = Stats()
         _check(lib().nmt_translate_device(self.h, _ptr(d_ids), off.ctypes.data_as(C.c_void_p),
                                           C.c_int64(n), C.byref(o), _ptr(d_out),
