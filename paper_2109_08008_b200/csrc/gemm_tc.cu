@@ -29,7 +29,7 @@ namespace tc {
 constexpr int BM = 128;       // UMMA M (cta_group::1): one TMEM lane per output row
 constexpr int BK = 64;        // 64 halves = 128 B = one swizzle-128B atom row
 constexpr int UMMA_K = 16;    // K per tcgen05.mma for 16-bit inputs
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-11: epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -147,7 +147,7 @@ struct Smem {
 
 // Epilogue for 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators).
 __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float* v,
-                                           unsigned long long& best) {
+                                           unsigned long long& best, const uint4* pre = nullptr) {
   const int nv = min(32, p.N - nb);
   const bool full = nv == 32;
   if (p.bias) {
@@ -167,7 +167,18 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
   }
   if (p.R) {
     const __half* rr = p.R + (size_t)m * p.ldr + nb;
-    if (full && ((reinterpret_cast<uintptr_t>(rr) & 15) == 0)) {
+    if (pre) {  // residual prefetched before the accumulator wait
+#pragma unroll
+      for (int j8 = 0; j8 < 4; ++j8) {
+        const __half2* h = reinterpret_cast<const __half2*>(&pre[j8]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          v[j8 * 8 + 2 * e] += f.x;
+          v[j8 * 8 + 2 * e + 1] += f.y;
+        }
+      }
+    } else if (full && ((reinterpret_cast<uintptr_t>(rr) & 15) == 0)) {
 #pragma unroll
       for (int j8 = 0; j8 < 4; ++j8) {
         float f[8];
@@ -245,10 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int M = p.dM ? min(p.M, *p.dM) : p.M;
   const int num_m = (M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
-  const int S = p.splits;
-  const int units = num_m * num_n * S;
+  const int units = num_m * num_n;
   const int kb_total = (p.K + BK - 1) / BK;
-  const int kps = kb_total / S;
   if ((int)blockIdx.x >= units) return;  // uniform: nothing for this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -280,9 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int s = u % S, rest = u / S;
-        const int m0 = (rest % num_m) * BM, n0 = (rest / num_m) * BN;
-        for (int kb = s * kps; kb < (s + 1) * kps; ++kb, ++it) {
+        const int m0 = (u % num_m) * BM, n0 = (u / num_m) * BN;
+        for (int kb = 0; kb < kb_total; ++kb, ++it) {
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[st], ph ^ 1);
@@ -301,13 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  | ((uint32_t)(BM >> 4) << 24);    // M
       int it = 0, local = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-        const int s = u % S;
         const int acc = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);   // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * ACC_COLS;
-        for (int kb = s * kps, first = 1; kb < (s + 1) * kps; ++kb, ++it, first = 0) {
+        for (int kb = 0, first = 1; kb < kb_total; ++kb, ++it, first = 0) {
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[st], ph);
@@ -322,87 +329,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue
-    const int q = warp & 3;  // TMEM lanes 32q..32q+31
+  } else if (warp >= 4) {  // ---------------- epilogue: 8 warps = 4 TMEM lane quadrants x 2 column halves
+    const int e = warp - 4, q = warp & 3, half = e >> 2;
+    constexpr int HALF = BN / 2, NPF = HALF / 8;
     int local = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-      const int s = u % S, rest = u / S, tile = rest;
-      const int m0 = (rest % num_m) * BM, n0 = (rest / num_m) * BN;
+      const int m0 = (u % num_m) * BM, n0 = (u / num_m) * BN;
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int r = q * 32 + lane;
       const int m = m0 + r;
       const bool row_ok = m < M;
-      const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
-      if (S == 1) {
-        unsigned long long best = 0ull;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          __syncwarp();
-          tmem_ld32(tbase + c0, v);
-          if (c0 + 32 >= BN) {  // accumulator fully read: hand it back to the MMA warp
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          if (row_ok && n0 + c0 < p.N) epilogue32(p, m, n0 + c0, v, best);
-        }
-        if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
-      } else {
-        // split-K: FP32 partial -> workspace, last arrival reduces in split order
-        float* wsp = p.ws + ((size_t)tile * S + s) * BM * BN + (size_t)r * BN;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          __syncwarp();
-          tmem_ld32(tbase + c0, v);
-          if (c0 + 32 >= BN) {
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          if (row_ok) {
+      const int cb = half * HALF;
+      // residual rows prefetched while the MMAs of this unit are still running
+      uint4 res[NPF];
+      const bool pf = p.R && row_ok && n0 + cb + HALF <= p.N &&
+                      ((reinterpret_cast<uintptr_t>(p.R + (size_t)m * p.ldr + n0 + cb) & 15) == 0);
+      if (pf) {
+        const uint4* rp = reinterpret_cast<const uint4*>(p.R + (size_t)m * p.ldr + n0 + cb);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(wsp + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          }
-        }
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 128) {
-          const int old = atomicAdd(p.counters + tile, 1);
-          const int last = (old == S - 1);
-          if (last) p.counters[tile] = 0;  // self-reset for the next launch / graph replay
-          *s_flag = last;
-        }
-        epi_bar();
-        if (*s_flag) {
-          __threadfence();
-          unsigned long long best = 0ull;
-          const float* w0 = p.ws + (size_t)tile * S * BM * BN + (size_t)r * BN;
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
-            if (!row_ok || n0 + c0 >= p.N) continue;
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            for (int sp = 0; sp < S; ++sp) {
-              const float* src = w0 + (size_t)sp * BM * BN + c0;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
-                v[j] += f.x; v[j + 1] += f.y; v[j + 2] += f.z; v[j + 3] += f.w;
-              }
-            }
-            epilogue32(p, m, n0 + c0, v, best);
-          }
-          if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
-        }
-        epi_bar();  // s_flag reused by the next unit
+        for (int i = 0; i < NPF; ++i) res[i] = rp[i];
       }
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      unsigned long long best = 0ull;
+#pragma unroll
+      for (int c0 = cb; c0 < cb + HALF; c0 += 32) {
+        float v[32];
+        __syncwarp();
+        tmem_ld32(tbase + c0, v);
+        if (c0 + 32 >= cb + HALF) {  // this warp's columns read: release the accumulator
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (row_ok && n0 + c0 < p.N)
+          epilogue32(p, m, n0 + c0, v, best, pf ? res + (c0 - cb) / 8 : nullptr);
+      }
+      if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -690,10 +655,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     attr = true;
   }
-  const int splits = a.splits > 0 ? a.splits : 1;
-  const int kb_total = (a.K + BK - 1) / BK;
-  if (kb_total % splits) throw CudaError("gemm_tc: K blocks not divisible by splits");
-  if (splits > 1 && (!a.ws || !a.counters)) throw CudaError("gemm_tc: split-K needs workspace");
+  if (a.splits > 1) throw CudaError("gemm_tc: persistent kernel has no split-K (use the cluster path)");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN);
   Params p;
@@ -707,10 +669,8 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.dM = a.dM;
   p.argmax = a.argmax;
   p.logits = a.logits;
-  p.splits = splits;
-  p.ws = a.ws;
-  p.counters = a.counters;
-  const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN) * splits;
+  p.splits = 1;
+  const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
   k_gemm_tc<BN, STAGES><<<grid, kThreads, SM::BYTES, s>>>(ma, mb, p);
   NMT_LAUNCH_CHECK();
