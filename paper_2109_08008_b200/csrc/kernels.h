@@ -29,7 +29,7 @@ struct GemmArgs {
   float* logits = nullptr;
   // tcgen05 path only: output tile width (128, or 64 for decode-size GEMMs) and a
   // deterministic split-K factor with its FP32 workspace / self-resetting counters.
-  int tile_n = 128;
+  int tile_n = 256;
   int splits = 1;
   float* ws = nullptr;
   int* counters = nullptr;
