@@ -567,6 +567,8 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
     const int* __restrict__ dR, const int* __restrict__ anc) {
   extern __shared__ float sm[];
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
@@ -665,8 +667,8 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
   size_t smem = sizeof(float) * nw * (dh + 32 + Tmax);
   dim3 grid(ceil_div(rows * H, nw));
 #define NMT_DS(DH)                                                                             \
-  k_attn_dec_self<T, DH><<<grid, nw * 32, smem, s>>>(qkv, kc, vc, Tmax, row_slot, relk, relv, \
-                                                     out, rows, d, H, kclip, use_rpr, d_t, dR, anc)
+  launch_k(k_attn_dec_self<T, DH>, grid, nw * 32, smem, s, qkv, kc, vc, Tmax, row_slot, relk, \
+           relv, out, rows, d, H, kclip, use_rpr, d_t, dR, anc)
   switch (dh) {
     case 16: NMT_DS(16); break;
     case 32: NMT_DS(32); break;
@@ -688,6 +690,8 @@ __global__ void __launch_bounds__(128) k_attn_cross(
     const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,
     const int* __restrict__ dR, int beam) {
   extern __shared__ float sm[];
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
@@ -747,8 +751,8 @@ void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const in
   size_t smem = sizeof(float) * nw * (dh + Smax);
   dim3 grid(ceil_div(rows * H, nw));
 #define NMT_CS(DH)                                                                          \
-  k_attn_cross<T, DH><<<grid, nw * 32, smem, s>>>(q, ckv, ldkv, koff, voff, dS, Smax, src_len, \
-                                                  row_slot, out, rows, d, H, dR, beam)
+  launch_k(k_attn_cross<T, DH>, grid, nw * 32, smem, s, q, ckv, ldkv, koff, voff, dS, Smax, \
+           src_len, row_slot, out, rows, d, H, dR, beam)
   switch (dh) {
     case 16: NMT_CS(16); break;
     case 32: NMT_CS(32); break;

@@ -17,6 +17,7 @@
 
 namespace nmt {
 std::atomic<unsigned long long> g_launches{0};
+thread_local bool g_pdl = false;
 thread_local std::string g_err;
 }  // namespace nmt
 
@@ -417,6 +418,14 @@ void poll_state(nmt_model* m, cudaStream_t s) {
   if (!m->prof.pending.empty()) prof_flush(m);
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NMT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // One greedy step + pruning decision for `rows` live rows.  After one eager step the
 // pair is captured once per (rows bucket, cadence, ratio) into a CUDA graph and
 // replayed: every kernel reads t, the live count and S from device memory, so a graph
@@ -453,12 +462,15 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
     b.rows_upper = bucket;
     cudaGraph_t g;
     NMT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    g_pdl = pdl_enabled();  // programmatic edges between the step's kernels
     try {
       eager();
     } catch (...) {
+      g_pdl = false;
       cudaStreamEndCapture(s, &g);
       throw;
     }
+    g_pdl = false;
     NMT_CUDA(cudaStreamEndCapture(s, &g));
     cudaGraphExec_t ex;
     NMT_CUDA(cudaGraphInstantiate(&ex, g, 0));

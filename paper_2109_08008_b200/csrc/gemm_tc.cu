@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
+  pdl_trigger();
+  pdl_wait();  // PDL: operands / live-row count come from the preceding kernel
   const int M = p.dM ? min(p.M, *p.dM) : p.M;
   const int num_m = (M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
   const int units = num_m * num_n;
@@ -469,6 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
+  pdl_trigger();
+  pdl_wait();
   const int S = p.splits;
   const int s = (int)cluster_ctarank();          // split index == rank in the cluster
   const int tile = blockIdx.x / S;
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(tfull);
       }
-    } else if (warp >= 4) {  // TMEM -> FP32 partial in this CTA's shared memory
+    } else if (warp >= 4 && warp < 8) {  // TMEM -> FP32 partial in this CTA's shared memory
       mbar_wait(tfull, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int q = warp & 3, r = q * 32 + lane;
@@ -672,7 +676,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.splits = 1;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
-  k_gemm_tc<BN, STAGES><<<grid, kThreads, SM::BYTES, s>>>(ma, mb, p);
+  launch_k(k_gemm_tc<BN, STAGES>, grid, kThreads, SM::BYTES, s, ma, mb, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -708,13 +712,15 @@ void launch_cluster(const GemmArgs& a, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = S;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc_cluster<STAGES>, ma, mb, p));
   NMT_LAUNCH_CHECK();
 }
@@ -739,6 +745,12 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     tc::launch<64, 4>(a, s);
   } else if (a.tile_n == 128) {
     tc::launch<128, 4>(a, s);
+  } else if (const char* e = getenv("NMT_GEMM_CFG")) {  // tuning experiments only
+    const std::string c(e);
+    if (c == "128x6") tc::launch<128, 6>(a, s);
+    else if (c == "128x4") tc::launch<128, 4>(a, s);
+    else if (c == "256x3") tc::launch<256, 3>(a, s);
+    else tc::launch<256, 4>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per L2 byte at K = 512 (vs 64 for 128 x 128) — the encoder
     // GEMMs are bound by L2 -> SM operand traffic

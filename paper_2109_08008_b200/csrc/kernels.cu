@@ -315,6 +315,8 @@ __global__ void __launch_bounds__(256) k_layernorm_vec(const T* __restrict__ in,
                                                        const T* __restrict__ b,
                                                        T* __restrict__ out, int ldo, int rows,
                                                        float eps, const int* __restrict__ dR) {
+  pdl_trigger();
+  pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nrows = dR ? min(rows, *dR) : rows;
   if (row >= nrows) return;
@@ -329,9 +331,11 @@ bool layernorm_vec(const T* in, int ldi, const T* g, const T* b, T* out, int ldo
                    float eps, const int* dR, cudaStream_t s) {
   const bool al = (ldi % 8 == 0) && (ldo % 8 == 0);
   if (d == 512 && al)
-    k_layernorm_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(in, ldi, g, b, out, ldo, rows, eps, dR);
+    launch_k(k_layernorm_vec<T, 16>, ceil_div(rows, 8), 256, 0, s, in, ldi, g, b, out, ldo, rows,
+             eps, dR);
   else if (d == 256 && al)
-    k_layernorm_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(in, ldi, g, b, out, ldo, rows, eps, dR);
+    launch_k(k_layernorm_vec<T, 8>, ceil_div(rows, 8), 256, 0, s, in, ldi, g, b, out, ldo, rows,
+             eps, dR);
   else
     return false;
   NMT_LAUNCH_CHECK();
@@ -343,6 +347,8 @@ __global__ void __launch_bounds__(256) k_embed_dec_ln_vec(
     const int* __restrict__ ids, const T* __restrict__ Em, const float* __restrict__ pe,
     const T* __restrict__ gam, const T* __restrict__ bet, T* __restrict__ g, T* __restrict__ u,
     int rows, float scale, float eps, const int* __restrict__ d_t, const int* __restrict__ dR) {
+  pdl_trigger();
+  pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= min(rows, *dR)) return;
   constexpr int d = 32 * E;
@@ -367,11 +373,11 @@ bool embed_dec_ln_vec(const int* ids, const T* E, const float* pe, const T* gam,
                       T* u, int rows, int d, float scale, float eps, const int* d_t, const int* dR,
                       cudaStream_t s) {
   if (d == 512)
-    k_embed_dec_ln_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows,
-                                                                scale, eps, d_t, dR);
+    launch_k(k_embed_dec_ln_vec<T, 16>, ceil_div(rows, 8), 256, 0, s, ids, E, pe, gam, bet, g, u,
+             rows, scale, eps, d_t, dR);
   else if (d == 256)
-    k_embed_dec_ln_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(ids, E, pe, gam, bet, g, u, rows,
-                                                               scale, eps, d_t, dR);
+    launch_k(k_embed_dec_ln_vec<T, 8>, ceil_div(rows, 8), 256, 0, s, ids, E, pe, gam, bet, g, u,
+             rows, scale, eps, d_t, dR);
   else
     return false;
   NMT_LAUNCH_CHECK();
@@ -451,6 +457,7 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
 __global__ void __launch_bounds__(1024) k_prune(DevState* st, int* row_slot, int* prev_tok,
                                                 uint8_t* done, int every, float ratio,
                                                 int* new_to_old, float* score) {
+  pdl_wait();
   prune_body(st, row_slot, prev_tok, done, every, ratio, new_to_old, score);
 }
 
@@ -460,6 +467,7 @@ __global__ void __launch_bounds__(1024) k_finish_prune(
     unsigned long long* __restrict__ keys, int* __restrict__ prev_tok, uint8_t* __restrict__ done,
     int* __restrict__ row_slot, const int* __restrict__ cap, int* __restrict__ out_tok,
     int out_stride, int* __restrict__ gen_len, DevState* st, int eos, int every, float ratio) {
+  pdl_wait();
   __shared__ int s_new;
   if (threadIdx.x == 0) s_new = 0;
   __syncthreads();
@@ -492,8 +500,8 @@ void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* r
                   const int* cap, int* out_tok, int out_stride, int* gen_len, DevState* st,
                   int eos, int every, float ratio, int rows_upper, cudaStream_t s) {
   if (rows_upper > kPruneMaxRows) throw CudaError("finish_prune: too many rows");
-  k_finish_prune<<<1, 1024, 0, s>>>(keys, prev_tok, done, row_slot, cap, out_tok, out_stride,
-                                    gen_len, st, eos, every, ratio);
+  launch_k(k_finish_prune, 1, 1024, 0, s, keys, prev_tok, done, row_slot, cap, out_tok, out_stride,
+           gen_len, st, eos, every, ratio);
   NMT_LAUNCH_CHECK();
 }
 
@@ -567,7 +575,7 @@ __device__ void prune_body(DevState* st, int* row_slot, int* prev_tok, uint8_t* 
 void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, int every,
                    float ratio, int* new_to_old, int rows_upper, cudaStream_t s, float* score) {
   if (rows_upper > kPruneMaxRows) throw CudaError("prune_compact: too many rows");
-  k_prune<<<1, 1024, 0, s>>>(st, row_slot, prev_tok, done, every, ratio, new_to_old, score);
+  launch_k(k_prune, 1, 1024, 0, s, st, row_slot, prev_tok, done, every, ratio, new_to_old, score);
   NMT_LAUNCH_CHECK();
 }
 
