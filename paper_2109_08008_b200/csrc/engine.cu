@@ -18,6 +18,7 @@
 namespace nmt {
 std::atomic<unsigned long long> g_launches{0};
 thread_local bool g_pdl = false;
+thread_local std::vector<nmt_model::ProfRec>* g_prof_capture = nullptr;
 thread_local std::string g_err;
 }  // namespace nmt
 
@@ -451,32 +452,59 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
   unsigned rb;
   memcpy(&rb, &ratio, 4);
   auto key = std::make_tuple(bucket, every, rb, b.K);
-  if (m->prof.on || s == nullptr || !m->eager_keys.count(key)) {
+  if (s == nullptr || !m->eager_keys.count(key)) {
     b.rows_upper = rows;
     eager();  // first use of a configuration runs eagerly (sets kernel attributes)
     m->eager_keys.insert(key);
     return;
   }
-  auto it = m->graphs.find(key);
-  if (it == m->graphs.end()) {
+  auto capture = [&](std::vector<nmt_model::ProfRec>* recs) {
     b.rows_upper = bucket;
     cudaGraph_t g;
     NMT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     g_pdl = pdl_enabled();  // programmatic edges between the step's kernels
+    g_prof_capture = recs;
     try {
       eager();
     } catch (...) {
       g_pdl = false;
+      g_prof_capture = nullptr;
       cudaStreamEndCapture(s, &g);
       throw;
     }
     g_pdl = false;
+    g_prof_capture = nullptr;
     NMT_CUDA(cudaStreamEndCapture(s, &g));
     cudaGraphExec_t ex;
     NMT_CUDA(cudaGraphInstantiate(&ex, g, 0));
     NMT_CUDA(cudaGraphDestroy(g));
-    it = m->graphs.emplace(key, ex).first;
+    return ex;
+  };
+  if (m->prof.on) {
+    // profiled replay: the same graph with an external event pair around every kernel,
+    // read back after each step (timings of the kernels as they run in the graph)
+    auto it = m->pgraphs.find(key);
+    if (it == m->pgraphs.end()) {
+      std::vector<nmt_model::ProfRec> recs;
+      cudaGraphExec_t ex = capture(&recs);
+      it = m->pgraphs.emplace(key, std::make_pair(ex, std::move(recs))).first;
+    }
+    NMT_CUDA(cudaGraphLaunch(it->second.first, s));
+    NMT_CUDA(cudaStreamSynchronize(s));
+    auto& P = m->prof;
+    for (auto& r : it->second.second) {
+      float ms = 0.f;
+      NMT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      P.ms[r.cls] += ms;
+      P.flops[r.cls] += r.flops;
+      P.bytes[r.cls] += r.bytes;
+      P.n[r.cls] += 1;
+    }
+    g_launches += 1;
+    return;
   }
+  auto it = m->graphs.find(key);
+  if (it == m->graphs.end()) it = m->graphs.emplace(key, capture(nullptr)).first;
   NMT_CUDA(cudaGraphLaunch(it->second, s));
   g_launches += 1;
 }

@@ -128,6 +128,9 @@ struct nmt_model {
   // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits)
   std::map<std::tuple<int, int, unsigned, int>, cudaGraphExec_t> graphs;
   std::set<std::tuple<int, int, unsigned, int>> eager_keys;  // configurations run eagerly once
+  // profiled variants of the step graphs: the graph plus its per-launch event pairs
+  std::map<std::tuple<int, int, unsigned, int>,
+           std::pair<cudaGraphExec_t, std::vector<ProfRec>>> pgraphs;
   // Concurrent batch workers (the GPU analog of the paper's parallel decoding processes,
   // PAPER.md:129-131): clones sharing this model's weights, each with its own arena,
   // stream, batch state and graphs.  Created lazily by nmt_translate*(n_workers > 1).
@@ -137,6 +140,13 @@ struct nmt_model {
   ~nmt_model() {
     for (auto* w : workers) delete w;
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : pgraphs) {
+      cudaGraphExecDestroy(kv.second.first);
+      for (auto& r : kv.second.second) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+      }
+    }
     for (auto e : prof.pool) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (wbuf && owns_weights) cudaFree(wbuf);
@@ -152,11 +162,24 @@ void encode_any(nmt_model* m, int B, int S, cudaStream_t s);
 void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
                      cudaStream_t s, bool finish = true);
 void prof_flush(nmt_model* m);
+// While a profiled decode step is being captured, its event pairs are recorded as external
+// event nodes of the graph (replayed and read after every launch of that graph).
+extern thread_local std::vector<nmt_model::ProfRec>* g_prof_capture;
 template <class F>
 void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {
   auto& P = m->prof;
   if (!P.on) {
     f();
+    return;
+  }
+  if (g_prof_capture) {
+    cudaEvent_t a, b;
+    NMT_CUDA(cudaEventCreate(&a));
+    NMT_CUDA(cudaEventCreate(&b));
+    NMT_CUDA(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
+    f();
+    NMT_CUDA(cudaEventRecordWithFlags(b, s, cudaEventRecordExternal));
+    g_prof_capture->push_back({cls, a, b, flops, bytes});
     return;
   }
   while (P.pool.size() < P.used + 2) {
