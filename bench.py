@@ -2,7 +2,7 @@
 """Benchmark of the B200 hot path: FP16 greedy translation with the 35-1 Transformer-DLCL-RPR
 student (BASELINE.json configs[2], metric "target tokens/sec ... ms/decode step").
 
-A step = nmt_translate_device over one newstest-sized chunk (2998 sentences) of the
+A step = nmt_translate_device over one 12000-sentence chunk (4 x newstest2018) of the
 synthetic 1M-sentence set (DESIGN.md input recipe): length sort, dynamic 4096-token /
 512-sentence batches, 35-layer encoder with RPR + DLCL, cached greedy
 decoding with the fused vocab argmax, batch pruning (rho = 0.25).  Each rank/step gets a
@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "target tokens/sec (FP16 greedy, 35-1 student) at 1/2/4/8 B200; ms/decode step"
 UNIT = "target tokens/s"
-CHUNK = 2998            # newstest2018-sized chunk
+CHUNK = 12000           # 4 newstest2018-sized sets (2998 sentences each)
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # Encoder GEMMs are dense contractions at N = 16K rows (tensor-bound); the decoder GEMMs and
 # the vocab projection run at B_live ~ 100-500 rows, below the ~250 FLOP/B ridge: HBM/L2-bound
@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--max-tokens", type=int, default=16384)
     ap.add_argument("--max-sents", type=int, default=2048)
     ap.add_argument("--sync-every", type=int, default=4)
-    ap.add_argument("--workers", type=int, default=2,
+    ap.add_argument("--workers", type=int, default=3,
                     help="concurrent batch workers per GPU (own arena + stream, shared weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
@@ -315,7 +315,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": f"{args.config} FP16 greedy, {args.chunk}-sentence newstest-shaped "
-                                   f"chunk per rank per step, batch pruning rho=0.25",
+                                   f"chunk per rank per step, batch pruning rho=0.25, "
+                                   f"{args.workers} concurrent batch workers",
                        "max_tokens": args.max_tokens, "max_sents": args.max_sents,
                        "parallelism": f"sentence-sharded x{world}",
                        "l2": "working set > L2 (262 MB FP16 weights + DLCL history)"},
