@@ -248,261 +248,6 @@ void launch_enc(const T* qkv, const int* len, const T* relk, const T* relv, T* o
   NMT_LAUNCH_CHECK();
 }
 
-// ----------------------------------------------------------------- encoder, FP16 tensor cores
-// Same computation for the FP16 path with warp-level mma.sync (m16n8k16, FP16 in / FP32
-// accumulate): S = Q K^T and O = P V on tensor cores, the RPR terms q . A^K[r] and
-// sum_r B_ir A^V[r] in FP32 SIMT.  Scores, softmax and bucket sums stay in registers
-// (FP32); P is rounded to FP16 only as the A operand of P V (within the FP16-mode
-// tolerance).  One CTA per (sentence, head), 4 warps, each owning 16-query blocks.
-__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"((uint32_t)__cvta_generic_to_shared(p)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"((uint32_t)__cvta_generic_to_shared(p)));
-}
-__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
-  __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-template <int DH, int NT>  // NT = number of 8-wide key tiles (Sp = 8*NT, multiple of 16)
-__global__ void __launch_bounds__(128) k_attn_enc_mma(const __half* __restrict__ qkv,
-                                                      const int* __restrict__ len,
-                                                      const __half* __restrict__ relk,
-                                                      const __half* __restrict__ relv,
-                                                      __half* __restrict__ out, int S, int d,
-                                                      int kclip, int use_rpr) {
-  constexpr int SP = NT * 8, LDH = DH + 8;  // padded row (16-B multiple, conflict-free ldmatrix)
-  extern __shared__ __align__(16) uint8_t smraw[];
-  __half* sQ = reinterpret_cast<__half*>(smraw);   // [SP][LDH]
-  __half* sK = sQ + SP * LDH;                       // [SP][LDH]
-  __half* sV = sK + SP * LDH;                       // [SP][LDH]
-  float* sAK = reinterpret_cast<float*>(sV + SP * LDH);  // [R][DH]
-  float* sAV = sAK + 32 * (DH + 1);                       // [R][DH]  (sAK rows padded: DH+1)
-  float* sQA = sAV + 32 * DH;                             // [SP][R+1]
-  float* sB = sQA + SP * 33;                              // [SP][R+1]
-  const int b = blockIdx.x, h = blockIdx.y;
-  const int R = 2 * kclip + 1, LB = 33;
-  const int n = len[b];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const size_t rs = 3 * (size_t)d;
-  const __half* base = qkv + (size_t)b * S * rs + h * DH;
-  // stage Q, K, V (zero rows >= n) and the relative tables
-  for (int idx = tid; idx < SP * (DH / 8); idx += 128) {
-    const int j = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
-    uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
-    if (j < n) {
-      const __half* rp = base + (size_t)j * rs + c;
-      q = *reinterpret_cast<const uint4*>(rp);
-      k = *reinterpret_cast<const uint4*>(rp + d);
-      v = *reinterpret_cast<const uint4*>(rp + 2 * d);
-    }
-    *reinterpret_cast<uint4*>(sQ + j * LDH + c) = q;
-    *reinterpret_cast<uint4*>(sK + j * LDH + c) = k;
-    *reinterpret_cast<uint4*>(sV + j * LDH + c) = v;
-  }
-  if (use_rpr) {
-    for (int idx = tid; idx < R * DH; idx += 128) {
-      sAK[(idx / DH) * (DH + 1) + idx % DH] = __half2float(relk[idx]);
-      sAV[idx] = __half2float(relv[idx]);
-    }
-    for (int idx = tid; idx < SP * LB; idx += 128) sB[idx] = 0.f;
-  }
-  __syncthreads();
-  if (use_rpr)  // q_i . A^K[r] (FP32 SIMT)
-    for (int idx = tid; idx < n * R; idx += 128) {
-      const int i = idx / R, r = idx - i * R;
-      float a = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < DH; ++c) a = fmaf(__half2float(sQ[i * LDH + c]), sAK[r * (DH + 1) + c], a);
-      sQA[i * LB + r] = a;
-    }
-  __syncthreads();
-  const float scale = rsqrtf((float)DH);
-  const int g = lane >> 2, tig = lane & 3;
-  const int nblk = (n + 15) >> 4;
-  for (int mb = warp; mb < nblk; mb += 4) {
-    const int m0 = mb * 16;
-    // ---- S = Q K^T for rows m0..m0+15, all SP key columns
-    float sc[NT][4];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
-#pragma unroll
-    for (int k0 = 0; k0 < DH; k0 += 16) {
-      uint32_t af[4];
-      {
-        const int mi = lane >> 3, rr = lane & 7;
-        ldsm_x4(af, sQ + (m0 + rr + (mi & 1) * 8) * LDH + k0 + (mi >> 1) * 8);
-      }
-#pragma unroll
-      for (int t = 0; t < NT; t += 2) {
-        uint32_t bf[4];  // matrices (t, k0) (t, k0+8) (t+1, k0) (t+1, k0+8)
-        const int mi = lane >> 3, rr = lane & 7;
-        ldsm_x4(bf, sK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
-        mma16816(sc[t], af, bf[0], bf[1]);
-        mma16816(sc[t + 1], af, bf[2], bf[3]);
-      }
-    }
-    // ---- RPR key term, mask, scale, softmax (rows r0 = m0+g, r1 = m0+g+8)
-    const int r0 = m0 + g, r1 = r0 + 8;
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = e < 2 ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
-        float v = sc[t][e];
-        if (j < n && i < n) {
-          if (use_rpr) v += sQA[i * LB + min(max(j - i, -kclip), kclip) + kclip];
-          v *= scale;
-        } else {
-          v = -INFINITY;
-        }
-        sc[t][e] = v;
-        if (e < 2) mx0 = fmaxf(mx0, v);
-        else mx1 = fmaxf(mx1, v);
-      }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
-    if (mx1 == -INFINITY) mx1 = 0.f;
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float v = __expf(sc[t][e] - (e < 2 ? mx0 : mx1));
-        sc[t][e] = v;
-        if (e < 2) s0 += v;
-        else s1 += v;
-      }
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    const float inv0 = s0 > 0.f ? 1.f / s0 : 0.f, inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
-    float lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool top = e < 2;
-        const int i = top ? r0 : r1, j = t * 8 + 2 * tig + (e & 1);
-        const float p = sc[t][e] * (top ? inv0 : inv1);
-        sc[t][e] = p;
-        if (use_rpr && i < n && j < n) {
-          const int dj = j - i;
-          if (dj <= -kclip) { if (top) lo0 += p; else lo1 += p; }
-          else if (dj >= kclip) { if (top) hi0 += p; else hi1 += p; }
-          else sB[i * LB + dj + kclip] = p;  // unique writer per (i, middle bucket)
-        }
-      }
-    if (use_rpr) {
-      lo0 += __shfl_xor_sync(0xffffffffu, lo0, 1); lo0 += __shfl_xor_sync(0xffffffffu, lo0, 2);
-      hi0 += __shfl_xor_sync(0xffffffffu, hi0, 1); hi0 += __shfl_xor_sync(0xffffffffu, hi0, 2);
-      lo1 += __shfl_xor_sync(0xffffffffu, lo1, 1); lo1 += __shfl_xor_sync(0xffffffffu, lo1, 2);
-      hi1 += __shfl_xor_sync(0xffffffffu, hi1, 1); hi1 += __shfl_xor_sync(0xffffffffu, hi1, 2);
-      if (tig == 0) {
-        if (r0 < n) { sB[r0 * LB] = lo0; sB[r0 * LB + R - 1] = hi0; }
-        if (r1 < n) { sB[r1 * LB] = lo1; sB[r1 * LB + R - 1] = hi1; }
-      }
-    }
-    // ---- O = P V (P from registers as FP16 A fragments)
-    float oc[DH / 8][4];
-#pragma unroll
-    for (int t = 0; t < DH / 8; ++t) oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < NT / 2; ++kk) {
-      uint32_t af[4];
-      af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
-      af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
-      af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-      af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 16) {
-        uint32_t bf[4];  // .trans: (j0,c0) (j0+8,c0) (j0,c0+8) (j0+8,c0+8)
-        const int mi = lane >> 3, rr = lane & 7;
-        ldsm_x4_t(bf, sV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
-        mma16816(oc[c0 / 8], af, bf[0], bf[1]);
-        mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
-      }
-    }
-    __syncwarp();
-    // ---- + sum_r B_ir A^V[r][c], store (rows >= n written as 0)
-    __half* orow0 = out + ((size_t)b * S + r0) * d + h * DH;
-    __half* orow1 = out + ((size_t)b * S + r1) * d + h * DH;
-#pragma unroll
-    for (int t = 0; t < DH / 8; ++t) {
-      const int c = t * 8 + 2 * tig;
-      float o00 = oc[t][0], o01 = oc[t][1], o10 = oc[t][2], o11 = oc[t][3];
-      if (use_rpr) {
-        for (int r = 0; r < R; ++r) {
-          const float b0 = r0 < n ? sB[r0 * LB + r] : 0.f, b1 = r1 < n ? sB[r1 * LB + r] : 0.f;
-          const float a0 = sAV[r * DH + c], a1 = sAV[r * DH + c + 1];
-          o00 = fmaf(b0, a0, o00); o01 = fmaf(b0, a1, o01);
-          o10 = fmaf(b1, a0, o10); o11 = fmaf(b1, a1, o11);
-        }
-      }
-      if (r0 < S)
-        *reinterpret_cast<__half2*>(orow0 + c) =
-            r0 < n ? __floats2half2_rn(o00, o01) : __floats2half2_rn(0.f, 0.f);
-      if (r1 < S)
-        *reinterpret_cast<__half2*>(orow1 + c) =
-            r1 < n ? __floats2half2_rn(o10, o11) : __floats2half2_rn(0.f, 0.f);
-    }
-  }
-  // query rows beyond the last 16-block are padding: zero them
-  for (int idx = nblk * 16 * DH + tid; idx < S * DH; idx += 128) {
-    const int i = idx / DH, c = idx - i * DH;
-    out[((size_t)b * S + i) * d + h * DH + c] = __float2half(0.f);
-  }
-}
-
-template <int DH>
-void launch_enc_mma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
-                    __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
-  const int sp = (S + 15) / 16 * 16;
-  auto smem_for = [](int SP) {
-    return (size_t)3 * SP * (DH + 8) * 2 + 32 * (2 * DH + 1) * 4 + 2 * SP * 33 * 4;
-  };
-#define NMT_EM(NTV)                                                                          \
-  {                                                                                          \
-    static bool attr = false;                                                                \
-    if (!attr) {                                                                             \
-      NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_mma<DH, NTV>,                                \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-      attr = true;                                                                           \
-    }                                                                                        \
-    k_attn_enc_mma<DH, NTV><<<dim3(B, H), 128, smem_for(NTV * 8), s>>>(qkv, len, relk, relv, \
-                                                                      out, S, d, kclip,       \
-                                                                      use_rpr);               \
-  }
-  if (sp <= 16) NMT_EM(2)
-  else if (sp <= 32) NMT_EM(4)
-  else if (sp <= 48) NMT_EM(6)
-  else if (sp <= 64) NMT_EM(8)
-  else if (sp <= 80) NMT_EM(10)
-  else if (sp <= 96) NMT_EM(12)
-  else if (sp <= 112) NMT_EM(14)
-  else if (sp <= 128) NMT_EM(16)
-  else throw CudaError("attn_encoder: S > 128");
-#undef NMT_EM
-  NMT_LAUNCH_CHECK();
-}
-
 template <class T>
 void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T* out, int B, int S,
                   int d, int H, int kclip, int use_rpr, cudaStream_t s) {
@@ -521,141 +266,239 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
   }
 }
 
-// o[0..8) = sum_{j < n} p[j] * V[j][c0 .. c0+8) for this lane's 8-channel group (lanes
-// 0..DH/8-1 hold the result).  G = DH/8 lanes share a value row (one 16-B load each), a
-// warp covers 32/G rows per iteration; the row groups are combined by xor-shuffles.
-// Row j lives in slot (anc_row && j < t_own ? anc_row[j] : own_slot): beam hypotheses read
-// their ancestors' cached positions through the ancestry table (no K/V copies).
-template <class T, int DH>
-__device__ __forceinline__ void pv_accumulate(const float* __restrict__ p,
-                                              const T* __restrict__ v0, size_t slot_stride,
-                                              int own_slot, const int* __restrict__ anc_row,
-                                              int t_own, int stride, int n, int lane, float* o) {
-  constexpr int G = DH / 8, KP = 32 / G;
-  const int sub = lane % G, kq = lane / G;
-  float a[8];
+// ----------------------------------------------------------------- decoder attention
+// One warp per (live row, head).  The keys are split over lane groups: G = DH/8 lanes hold
+// the 8-channel slices of one key (one 16-B load each, a group reads the key's contiguous
+// DH-element head slice), KP = 32/G keys per warp pass, U passes per chunk of CH = KP*U
+// keys.  A chunk issues all of its K and V loads before any arithmetic (2U independent
+// loads per lane in flight), so a step costs about one memory round trip per chunk instead
+// of a dependent chain per key.  Softmax is online over chunks (running max and sum,
+// FP32, rescaled per chunk).  The RPR value term is folded per key, v_j + A^V[r(j)], which
+// is the same sum as the bucket form sum_r (sum_{j in r} a_j) A^V[r] above.
+template <class T> struct Raw8;   // 8 consecutive elements in their storage type
+template <> struct Raw8<__half> {
+  uint4 u;
+  __device__ __forceinline__ void load(const __half* p) { u = *reinterpret_cast<const uint4*>(p); }
+  __device__ __forceinline__ void store(__half* p) const { *reinterpret_cast<uint4*>(p) = u; }
+  __device__ __forceinline__ void zero() { u = make_uint4(0u, 0u, 0u, 0u); }
+  __device__ __forceinline__ void to_f(float* f) const {
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) a[e] = 0.f;
-#pragma unroll 2
-  for (int j0 = 0; j0 < n; j0 += KP) {
-    const int j = j0 + kq;
-    if (j < n) {
-      float v[8];
-      const int sl = (anc_row && j < t_own) ? anc_row[j] : own_slot;
-      Vec8<T>::load(v0 + (size_t)sl * slot_stride + (size_t)j * stride + sub * 8, v);
-      const float pj = p[j];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = fmaf(pj, v[e], a[e]);
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __half22float2(h[e]);
+      f[2 * e] = x.x;
+      f[2 * e + 1] = x.y;
     }
   }
+};
+template <> struct Raw8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = reinterpret_cast<const float4*>(p)[0];
+    b = reinterpret_cast<const float4*>(p)[1];
+  }
+  __device__ __forceinline__ void store(float* p) const {
+    reinterpret_cast<float4*>(p)[0] = a;
+    reinterpret_cast<float4*>(p)[1] = b;
+  }
+  __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ void to_f(float* f) const {
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+};
+
+template <class T, int DH>
+struct WarpAttn {
+  static constexpr int G = DH / 8, KP = 32 / G;
+  static constexpr int U = sizeof(T) == 2 ? G : (G >= 2 ? G / 2 : 1);
+  static constexpr int CH = KP * U;
+  int sub, kq;
+  float q[8], m, l, acc[8];
+
+  // q (this lane's 8 channels) pre-multiplied by 1/sqrt(dh)
+  __device__ __forceinline__ void init(int lane, const T* qhead, float scale) {
+    sub = lane % G;
+    kq = lane / G;
+    Raw8<T> r;
+    r.load(qhead + sub * 8);
+    r.to_f(q);
 #pragma unroll
-  for (int off = G; off < 32; off <<= 1)
+    for (int e = 0; e < 8; ++e) q[e] *= scale, acc[e] = 0.f;
+    m = -INFINITY;
+    l = 0.f;
+  }
+  // q . x over the head, x given as this lane's 8 channels (all lanes must call)
+  __device__ __forceinline__ float group_dot(const float* x) const {
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] += __shfl_xor_sync(0xffffffffu, a[e], off);
+    for (int e = 0; e < 8; e += 2) {
+      s0 = fmaf(q[e], x[e], s0);
+      s1 = fmaf(q[e + 1], x[e + 1], s1);
+    }
+    float s = s0 + s1;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) o[e] = a[e];
+    for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+  }
+  // Keys [j0, j0 + CH) with j < n (requires j0 < n).  addr(j, kp, vp) sets the head-slice
+  // pointers of key j; bias(j) is added to the scaled score; vadd(j, v) adds to v_j.
+  template <class ADDR, class BIAS, class VADD>
+  __device__ __forceinline__ void chunk(int j0, int n, ADDR addr, BIAS bias, VADD vadd) {
+    Raw8<T> kr[U], vr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * KP + kq;
+      if (j < n) {
+        const T *kp, *vp;
+        addr(j, kp, vp);
+        kr[u].load(kp + sub * 8);
+        vr[u].load(vp + sub * 8);
+      } else {
+        kr[u].zero();
+        vr[u].zero();
+      }
+    }
+    float s[U], cm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * KP + kq;
+      float f[8];
+      kr[u].to_f(f);
+      const float e = group_dot(f);
+      s[u] = j < n ? e + bias(j) : -INFINITY;
+      cm = fmaxf(cm, s[u]);
+    }
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+    const float mn = fmaxf(m, cm);
+    const float corr = __expf(m - mn);
+    l *= corr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * KP + kq;
+      if (j < n) {
+        const float p = __expf(s[u] - mn);
+        float f[8];
+        vr[u].to_f(f);
+        vadd(j, f);
+        l += p;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaf(p, f[e], acc[e]);
+      }
+    }
+    m = mn;
+  }
+  // Sum over the KP key groups; every lane ends with the normalised output of its channels.
+  __device__ __forceinline__ void finish(float* o) {
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, off);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
+    }
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = acc[e] * inv;
+  }
+};
+
+template <class T>
+__device__ __forceinline__ void store8(T* p, const float* o) {
+  if constexpr (sizeof(T) == 2) {
+    uint4 u;
+    __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2half2_rn(o[2 * e], o[2 * e + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  } else {
+    reinterpret_cast<float4*>(p)[0] = make_float4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(o[4], o[5], o[6], o[7]);
+  }
 }
 
 // ----------------------------------------------------------------- decoder self-attention
-// One warp per (live row, head) at step t = *d_t: k_t, v_t are appended to the cache slot,
-// then positions 0..t are attended; only buckets 0..k occur (j <= t) and every
-// j <= t - k falls in bucket 0.
+// Step t = *d_t: k_t, v_t are appended to the row's cache slot and
+// positions 0..t attended; key t is taken from the fresh projection.  Only buckets
+// r = clip(j - t, -k, k) + k in 0..k occur (j <= t).  Beam rows read their ancestors'
+// cached positions j < t through the ancestry table (no K/V copies).
 template <class T, int DH>
 __global__ void __launch_bounds__(128) k_attn_dec_self(
     const T* __restrict__ qkv, T* __restrict__ kc, T* __restrict__ vc, int Tmax,
     const int* __restrict__ row_slot, const T* __restrict__ relk, const T* __restrict__ relv,
     T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
     const int* __restrict__ dR, const int* __restrict__ anc) {
-  extern __shared__ float sm[];
+  __shared__ float s_relv[16][DH];  // A^V[0..k] (k <= 15), shared by every head
+  __shared__ float s_x[4][16];      // per warp: q . A^K[r] / sqrt(dh), r = 0..k
+  using WA = WarpAttn<T, DH>;
   pdl_trigger();
   pdl_wait();
+  if (use_rpr)
+    for (int i = threadIdx.x; i < (kclip + 1) * DH; i += blockDim.x)
+      s_relv[i / DH][i % DH] = to_f(relv[i]);
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
   if (row >= min(rows, *dR)) return;
   const int t = *d_t;
-  float* q = sm + warp * (DH + 32 + Tmax);
-  float* x = q + DH;   // q . A^K[r], then bucket sums
-  float* p = x + 32;
   const int slot = row_slot[row];
   const T* src = qkv + (size_t)row * 3 * d + h * DH;
-  T* kbase = kc + (size_t)slot * Tmax * d + h * DH;
-  T* vbase = vc + (size_t)slot * Tmax * d + h * DH;
-  for (int c = lane; c < DH; c += 32) {
-    q[c] = to_f(src[c]);
-    kbase[(size_t)t * d + c] = src[d + c];        // KV-cache append
-    vbase[(size_t)t * d + c] = src[2 * d + c];
+  WA w;
+  w.init(lane, src, rsqrtf((float)DH));
+  if (w.kq == 0) {  // KV-cache append at position t
+    Raw8<T> r;
+    r.load(src + d + w.sub * 8);
+    r.store(kc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
+    r.load(src + 2 * d + w.sub * 8);
+    r.store(vc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
   }
-  __syncwarp();
-  if (use_rpr && lane <= kclip) {
-    float a = 0.f;
-#pragma unroll 8
-    for (int c = 0; c < DH; ++c) a = fmaf(q[c], to_f(relk[lane * DH + c]), a);
-    x[lane] = a;
-  }
-  __syncwarp();
-  const float scale = rsqrtf((float)DH);
-  float mx = -INFINITY;
-  const int* anc_row = anc ? anc + (size_t)slot * Tmax : nullptr;
-  for (int j = lane; j <= t; j += 32) {
-    const int sl = (anc_row && j < t) ? anc_row[j] : slot;
-    const T* kr = kc + ((size_t)sl * Tmax + j) * d + h * DH;
-    float e0 = 0.f, e1 = 0.f;
-#pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      float f[8];
-      Vec8<T>::load(kr + c, f);
-#pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        e0 = fmaf(f[u], q[c + u], e0);
-        e1 = fmaf(f[u + 1], q[c + u + 1], e1);
-      }
-    }
-    float e = e0 + e1;
-    if (use_rpr) e += x[max(j - t, -kclip) + kclip];
-    e *= scale;
-    p[j] = e;
-    mx = fmaxf(mx, e);
-  }
-  mx = warp_max(mx);
-  float sum = 0.f, lo = 0.f;
-  for (int j = lane; j <= t; j += 32) {
-    const float e = __expf(p[j] - mx);
-    p[j] = e;
-    sum += e;
-    if (j <= t - kclip) lo += e;
-  }
-  const float inv = 1.f / warp_sum(sum);
-  lo = warp_sum(lo);
-  __syncwarp();
+  float* x = s_x[warp];
   if (use_rpr) {
-    if (lane <= kclip) {
-      float bsum;
-      if (lane == 0) bsum = lo;
-      else {
-        const int j = t - kclip + lane;
-        bsum = j >= 0 ? p[j] : 0.f;
+    for (int b0 = 0; b0 <= kclip; b0 += WA::KP) {
+      const int b = b0 + w.kq;
+      float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (b <= kclip) {
+        Raw8<T> r;
+        r.load(relk + b * DH + w.sub * 8);
+        r.to_f(f);
       }
-      x[lane] = bsum;  // (unnormalised)
+      const float e = w.group_dot(f);
+      if (b <= kclip && w.sub == 0) x[b] = e;
     }
     __syncwarp();
   }
-  float o[8];
-  pv_accumulate<T, DH>(p, vc + h * DH, (size_t)Tmax * d, slot, anc_row, t, d, t + 1, lane, o);
-  constexpr int G = DH / 8;
-  if (lane < G) {
-    const int c0 = lane * 8;
-    if (use_rpr)
-      for (int b = 0; b <= kclip; ++b) {
-        float rv[8];
-        Vec8<T>::load(relv + b * DH + c0, rv);
+  const int* anc_row = anc ? anc + (size_t)slot * Tmax : nullptr;
+  const size_t hoff = (size_t)h * DH;
+  auto addr = [&](int j, const T*& kp, const T*& vp) {
+    if (j == t) {
+      kp = src + d;
+      vp = src + 2 * d;
+    } else {
+      const int sl = anc_row ? anc_row[j] : slot;
+      const size_t o = ((size_t)sl * Tmax + j) * d + hoff;
+      kp = kc + o;
+      vp = vc + o;
+    }
+  };
+  const int n = t + 1;
+  if (use_rpr) {
+    auto bias = [&](int j) { return x[max(j - t, -kclip) + kclip]; };
+    auto vadd = [&](int j, float* f) {
+      const float* rv = s_relv[max(j - t, -kclip) + kclip] + w.sub * 8;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = fmaf(x[b], rv[e], o[e]);
-      }
-    T* orow = out + (size_t)row * d + h * DH + c0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) orow[e] = from_f<T>(o[e] * inv);
+      for (int e = 0; e < 8; ++e) f[e] += rv[e];
+    };
+    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
+  } else {
+    auto bias = [](int) { return 0.f; };
+    auto vadd = [](int, float*) {};
+    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
   }
+  float o[8];
+  w.finish(o);
+  if (w.kq == 0) store8(out + (size_t)row * d + hoff + w.sub * 8, o);
 }
 
 template <class T>
@@ -664,10 +507,9 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
                        const int* d_t, const int* dR, const int* anc, cudaStream_t s) {
   if (rows <= 0) return;
   const int nw = 4, dh = d / H;
-  size_t smem = sizeof(float) * nw * (dh + 32 + Tmax);
   dim3 grid(ceil_div(rows * H, nw));
-#define NMT_DS(DH)                                                                             \
-  launch_k(k_attn_dec_self<T, DH>, grid, nw * 32, smem, s, qkv, kc, vc, Tmax, row_slot, relk, \
+#define NMT_DS(DH)                                                                           \
+  launch_k(k_attn_dec_self<T, DH>, grid, nw * 32, 0, s, qkv, kc, vc, Tmax, row_slot, relk, \
            relv, out, rows, d, H, kclip, use_rpr, d_t, dR, anc)
   switch (dh) {
     case 16: NMT_DS(16); break;
@@ -680,16 +522,17 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
 }
 
 // ----------------------------------------------------------------- cross-attention
-// One warp per (live row, head); keys at ckv + (slot*S + j)*ldkv + koff + h*dh, values at
-// + voff; mask j < src_len[slot].  S = *dS (device) so a captured step graph serves every
-// batch; Smax sizes shared memory.
+// One warp per (live row, head) over the sentence's once-computed encoder K/V:
+// keys at ckv + (slot*S + j)*ldkv + koff + h*dh, values at + voff; mask j < src_len[slot].
+// S = *dS (device) so a captured step graph serves every batch.  Beam rows share their
+// sentence's K/V (slot = row slot / beam).
 template <class T, int DH>
 __global__ void __launch_bounds__(128) k_attn_cross(
     const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv, int koff, int voff,
-    const int* __restrict__ dS, int Smax, const int* __restrict__ src_len,
+    const int* __restrict__ dS, const int* __restrict__ src_len,
     const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,
     const int* __restrict__ dR, int beam) {
-  extern __shared__ float sm[];
+  using WA = WarpAttn<T, DH>;
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -697,49 +540,21 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   const int row = gw / H, h = gw - (gw / H) * H;
   if (row >= min(rows, *dR)) return;
   const int S = *dS;
-  float* q = sm + warp * (DH + Smax);
-  float* p = q + DH;
-  const int slot = row_slot[row] / beam;  // sentence slot (beam rows share the encoder K/V)
+  const int slot = row_slot[row] / beam;
   const int n = src_len[slot];
-  for (int c = lane; c < DH; c += 32) q[c] = to_f(qb[(size_t)row * d + h * DH + c]);
-  __syncwarp();
-  const float scale = rsqrtf((float)DH);
+  WA w;
+  w.init(lane, qb + (size_t)row * d + h * DH, rsqrtf((float)DH));
   const T* base = ckv + (size_t)slot * S * ldkv + h * DH;
-  float mx = -INFINITY;
-  for (int j = lane; j < n; j += 32) {
-    const T* kr = base + (size_t)j * ldkv + koff;
-    float e0 = 0.f, e1 = 0.f;
-#pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      float f[8];
-      Vec8<T>::load(kr + c, f);
-#pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        e0 = fmaf(f[u], q[c + u], e0);
-        e1 = fmaf(f[u + 1], q[c + u + 1], e1);
-      }
-    }
-    const float e = (e0 + e1) * scale;
-    p[j] = e;
-    mx = fmaxf(mx, e);
-  }
-  mx = warp_max(mx);
-  float sum = 0.f;
-  for (int j = lane; j < n; j += 32) {
-    const float e = __expf(p[j] - mx);
-    p[j] = e;
-    sum += e;
-  }
-  const float inv = 1.f / warp_sum(sum);
-  __syncwarp();
+  auto addr = [&](int j, const T*& kp, const T*& vp) {
+    kp = base + (size_t)j * ldkv + koff;
+    vp = base + (size_t)j * ldkv + voff;
+  };
+  auto bias = [](int) { return 0.f; };
+  auto vadd = [](int, float*) {};
+  for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
   float o[8];
-  pv_accumulate<T, DH>(p, base + voff, 0, 0, nullptr, 0, ldkv, n, lane, o);
-  constexpr int G = DH / 8;
-  if (lane < G) {
-    T* orow = out + (size_t)row * d + h * DH + lane * 8;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) orow[e] = from_f<T>(o[e] * inv);
-  }
+  w.finish(o);
+  if (w.kq == 0) store8(out + (size_t)row * d + h * DH + w.sub * 8, o);
 }
 
 template <class T>
@@ -747,12 +562,12 @@ void attn_cross(const T* q, const T* ckv, int ldkv, int koff, int voff, const in
                 const int* src_len, const int* row_slot, T* out, int rows, int d, int H,
                 const int* dR, int beam, cudaStream_t s) {
   if (rows <= 0) return;
+  (void)Smax;
   const int nw = 4, dh = d / H;
-  size_t smem = sizeof(float) * nw * (dh + Smax);
   dim3 grid(ceil_div(rows * H, nw));
 #define NMT_CS(DH)                                                                          \
-  launch_k(k_attn_cross<T, DH>, grid, nw * 32, smem, s, q, ckv, ldkv, koff, voff, dS, Smax, \
-           src_len, row_slot, out, rows, d, H, dR, beam)
+  launch_k(k_attn_cross<T, DH>, grid, nw * 32, 0, s, q, ckv, ldkv, koff, voff, dS, src_len, \
+           row_slot, out, rows, d, H, dR, beam)
   switch (dh) {
     case 16: NMT_CS(16); break;
     case 32: NMT_CS(32); break;
