@@ -44,6 +44,12 @@ template <> __device__ __forceinline__ __half from_f<__half>(float v) {
   v = fminf(fmaxf(v, -65504.f), 65504.f);
   return __float2half_rn(v);
 }
+// (lo, hi) -> saturating round-to-nearest half2 in one instruction (same values as from_f)
+__device__ __forceinline__ uint32_t pack_half2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -93,6 +93,52 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// ---- thread-block cluster / CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  return ra;
+}
+// TMA into this CTA's shared memory, completion counted on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                 int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// M = 256 MMA over the CTA pair: A rows 0-127 / 128-255 and B rows 0-N/2 / N/2-N from the
+// two CTAs' shared memory at the same offsets; D rows split the same way over their TMEM.
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                             uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+// arrive on the mbarrier at this offset in BOTH CTAs of the pair when the MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -135,37 +181,37 @@ struct Params {
   int splits;         // split-K factor (kb_total % splits == 0)
   float* ws;          // split-K partials [tile][split][BM][BN]
   int* counters;      // split-K arrival counters [tile] (self-resetting)
+  int dbg;            // tuning experiments only (NMT_GEMM_DBG): 1 = drain TMEM, no epilogue
+  int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool PAIR = false>
 struct Smem {
+  static constexpr int BROWS = PAIR ? BN / 2 : BN;   // B rows staged by one CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BROWS * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int BYTES = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  // epilogue: per warp a 32 x 32 FP16 staging tile (TMA store) and its FP32 bias slice
+  static constexpr int STG = 2048;
+  static constexpr int EPI = 8 * STG + 8 * (BN / 2) * 4;
+  static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
-// Epilogue for 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators).
-__device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float* v,
-                                           unsigned long long& best, const uint4* pre = nullptr) {
+// Epilogue math on 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators):
+// bias (from the warp's shared-memory slice, zero beyond N), residual (prefetched `pre` or
+// loaded here), ReLU.
+__device__ __forceinline__ void epi_math(const Params& p, int m, int nb, float* v,
+                                         const float* sb, const uint4* pre, bool row_ok) {
   const int nv = min(32, p.N - nb);
   const bool full = nv == 32;
   if (p.bias) {
-    if (full) {
 #pragma unroll
-      for (int j8 = 0; j8 < 4; ++j8) {
-        float f[8];
-        load8h(p.bias + nb + j8 * 8, f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[j8 * 8 + e] += f[e];
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nv) v[j] += __half2float(p.bias[nb + j]);
+    for (int j = 0; j < 32; j += 4) {
+      const float4 b = *reinterpret_cast<const float4*>(sb + j);
+      v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
     }
   }
-  if (p.R) {
+  if (p.R && row_ok && nv > 0) {
     const __half* rr = p.R + (size_t)m * p.ldr + nb;
     if (pre) {  // residual prefetched before the accumulator wait
 #pragma unroll
@@ -196,6 +242,14 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
   }
+}
+
+// Direct outputs of 32 columns (row m < M, nb < N): FP32 logits, the packed argmax, or
+// the FP16 row segment (paths without the TMA-store epilogue).
+__device__ __forceinline__ void epi_out(const Params& p, int m, int nb, const float* v,
+                                        unsigned long long& best) {
+  const int nv = min(32, p.N - nb);
+  const bool full = nv == 32;
   if (p.logits) {
     float* lr = p.logits + (size_t)m * p.N + nb;
     if (full && ((p.N & 3) == 0)) {
@@ -223,10 +277,10 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
 #pragma unroll
     for (int j8 = 0; j8 < 4; ++j8) {
       uint4 pk;
-      __half2* h2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        h2[e] = __halves2half2(from_f<__half>(v[j8 * 8 + 2 * e]), from_f<__half>(v[j8 * 8 + 2 * e + 1]));
+      pk.x = pack_half2_sat(v[j8 * 8 + 0], v[j8 * 8 + 1]);
+      pk.y = pack_half2_sat(v[j8 * 8 + 2], v[j8 * 8 + 3]);
+      pk.z = pack_half2_sat(v[j8 * 8 + 4], v[j8 * 8 + 5]);
+      pk.w = pack_half2_sat(v[j8 * 8 + 6], v[j8 * 8 + 7]);
       reinterpret_cast<uint4*>(cr)[j8] = pk;
     }
   } else {
@@ -236,31 +290,59 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int nb, float
   }
 }
 
-template <int BN, int STAGES>
+// ---- TMA store of a 32 x 32 FP16 tile staged with the 64-B swizzle
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// PAIR = true: a CTA pair (cluster of 2 on one TPC) computes 256 x BN output units with
+// tcgen05.mma.cta_group::2 (M = 256).  Each CTA stages its own 128 rows of A and BN/2 rows
+// of B per k-block, so every SM moves (128 + BN/2) * BK * 2 bytes per 2*128*BN*BK FLOP —
+// 1.5x the FLOP per staged byte of the single-CTA 128 x BN tile at BN = 256 (the encoder
+// GEMMs at K = 512 are bound by L2 -> SM operand traffic).  The leader (rank 0) waits for
+// both halves on its own `full` barrier (each CTA's TMA completes on it), issues the MMAs
+// and multicasts its commits to both CTAs' `empty` / `tfull` barriers; both CTAs drain
+// their own TMEM rows and release the accumulator on the leader's `tempty`.
+template <int BN, int STAGES, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-              Params p) {
-  using SM = Smem<BN, STAGES>;
+              const __grid_constant__ CUtensorMap mapC, Params p) {
+  using SM = Smem<BN, STAGES, PAIR>;
+  constexpr int UM = PAIR ? 2 * BM : BM;             // output rows per unit
   constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                  : 2 * BN <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
+  uint8_t* epi = smem + STAGES * SM::STAGE;   // 1024-B aligned (STAGE is a multiple of 1024)
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + SM::EPI);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   pdl_trigger();
   pdl_wait();  // PDL: operands / live-row count come from the preceding kernel
   const int M = p.dM ? min(p.M, *p.dM) : p.M;
-  const int num_m = (M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
+  const int num_m = (M + UM - 1) / UM, num_n = (p.N + BN - 1) / BN;
   const int units = num_m * num_n;
   const int kb_total = (p.K + BK - 1) / BK;
-  if ((int)blockIdx.x >= units) return;  // uniform: nothing for this CTA
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const int cid = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x;   // unit-stream index
+  const int ncl = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
+  if (cid >= units) return;  // uniform over the pair: nothing for it
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -270,50 +352,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote use
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
       int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int m0 = (u % num_m) * BM, n0 = (u / num_m) * BN;
+      for (int u = cid; u < units; u += ncl) {
+        const int m0 = (u % num_m) * UM + rank * BM, n0 = (u / num_m) * BN + rank * (SM::BROWS);
         for (int kb = 0; kb < kb_total; ++kb, ++it) {
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t* sa = smem + st * SM::STAGE;
-          mbar_expect_tx(&full[st], SM::STAGE);
-          tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
-          tma_load_2d(sa + SM::A_BYTES, &mapB, &full[st], kb * BK, n0);
+          if constexpr (PAIR) {
+            const uint32_t fb = mapa_u32(&full[st], 0);
+            if (rank == 0) mbar_expect_tx(&full[st], 2 * SM::STAGE);
+            tma_load_2d_pair(sa, &mapA, fb, kb * BK, m0);
+            tma_load_2d_pair(sa + SM::A_BYTES, &mapB, fb, kb * BK, n0);
+          } else {
+            mbar_expect_tx(&full[st], SM::STAGE);
+            tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
+            tma_load_2d(sa + SM::A_BYTES, &mapB, &full[st], kb * BK, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer (one thread)
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (one thread; pair leader)
       constexpr uint32_t idesc = (1u << 4)                        // D = F32
                                  | (0u << 7) | (0u << 10)          // A, B = F16
                                  | ((uint32_t)(BN >> 3) << 17)     // N
-                                 | ((uint32_t)(BM >> 4) << 24);    // M
+                                 | ((uint32_t)(UM >> 4) << 24);    // M
       int it = 0, local = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+      for (int u = cid; u < units; u += ncl, ++local) {
         const int acc = local & 1;
         const uint32_t aph = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);   // epilogue drained this accumulator
+        mbar_wait(&tempty[acc], aph ^ 1);   // epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * ACC_COLS;
         for (int kb = 0, first = 1; kb < kb_total; ++kb, ++it, first = 0) {
@@ -324,26 +421,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t da = make_desc_sw128(smem + st * SM::STAGE);
           const uint64_t db = make_desc_sw128(smem + st * SM::STAGE + SM::A_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk)  // +32 B along K inside the swizzle atom
-            mma_f16(d, da + 2 * kk, db + 2 * kk, idesc, (first == 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[st]);  // frees the stage when these MMAs complete
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {  // +32 B along K inside the swizzle atom
+            const uint32_t accum = (first == 0 || kk > 0) ? 1u : 0u;
+            if constexpr (PAIR) mma_f16_pair(d, da + 2 * kk, db + 2 * kk, idesc, accum);
+            else mma_f16(d, da + 2 * kk, db + 2 * kk, idesc, accum);
+          }
+          if constexpr (PAIR) mma_commit_pair(&empty[st]);  // frees the stage in both CTAs
+          else mma_commit(&empty[st]);
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
+        else mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue: 8 warps = 4 TMEM lane quadrants x 2 column halves
+    // FP16 outputs leave through TMA stores: each warp converts 32 rows x 32 columns into
+    // its 64-B-swizzled staging tile (conflict-free 16-B writes) and one lane issues the
+    // bulk store (full-line writes instead of 32 scattered row segments per instruction).
     const int e = warp - 4, q = warp & 3, half = e >> 2;
     constexpr int HALF = BN / 2, NPF = HALF / 8;
+    uint8_t* stg = epi + e * SM::STG;
+    float* sb = reinterpret_cast<float*>(epi + 8 * SM::STG) + e * HALF;
+    const uint32_t te0 = PAIR ? mapa_u32(&tempty[0], 0) : 0u, te1 = PAIR ? mapa_u32(&tempty[1], 0) : 0u;
     int local = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-      const int m0 = (u % num_m) * BM, n0 = (u / num_m) * BN;
+    for (int u = cid; u < units; u += ncl, ++local) {
+      const int m0 = (u % num_m) * UM + rank * BM, n0 = (u / num_m) * BN;
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       const int r = q * 32 + lane;
       const int m = m0 + r;
       const bool row_ok = m < M;
       const int cb = half * HALF;
-      // residual rows prefetched while the MMAs of this unit are still running
+      // residual rows and the bias slice fetched while the MMAs of this unit still run
       uint4 res[NPF];
       const bool pf = p.R && row_ok && n0 + cb + HALF <= p.N &&
                       ((reinterpret_cast<uintptr_t>(p.R + (size_t)m * p.ldr + n0 + cb) & 15) == 0);
@@ -352,6 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < NPF; ++i) res[i] = rp[i];
       }
+      __syncwarp();
+      if (p.bias)
+        for (int j = lane; j < HALF; j += 32) {
+          const int n = n0 + cb + j;
+          sb[j] = n < p.N ? __half2float(p.bias[n]) : 0.f;
+        }
+      __syncwarp();
       mbar_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
@@ -364,20 +479,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c0 + 32 >= cb + HALF) {  // this warp's columns read: release the accumulator
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster(acc ? te1 : te0);
+            else mbar_arrive(&tempty[acc]);
+          }
         }
-        if (row_ok && n0 + c0 < p.N)
-          epilogue32(p, m, n0 + c0, v, best, pf ? res + (c0 - cb) / 8 : nullptr);
+        if (p.dbg & 1) {
+          if (v[0] == 1234.5f) p.C[0] = __float2half(v[1]);
+        } else if (p.tstore) {
+          if (n0 + c0 < p.N) {  // warp-uniform
+            epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, row_ok);
+            uint32_t h[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat(v[2 * i], v[2 * i + 1]);
+            if (lane == 0) bulk_wait_read0();   // the previous store has read the staging tile
+            __syncwarp();
+            const int sw = (lane >> 1) & 3;     // 64-B swizzle: 16-B chunk c at c ^ ((row >> 1) & 3)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ sw) << 4)) =
+                  make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {  // rows >= M and columns >= N are clipped by the tensor map
+              tma_store_2d(&mapC, stg, n0 + c0, m0 + q * 32);
+              bulk_commit();
+            }
+          }
+        } else if (row_ok && n0 + c0 < p.N) {
+          epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, true);
+          epi_out(p, m, n0 + c0, v, best);
+        }
       }
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
     }
+    if (p.tstore && lane == 0) bulk_wait0();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's MMAs / remote arrives are done
+  else __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -388,15 +536,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 // memory (no global round trip, no atomics): after a cluster barrier, CTA c reduces rows
 // [c*128/S, (c+1)*128/S) by reading the S partials in split order 0..S-1 (deterministic,
 // independent of the row count) and applies the fused epilogue.
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
 __device__ __forceinline__ float4 ld_dsmem_f4(const float* local_addr, uint32_t rank) {
   uint32_t a = smem_u32(local_addr), ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
@@ -455,8 +594,12 @@ __device__ __forceinline__ void epilogue16(const Params& p, int m, int nb, float
   }
 }
 
+// 256 threads (warps 0-2 as in k_gemm_tc, warps 4-7 drain TMEM), a few stages, and the
+// FP32 partial aliased onto the drained stage buffers: small enough for several CTAs per SM,
+// so a decode GEMM's clusters run in one wave next to the other workers' kernels.
+constexpr int kCThreads = 256;
 template <int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kCThreads, 3)
     k_gemm_tc_cluster(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB, Params p) {
   constexpr int BN = 64;
@@ -465,8 +608,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  float* part = reinterpret_cast<float*>(smem + STAGES * SM::STAGE);      // [BM][LDP]
-  uint64_t* full = reinterpret_cast<uint64_t*>(part + BM * LDP);
+  // [BM][LDP] FP32 partial, written after the last MMA has drained every stage buffer
+  float* part = reinterpret_cast<float*>(smem);
+  static_assert(BM * LDP * 4 <= STAGES * SM::STAGE, "partial must fit in the stage buffers");
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
@@ -556,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (live) {
     // CTA s reduces rows [s*BM/S, (s+1)*BM/S) of the tile: (row, 16-column group) per item
     const int rows = BM / S;
-    for (int it = threadIdx.x; it < rows * (BN / 16); it += kThreads) {
+    for (int it = threadIdx.x; it < rows * (BN / 16); it += kCThreads) {
       const int rr = s * rows + it / (BN / 16), cg = (it % (BN / 16)) * 16;
       const int m = m0 + rr, nb = n0 + cg;
       if (m >= Meff || nb >= p.N) continue;
@@ -598,28 +743,33 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 struct MapKey {
   const void* p;
   int rows, cols, ld, box;
+  bool out;
   bool operator==(const MapKey& o) const {
-    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box &&
+           out == o.out;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
     size_t h = std::hash<const void*>()(k.p);
     h ^= (size_t)k.rows * 0x9E3779B97F4A7C15ull + ((size_t)k.cols << 20) + ((size_t)k.ld << 40) +
-         (size_t)k.box;
+         (size_t)k.box + (k.out ? 0x5bd1e995ull : 0ull);
     return h;
   }
 };
 
-CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
+// Operand maps: box {BK, box_rows}, 128-B swizzle (UMMA K-major layout).  Output maps
+// (out = true): box {32, 32}, 64-B swizzle (the epilogue's staging tile).
+CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows, bool out) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(out ? 32 : BK), (cuuint32_t)(out ? 32 : box_rows)};
   cuuint32_t es[2] = {1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
                             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            out ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
@@ -627,17 +777,26 @@ CUtensorMap encode_map(const void* ptr, int rows, int cols, int ld, int box_rows
 
 // Tensor maps are pure functions of (pointer, shape, box): cache them (the arena and the
 // weights never move), so a steady-state launch does no host-side encoding.
-CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows) {
+CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows, bool out = false) {
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
   static std::mutex mu;
-  MapKey k{ptr, rows, cols, ld, box_rows};
+  MapKey k{ptr, rows, cols, ld, box_rows, out};
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(k);
   if (it != cache.end()) return it->second;
   if (cache.size() > 65536) cache.clear();
-  CUtensorMap m = encode_map(ptr, rows, cols, ld, box_rows);
+  CUtensorMap m = encode_map(ptr, rows, cols, ld, box_rows, out);
   cache.emplace(k, m);
   return m;
+}
+
+// The TMA-store epilogue serves plain FP16 outputs with a host-known row count (rows of a
+// device-side count dM beyond the live rows must not be written); else mapC is unused.
+CUtensorMap out_map(const GemmArgs& a, Params& p) {
+  p.tstore = getenv("NMT_NO_TSTORE") == nullptr && a.C && !a.argmax && !a.logits && !a.dM &&
+             (a.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+  if (!p.tstore) return CUtensorMap{};
+  return make_map(a.C, a.M, a.N, a.ldc, 32, true);
 }
 
 int num_sms() {
@@ -662,7 +821,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   if (a.splits > 1) throw CudaError("gemm_tc: persistent kernel has no split-K (use the cluster path)");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN);
-  Params p;
+  Params p{};
   p.M = a.M; p.N = a.N; p.K = a.K;
   p.bias = static_cast<const __half*>(a.bias);
   p.R = static_cast<const __half*>(a.R);
@@ -674,16 +833,64 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.argmax = a.argmax;
   p.logits = a.logits;
   p.splits = 1;
+  p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
-  launch_k(k_gemm_tc<BN, STAGES>, grid, kThreads, SM::BYTES, s, ma, mb, p);
+  const CUtensorMap mc = out_map(a, p);
+  launch_k(k_gemm_tc<BN, STAGES>, grid, kThreads, SM::BYTES, s, ma, mb, mc, p);
+  NMT_LAUNCH_CHECK();
+}
+
+// CTA-pair launch: clusters of 2 (one TPC), persistent over 256 x BN units.
+template <int BN, int STAGES>
+void launch_pair(const GemmArgs& a, cudaStream_t s) {
+  using SM = Smem<BN, STAGES, true>;
+  static bool attr = false;
+  if (!attr) {
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
+    attr = true;
+  }
+  CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
+  CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN / 2);
+  Params p{};
+  p.M = a.M; p.N = a.N; p.K = a.K;
+  p.bias = static_cast<const __half*>(a.bias);
+  p.R = static_cast<const __half*>(a.R);
+  p.ldr = a.ldr;
+  p.C = static_cast<__half*>(a.C);
+  p.ldc = a.ldc;
+  p.relu = a.relu;
+  p.dM = a.dM;
+  p.argmax = a.argmax;
+  p.logits = a.logits;
+  p.splits = 1;
+  p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
+  const int units = ceil_div(a.M, 2 * BM) * ceil_div(a.N, BN);
+  const int pairs = std::min(units, num_sms() / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SM::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  const CUtensorMap mc = out_map(a, p);
+  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true>, ma, mb, mc, p));
   NMT_LAUNCH_CHECK();
 }
 
 void launch_cluster(const GemmArgs& a, cudaStream_t s) {
-  constexpr int STAGES = 4;
+  constexpr int STAGES = 3;
   using SM = Smem<64, STAGES>;
-  const int bytes = SM::BYTES + BM * (64 + 4) * 4;
+  const int bytes = SM::BYTES;
   static bool attr = false;
   if (!attr) {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc_cluster<STAGES>,
@@ -709,7 +916,7 @@ void launch_cluster(const GemmArgs& a, cudaStream_t s) {
   const int tiles = ceil_div(a.M, BM) * ceil_div(a.N, 64);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles * S);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kCThreads);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -750,6 +957,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (c == "128x6") tc::launch<128, 6>(a, s);
     else if (c == "128x4") tc::launch<128, 4>(a, s);
     else if (c == "256x3") tc::launch<256, 3>(a, s);
+    else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
+    else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
     else tc::launch<256, 4>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per L2 byte at K = 512 (vs 64 for 128 x 128) — the encoder
