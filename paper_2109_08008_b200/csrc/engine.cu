@@ -952,7 +952,8 @@ nmt_status nmt_dev_gemm_decode(int32_t M, int32_t N, int32_t K, const void* d_A,
     GemmArgs a;
     a.M = M; a.N = N; a.K = K; a.A = d_A; a.lda = lda; a.B = d_B; a.ldb = ldb; a.bias = d_bias;
     a.R = d_R; a.ldr = ldr; a.C = d_C; a.ldc = ldc; a.relu = relu;
-    a.tile_n = 64; a.splits = sp; a.ws = ws; a.counters = cnt;
+    a.ws = ws; a.counters = cnt;
+    decode_config(a);
     gemm<__half>(a, (cudaStream_t)stream);
   });
 }

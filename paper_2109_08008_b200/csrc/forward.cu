@@ -64,8 +64,7 @@ template <class T> const T* cT(const void* p) { return static_cast<const T*>(p);
 // Decode-size GEMM (rows = live batch rows): 64-wide output tiles and a fixed split-K
 // factor that depends on the weight shape only (batch invariance), see gemm_tc.cu.
 GemmArgs dec_cfg(nmt_model* m, GemmArgs a) {
-  a.tile_n = 64;
-  a.splits = decode_splits(a.N, a.K);
+  decode_config(a);
   a.ws = m->gemm_ws;
   a.counters = m->gemm_cnt;
   return a;

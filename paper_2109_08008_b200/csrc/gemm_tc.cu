@@ -941,6 +941,23 @@ int decode_splits(int N, int K) {
   return sp;
 }
 
+// Decode GEMMs use the persistent kernel with 128 x 128 tiles and no split-K: measured in
+// captured graphs (tools/dec_gemm_sweep.py) it beats the cluster split-K kernel at every
+// live-row count of the 35-1 decode step (6 projections: 46.7 vs 112.7 us at 1024 rows,
+// 45.4 vs 54.4 us at 256), and every output row depends on its own input row only.
+// NMT_DEC_TILE / NMT_DEC_SPLITS select other configurations for tuning experiments.
+void decode_config(GemmArgs& a) {
+  static const int env_tile = getenv("NMT_DEC_TILE") ? atoi(getenv("NMT_DEC_TILE")) : 0;
+  static const int env_splits = getenv("NMT_DEC_SPLITS") ? atoi(getenv("NMT_DEC_SPLITS")) : 0;
+  if (env_splits > 1) {
+    a.tile_n = 64;
+    a.splits = env_splits;
+  } else {
+    a.tile_n = env_tile ? env_tile : 128;
+    a.splits = 1;
+  }
+}
+
 void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
   if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||

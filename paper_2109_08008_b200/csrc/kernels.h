@@ -38,6 +38,8 @@ struct GemmArgs {
 // Split-K factor for a decode-size GEMM of shape (N, K) with 64-wide tiles: a function of
 // the weight shape only (never of the live-row count), so results are batch invariant.
 int decode_splits(int N, int K);
+// Decode-step GEMM configuration (tile width, split-K factor) from the weight shape only.
+void decode_config(GemmArgs& a);
 
 template <class T> void gemm_simt(const GemmArgs& a, cudaStream_t s);
 void gemm_tc(const GemmArgs& a, cudaStream_t s);   // FP16 tcgen05 / TMEM / TMA

@@ -42,8 +42,9 @@ def test_gemm_unit(prec, M, N, K):
 
 @pytest.mark.parametrize("M,N,K", [(1, 1536, 512), (148, 512, 512), (148, 2048, 512), (300, 512, 2048),
                                    (512, 1536, 512), (37, 64, 64), (9, 256, 64)])
-def test_gemm_decode_splitk_unit(M, N, K):
-    """Decode configuration: 64-wide tiles + deterministic split-K (last CTA reduces)."""
+def test_gemm_decode_unit(M, N, K):
+    """The decode-step GEMM configuration (gemm_tc.cu decode_config): correct, deterministic
+    and batch invariant (a row's result does not depend on the other rows)."""
     from paper_2109_08008_b200 import dev_gemm_decode, dev_gemm
     g = torch.Generator().manual_seed(M + 3 * N + K)
     A = (torch.randn(M, K, generator=g) / 2).half()
