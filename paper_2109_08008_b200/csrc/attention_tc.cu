@@ -74,10 +74,11 @@ __global__ void __launch_bounds__(128) k_attn_enc_tc(const __half* __restrict__ 
   const int R = 2 * kclip + 1;
   const int n = len[b];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nthr = blockDim.x, nwarp = nthr >> 5;   // min(4, SP/16) warps (launch_nt)
   const size_t rs = 3 * (size_t)d;
   const __half* base = qkv + (size_t)b * S * rs + h * DH;
   // ---- stage Q, K, V asynchronously (rows >= n zero-filled) + relative tables
-  for (int idx = tid; idx < SP * (DH / 8); idx += 128) {
+  for (int idx = tid; idx < SP * (DH / 8); idx += nthr) {
     const int j = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
     const bool ok = j < n;
     const __half* rp = base + (size_t)(ok ? j : 0) * rs + c;
@@ -85,21 +86,22 @@ __global__ void __launch_bounds__(128) k_attn_enc_tc(const __half* __restrict__ 
     cp_async16(sK + j * LDH + c, rp + d, ok ? 16 : 0);
     cp_async16(sV + j * LDH + c, rp + 2 * d, ok ? 16 : 0);
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int idx = tid; idx < RP * DH; idx += 128) {
-    const int r = idx / DH, c = idx % DH;
+  for (int idx = tid; idx < RP * (DH / 8); idx += nthr) {  // A^K, A^V rows >= R zero-filled
+    const int r = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
     const bool ok = use_rpr && r < R;
-    sAK[r * LDH + c] = ok ? relk[r * DH + c] : __float2half(0.f);
-    sAV[r * LDH + c] = ok ? relv[r * DH + c] : __float2half(0.f);
+    cp_async16(sAK + r * LDH + c, relk + (ok ? r * DH + c : 0), ok ? 16 : 0);
+    cp_async16(sAV + r * LDH + c, relv + (ok ? r * DH + c : 0), ok ? 16 : 0);
   }
-  for (int idx = tid; idx < SP * LDB / 2; idx += 128) reinterpret_cast<uint32_t*>(sB)[idx] = 0u;
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int idx = tid; idx < SP * LDB / 8; idx += nthr)
+    reinterpret_cast<uint4*>(sB)[idx] = make_uint4(0u, 0u, 0u, 0u);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
   const float scale = rsqrtf((float)DH);
   const int g = lane >> 2, tig = lane & 3, mi = lane >> 3, rr = lane & 7;
   const int nblk = (n + 15) >> 4;
-  for (int mb = warp; mb < nblk; mb += 4) {
+  for (int mb = warp; mb < nblk; mb += nwarp) {
     const int m0 = mb * 16;
     // ---- S = Q K^T and QA = Q A^K^T
     float sc[NT][4], qa[RP / 8][4];
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(128) k_attn_enc_tc(const __half* __restrict__ 
     }
   }
   // query rows beyond the last 16-block are padding: zero them
-  for (int idx = nblk * 16 * (DH / 8) + tid; idx < S * (DH / 8); idx += 128) {
+  for (int idx = nblk * 16 * (DH / 8) + tid; idx < S * (DH / 8); idx += nthr) {
     const int i = idx / (DH / 8), c = (idx % (DH / 8)) * 8;
     *reinterpret_cast<uint4*>(out + ((size_t)b * S + i) * d + h * DH + c) = make_uint4(0, 0, 0, 0);
   }
@@ -270,8 +272,10 @@ void launch_nt(const __half* qkv, const int* len, const __half* relk, const __ha
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
     attr = true;
   }
-  k_attn_enc_tc<DH, NT><<<dim3(B, H), 128, L::BYTES, s>>>(qkv, len, relk, relv, out, S, d, kclip,
-                                                         use_rpr);
+  // one warp per 16-query block up to 4: short sentences do not hold idle warps
+  constexpr int threads = 32 * (NT / 2 < 4 ? NT / 2 : 4);
+  k_attn_enc_tc<DH, NT><<<dim3(B, H), threads, L::BYTES, s>>>(qkv, len, relk, relv, out, S, d,
+                                                             kclip, use_rpr);
 }
 
 template <int DH>

@@ -221,6 +221,38 @@ __device__ __forceinline__ void ldrow(const T* p, float* v) {
 #pragma unroll
   for (int i = 0; i < E; i += VecIO<T>::W) VecIO<T>::ld(p + i, v + i);
 }
+// E contiguous elements of a row held raw (16-B vectors) until their fma into x.
+template <class T, int E>
+struct RawRow {
+  static constexpr int NV = E * (int)sizeof(T) / 16;
+  uint4 u[NV];
+  __device__ __forceinline__ void load(const T* p) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) u[i] = reinterpret_cast<const uint4*>(p)[i];
+  }
+  __device__ __forceinline__ void fma_into(float wk, float* x) const {
+    if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const __half2* h = reinterpret_cast<const __half2*>(&u[i]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          x[8 * i + 2 * e] = fmaf(wk, f.x, x[8 * i + 2 * e]);
+          x[8 * i + 2 * e + 1] = fmaf(wk, f.y, x[8 * i + 2 * e + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        x[4 * i] = fmaf(wk, __uint_as_float(u[i].x), x[4 * i]);
+        x[4 * i + 1] = fmaf(wk, __uint_as_float(u[i].y), x[4 * i + 1]);
+        x[4 * i + 2] = fmaf(wk, __uint_as_float(u[i].z), x[4 * i + 2]);
+        x[4 * i + 3] = fmaf(wk, __uint_as_float(u[i].w), x[4 * i + 3]);
+      }
+    }
+  }
+};
 template <class T, int E>
 __device__ __forceinline__ void strow(T* p, const float* v) {
 #pragma unroll
@@ -266,14 +298,16 @@ __global__ void __launch_bounds__(256) k_dlcl_vec(
   for (int i = 0; i < E; ++i) z[i] = to_f(from_f<T>(z[i]));
 #pragma unroll
   for (int i = 0; i < E; ++i) x[i] = 0.f;
+  // U history rows in flight per lane (raw 16-B loads issued before any arithmetic): the
+  // combine is bound by HBM bandwidth, not by one memory latency per history row
+  constexpr int U = sizeof(T) == 2 ? 8 : 4;
   int k = 0;
-  for (; k + 1 < l; k += 2) {  // two history rows in flight per lane
-    float a[E], b[E];
-    ldrow<T, E>(hist + (size_t)k * hist_stride + off, a);
-    ldrow<T, E>(hist + (size_t)(k + 1) * hist_stride + off, b);
-    const float wa = w[k], wb = w[k + 1];
+  for (; k + U <= l; k += U) {
+    RawRow<T, E> a[U];
 #pragma unroll
-    for (int i = 0; i < E; ++i) x[i] = fmaf(wb, b[i], fmaf(wa, a[i], x[i]));
+    for (int u = 0; u < U; ++u) a[u].load(hist + (size_t)(k + u) * hist_stride + off);
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u].fma_into(w[k + u], x);
   }
   for (; k < l; ++k) {
     float a[E];
