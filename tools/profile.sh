@@ -15,7 +15,7 @@ full() {  # name regex, skip, count
     -o $out/${tag}_$1 -f $B > $out/${tag}_$1.log 2>&1
   echo "$1 rc=$?"
 }
-full dec_gemm '^k_gemm_tc_cluster$' 40 3
+full dec_gemm '^k_gemm_tc$' 300 2
 full enc_gemm '^k_gemm_tc$' 4 2
 full dlcl '^k_dlcl_vec$' 10 1
 full enc_attn '^k_attn_enc_tc$' 4 1
