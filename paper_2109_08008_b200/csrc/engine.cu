@@ -153,6 +153,7 @@ void init_arena(nmt_model* m) {
       {(void**)&m->htok, L.beam > 1 ? R * Tm * 4 : 256},
       {(void**)&m->best_score, L.beam > 1 ? Bm * 4 : 256},
       {(void**)&m->blogits, L.beam > 1 ? R * (size_t)c.vocab_size * 4 : 256},
+      {(void**)&m->lnst, R * (d / 32) * 8},
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
   };
@@ -179,6 +180,41 @@ void init_arena(nmt_model* m) {
   m->hp.gen_len = (int*)take(Bm * 4);
   m->hp.st = (DevState*)take(sizeof(DevState));
   m->hp.bad = (int*)take(4);
+}
+
+// LN folding for the FP16 decode step: the decoder LayerNorms that
+// feed a projection GEMM (LN_self of layers >= 1, LN_cross, LN_ffn) are folded into that
+// GEMM's weights, bias and epilogue; the final LN before the tied vocab projection stays a
+// kernel (see decode_step_impl).
+void fold_weights(nmt_model* m) {
+  const nmt_config& c = m->cfg;
+  const size_t d = c.d_model, F = c.d_ffn, Ld = c.dec_layers;
+  const size_t rows = Ld * (3 * d + d + F);
+  const size_t wbytes = rows * d * 2, cbytes = rows * 4, bbytes = rows * 2;
+  cudaError_t e = cudaMalloc(&m->foldbuf, wbytes + cbytes + bbytes + 1024);
+  NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
+              std::string("fold cudaMalloc failed: ") + cudaGetErrorString(e));
+  char* wp = (char*)m->foldbuf;
+  float* cp = (float*)(wp + wbytes);
+  char* bp = (char*)(cp + rows) + 256;
+  size_t r0 = 0;
+  auto fold = [&](const void* W, const void* g, const void* beta, const void* bias, size_t N) {
+    FoldW f;
+    f.w = wp + r0 * d * 2;
+    f.c = cp + r0;
+    f.b = bp + r0 * 2;
+    fold_ln(W, g, beta, bias, (int)N, (int)d, (void*)f.w, (float*)f.c, (void*)f.b, 0);
+    r0 += N;
+    return f;
+  };
+  for (size_t l = 0; l < Ld; ++l) {
+    const DecW& w = m->dec[l];
+    DecFold df;
+    df.qkv = fold(w.qkv_w, w.self_g, w.self_b, w.qkv_b, 3 * d);
+    df.cq = fold(w.cq_w, w.cross_g, w.cross_b, w.cq_b, d);
+    df.w1 = fold(w.w1, w.ffn_g, w.ffn_b, w.b1, F);
+    m->fold.push_back(df);
+  }
 }
 
 void bind_weights(nmt_model* m) {
@@ -367,6 +403,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->dlcl_w = (float*)(base + dlcl_off);
   m->pe = (float*)(base + pe_off);
   bind_weights(m.get());
+  if (prec == NMT_FP16) fold_weights(m.get());
   init_arena(m.get());
   NMT_CUDA(cudaDeviceSynchronize());
   return m.release();
@@ -544,6 +581,7 @@ nmt_model* clone_worker(nmt_model* m) {
   c->emb = m->emb; c->dl0_g = m->dl0_g; c->dl0_b = m->dl0_b; c->enc_fg = m->enc_fg;
   c->enc_fb = m->enc_fb; c->dec_fg = m->dec_fg; c->dec_fb = m->dec_fb;
   c->ckv_w = m->ckv_w; c->ckv_b = m->ckv_b; c->dlcl_w = m->dlcl_w; c->pe = m->pe;
+  c->foldbuf = m->foldbuf; c->fold = m->fold;
   init_arena(c.get());
   NMT_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   return c.release();

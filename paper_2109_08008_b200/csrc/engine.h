@@ -42,6 +42,15 @@ struct EncW {
       *b1, *w2, *b2;
   const void *dl_g, *dl_b;  // LN^dl_{l+1} (applied to y_{l+1}), DLCL only
 };
+// LN-folded decoder weights (FP16 path, see fold_ln): B operand, c[n], folded bias.
+struct FoldW {
+  const void* w = nullptr;
+  const float* c = nullptr;
+  const void* b = nullptr;
+};
+struct DecFold {
+  FoldW qkv, cq, w1;   // behind LN_self (layers >= 1), LN_cross, LN_ffn
+};
 struct DecW {
   const void *self_g, *self_b, *qkv_w, *qkv_b, *so_w, *so_b, *relk, *relv, *cross_g, *cross_b,
       *cq_w, *cq_b, *co_w, *co_b, *ffn_g, *ffn_b, *w1, *b1, *w2, *b2;
@@ -83,6 +92,9 @@ struct nmt_model {
   void* ckv_b = nullptr;   // [Ld*2d]
   float* dlcl_w = nullptr; // packed rows m = 1..L+1 (row m at offset m(m-1)/2)
   float* pe = nullptr;     // [max_pos][d] FP32 sinusoid table
+  // LN folding (FP16): per decoder layer (LN_self of layers >= 1, LN_cross, LN_ffn)
+  void* foldbuf = nullptr;
+  std::vector<nmt::DecFold> fold;
   // arena
   nmt::Arena ar;
   int *src = nullptr, *src_len = nullptr, *tgt_cap = nullptr;
@@ -106,6 +118,7 @@ struct nmt_model {
   int* htok = nullptr;        // [R][Tmax] token history per slot (j = 0: BOS)
   float* best_score = nullptr;  // [max_sents] best finished hypothesis score
   float* blogits = nullptr;   // [R][V] FP32 logits of the step
+  float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
   float* cand_v = nullptr;    // [R][2K] top log-probs per row
   int* cand_i = nullptr;      // [R][2K] their token ids
   // pinned host staging
@@ -150,6 +163,7 @@ struct nmt_model {
     for (auto e : prof.pool) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (wbuf && owns_weights) cudaFree(wbuf);
+    if (foldbuf && owns_weights) cudaFree(foldbuf);
     if (ar.base) cudaFree(ar.base);
     if (pinned) cudaFreeHost(pinned);
   }

@@ -152,14 +152,29 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
        embed_dec_ln<T>(d_prev ? d_prev : m->prev_tok, cT<T>(m->emb), m->pe,
                        cT<T>(m->dec[0].self_g), cT<T>(m->dec[0].self_b), g, du, R, d,
                        std::sqrt((float)d), eps, dt, dR, s));
+  // FP16: the LayerNorms in front of GEMMs are folded into them:
+  // residual-producing GEMMs emit row-chunk statistics, the consumers run on the raw
+  // stream g with W o gamma and apply rstd (acc - mu c) + b' in their epilogue.
+  static const bool no_fold = getenv("NMT_NO_FOLD") != nullptr;   // A/B experiments only
+  const bool FOLD = sizeof(T) == 2 && !no_fold;
+  auto folded = [&](GemmArgs a, const FoldW& f) {
+    a.B = f.w; a.bias = f.b;
+    a.ln_st = m->lnst; a.ln_c = f.c; a.ln_eps = eps;
+    return a;
+  };
   for (int l = 0; l < Ld; ++l) {
     const DecW& w = m->dec[l];
     T* kc = (T*)m->kc + (size_t)l * Rmax * Tm * d;
     T* vc = (T*)m->vc + (size_t)l * Rmax * Tm * d;
-    if (l > 0)
-      PROF(P_DEC_LN, 0, 2 * row,
-           layernorm<T>(g, d, cT<T>(w.self_g), cT<T>(w.self_b), du, d, R, d, eps, dR, s));
-    GemmArgs a = mk(R, 3 * d, d, du, d, w.qkv_w, d, w.qkv_b, dqkv, 3 * d);
+    GemmArgs a;
+    if (FOLD && l > 0) {
+      a = folded(mk(R, 3 * d, d, g, d, nullptr, d, nullptr, dqkv, 3 * d), m->fold[l].qkv);
+    } else {
+      if (l > 0)
+        PROF(P_DEC_LN, 0, 2 * row,
+             layernorm<T>(g, d, cT<T>(w.self_g), cT<T>(w.self_b), du, d, R, d, eps, dR, s));
+      a = mk(R, 3 * d, d, du, d, w.qkv_w, d, w.qkv_b, dqkv, 3 * d);
+    }
     a.dM = dR;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_SELF, 4.0 * R * (t + 1) * d, (2.0 * (t + 1) + 6) * row,
@@ -168,10 +183,15 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
                               b->K > 1 ? m->anc : nullptr, s));
     a = mk(R, d, d, dout, d, w.so_w, d, w.so_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
+    if (FOLD) a.st_out = m->lnst;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
-    PROF(P_DEC_LN, 0, 2 * row,
-         layernorm<T>(g, d, cT<T>(w.cross_g), cT<T>(w.cross_b), du, d, R, d, eps, dR, s));
-    a = mk(R, d, d, du, d, w.cq_w, d, w.cq_b, dq, d);
+    if (FOLD) {
+      a = folded(mk(R, d, d, g, d, nullptr, d, nullptr, dq, d), m->fold[l].cq);
+    } else {
+      PROF(P_DEC_LN, 0, 2 * row,
+           layernorm<T>(g, d, cT<T>(w.cross_g), cT<T>(w.cross_b), du, d, R, d, eps, dR, s));
+      a = mk(R, d, d, du, d, w.cq_w, d, w.cq_b, dq, d);
+    }
     a.dM = dR;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * row,
@@ -179,22 +199,36 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
                        c.max_src_len, m->src_len, m->row_slot, dout, R, d, H, dR, b->K, s));
     a = mk(R, d, d, dout, d, w.co_w, d, w.co_b, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
+    if (FOLD) a.st_out = m->lnst;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
-    PROF(P_DEC_LN, 0, 2 * row,
-         layernorm<T>(g, d, cT<T>(w.ffn_g), cT<T>(w.ffn_b), du, d, R, d, eps, dR, s));
-    a = mk(R, F, d, du, d, w.w1, d, w.b1, dh, F);
+    if (FOLD) {
+      a = folded(mk(R, F, d, g, d, nullptr, d, nullptr, dh, F), m->fold[l].w1);
+    } else {
+      PROF(P_DEC_LN, 0, 2 * row,
+           layernorm<T>(g, d, cT<T>(w.ffn_g), cT<T>(w.ffn_b), du, d, R, d, eps, dR, s));
+      a = mk(R, F, d, du, d, w.w1, d, w.b1, dh, F);
+    }
     a.relu = 1; a.dM = dR;
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
     a = mk(R, d, F, dh, F, w.w2, F, w.b2, g, d);
     a.R = g; a.ldr = d; a.dM = dR;
+    if (FOLD && l + 1 < Ld) a.st_out = m->lnst;   // for the next layer's folded QKV
     PROF(P_DEC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(dec_cfg(m, a), s));
   }
+  // The final LN stays a kernel: the vocab GEMM's epilogue-bound K = 512 units (V / 256 per
+  // row tile) would pay the folded-LN epilogue once per unit (measured +40% vocab time).
   PROF(P_DEC_LN, 0, 2 * row,
        layernorm<T>(g, d, cT<T>(m->dec_fg), cT<T>(m->dec_fb), du, d, R, d, eps, dR, s));
+  // the tied vocab projection behind the final LN
+  auto vocab_args = [&]() {
+    GemmArgs v = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
+    v.dM = dR;
+    return v;
+  };
   if (b->K == 1) {
-    // tied vocab projection fused with argmax: logits never stored
-    GemmArgs a = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);
-    a.dM = dR; a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
+    // vocab projection fused with argmax: logits never stored
+    GemmArgs a = vocab_args();
+    a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
     PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
     if (finish)
       PROF(P_BOOK, 0, 0,
@@ -205,8 +239,8 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   }
   // beam: FP32 logits -> per-row LSE + top-2K -> per-sentence select
   const int K = b->K, V = c.vocab_size;
-  GemmArgs a = mk(R, V, d, du, d, m->emb, d, nullptr, nullptr, 0);
-  a.dM = dR; a.logits = m->blogits;
+  GemmArgs a = vocab_args();
+  a.logits = m->blogits;
   PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) + (double)R * V * 4, gemm<T>(a, s));
   if (out && out->d_logits)
     NMT_CUDA(cudaMemcpyAsync(out->d_logits, m->blogits, (size_t)R * V * 4,

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 
 template <class T> void gemm_simt(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
+  if (a.st_out || a.ln_st) throw CudaError("gemm_simt: LN folding is an FP16 tcgen05 feature");
   dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM));
   k_gemm_simt<T><<<grid, 256, 0, s>>>(a);
   NMT_LAUNCH_CHECK();

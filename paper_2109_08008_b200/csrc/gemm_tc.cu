@@ -183,7 +183,65 @@ struct Params {
   int* counters;      // split-K arrival counters [tile] (self-resetting)
   int dbg;            // tuning experiments only (NMT_GEMM_DBG): 1 = drain TMEM, no epilogue
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
+  float2* st_out;     // LN folding, producer side (GemmArgs)
+  const float2* ln_st;
+  const float* ln_c;
+  float ln_eps;
 };
+
+// (mean, M2) of 32 values as stored (FP16-rounded), two-pass in registers
+__device__ __forceinline__ float2 chunk_stats(const float* v) {
+  float r[32], s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const uint32_t h = pack_half2_sat(v[j], v[j + 1]);
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    r[j] = f.x;
+    r[j + 1] = f.y;
+    s += f.x + f.y;
+  }
+  const float mu = s * (1.f / 32.f);
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) q = fmaf(r[j] - mu, r[j] - mu, q);
+  return make_float2(mu, q);
+}
+// Row mean / rstd from NCH chunk partials of 32 columns each (Chan et al. merge of
+// equal-size groups).  All partials are loaded at once (16-B vectors) before the merge.
+template <int NCH>
+__device__ __forceinline__ float2 merge_stats_n(const float2* st, float eps) {
+  float4 q[NCH / 2];
+#pragma unroll
+  for (int i = 0; i < NCH / 2; ++i) q[i] = reinterpret_cast<const float4*>(st)[i];
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < NCH / 2; ++i) sm += q[i].x + q[i].z;
+  const float mu = sm * (1.f / NCH);
+  float m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NCH / 2; ++i) {
+    const float a = q[i].x - mu, b = q[i].z - mu;
+    m2 += q[i].y + q[i].w + 32.f * (a * a + b * b);
+  }
+  return make_float2(mu, rsqrtf(m2 * (1.f / (32 * NCH)) + eps));
+}
+__device__ __forceinline__ float2 merge_stats(const float2* st, int nch, float eps) {
+  switch (nch) {
+    case 16: return merge_stats_n<16>(st, eps);   // d = 512
+    case 8: return merge_stats_n<8>(st, eps);     // d = 256
+    case 32: return merge_stats_n<32>(st, eps);   // d = 1024
+    default: break;
+  }
+  float sm = 0.f;
+  for (int i = 0; i < nch; ++i) sm += st[i].x;
+  const float mu = sm / nch;
+  float m2 = 0.f;
+  for (int i = 0; i < nch; ++i) {
+    const float dm = st[i].x - mu;
+    m2 += st[i].y + 32.f * dm * dm;
+  }
+  return make_float2(mu, rsqrtf(m2 / (32.f * nch) + eps));
+}
 
 template <int BN, int STAGES, bool PAIR = false>
 struct Smem {
@@ -193,7 +251,7 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // epilogue: per warp a 32 x 32 FP16 staging tile (TMA store) and its FP32 bias slice
   static constexpr int STG = 2048;
-  static constexpr int EPI = 8 * STG + 8 * (BN / 2) * 4;
+  static constexpr int EPI = 8 * STG + 2 * 8 * (BN / 2) * 4;   // + bias and LN c[n] slices
   static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -201,9 +259,20 @@ struct Smem {
 // bias (from the warp's shared-memory slice, zero beyond N), residual (prefetched `pre` or
 // loaded here), ReLU.
 __device__ __forceinline__ void epi_math(const Params& p, int m, int nb, float* v,
-                                         const float* sb, const uint4* pre, bool row_ok) {
+                                         const float* sb, const uint4* pre, bool row_ok,
+                                         const float* sc = nullptr, float2 ln = {0.f, 0.f}) {
   const int nv = min(32, p.N - nb);
   const bool full = nv == 32;
+  if (p.ln_st) {  // folded LayerNorm: rstd * (acc - mu * c[n])
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 c = *reinterpret_cast<const float4*>(sc + j);
+      v[j] = ln.y * fmaf(-ln.x, c.x, v[j]);
+      v[j + 1] = ln.y * fmaf(-ln.x, c.y, v[j + 1]);
+      v[j + 2] = ln.y * fmaf(-ln.x, c.z, v[j + 2]);
+      v[j + 3] = ln.y * fmaf(-ln.x, c.w, v[j + 3]);
+    }
+  }
   if (p.bias) {
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
@@ -441,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int HALF = BN / 2, NPF = HALF / 8;
     uint8_t* stg = epi + e * SM::STG;
     float* sb = reinterpret_cast<float*>(epi + 8 * SM::STG) + e * HALF;
+    float* sc = reinterpret_cast<float*>(epi + 8 * SM::STG) + 8 * HALF + e * HALF;
     const uint32_t te0 = PAIR ? mapa_u32(&tempty[0], 0) : 0u, te1 = PAIR ? mapa_u32(&tempty[1], 0) : 0u;
     int local = 0;
     for (int u = cid; u < units; u += ncl, ++local) {
@@ -466,6 +536,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n = n0 + cb + j;
           sb[j] = n < p.N ? __half2float(p.bias[n]) : 0.f;
         }
+      float2 ln = make_float2(0.f, 0.f);
+      if (p.ln_st) {
+        for (int j = lane; j < HALF; j += 32) {
+          const int n = n0 + cb + j;
+          sc[j] = n < p.N ? p.ln_c[n] : 0.f;
+        }
+        if (row_ok) ln = merge_stats(p.ln_st + (size_t)m * (p.K / 32), p.K / 32, p.ln_eps);
+      }
       __syncwarp();
       mbar_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -488,7 +566,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (v[0] == 1234.5f) p.C[0] = __float2half(v[1]);
         } else if (p.tstore) {
           if (n0 + c0 < p.N) {  // warp-uniform
-            epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, row_ok);
+            epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, row_ok,
+                     sc + (c0 - cb), ln);
+            if (p.st_out && row_ok) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
             uint32_t h[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat(v[2 * i], v[2 * i + 1]);
@@ -507,7 +587,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else if (row_ok && n0 + c0 < p.N) {
-          epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, true);
+          epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, true,
+                   sc + (c0 - cb), ln);
+          if (p.st_out) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
           epi_out(p, m, n0 + c0, v, best);
         }
       }
@@ -833,6 +915,10 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.argmax = a.argmax;
   p.logits = a.logits;
   p.splits = 1;
+  p.st_out = a.st_out;
+  p.ln_st = a.ln_st;
+  p.ln_c = a.ln_c;
+  p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
@@ -865,6 +951,10 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   p.argmax = a.argmax;
   p.logits = a.logits;
   p.splits = 1;
+  p.st_out = a.st_out;
+  p.ln_st = a.ln_st;
+  p.ln_c = a.ln_c;
+  p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
   const int units = ceil_div(a.M, 2 * BM) * ceil_div(a.N, BN);
   const int pairs = std::min(units, num_sms() / 2);
@@ -963,6 +1053,9 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||
       (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
     throw CudaError("gemm_tc: K / leading dims must be multiples of 8 and 16-B aligned");
+  if ((a.st_out && a.N % 32) || (a.ln_st && (a.K % 32 || !a.ln_c)) ||
+      ((a.st_out || a.ln_st) && a.splits > 1))
+    throw CudaError("gemm_tc: LN folding needs N, K % 32 == 0 and the persistent kernel");
   if (a.tile_n == 64 && a.splits > 1) {
     tc::launch_cluster(a, s);   // split-K reduced through distributed shared memory
   } else if (a.tile_n == 64) {

@@ -718,4 +718,42 @@ void argmax_ids(unsigned long long* keys, int* ids, int rows, cudaStream_t s) {
 NMT_INST(float)
 NMT_INST(__half)
 
+// ------------------------------------------------------------------- LN folding (load time)
+// For y = LN(x) W^T + b with LN(x)_k = (x_k - mu) rstd g_k + beta_k:
+//   y_n = rstd (sum_k x_k W'_nk - mu c_n) + b'_n,   W' = W o g (FP16),
+//   c_n = sum_k W'_nk (of the rounded W'),           b'_n = b_n + sum_k W_nk beta_k.
+// One warp per output row n; fixed reduction order (deterministic).
+__global__ void k_fold_ln(const __half* __restrict__ W, const __half* __restrict__ g,
+                          const __half* __restrict__ beta, const __half* __restrict__ bias, int N,
+                          int K, __half* __restrict__ Wf, float* __restrict__ c,
+                          __half* __restrict__ bf) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (n >= N) return;
+  double cs = 0.0, bs = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const float w = __half2float(W[(size_t)n * K + k]);
+    const __half wf = __float2half_rn(w * __half2float(g[k]));
+    Wf[(size_t)n * K + k] = wf;
+    cs += (double)__half2float(wf);
+    bs += (double)w * (double)__half2float(beta[k]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    bs += __shfl_xor_sync(0xffffffffu, bs, o);
+  }
+  if (lane == 0) {
+    c[n] = (float)cs;
+    bf[n] = __float2half_rn((float)((bias ? (double)__half2float(bias[n]) : 0.0) + bs));
+  }
+}
+
+void fold_ln(const void* W, const void* g, const void* beta, const void* bias, int N, int K,
+             void* Wf, float* c, void* bf, cudaStream_t s) {
+  k_fold_ln<<<ceil_div(N, 8), 256, 0, s>>>((const __half*)W, (const __half*)g,
+                                          (const __half*)beta, (const __half*)bias, N, K,
+                                          (__half*)Wf, c, (__half*)bf);
+  NMT_LAUNCH_CHECK();
+}
+
 }  // namespace nmt

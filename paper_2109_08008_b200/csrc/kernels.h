@@ -33,6 +33,14 @@ struct GemmArgs {
   int splits = 1;
   float* ws = nullptr;
   int* counters = nullptr;
+  // LayerNorm folded into the GEMM (FP16 tcgen05 path):
+  // producer: per-row (mean, M2) of every 32 FP16-rounded output columns -> st_out[M][N/32];
+  // consumer: A = the raw residual stream x, B = W o gamma, bias = b + W beta, and the
+  // epilogue applies y = rstd (acc - mu c[n]) + bias with (mu, rstd) merged from ln_st.
+  float2* st_out = nullptr;
+  const float2* ln_st = nullptr;
+  const float* ln_c = nullptr;
+  float ln_eps = 0.f;
 };
 
 // Split-K factor for a decode-size GEMM of shape (N, K) with 64-wide tiles: a function of
@@ -40,6 +48,9 @@ struct GemmArgs {
 int decode_splits(int N, int K);
 // Decode-step GEMM configuration (tile width, split-K factor) from the weight shape only.
 void decode_config(GemmArgs& a);
+// LN folding at load time (FP16): Wf = W o g, c[n] = sum_k Wf[n][k], bf = bias + W beta.
+void fold_ln(const void* W, const void* g, const void* beta, const void* bias, int N, int K,
+             void* Wf, float* c, void* bf, cudaStream_t s);
 
 template <class T> void gemm_simt(const GemmArgs& a, cudaStream_t s);
 void gemm_tc(const GemmArgs& a, cudaStream_t s);   // FP16 tcgen05 / TMEM / TMA
