@@ -243,7 +243,7 @@ __device__ __forceinline__ float2 merge_stats(const float2* st, int nch, float e
   return make_float2(mu, rsqrtf(m2 / (32.f * nch) + eps));
 }
 
-template <int BN, int STAGES, bool PAIR = false>
+template <int BN, int STAGES, bool PAIR = false, int EW = 8>
 struct Smem {
   static constexpr int BROWS = PAIR ? BN / 2 : BN;   // B rows staged by one CTA
   static constexpr int A_BYTES = BM * BK * 2;
@@ -251,7 +251,7 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // epilogue: per warp a 32 x 32 FP16 staging tile (TMA store) and its FP32 bias slice
   static constexpr int STG = 2048;
-  static constexpr int EPI = 8 * STG + 2 * 8 * (BN / 2) * 4;   // + bias and LN c[n] slices
+  static constexpr int EPI = EW * STG + 2 * 4 * BN * 4;   // + per-warp bias and LN c[n] slices
   static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -383,11 +383,11 @@ __device__ __forceinline__ void fence_async_smem() {
 // both halves on its own `full` barrier (each CTA's TMA completes on it), issues the MMAs
 // and multicasts its commits to both CTAs' `empty` / `tfull` barriers; both CTAs drain
 // their own TMEM rows and release the accumulator on the leader's `tempty`.
-template <int BN, int STAGES, bool PAIR = false>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, bool PAIR = false, int EW = 8>
+__global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, Params p) {
-  using SM = Smem<BN, STAGES, PAIR>;
+  using SM = Smem<BN, STAGES, PAIR, EW>;
   constexpr int UM = PAIR ? 2 * BM : BM;             // output rows per unit
   constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
+      mbar_init(&tempty[a], PAIR ? 2 * EW : EW);  // one arrive per epilogue warp (both CTAs)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -502,15 +502,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue: 8 warps = 4 TMEM lane quadrants x 2 column halves
+  } else if (warp >= 4) {  // ---------------- epilogue
     // FP16 outputs leave through TMA stores: each warp converts 32 rows x 32 columns into
     // its 64-B-swizzled staging tile (conflict-free 16-B writes) and one lane issues the
     // bulk store (full-line writes instead of 32 scattered row segments per instruction).
+    // EW warps = 4 TMEM lane quadrants x EW/4 column parts of HALF columns each
     const int e = warp - 4, q = warp & 3, half = e >> 2;
-    constexpr int HALF = BN / 2, NPF = HALF / 8;
+    constexpr int HALF = BN / (EW / 4), NPF = HALF / 8;
     uint8_t* stg = epi + e * SM::STG;
-    float* sb = reinterpret_cast<float*>(epi + 8 * SM::STG) + e * HALF;
-    float* sc = reinterpret_cast<float*>(epi + 8 * SM::STG) + 8 * HALF + e * HALF;
+    float* sb = reinterpret_cast<float*>(epi + EW * SM::STG) + e * HALF;
+    float* sc = reinterpret_cast<float*>(epi + EW * SM::STG) + EW * HALF + e * HALF;
     const uint32_t te0 = PAIR ? mapa_u32(&tempty[0], 0) : 0u, te1 = PAIR ? mapa_u32(&tempty[1], 0) : 0u;
     int local = 0;
     for (int u = cid; u < units; u += ncl, ++local) {
@@ -891,12 +892,12 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EW = 8>
 void launch(const GemmArgs& a, cudaStream_t s) {
-  using SM = Smem<BN, STAGES>;
+  using SM = Smem<BN, STAGES, false, EW>;
   static bool attr = false;
   if (!attr) {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     attr = true;
   }
@@ -923,7 +924,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
   const CUtensorMap mc = out_map(a, p);
-  launch_k(k_gemm_tc<BN, STAGES>, grid, kThreads, SM::BYTES, s, ma, mb, mc, p);
+  launch_k(k_gemm_tc<BN, STAGES, false, EW>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -1068,6 +1069,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "128x4") tc::launch<128, 4>(a, s);
     else if (c == "256x3") tc::launch<256, 3>(a, s);
     else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
+    else if (c == "256x3w16") tc::launch<256, 3, 16>(a, s);
+    else if (c == "128x4w16") tc::launch<128, 4, 16>(a, s);
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
     else tc::launch<256, 4>(a, s);
   } else {
