@@ -181,7 +181,8 @@ struct Params {
   int splits;         // split-K factor (kb_total % splits == 0)
   float* ws;          // split-K partials [tile][split][BM][BN]
   int* counters;      // split-K arrival counters [tile] (self-resetting)
-  int dbg;            // tuning experiments only (NMT_GEMM_DBG): 1 = drain TMEM, no epilogue
+  int dbg;            // tuning experiments only (NMT_GEMM_DBG bits): 1 = drain TMEM only,
+                      // 2 = no TMA stores, 4 = no staging / stores, 8 = no epilogue math
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
   float2* st_out;     // LN folding, producer side (GemmArgs)
   const float2* ln_st;
@@ -251,16 +252,32 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // epilogue: per warp a 32 x 32 FP16 staging tile (TMA store) and its FP32 bias slice
   static constexpr int STG = 2048;
-  static constexpr int EPI = EW * STG + 2 * 4 * BN * 4;   // + per-warp bias and LN c[n] slices
+  // per epilogue warp: a 32 x 32 staging tile (TMA store) + bias and LN c[n] slices
+  static constexpr int EPI = EW * STG + 2 * 4 * BN * 4;
   static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
 // Epilogue math on 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators):
 // bias (from the warp's shared-memory slice, zero beyond N), residual (prefetched `pre` or
 // loaded here), ReLU.
+// a.lo/hi (FP16 pair) added to two FP32 values, one mixed-precision add each (FHADD)
+__device__ __forceinline__ void add_h2(uint32_t pair, float& lo, float& hi) {
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "add.rn.f32.f16 %0, l, %0;\n\tadd.rn.f32.f16 %1, h, %1;\n\t}"
+      : "+f"(lo), "+f"(hi)
+      : "r"(pair));
+}
+// (lo, hi) -> max(., 0) rounded to a saturating half2 in one instruction
+__device__ __forceinline__ uint32_t pack_half2_sat_relu(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 __device__ __forceinline__ void epi_math(const Params& p, int m, int nb, float* v,
                                          const float* sb, const uint4* pre, bool row_ok,
-                                         const float* sc = nullptr, float2 ln = {0.f, 0.f}) {
+                                         const float* sc = nullptr, float2 ln = {0.f, 0.f},
+                                         bool relu_in_pack = false) {
   const int nv = min(32, p.N - nb);
   const bool full = nv == 32;
   if (p.ln_st) {  // folded LayerNorm: rstd * (acc - mu * c[n])
@@ -282,16 +299,12 @@ __device__ __forceinline__ void epi_math(const Params& p, int m, int nb, float* 
   }
   if (p.R && row_ok && nv > 0) {
     const __half* rr = p.R + (size_t)m * p.ldr + nb;
-    if (pre) {  // residual prefetched before the accumulator wait
+    if (pre) {  // residual prefetched before the accumulator wait; FP16 + FP32 adds
 #pragma unroll
       for (int j8 = 0; j8 < 4; ++j8) {
-        const __half2* h = reinterpret_cast<const __half2*>(&pre[j8]);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&pre[j8]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __half22float2(h[e]);
-          v[j8 * 8 + 2 * e] += f.x;
-          v[j8 * 8 + 2 * e + 1] += f.y;
-        }
+        for (int e = 0; e < 4; ++e) add_h2(w[e], v[j8 * 8 + 2 * e], v[j8 * 8 + 2 * e + 1]);
       }
     } else if (full && ((reinterpret_cast<uintptr_t>(rr) & 15) == 0)) {
 #pragma unroll
@@ -307,7 +320,7 @@ __device__ __forceinline__ void epi_math(const Params& p, int m, int nb, float* 
         if (j < nv) v[j] += __half2float(rr[j]);
     }
   }
-  if (p.relu) {
+  if (p.relu && !relu_in_pack) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
   }
@@ -331,13 +344,17 @@ __device__ __forceinline__ void epi_out(const Params& p, int m, int nb, const fl
         if (j < nv) lr[j] = v[j];
     }
   }
-  if (p.argmax) {
+  if (p.argmax) {  // ascending scan, strict '>' keeps the lowest id among equal maxima
+    float bv = v[0];
+    int bj = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nv) {
-        const unsigned long long k = pack_argmax(v[j], nb + j);
-        best = k > best ? k : best;
+    for (int j = 1; j < 32; ++j)
+      if (j < nv && v[j] > bv) {
+        bv = v[j];
+        bj = j;
       }
+    const unsigned long long k = pack_argmax(bv, nb + bj);
+    best = k > best ? k : best;
     return;
   }
   if (!p.C) return;  // logits-only (beam search) epilogue
@@ -567,12 +584,26 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           if (v[0] == 1234.5f) p.C[0] = __float2half(v[1]);
         } else if (p.tstore) {
           if (n0 + c0 < p.N) {  // warp-uniform
-            epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, row_ok,
-                     sc + (c0 - cb), ln);
+            const bool rp = p.relu && !p.st_out;   // ReLU inside the pack instruction
+            if (!(p.dbg & 8))
+              epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr,
+                       row_ok, sc + (c0 - cb), ln, rp);
             if (p.st_out && row_ok) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
             uint32_t h[16];
+            if (rp) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat(v[2 * i], v[2 * i + 1]);
+              for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat_relu(v[2 * i], v[2 * i + 1]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat(v[2 * i], v[2 * i + 1]);
+            }
+            if (p.dbg & 4) {  // tuning: no staging / store
+              uint32_t x = 0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) x ^= h[i];
+              if (x == 0x12345678u) p.C[0] = __float2half(1.f);
+              continue;
+            }
             if (lane == 0) bulk_wait_read0();   // the previous store has read the staging tile
             __syncwarp();
             const int sw = (lane >> 1) & 3;     // 64-B swizzle: 16-B chunk c at c ^ ((row >> 1) & 3)
@@ -582,7 +613,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
                   make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) {  // rows >= M and columns >= N are clipped by the tensor map
+            if (lane == 0 && !(p.dbg & 2)) {  // rows >= M / columns >= N clipped by the map
               tma_store_2d(&mapC, stg, n0 + c0, m0 + q * 32);
               bulk_commit();
             }
@@ -877,7 +908,7 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows, 
 // device-side count dM beyond the live rows must not be written); else mapC is unused.
 CUtensorMap out_map(const GemmArgs& a, Params& p) {
   p.tstore = getenv("NMT_NO_TSTORE") == nullptr && a.C && !a.argmax && !a.logits && !a.dM &&
-             (a.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+             (a.ldc % 8) == 0 && (a.N % 8) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
   if (!p.tstore) return CUtensorMap{};
   return make_map(a.C, a.M, a.N, a.ldc, 32, true);
 }
@@ -895,6 +926,7 @@ int num_sms() {
 template <int BN, int STAGES, int EW = 8>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW>;
+  static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   static bool attr = false;
   if (!attr) {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW>,
@@ -932,6 +964,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
 template <int BN, int STAGES>
 void launch_pair(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, true>;
+  static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   static bool attr = false;
   if (!attr) {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true>,
@@ -1065,17 +1098,14 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     tc::launch<128, 4>(a, s);
   } else if (const char* e = getenv("NMT_GEMM_CFG")) {  // tuning experiments only
     const std::string c(e);
-    if (c == "128x6") tc::launch<128, 6>(a, s);
-    else if (c == "128x4") tc::launch<128, 4>(a, s);
+    if (c == "128x4") tc::launch<128, 4>(a, s);
     else if (c == "256x3") tc::launch<256, 3>(a, s);
-    else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
     else if (c == "256x3w16") tc::launch<256, 3, 16>(a, s);
     else if (c == "128x4w16") tc::launch<128, 4, 16>(a, s);
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
     else tc::launch<256, 4>(a, s);
   } else {
-    // 128 x 256 tiles: 85 FLOP per L2 byte at K = 512 (vs 64 for 128 x 128) — the encoder
-    // GEMMs are bound by L2 -> SM operand traffic
+    // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
     tc::launch<256, 4>(a, s);
   }
 }
