@@ -904,10 +904,11 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows, 
   return m;
 }
 
-// The TMA-store epilogue serves plain FP16 outputs with a host-known row count (rows of a
-// device-side count dM beyond the live rows must not be written); else mapC is unused.
+// The TMA-store epilogue serves plain FP16 outputs (else mapC is unused).  With a device
+// row count dM it also writes the rows of the last live tile beyond dM (up to the host
+// bound M): those rows are dead (compacted away by pruning) and never read as live data.
 CUtensorMap out_map(const GemmArgs& a, Params& p) {
-  p.tstore = getenv("NMT_NO_TSTORE") == nullptr && a.C && !a.argmax && !a.logits && !a.dM &&
+  p.tstore = getenv("NMT_NO_TSTORE") == nullptr && a.C && !a.argmax && !a.logits &&
              (a.ldc % 8) == 0 && (a.N % 8) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
   if (!p.tstore) return CUtensorMap{};
   return make_map(a.C, a.M, a.N, a.ldc, 32, true);
