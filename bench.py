@@ -181,6 +181,8 @@ def main():
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
     ap.add_argument("--ref-sents-per-worker", type=int, default=12)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cap-clip", type=int, default=0,
+                    help="analysis only: clip target caps (1 = encoder-dominated run); not a bench value")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -235,7 +237,8 @@ def main():
 
     def dev_step(k, workers=None):
         wl, d_ids = chunks[k]
-        return model.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps,
+        caps = wl.caps if args.cap_clip <= 0 else np.minimum(wl.caps, args.cap_clip)
+        return model.translate_device(d_ids, wl.off, d_out, d_len, caps=caps,
                                       max_tokens=args.max_tokens, max_sents=args.max_sents,
                                       sync_every=args.sync_every,
                                       workers=args.workers if workers is None else workers)
