@@ -407,8 +407,14 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   using SM = Smem<BN, STAGES, PAIR, EW>;
   constexpr int UM = PAIR ? 2 * BM : BM;             // output rows per unit
   constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
-  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                 : 2 * BN <= 256 ? 256 : 512;
+  // BN <= 256: two accumulators (the epilogue of unit i overlaps the MMAs of unit i+1);
+  // BN = 512 fills TMEM with one (full-row tiles for the N = 512 projections: half the
+  // units of BN = 256, so M = 16K..32K rows fit one or two waves of 148 SMs)
+  constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
+  constexpr uint32_t TMEM_COLS = NACC * BN <= 32 ? 32 : NACC * BN <= 64 ? 64
+                                 : NACC * BN <= 128 ? 128 : NACC * BN <= 256 ? 256 : 512;
+  constexpr int BBOX = BN > 256 ? 256 : BN;         // TMA box rows of B (<= 256)
+  static_assert(!(PAIR && BN > 256), "pair units use BN <= 256");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -481,7 +487,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           } else {
             mbar_expect_tx(&full[st], SM::STAGE);
             tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
-            tma_load_2d(sa + SM::A_BYTES, &mapB, &full[st], kb * BK, n0);
+#pragma unroll
+            for (int bo = 0; bo < BN; bo += BBOX)
+              tma_load_2d(sa + SM::A_BYTES + bo * BK * 2, &mapB, &full[st], kb * BK, n0 + bo);
           }
         }
       }
@@ -490,12 +498,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (one thread; pair leader)
       constexpr uint32_t idesc = (1u << 4)                        // D = F32
                                  | (0u << 7) | (0u << 10)          // A, B = F16
-                                 | ((uint32_t)(BN >> 3) << 17)     // N
+                                 | ((uint32_t)(BBOX >> 3) << 17)   // N (per instruction)
                                  | ((uint32_t)(UM >> 4) << 24);    // M
       int it = 0, local = 0;
       for (int u = cid; u < units; u += ncl, ++local) {
-        const int acc = local & 1;
-        const uint32_t aph = (local >> 1) & 1;
+        const int acc = NACC == 2 ? (local & 1) : 0;
+        const uint32_t aph = NACC == 2 ? (local >> 1) & 1 : local & 1;
         mbar_wait(&tempty[acc], aph ^ 1);   // epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * ACC_COLS;
@@ -509,8 +517,13 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {  // +32 B along K inside the swizzle atom
             const uint32_t accum = (first == 0 || kk > 0) ? 1u : 0u;
-            if constexpr (PAIR) mma_f16_pair(d, da + 2 * kk, db + 2 * kk, idesc, accum);
-            else mma_f16(d, da + 2 * kk, db + 2 * kk, idesc, accum);
+            if constexpr (PAIR) {
+              mma_f16_pair(d, da + 2 * kk, db + 2 * kk, idesc, accum);
+            } else {
+#pragma unroll
+              for (int bo = 0; bo < BN; bo += BBOX)   // N > 256: one MMA per 256-column half
+                mma_f16(d + bo, da + 2 * kk, db + ((bo * BK * 2) >> 4) + 2 * kk, idesc, accum);
+            }
           }
           if constexpr (PAIR) mma_commit_pair(&empty[st]);  // frees the stage in both CTAs
           else mma_commit(&empty[st]);
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     // bulk store (full-line writes instead of 32 scattered row segments per instruction).
     // EW warps = 4 TMEM lane quadrants x EW/4 column parts of HALF columns each
     const int e = warp - 4, q = warp & 3, half = e >> 2;
-    constexpr int HALF = BN / (EW / 4), NPF = HALF / 8;
+    constexpr int HALF = BN / (EW / 4), NPF = HALF <= 128 ? HALF / 8 : 1;
     uint8_t* stg = epi + e * SM::STG;
     float* sb = reinterpret_cast<float*>(epi + EW * SM::STG) + e * HALF;
     float* sc = reinterpret_cast<float*>(epi + EW * SM::STG) + EW * HALF + e * HALF;
@@ -533,15 +546,15 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     int local = 0;
     for (int u = cid; u < units; u += ncl, ++local) {
       const int m0 = (u % num_m) * UM + rank * BM, n0 = (u / num_m) * BN;
-      const int acc = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
+      const int acc = NACC == 2 ? (local & 1) : 0;
+      const uint32_t aph = NACC == 2 ? (local >> 1) & 1 : local & 1;
       const int r = q * 32 + lane;
       const int m = m0 + r;
       const bool row_ok = m < M;
       const int cb = half * HALF;
       // residual rows and the bias slice fetched while the MMAs of this unit still run
       uint4 res[NPF];
-      const bool pf = p.R && row_ok && n0 + cb + HALF <= p.N &&
+      const bool pf = HALF <= 128 && p.R && row_ok && n0 + cb + HALF <= p.N &&
                       ((reinterpret_cast<uintptr_t>(p.R + (size_t)m * p.ldr + n0 + cb) & 15) == 0);
       if (pf) {
         const uint4* rp = reinterpret_cast<const uint4*>(p.R + (size_t)m * p.ldr + n0 + cb);
@@ -936,7 +949,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   }
   if (a.splits > 1) throw CudaError("gemm_tc: persistent kernel has no split-K (use the cluster path)");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
-  CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN);
+  CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN > 256 ? 256 : BN);
   Params p{};
   p.M = a.M; p.N = a.N; p.K = a.K;
   p.bias = static_cast<const __half*>(a.bias);
@@ -1104,6 +1117,7 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "256x3w16") tc::launch<256, 3, 16>(a, s);
     else if (c == "128x4w16") tc::launch<128, 4, 16>(a, s);
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
+    else if (c == "512x2") tc::launch<512, 2>(a, s);
     else tc::launch<256, 4>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
