@@ -17,4 +17,5 @@ R2-R8, R10) and end-to-end quality (BLEU), which needs trained weights.
 from .nn import layer_norm, softmax, log_softmax, sinusoid_pe, rel_index  # noqa: F401
 from .model import OracleModel  # noqa: F401
 from .batching import plan_batches, restore_order  # noqa: F401
-from .search import greedy_def, translate_fast, beam_search, exhaustive_best  # noqa: F401
+from .search import (greedy_def, translate_fast, beam_search, exhaustive_best,  # noqa: F401
+                     beam_search_nbest, exhaustive_nbest, ensemble_step_logprobs)

@@ -23,6 +23,18 @@
   fin is non-empty and max fin >= max active, or at the cap (actives finalised).
   Pinned: K >= V^T equals ``exhaustive_best`` (brute force); K = 1 == greedy;
   early stop on == off.
+* beam_search_nbest: the N-best lists used for sequence-level KD ("we collected
+  the 4-best list for each sentence"), reading R27: the finished
+  list keeps the N best (score desc, ties -> earlier finalised); the search stops
+  when N hypotheses are finished and the N-th best >= the best active (sound:
+  scores never increase), or at the cap (actives finalised).  N = 1 is
+  beam_search.  Pinned: K >= V^T equals ``exhaustive_nbest`` (brute force);
+  early stop on == off; N = 1 == beam_search.
+* ensemble_step_logprobs: the teacher ensemble ("a simple
+  ensemble strategy"), reading R26: per step the members' next-token
+  distributions are averaged, log p = logsumexp_m(log p_m) - log M (fairseq's
+  ensemble).  Pinned: M copies of one model == that model; K >= V^T ensemble
+  beam == brute force over the averaged distribution.
 """
 from __future__ import annotations
 
@@ -135,6 +147,21 @@ def prefix_logprobs(model, enc_kv, src_len, prefixes):
 
 def beam_search(model, src, cap: int, K: int, early_stop: bool = True, step_logprobs=None):
     """Single-sentence beam search (reading R15).  Returns (tokens, score)."""
+    return beam_search_nbest(model, src, cap, K, 1, early_stop, step_logprobs)[0]
+
+
+def _strip(seq):
+    toks = seq[1:]
+    if toks and toks[-1] == EOS_ID:
+        toks = toks[:-1]
+    return toks
+
+
+def beam_search_nbest(model, src, cap: int, K: int, nbest: int, early_stop: bool = True,
+                      step_logprobs=None):
+    """Beam search returning the ``nbest`` best finished hypotheses [(tokens, score)],
+    best first (reading R27; nbest <= K)."""
+    assert 1 <= nbest <= K
     cfg = model.cfg
     V = cfg.vocab_size
     cap = _cap(cfg, cap)
@@ -168,13 +195,58 @@ def beam_search(model, src, cap: int, K: int, early_stop: bool = True, step_logp
         active = new_active
         if not active:
             break
-        if early_stop and fin and max(f[0] for f in fin) >= max(a[0] for a in active):
-            break
-    best = sorted(fin, key=lambda f: (-f[0], f[2]))[0]
-    toks = best[1][1:]
-    if toks and toks[-1] == EOS_ID:
-        toks = toks[:-1]
-    return toks, best[0]
+        if early_stop and len(fin) >= nbest:
+            nth = sorted(fin, key=lambda f: (-f[0], f[2]))[nbest - 1][0]
+            if nth >= max(a[0] for a in active):
+                break
+    ranked = sorted(fin, key=lambda f: (-f[0], f[2]))[:nbest]
+    return [(_strip(f[1]), f[0]) for f in ranked]
+
+
+def exhaustive_nbest(model, src, cap: int, nbest: int, step_logprobs=None):
+    """Brute force: the ``nbest`` highest-scoring complete sequences (EOS-terminated or
+    cap-long) over every sequence of length <= cap; ties -> lexicographically smaller
+    (token ids) first.  Returns [(tokens, score)]."""
+    cfg = model.cfg
+    cap = _cap(cfg, cap)
+    if step_logprobs is None:
+        enc, src_len = model.encode_batch([src])
+        ckv = model.cross_kv(enc)
+
+        def step_logprobs(prefixes):
+            return prefix_logprobs(model, ckv, src_len, prefixes)
+    done = []
+
+    def rec(prefix, score):
+        lp = step_logprobs([prefix])[0]
+        for v in range(cfg.vocab_size):
+            s = score + float(lp[v])
+            seq = prefix + [v]
+            if v == EOS_ID or len(seq) - 1 == cap:
+                done.append((s, seq))
+            else:
+                rec(seq, s)
+
+    rec([BOS_ID], 0.0)
+    done.sort(key=lambda f: (-f[0], f[1]))
+    return [(_strip(f[1]), f[0]) for f in done[:nbest]]
+
+
+def ensemble_step_logprobs(models, srcs_or_src):
+    """Step function for beam_search(_nbest): the members' log-probabilities averaged in
+    probability space, logsumexp_m(lp_m) - log M (reading R26).  ``models`` are
+    OracleModel instances with equal vocabularies; the source is encoded by each."""
+    src = srcs_or_src
+    ctx = []
+    for mdl in models:
+        enc, src_len = mdl.encode_batch([src])
+        ctx.append((mdl, mdl.cross_kv(enc), src_len))
+
+    def step(prefixes):
+        lps = np.stack([prefix_logprobs(mdl, ckv, sl, prefixes) for mdl, ckv, sl in ctx])
+        mx = lps.max(axis=0)
+        return mx + np.log(np.exp(lps - mx).sum(axis=0)) - math.log(len(models))
+    return step
 
 
 def exhaustive_best(model, src, cap: int):
