@@ -142,6 +142,8 @@ typedef struct {
   int32_t n_workers;     /* concurrent batch workers (own arena + stream each, shared
                             weights); 0/1 = one.  Outputs do not depend on it.     */
   int32_t beam;          /* 0/1 = greedy; 2..4 = beam search     */
+  int32_t nbest;         /* 0/1 = best only; 2..beam = keep the N best finished
+                            hypotheses (the KD "4-best list"; reading R27) */
 } nmt_translate_opts;
 
 typedef struct {
@@ -158,6 +160,19 @@ typedef struct {
 nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
                          const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
                          int64_t* h_out_off, nmt_stats* stats, void* stream);
+
+/* N-best translation (beam search, opts->beam >= opts->nbest >= 2), HOST buffers
+ * (synchronous).  "We collected the 4-best list for each sentence": per
+ * sentence the N best finished hypotheses, best first (score desc, ties -> earlier
+ * finalised; the search stops once N are finished and the N-th best is >= every active
+ * hypothesis, or at the cap — reading R27).
+ *   h_out [out_cap] flat outputs of hypothesis (i, r) at index i*nbest + r (EOS stripped),
+ *   h_out_off [n*nbest + 1] their offsets (an empty entry when fewer than N finished),
+ *   h_score [n*nbest] (may be NULL) their scores (sum of log-probabilities; -inf if empty).
+ * Errors: NMT_E_ARG for nbest outside [2, beam] or beam > limits.beam. */
+nmt_status nmt_translate_nbest(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
+                               const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
+                               int64_t* h_out_off, float* h_score, nmt_stats* stats, void* stream);
 
 /* Same with DEVICE-resident sources and outputs (inputs already in HBM):
  *   d_ids [h_off[n]] int32 flat sources on the device; h_off [n+1] host offsets (plan);

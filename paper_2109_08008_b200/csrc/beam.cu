@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(128) k_beam_select(
     int* __restrict__ prev_tok, uint8_t* __restrict__ done, const int* __restrict__ row_slot,
     const int* __restrict__ cap, int* __restrict__ anc, int* __restrict__ htok, int Tmax,
     float* __restrict__ best_score, int* __restrict__ out_tok, int* __restrict__ gen_len,
-    DevState* st, int V, int eos) {
+    DevState* st, int V, int eos, int NB, float* __restrict__ nb_score,
+    int* __restrict__ nb_len, int* __restrict__ nb_tok, int* __restrict__ nb_cnt) {
   extern __shared__ int sm_i[];
   constexpr int KB = 2 * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -164,47 +165,86 @@ __global__ void __launch_bounds__(128) k_beam_select(
     }
     __syncwarp();
   }
-  // sequential bookkeeping by lane 0 (K tiny)
-  __shared__ int s_fin_k[4], s_fin_tok[4], s_done[4];
+  // sequential bookkeeping by lane 0 (K tiny).  The finished list keeps the NB best
+  // (score desc, ties -> earlier finalised; NB = 1: the best only, reading R27).
+  __shared__ int s_done[4], s_nops[4], s_op_pos[4][3 * K], s_op_k[4][3 * K], s_op_tok[4][3 * K];
   __shared__ SelCand s_new[4][K];
   if (lane == 0) {
-    float fin = best_score[sent];
-    int fk = -1, ftok = 0;
-    float fsc = -INFINITY;
+    float lst[4];
+    int cnt = NB == 1 ? (best_score[sent] > -INFINITY ? 1 : 0) : nb_cnt[sent];
+    if (NB == 1) lst[0] = best_score[sent];
+    else
+      for (int i = 0; i < cnt; ++i) lst[i] = nb_score[(size_t)sent * NB + i];
+    int nops = 0;
+    auto try_insert = [&](const SelCand& c) {
+      if (cnt == NB && !(c.v > lst[NB - 1])) return;
+      int pos = 0;
+      while (pos < cnt && lst[pos] >= c.v) ++pos;
+      for (int i = min(cnt, NB - 1); i > pos; --i) lst[i] = lst[i - 1];
+      lst[pos] = c.v;
+      cnt = min(cnt + 1, NB);
+      s_op_pos[warp][nops] = pos;
+      s_op_k[warp][nops] = c.k;
+      s_op_tok[warp][nops] = c.tok;
+      ++nops;
+    };
     int n_new = 0;
     for (int rank = 0; rank < 2 * K; ++rank) {
       const SelCand c = s_sel[warp][rank];
       if (!(c.v > -INFINITY)) break;
       if (c.tok == eos) {
-        if (rank < K && c.v > fin) { fin = c.v; fk = c.k; ftok = c.tok; fsc = c.v; }
+        if (rank < K) try_insert(c);
       } else if (n_new < K) {
         s_new[warp][n_new++] = c;
       }
     }
     const bool at_cap = t + 1 >= cap[sent];
     if (at_cap)
-      for (int i = 0; i < n_new; ++i)
-        if (s_new[warp][i].v > fin) { fin = s_new[warp][i].v; fk = s_new[warp][i].k; ftok = s_new[warp][i].tok; fsc = fin; }
+      for (int i = 0; i < n_new; ++i) try_insert(s_new[warp][i]);
     float best_act = -INFINITY;
     for (int i = 0; i < n_new; ++i) best_act = fmaxf(best_act, s_new[warp][i].v);
-    const bool early = fin > -INFINITY && fin >= best_act;
+    const bool early = cnt >= NB && lst[NB - 1] >= best_act;
     s_done[warp] = at_cap || n_new == 0 || early;
-    s_fin_k[warp] = fk;
-    s_fin_tok[warp] = ftok;
     s_cnt[warp] = n_new;
-    if (fk >= 0) best_score[sent] = fsc;
+    s_nops[warp] = nops;
+    if (NB == 1) {
+      if (cnt) best_score[sent] = lst[0];
+    } else {
+      for (int i = 0; i < cnt; ++i) nb_score[(size_t)sent * NB + i] = lst[i];
+      nb_cnt[sent] = cnt;
+      best_score[sent] = cnt ? lst[0] : -INFINITY;
+    }
   }
   __syncwarp();
-  const int fk = s_fin_k[warp], n_new = s_cnt[warp];
+  const int n_new = s_cnt[warp], nops = s_nops[warp];
   const bool sdone = s_done[warp];
-  // a new best finished hypothesis: tokens = htok[parent][1..t] + token
-  if (fk >= 0) {
-    const int ps = row_slot[r0 + fk];
-    for (int j = lane; j < t; j += 32) out_tok[(size_t)sent * Tmax + j] = htok[(size_t)ps * Tmax + j + 1];
-    if (lane == 0) {
-      out_tok[(size_t)sent * Tmax + t] = s_fin_tok[warp];
-      gen_len[sent] = t + 1;
+  // apply the insertions in order: shift the list rows below `pos`, then write the new
+  // hypothesis = htok[parent][1..t] + token.  Position 0 is mirrored to out_tok.
+  for (int o = 0; o < nops; ++o) {
+    const int pos = s_op_pos[warp][o];
+    const int ps = row_slot[r0 + s_op_k[warp][o]];
+    if (NB > 1) {
+      int* base = nb_tok + (size_t)sent * NB * Tmax;
+      for (int i = NB - 1; i > pos; --i) {
+        const int len = nb_len[(size_t)sent * NB + i - 1];
+        for (int j = lane; j < len; j += 32) base[(size_t)i * Tmax + j] = base[(size_t)(i - 1) * Tmax + j];
+        __syncwarp();
+        if (lane == 0) nb_len[(size_t)sent * NB + i] = len;
+      }
+      for (int j = lane; j < t; j += 32) base[(size_t)pos * Tmax + j] = htok[(size_t)ps * Tmax + j + 1];
+      if (lane == 0) {
+        base[(size_t)pos * Tmax + t] = s_op_tok[warp][o];
+        nb_len[(size_t)sent * NB + pos] = t + 1;
+      }
     }
+    if (pos == 0) {
+      for (int j = lane; j < t; j += 32) out_tok[(size_t)sent * Tmax + j] = htok[(size_t)ps * Tmax + j + 1];
+      if (lane == 0) {
+        out_tok[(size_t)sent * Tmax + t] = s_op_tok[warp][o];
+        gen_len[sent] = t + 1;
+      }
+    }
+    __syncwarp();
   }
   if (sdone) {
     if (lane < K) done[r0 + lane] = 1;
@@ -250,14 +290,16 @@ void beam_row_topk(const float* logits, int V, int KB, const int* dR, int rows_u
 void beam_select(int K, const float* cand_v, const int* cand_i, float* score, int* prev_tok,
                  uint8_t* done, const int* row_slot, const int* cap, int* anc, int* htok,
                  int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st, int V,
-                 int eos, int rows_upper, cudaStream_t s) {
+                 int eos, int rows_upper, cudaStream_t s, int NB, float* nb_score, int* nb_len,
+                 int* nb_tok, int* nb_cnt) {
   if (rows_upper <= 0) return;
+  if (NB < 1 || NB > K) throw CudaError("beam_select: nbest must be in [1, beam]");
   const int groups = (rows_upper + K - 1) / K, nw = 4;
   const size_t smem = (size_t)nw * 2 * K * (Tmax + 1) * sizeof(int);
 #define NMT_BS(KK)                                                                            \
   k_beam_select<KK><<<ceil_div(groups, nw), nw * 32, smem, s>>>(                              \
       cand_v, cand_i, score, prev_tok, done, row_slot, cap, anc, htok, Tmax, best_score,       \
-      out_tok, gen_len, st, V, eos)
+      out_tok, gen_len, st, V, eos, NB, nb_score, nb_len, nb_tok, nb_cnt)
   switch (K) {
     case 1: NMT_BS(1); break;
     case 2: NMT_BS(2); break;
@@ -271,7 +313,7 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
 
 __global__ void k_beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok,
                             int Tmax, float* best_score, int* gen_len, DevState* st, int B, int K,
-                            int S, int bos) {
+                            int S, int bos, int* nb_cnt) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < B * K) {
     row_slot[r] = r;
@@ -283,6 +325,7 @@ __global__ void k_beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* 
   if (r < B) {
     best_score[r] = -INFINITY;
     gen_len[r] = 0;
+    if (nb_cnt) nb_cnt[r] = 0;
   }
   if (r == 0) {
     st->t = 0;
@@ -295,11 +338,11 @@ __global__ void k_beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* 
 
 void beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok, int Tmax,
                float* best_score, int* gen_len, DevState* st, int B, int K, int S, int bos,
-               cudaStream_t s) {
+               cudaStream_t s, int* nb_cnt) {
   const int n = B * K;
   k_beam_init<<<ceil_div(n > 0 ? n : 1, 128), 128, 0, s>>>(row_slot, prev_tok, done, score, htok,
                                                            Tmax, best_score, gen_len, st, B, K, S,
-                                                           bos);
+                                                           bos, nb_cnt);
   NMT_LAUNCH_CHECK();
 }
 

@@ -152,6 +152,10 @@ void init_arena(nmt_model* m) {
       {(void**)&m->anc, L.beam > 1 ? R * Tm * 4 : 256},
       {(void**)&m->htok, L.beam > 1 ? R * Tm * 4 : 256},
       {(void**)&m->best_score, L.beam > 1 ? Bm * 4 : 256},
+      {(void**)&m->nb_score, L.beam > 1 ? Bm * L.beam * 4 : 256},
+      {(void**)&m->nb_len, L.beam > 1 ? Bm * L.beam * 4 : 256},
+      {(void**)&m->nb_tok, L.beam > 1 ? Bm * L.beam * Tm * 4 : 256},
+      {(void**)&m->nb_cnt, L.beam > 1 ? Bm * 4 : 256},
       {(void**)&m->blogits, L.beam > 1 ? R * (size_t)c.vocab_size * 4 : 256},
       {(void**)&m->lnst, R * (d / 32) * 8},
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
@@ -433,9 +437,10 @@ void encode_common(nmt_model* m, int B, int S, const int* h_len, const int* h_ca
   else
     PROF(P_BOOK, 0, 0,
          beam_init(m->row_slot, m->prev_tok, m->done, m->bscore, m->htok, Tm, m->best_score,
-                   m->gen_len, m->st, B, K, S, m->cfg.bos_id, s));
+                   m->gen_len, m->st, B, K, S, m->cfg.bos_id, s, m->nb_cnt));
   b.m = m; b.B = B; b.S = S; b.step = 0; b.rows_upper = B * K; b.max_cap = mc; b.valid = true;
   b.K = K;
+  b.NB = 1;
   b.pending_step_done = false;
 }
 
@@ -488,7 +493,7 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
   };
   unsigned rb;
   memcpy(&rb, &ratio, 4);
-  auto key = std::make_tuple(bucket, every, rb, b.K);
+  auto key = std::make_tuple(bucket, every, rb, b.K * 8 + b.NB);
   if (s == nullptr || !m->eager_keys.count(key)) {
     b.rows_upper = rows;
     eager();  // first use of a configuration runs eagerly (sets kernel attributes)
@@ -602,6 +607,8 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
   const int W = o && o->n_workers > 1 ? std::min(o->n_workers, 8) : 1;
   const int K = o && o->beam > 1 ? o->beam : 1;  // beam width; 1 = greedy
+  const int NB = o && o->nbest > 1 ? o->nbest : 1;  // n-best lists
+  NMT_REQUIRE(NB <= K, NMT_E_ARG, "nbest must be <= beam");
   NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
               "translate opts exceed the model limits");
   for (int64_t i = 0; i < n; ++i) {
@@ -636,6 +643,7 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
       load_src(wm, ws, &p.order[lo], B, S, lens.data());
       encode_common(wm, B, S, lens.data(), caps.data(), ws, K);
       nmt_batch& b = wm->batch;
+      b.NB = NB;
       int rows = B * K;
       int t = 0;
       // the live count is polled every `sync_every` steps (lagged upper bound for grids)
@@ -872,6 +880,68 @@ nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_of
       std::copy(outs[i].begin(), outs[i].end(), h_out + pos);
       pos += outs[i].size();
       h_out_off[i + 1] = pos;
+    }
+    if (stats) stats->out_tokens = pos;
+  });
+}
+
+nmt_status nmt_translate_nbest(nmt_model* m, const int32_t* h_ids, const int64_t* h_off,
+                               int64_t n, const nmt_translate_opts* opts, int32_t* h_out,
+                               int64_t out_cap, int64_t* h_out_off, float* h_score,
+                               nmt_stats* stats, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(m && h_ids && h_off && h_out && h_out_off && opts && n >= 0, NMT_E_ARG,
+                "null argument");
+    const int K = opts->beam > 1 ? opts->beam : 1, NB = opts->nbest > 1 ? opts->nbest : 1;
+    NMT_REQUIRE(NB >= 2 && NB <= K, NMT_E_ARG, "nmt_translate_nbest needs 2 <= nbest <= beam");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int V = m->cfg.vocab_size, eos = m->cfg.eos_id;
+    const int Tm = m->lim.max_tgt_len;
+    std::vector<std::vector<int>> outs((size_t)n * NB);
+    std::vector<float> scores((size_t)n * NB, -INFINITY);
+    auto load_src = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B, int S,
+                        const int* lens) {
+      for (int j = 0; j < B; ++j) {
+        const int32_t* src = h_ids + h_off[order[j]];
+        for (int p = 0; p < S; ++p) {
+          int v = p < lens[j] ? src[p] : wm->cfg.pad_id;
+          NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          wm->hp.src[(size_t)j * S + p] = v;
+        }
+      }
+      NMT_CUDA(cudaMemcpyAsync(wm->src, wm->hp.src, (size_t)B * S * 4, cudaMemcpyHostToDevice, ws));
+    };
+    auto emit = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B) -> int64_t {
+      std::vector<int> tok((size_t)B * NB * Tm), len((size_t)B * NB), cnt(B), gl(B);
+      std::vector<float> sc((size_t)B * NB);
+      NMT_CUDA(cudaMemcpyAsync(tok.data(), wm->nb_tok, tok.size() * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaMemcpyAsync(len.data(), wm->nb_len, len.size() * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaMemcpyAsync(sc.data(), wm->nb_score, sc.size() * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaMemcpyAsync(cnt.data(), wm->nb_cnt, B * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaMemcpyAsync(gl.data(), wm->gen_len, B * 4, cudaMemcpyDeviceToHost, ws));
+      NMT_CUDA(cudaStreamSynchronize(ws));
+      int64_t g = 0;
+      for (int j = 0; j < B; ++j) {
+        g += gl[j];
+        for (int r = 0; r < cnt[j] && r < NB; ++r) {
+          const int L = len[(size_t)j * NB + r];
+          const int* t = tok.data() + ((size_t)j * NB + r) * Tm;
+          const int ol = (L > 0 && t[L - 1] == eos) ? L - 1 : L;
+          outs[(size_t)order[j] * NB + r].assign(t, t + ol);
+          scores[(size_t)order[j] * NB + r] = sc[(size_t)j * NB + r];
+        }
+      }
+      return g;
+    };
+    translate_core(m, h_off, n, opts, load_src, emit, stats, s);
+    int64_t pos = 0;
+    h_out_off[0] = 0;
+    for (size_t i = 0; i < outs.size(); ++i) {
+      NMT_REQUIRE(pos + (int64_t)outs[i].size() <= out_cap, NMT_E_SHAPE, "out_cap too small");
+      std::copy(outs[i].begin(), outs[i].end(), h_out + pos);
+      pos += outs[i].size();
+      h_out_off[i + 1] = pos;
+      if (h_score) h_score[i] = scores[i];
     }
     if (stats) stats->out_tokens = pos;
   });

@@ -71,6 +71,7 @@ struct nmt_batch {
   int rows_upper = 0;    // host upper bound of live rows (grid sizing)
   int max_cap = 0;
   int K = 1;             // beam width (1 = greedy)
+  int NB = 1;            // finished hypotheses kept per sentence (n-best, <= K)
   bool valid = false;
   bool pending_step_done = false;  // nmt_decode_step issued, nmt_prune_batch not yet
 };
@@ -117,6 +118,10 @@ struct nmt_model {
   int* anc = nullptr;         // [R][Tmax] ancestry (slot holding position j)
   int* htok = nullptr;        // [R][Tmax] token history per slot (j = 0: BOS)
   float* best_score = nullptr;  // [max_sents] best finished hypothesis score
+  float* nb_score = nullptr;  // [max_sents][beam] n-best finished scores (desc)
+  int* nb_len = nullptr;      // [max_sents][beam] their generated lengths
+  int* nb_tok = nullptr;      // [max_sents][beam][Tmax] their tokens
+  int* nb_cnt = nullptr;      // [max_sents] list sizes
   float* blogits = nullptr;   // [R][V] FP32 logits of the step
   float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
   float* cand_v = nullptr;    // [R][2K] top log-probs per row

@@ -251,7 +251,7 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   PROF(P_BOOK, 0, 0,
        beam_select(K, m->cand_v, m->cand_i, m->bscore, m->prev_tok, m->done, m->row_slot,
                    m->tgt_cap, m->anc, m->htok, Tm, m->best_score, m->out_tok, m->gen_len, m->st,
-                   V, c.eos_id, R, s));
+                   V, c.eos_id, R, s, b->NB, m->nb_score, m->nb_len, m->nb_tok, m->nb_cnt));
 }
 
 }  // namespace

@@ -113,14 +113,17 @@ void beam_row_topk(const float* logits, int V, int KB, const int* dR, int rows_u
                    float* cand_v, int* cand_i, cudaStream_t s);
 // Per sentence (K consecutive live rows): top-2K candidates, EOS finalisation, early stop
 // (PAPER.md:103), new rows (tokens, scores, ancestry / token histories), winner written to
-// out_tok / gen_len of the sentence slot.
+// out_tok / gen_len of the sentence slot.  NB > 1 also keeps the NB best finished
+// hypotheses (reading R27): nb_score / nb_len [B][NB], nb_tok [B][NB][Tmax], nb_cnt [B].
 void beam_select(int K, const float* cand_v, const int* cand_i, float* score, int* prev_tok,
                  uint8_t* done, const int* row_slot, const int* cap, int* anc, int* htok,
                  int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st,
-                 int V, int eos, int rows_upper, cudaStream_t s);
+                 int V, int eos, int rows_upper, cudaStream_t s, int NB = 1,
+                 float* nb_score = nullptr, int* nb_len = nullptr, int* nb_tok = nullptr,
+                 int* nb_cnt = nullptr);
 void beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok, int Tmax,
                float* best_score, int* gen_len, DevState* st, int B, int K, int S, int bos,
-               cudaStream_t s);
+               cudaStream_t s, int* nb_cnt = nullptr);
 
 // Decoder input + first pre-norm, fused (one warp per live row):
 //   g = sqrt(d) E[w_r] + PE(t),  u = LN(g; gam, bet)     (t = *d_t)

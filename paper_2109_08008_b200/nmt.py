@@ -23,7 +23,8 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_INPUT", 4: "E_STATE", 5: "E_F
 EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_batch_encoder_output", "nmt_decode_step", "nmt_prune_batch", "nmt_batch_live",
            "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
-           "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode"]
+           "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode",
+           "nmt_translate_nbest"]
 
 
 class ProfEntry(C.Structure):
@@ -49,7 +50,7 @@ class StepOut(C.Structure):
 class TranslateOpts(C.Structure):
     _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("prune_every", C.c_int32),
                 ("prune_ratio", C.c_float), ("sync_every", C.c_int32), ("h_tgt_cap", C.c_void_p),
-                ("n_workers", C.c_int32), ("beam", C.c_int32)]
+                ("n_workers", C.c_int32), ("beam", C.c_int32), ("nbest", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -163,6 +164,33 @@ class Model:
                                    _stream(stream)))
         outs = [out[out_off[i]:out_off[i + 1]].tolist() for i in range(n)]
         return outs, st.as_dict()
+
+    def translate_nbest(self, ids, off, nbest, beam, caps=None, max_tokens=None, max_sents=None,
+                        prune_every=1, prune_ratio=0.25, sync_every=4, workers=1, stream=None):
+        """N-best beam translation (C-ABI nmt_translate_nbest).  Returns
+        ([[tokens of rank 0..N-1] per sentence], [[scores]], stats dict)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        n = len(off) - 1
+        capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
+        o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
+                          prune_every, prune_ratio, sync_every,
+                          None if capa is None else capa.ctypes.data, workers, beam, nbest)
+        out_cap = n * nbest * self.Tmax
+        out = np.empty(max(out_cap, 1), dtype=np.int32)
+        out_off = np.empty(n * nbest + 1, dtype=np.int64)
+        score = np.empty(max(n * nbest, 1), dtype=np.float32)
+        st = Stats()
+        _check(lib().nmt_translate_nbest(self.h, ids.ctypes.data_as(C.c_void_p),
+                                         off.ctypes.data_as(C.c_void_p), C.c_int64(n), C.byref(o),
+                                         out.ctypes.data_as(C.c_void_p), C.c_int64(out_cap),
+                                         out_off.ctypes.data_as(C.c_void_p),
+                                         score.ctypes.data_as(C.c_void_p), C.byref(st),
+                                         _stream(stream)))
+        hyps = [[out[out_off[i * nbest + r]:out_off[i * nbest + r + 1]].tolist() for r in range(nbest)]
+                for i in range(n)]
+        scores = [[float(score[i * nbest + r]) for r in range(nbest)] for i in range(n)]
+        return hyps, scores, st.as_dict()
 
     def translate_device(self, d_ids, off, d_out, d_out_len, caps=None, max_tokens=None,
                          max_sents=None, prune_every=1, prune_ratio=0.25, sync_every=4, workers=1,

@@ -265,6 +265,32 @@ def test_beam_tiny_matches_oracle(prec):
     assert sum(o == r for o, r in zip(out2, ref2)) >= (wl.n if prec == "fp32" else wl.n - 2)
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_nbest_tiny_matches_oracle(prec):
+    """N-best lists (the KD 4-best lists, reading R27): the GPU's N best finished
+    hypotheses and their scores vs the oracle's beam_search_nbest; rank 0 equals the 1-best
+    translate output."""
+    from oracle import beam_search_nbest
+    wl = tiny_workload(n=10, seed=11, max_cap=12)
+    om = oracle_model("tiny", 3.0)
+    gm = gpu_model("tiny", prec, 3.0, max_tokens=256, max_sents=8, max_tgt_len=32, beam=4)
+    for K, N in ((4, 4), (4, 2), (3, 3)):
+        ref = [beam_search_nbest(om, wl.sentence(i), wl.caps[i], K=K, nbest=N) for i in range(wl.n)]
+        hyps, scores, st = gm.translate_nbest(wl.ids, wl.off, N, K, caps=wl.caps, max_tokens=48,
+                                              max_sents=4)
+        best, _ = gm.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=48, max_sents=4, beam=K)
+        assert [h[0] for h in hyps] == best
+        same = 0
+        for i in range(wl.n):
+            ok = [t for t, _ in ref[i]] == hyps[i]
+            tol = 1e-4 if prec == "fp32" else 5e-2
+            ok = ok and all(abs(a - b[1]) <= tol * max(1.0, abs(b[1])) for a, b in zip(scores[i], ref[i]))
+            same += ok
+        assert same >= (wl.n if prec == "fp32" else wl.n - 3), (K, N, same)
+        for sc in scores:   # best first
+            assert all(sc[r] >= sc[r + 1] for r in range(len(sc) - 1))
+
+
 def test_beam_teacher_30_6_subset():
     """C4: teacher-scale 30-6 Transformer-DLCL-RPR, FP16 beam 4 with cached attention."""
     from oracle import beam_search
