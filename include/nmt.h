@@ -174,6 +174,26 @@ nmt_status nmt_translate_nbest(nmt_model* m, const int32_t* h_ids, const int64_t
                                const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
                                int64_t* h_out_off, float* h_score, nmt_stats* stats, void* stream);
 
+/* Teacher ensemble ("a simple ensemble strategy"; §8(f) row f1).
+ * members: 1..8 loaded models with one vocabulary, special ids, precision, device and
+ * equal limits (limits.beam >= 2); they may differ in depth, DLCL and RPR (the paper's
+ * 35-6 / 35-6+DLCL / 40-6 / 40-6+DLCL teachers).  The ensemble clones every member
+ * (own arena, weights shared with the member) — the members must outlive it.  Per beam
+ * step each member decodes its own caches and the next-token distributions are averaged:
+ * log p = logsumexp_m(log_softmax(logits_m)) - log M (reading R26), then beam search
+ * (reading R15) and optional N-best lists (R27) run once on the average. */
+typedef struct nmt_ensemble nmt_ensemble;
+nmt_status nmt_ensemble_create(nmt_model* const* members, int32_t n_members, nmt_ensemble** out);
+void nmt_ensemble_free(nmt_ensemble* e);
+/* Host-buffer ensemble translation (synchronous; one stream, batches in plan order).
+ * opts->beam in [2, min(4, limits.beam)], opts->nbest in [0, beam].  Output layout as
+ * nmt_translate_nbest with N = max(1, nbest): entry i*N + r is hypothesis r of sentence i
+ * (EOS stripped), h_out_off [n*N + 1], h_score [n*N] (may be NULL) the ensemble scores. */
+nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const int64_t* h_off,
+                                  int64_t n, const nmt_translate_opts* opts, int32_t* h_out,
+                                  int64_t out_cap, int64_t* h_out_off, float* h_score,
+                                  nmt_stats* stats, void* stream);
+
 /* Same with DEVICE-resident sources and outputs (inputs already in HBM):
  *   d_ids [h_off[n]] int32 flat sources on the device; h_off [n+1] host offsets (plan);
  *   d_out [n][out_stride] int32 generated tokens (EOS included if produced),

@@ -109,6 +109,70 @@ __global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__
   }
 }
 
+// ------------------------------------------------------------------ teacher ensemble
+// "a simple ensemble strategy", reading R26: per row the members' next-token
+// distributions are averaged, ens[v] = logsumexp_m(x_m[v] - LSE_m) - log M (FP32).  One
+// block per live row; pass 1: each member's LSE (online max / sum, block reduce); pass 2:
+// the ensemble log-probabilities.  The per-row top-2K then runs on `ens` as for one model.
+struct EnsLogits { const float* x[8]; };
+
+__device__ __forceinline__ float block_lse(float m, float s) {
+  __shared__ float bm[8], bs[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float mm = m;
+  for (int o = 16; o; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  float ss = (m == -INFINITY) ? 0.f : s * __expf(m - mm);
+  ss = warp_sum(ss);
+  __syncthreads();
+  if (lane == 0) { bm[warp] = mm; bs[warp] = ss; }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, bm[w]);
+  float S = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+    if (bm[w] > -INFINITY) S += bs[w] * __expf(bm[w] - M);
+  return M + __logf(S);
+}
+
+__global__ void __launch_bounds__(256) k_ens_combine(EnsLogits L, int nm, int V,
+                                                     const int* __restrict__ dR,
+                                                     float* __restrict__ ens) {
+  const int row = blockIdx.x;
+  if (row >= *dR) return;
+  float lse[8];
+  for (int k = 0; k < nm; ++k) {
+    const float* x = L.x[k] + (size_t)row * V;
+    float m = -INFINITY, s = 0.f;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      const float f = x[v];
+      if (f > m) { s = s * __expf(m - f) + 1.f; m = f; }
+      else s += __expf(f - m);
+    }
+    lse[k] = block_lse(m, s);
+  }
+  const float logm = __logf((float)nm);
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float a[8], mx = -INFINITY;
+    for (int k = 0; k < nm; ++k) {
+      a[k] = L.x[k][(size_t)row * V + v] - lse[k];
+      mx = fmaxf(mx, a[k]);
+    }
+    float sum = 0.f;
+    for (int k = 0; k < nm; ++k) sum += __expf(a[k] - mx);
+    ens[(size_t)row * V + v] = mx + __logf(sum) - logm;
+  }
+}
+
+void ens_combine(const float* const* logits, int nm, int V, const int* dR, int rows_upper,
+                 float* ens, cudaStream_t s) {
+  if (rows_upper <= 0) return;
+  if (nm < 1 || nm > 8) throw CudaError("ens_combine: 1..8 members");
+  EnsLogits L{};
+  for (int k = 0; k < nm; ++k) L.x[k] = logits[k];
+  k_ens_combine<<<rows_upper, 256, 0, s>>>(L, nm, V, dR, ens);
+  NMT_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ per-sentence select
 // One warp per live sentence group.  Shared staging per warp: the K parents' ancestry and
 // token histories (t+1 ints each), so the in-place rewrite of the group's slots is safe.

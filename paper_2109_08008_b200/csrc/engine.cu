@@ -947,6 +947,184 @@ nmt_status nmt_translate_nbest(nmt_model* m, const int32_t* h_ids, const int64_t
   });
 }
 
+nmt_status nmt_ensemble_create(nmt_model* const* members, int32_t n, nmt_ensemble** out) {
+  return guard([&] {
+    NMT_REQUIRE(members && out && n >= 1 && n <= 8, NMT_E_ARG, "need 1..8 members");
+    nmt_model* m0 = members[0];
+    NMT_REQUIRE(m0, NMT_E_ARG, "null member");
+    for (int k = 0; k < n; ++k) {
+      const nmt_model* m = members[k];
+      NMT_REQUIRE(m, NMT_E_ARG, "null member");
+      NMT_REQUIRE(m->cfg.vocab_size == m0->cfg.vocab_size && m->cfg.eos_id == m0->cfg.eos_id &&
+                      m->cfg.bos_id == m0->cfg.bos_id && m->cfg.pad_id == m0->cfg.pad_id &&
+                      m->cfg.max_src_len == m0->cfg.max_src_len,
+                  NMT_E_SHAPE, "ensemble members need one vocabulary and special ids");
+      NMT_REQUIRE(m->prec == m0->prec && m->device == m0->device, NMT_E_ARG,
+                  "ensemble members need one precision and device");
+      NMT_REQUIRE(m->lim.max_tokens == m0->lim.max_tokens && m->lim.max_sents == m0->lim.max_sents &&
+                      m->lim.max_tgt_len == m0->lim.max_tgt_len && m->lim.beam == m0->lim.beam,
+                  NMT_E_SHAPE, "ensemble members need equal limits");
+      NMT_REQUIRE(m->lim.beam >= 2, NMT_E_ARG, "ensembles decode with beam search (limits.beam >= 2)");
+    }
+    std::unique_ptr<nmt_ensemble> e(new nmt_ensemble());
+    for (int k = 0; k < n; ++k) e->members.push_back(clone_worker(members[k]));
+    nmt_model* c0 = e->members[0];
+    for (int k = 1; k < n; ++k) {   // one search state: alias clone 0's
+      nmt_model* c = e->members[k];
+      c->src = c0->src; c->src_len = c0->src_len; c->tgt_cap = c0->tgt_cap;
+      c->row_slot = c0->row_slot; c->prev_tok = c0->prev_tok; c->done = c0->done;
+      c->out_tok = c0->out_tok; c->gen_len = c0->gen_len; c->st = c0->st; c->bad = c0->bad;
+      c->keys = c0->keys; c->bscore = c0->bscore; c->anc = c0->anc; c->htok = c0->htok;
+      c->best_score = c0->best_score; c->cand_v = c0->cand_v; c->cand_i = c0->cand_i;
+      c->nb_score = c0->nb_score; c->nb_len = c0->nb_len; c->nb_tok = c0->nb_tok;
+      c->nb_cnt = c0->nb_cnt;
+    }
+    const size_t R = (size_t)c0->lim.max_sents * c0->lim.beam;
+    cudaError_t err = cudaMalloc(&e->ens, R * c0->cfg.vocab_size * 4);
+    NMT_REQUIRE(err == cudaSuccess, NMT_E_RESOURCE, "ensemble buffer cudaMalloc failed");
+    *out = e.release();
+  });
+}
+
+void nmt_ensemble_free(nmt_ensemble* e) { delete e; }
+
+nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const int64_t* h_off,
+                                  int64_t n, const nmt_translate_opts* opts, int32_t* h_out,
+                                  int64_t out_cap, int64_t* h_out_off, float* h_score,
+                                  nmt_stats* stats, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(e && h_ids && h_off && h_out && h_out_off && opts && n >= 0, NMT_E_ARG,
+                "null argument");
+    nmt_model* c0 = e->members[0];
+    const int nm = (int)e->members.size();
+    const int K = opts->beam, NB = opts->nbest > 1 ? opts->nbest : 1;
+    NMT_REQUIRE(K >= 2 && K <= c0->lim.beam && K <= 4, NMT_E_ARG,
+                "ensemble beam must be in [2, min(4, limits.beam)]");
+    NMT_REQUIRE(NB <= K, NMT_E_ARG, "nbest must be <= beam");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int V = c0->cfg.vocab_size, eos = c0->cfg.eos_id, Tm = c0->lim.max_tgt_len;
+    const int max_tokens = opts->max_tokens > 0 ? opts->max_tokens : c0->lim.max_tokens;
+    const int max_sents = opts->max_sents > 0 ? opts->max_sents : c0->lim.max_sents;
+    const int every = opts->prune_every > 0 ? opts->prune_every : 1;
+    const float ratio = opts->prune_ratio;
+    const int sync_every = opts->sync_every > 0 ? opts->sync_every : 4;
+    NMT_REQUIRE(max_tokens <= c0->lim.max_tokens && max_sents <= c0->lim.max_sents, NMT_E_ARG,
+                "translate opts exceed the model limits");
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t len = h_off[i + 1] - h_off[i];
+      NMT_REQUIRE(len >= 1 && len <= c0->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
+                  "source " + std::to_string(i) + " empty or longer than max_src_len");
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+    const int nb = (int)p.bstart.size() - 1;
+    std::vector<std::vector<int>> outs((size_t)n * NB);
+    std::vector<float> scores((size_t)n * NB, -INFINITY);
+    std::vector<const float*> lg(nm);
+    for (int k = 0; k < nm; ++k) lg[k] = e->members[k]->blogits;
+    int64_t steps = 0, prunes = 0, gen = 0;
+    std::vector<int> lens, caps;
+    for (int bi = 0; bi < nb; ++bi) {
+      const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
+      const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+      lens.resize(B);
+      caps.resize(B);
+      for (int j = 0; j < B; ++j) {
+        const int sid = p.order[lo + j];
+        lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+        caps[j] = opts->h_tgt_cap ? opts->h_tgt_cap[sid] : Tm;
+        const int32_t* src = h_ids + h_off[sid];
+        for (int q = 0; q < S; ++q) {
+          const int v = q < lens[j] ? src[q] : c0->cfg.pad_id;
+          NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          c0->hp.src[(size_t)j * S + q] = v;
+        }
+      }
+      NMT_CUDA(cudaMemcpyAsync(c0->src, c0->hp.src, (size_t)B * S * 4, cudaMemcpyHostToDevice, s));
+      for (auto* c : e->members) encode_common(c, B, S, lens.data(), caps.data(), s, K);
+      c0->batch.NB = NB;
+      const int* dR = &c0->st->n_live;
+      int rows = B * K, t = 0;
+      for (; t < c0->batch.max_cap && rows > 0; ++t) {
+        for (auto* c : e->members) {
+          c->batch.rows_upper = rows;
+          decode_step_any(c, &c->batch, nullptr, nullptr, s, /*finish=*/false);
+        }
+        ens_combine(lg.data(), nm, V, dR, rows, e->ens, s);
+        beam_row_topk(e->ens, V, 2 * K, dR, rows, c0->cand_v, c0->cand_i, s);
+        beam_select(K, c0->cand_v, c0->cand_i, c0->bscore, c0->prev_tok, c0->done, c0->row_slot,
+                    c0->tgt_cap, c0->anc, c0->htok, Tm, c0->best_score, c0->out_tok, c0->gen_len,
+                    c0->st, V, eos, rows, s, NB, c0->nb_score, c0->nb_len, c0->nb_tok, c0->nb_cnt);
+        prune_compact(c0->st, c0->row_slot, c0->prev_tok, c0->done, every, ratio, nullptr, rows, s,
+                      c0->bscore);
+        for (auto* c : e->members) c->batch.step = t + 1;
+        if ((t + 1) % sync_every == 0) {
+          poll_state(c0, s);
+          rows = c0->hp.st->n_live;
+        }
+      }
+      poll_state(c0, s);
+      steps += t;
+      prunes += c0->hp.st->prunes;
+      // results: the N-best lists (NB >= 2) or the best hypothesis
+      std::vector<int> gl(B);
+      NMT_CUDA(cudaMemcpyAsync(gl.data(), c0->gen_len, B * 4, cudaMemcpyDeviceToHost, s));
+      if (NB >= 2) {
+        std::vector<int> tok((size_t)B * NB * Tm), len((size_t)B * NB), cnt(B);
+        std::vector<float> sc((size_t)B * NB);
+        NMT_CUDA(cudaMemcpyAsync(tok.data(), c0->nb_tok, tok.size() * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaMemcpyAsync(len.data(), c0->nb_len, len.size() * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaMemcpyAsync(sc.data(), c0->nb_score, sc.size() * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaMemcpyAsync(cnt.data(), c0->nb_cnt, B * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < B; ++j)
+          for (int r = 0; r < cnt[j] && r < NB; ++r) {
+            const int L = len[(size_t)j * NB + r];
+            const int* tk = tok.data() + ((size_t)j * NB + r) * Tm;
+            const int ol = (L > 0 && tk[L - 1] == eos) ? L - 1 : L;
+            outs[(size_t)p.order[lo + j] * NB + r].assign(tk, tk + ol);
+            scores[(size_t)p.order[lo + j] * NB + r] = sc[(size_t)j * NB + r];
+          }
+      } else {
+        std::vector<int> tok((size_t)B * Tm);
+        std::vector<float> sc(B);
+        NMT_CUDA(cudaMemcpyAsync(tok.data(), c0->out_tok, tok.size() * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaMemcpyAsync(sc.data(), c0->best_score, B * 4, cudaMemcpyDeviceToHost, s));
+        NMT_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < B; ++j) {
+          const int L = gl[j];
+          const int* tk = tok.data() + (size_t)j * Tm;
+          const int ol = (L > 0 && tk[L - 1] == eos) ? L - 1 : L;
+          outs[p.order[lo + j]].assign(tk, tk + ol);
+          scores[p.order[lo + j]] = sc[j];
+        }
+      }
+      for (int j = 0; j < B; ++j) gen += gl[j];
+      for (auto* c : e->members) c->batch.valid = false;
+    }
+    int64_t pos = 0;
+    h_out_off[0] = 0;
+    for (size_t i = 0; i < outs.size(); ++i) {
+      NMT_REQUIRE(pos + (int64_t)outs[i].size() <= out_cap, NMT_E_SHAPE, "out_cap too small");
+      std::copy(outs[i].begin(), outs[i].end(), h_out + pos);
+      pos += outs[i].size();
+      h_out_off[i + 1] = pos;
+      if (h_score) h_score[i] = scores[i];
+    }
+    if (stats) {
+      *stats = nmt_stats{};
+      stats->sentences = n;
+      stats->gen_tokens = gen;
+      stats->out_tokens = pos;
+      stats->decode_steps = steps;
+      stats->prunes = prunes;
+      stats->batches = nb;
+      stats->ms_total = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
 nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_t* h_off,
                                 int64_t n, const nmt_translate_opts* opts, int32_t* d_out,
                                 int32_t out_stride, int32_t* d_out_len, nmt_stats* stats,

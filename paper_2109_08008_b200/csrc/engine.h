@@ -174,6 +174,18 @@ struct nmt_model {
   }
 };
 
+// Teacher ensemble: one clone per member (own arena + caches, shared
+// weights); the search state (row_slot, tokens, scores, ancestry, DevState ...) of clones
+// 1.. aliases clone 0's, so one beam search drives every member's decoder.
+struct nmt_ensemble {
+  std::vector<nmt_model*> members;
+  float* ens = nullptr;   // [R][V] FP32 ensemble log-probabilities of the step
+  ~nmt_ensemble() {
+    for (auto* c : members) delete c;
+    if (ens) cudaFree(ens);
+  }
+};
+
 namespace nmt {
 // forward.cu
 void encode_any(nmt_model* m, int B, int S, cudaStream_t s);

@@ -121,6 +121,9 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
                  int V, int eos, int rows_upper, cudaStream_t s, int NB = 1,
                  float* nb_score = nullptr, int* nb_len = nullptr, int* nb_tok = nullptr,
                  int* nb_cnt = nullptr);
+// Teacher ensemble (reading R26): ens[r][v] = logsumexp_m(log_softmax(logits_m[r])[v]) - log M.
+void ens_combine(const float* const* logits, int nm, int V, const int* dR, int rows_upper,
+                 float* ens, cudaStream_t s);
 void beam_init(int* row_slot, int* prev_tok, uint8_t* done, float* score, int* htok, int Tmax,
                float* best_score, int* gen_len, DevState* st, int B, int K, int S, int bos,
                cudaStream_t s, int* nb_cnt = nullptr);

@@ -24,7 +24,8 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_batch_encoder_output", "nmt_decode_step", "nmt_prune_batch", "nmt_batch_live",
            "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
            "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode",
-           "nmt_translate_nbest"]
+           "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
+           "nmt_translate_ensemble"]
 
 
 class ProfEntry(C.Structure):
@@ -296,3 +297,56 @@ def dev_gemm_argmax(A, B, logits=False, stream=None):
     _check(lib().nmt_dev_gemm_argmax(prec, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                                      _ptr(nxt), _ptr(lg), _stream(stream)))
     return (nxt, lg) if logits else nxt
+
+
+class Ensemble:
+    """Teacher ensemble (C-ABI nmt_ensemble_*): member Models with one
+    vocabulary decode together; per beam step their distributions are averaged (R26)."""
+
+    def __init__(self, models):
+        self.models = list(models)   # the members must outlive the ensemble
+        arr = (C.c_void_p * len(self.models))(*[m.h for m in self.models])
+        h = C.c_void_p()
+        _check(lib().nmt_ensemble_create(arr, C.c_int32(len(self.models)), C.byref(h)))
+        self.h = h
+        self.Tmax = self.models[0].Tmax
+        self.limits = self.models[0].limits
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nmt_ensemble_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def translate(self, ids, off, beam, nbest=1, caps=None, max_tokens=None, max_sents=None,
+                  prune_every=1, prune_ratio=0.25, sync_every=4, stream=None):
+        """Returns ([[tokens of rank 0..N-1]] per sentence, [[scores]], stats), N = nbest."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        n = len(off) - 1
+        N = max(1, nbest)
+        capa = None if caps is None else np.ascontiguousarray(caps, dtype=np.int32)
+        o = TranslateOpts(max_tokens or self.limits.max_tokens, max_sents or self.limits.max_sents,
+                          prune_every, prune_ratio, sync_every,
+                          None if capa is None else capa.ctypes.data, 1, beam, nbest)
+        out_cap = n * N * self.Tmax
+        out = np.empty(max(out_cap, 1), dtype=np.int32)
+        out_off = np.empty(n * N + 1, dtype=np.int64)
+        score = np.empty(max(n * N, 1), dtype=np.float32)
+        st = Stats()
+        _check(lib().nmt_translate_ensemble(self.h, ids.ctypes.data_as(C.c_void_p),
+                                            off.ctypes.data_as(C.c_void_p), C.c_int64(n),
+                                            C.byref(o), out.ctypes.data_as(C.c_void_p),
+                                            C.c_int64(out_cap), out_off.ctypes.data_as(C.c_void_p),
+                                            score.ctypes.data_as(C.c_void_p), C.byref(st),
+                                            _stream(stream)))
+        hyps = [[out[out_off[i * N + r]:out_off[i * N + r + 1]].tolist() for r in range(N)]
+                for i in range(n)]
+        scores = [[float(score[i * N + r]) for r in range(N)] for i in range(n)]
+        return hyps, scores, st.as_dict()
+

@@ -291,6 +291,44 @@ def test_nbest_tiny_matches_oracle(prec):
             assert all(sc[r] >= sc[r + 1] for r in range(len(sc) - 1))
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_ensemble_tiny_matches_oracle(prec):
+    """Teacher ensemble (reading R26): two tiny members with different
+    weights, beam 4 (1-best and 3-best) vs the oracle's beam search over the averaged
+    distribution; a one-member ensemble equals the member's own beam search."""
+    from synth import generate_weights
+    from oracle import OracleModel, beam_search_nbest, ensemble_step_logprobs
+    from paper_2109_08008_b200 import Model, Ensemble
+    cfg, W1 = weights("tiny", 3.0)
+    W2 = generate_weights(cfg, seed=2110, eos_boost=3.0)
+    om1, om2 = oracle_model("tiny", 3.0), OracleModel(W2, cfg)
+    lim = dict(max_tokens=256, max_sents=8, max_tgt_len=32, beam=4)
+    g1 = Model(cfg, W1, precision=prec, **lim)
+    g2 = Model(cfg, W2, precision=prec, **lim)
+    ens = Ensemble([g1, g2])
+    wl = tiny_workload(n=10, seed=12, max_cap=12)
+    tol = 1e-4 if prec == "fp32" else 5e-2
+    for K, N in ((4, 1), (4, 3)):
+        hyps, scores, st = ens.translate(wl.ids, wl.off, beam=K, nbest=N, caps=wl.caps,
+                                         max_tokens=48, max_sents=4)
+        same = 0
+        for i in range(wl.n):
+            src = wl.sentence(i)
+            ref = beam_search_nbest(om1, src, wl.caps[i], K=K, nbest=N,
+                                    step_logprobs=ensemble_step_logprobs([om1, om2], src))
+            ok = [t for t, _ in ref] == hyps[i]
+            ok = ok and all(abs(a - b[1]) <= tol * max(1.0, abs(b[1])) for a, b in zip(scores[i], ref))
+            same += ok
+        assert same >= (wl.n if prec == "fp32" else wl.n - 2), (K, N, same)
+        assert st["sentences"] == wl.n and st["gen_tokens"] > 0
+    solo = Ensemble([g1])
+    hyps, _, _ = solo.translate(wl.ids, wl.off, beam=4, caps=wl.caps, max_tokens=48, max_sents=4)
+    best, _ = g1.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=48, max_sents=4, beam=4)
+    assert sum(h[0] == b for h, b in zip(hyps, best)) >= wl.n - (0 if prec == "fp32" else 1)
+    ens.close()
+    solo.close()
+
+
 def test_beam_teacher_30_6_subset():
     """C4: teacher-scale 30-6 Transformer-DLCL-RPR, FP16 beam 4 with cached attention."""
     from oracle import beam_search
