@@ -65,4 +65,9 @@ PRESETS = {
     "student-18-1": ModelConfig(enc_layers=18, dec_layers=1),
     "student-9-1": ModelConfig(enc_layers=9, dec_layers=1),
     "teacher-40-6": ModelConfig(enc_layers=40, dec_layers=6),
+    # the four ensemble teachers (Table 1), §8(f) row f1
+    "ens-35-6": ModelConfig(enc_layers=35, dec_layers=6, use_dlcl=False),
+    "ens-35-6-dlcl": ModelConfig(enc_layers=35, dec_layers=6),
+    "ens-40-6": ModelConfig(enc_layers=40, dec_layers=6, use_dlcl=False),
+    "ens-40-6-dlcl": ModelConfig(enc_layers=40, dec_layers=6),
 }

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 import torch
 
-from synth import tiny_workload, newstest_like, random_tokens, BOS_ID
+from synth import tiny_workload, newstest_like, random_tokens, BOS_ID, PRESETS
 from gpu_common import TOL, SAFE_GAP, weights, oracle_model, gpu_model, logits_close, margin_safe, pad_batch
 
 pytestmark = pytest.mark.gpu
@@ -327,6 +327,31 @@ def test_ensemble_tiny_matches_oracle(prec):
     assert sum(h[0] == b for h, b in zip(hyps, best)) >= wl.n - (0 if prec == "fp32" else 1)
     ens.close()
     solo.close()
+
+
+def test_ensemble_heterogeneous_teachers_subset():
+    """Ensemble of two teacher-scale members that differ in depth and DLCL (30-6+DLCL and
+    24-6 without DLCL, FP16, beam 4, 2-best) vs the oracle ensemble beam on a subset."""
+    from synth import generate_weights
+    from oracle import OracleModel, beam_search_nbest, ensemble_step_logprobs
+    from paper_2109_08008_b200 import Model, Ensemble
+    cfg1, W1 = weights("teacher-30-6")
+    cfg2 = PRESETS["teacher-30-6"].replace(enc_layers=24, use_dlcl=False)
+    W2 = generate_weights(cfg2, seed=2111)
+    om1, om2 = oracle_model("teacher-30-6"), OracleModel(W2, cfg2)
+    wl = newstest_like(2, 32000, start=91)
+    caps = np.minimum(wl.caps, 6)
+    lim = dict(max_tokens=512, max_sents=4, max_tgt_len=16, beam=4)
+    ens = Ensemble([Model(cfg1, W1, precision="fp16", **lim), Model(cfg2, W2, precision="fp16", **lim)])
+    hyps, scores, _ = ens.translate(wl.ids, wl.off, beam=4, nbest=2, caps=caps)
+    same = 0
+    for i in range(wl.n):
+        src = wl.sentence(i)
+        ref = beam_search_nbest(om1, src, caps[i], K=4, nbest=2,
+                                step_logprobs=ensemble_step_logprobs([om1, om2], src))
+        same += [t for t, _ in ref] == hyps[i]
+    assert same >= wl.n - 1, (hyps, same)
+    ens.close()
 
 
 def test_beam_teacher_30_6_subset():

@@ -26,6 +26,16 @@ def test_param_counts_match_tables():
     assert round(ens / 1e6) == g["ensemble"]
 
 
+def test_ensemble_presets_match_table1():
+    """The four teacher presets used by the GPU ensemble: each member's
+    printed size and the ensemble's 640M (DLCL members counted with their DLCL params)."""
+    g = _golden()
+    sizes = {n: param_count(PRESETS[n]) for n in ("ens-35-6", "ens-35-6-dlcl", "ens-40-6", "ens-40-6-dlcl")}
+    assert round(sizes["ens-35-6"] / 1e6) == round(sizes["ens-35-6-dlcl"] / 1e6) == g["student-35-6"]
+    assert round(sizes["ens-40-6"] / 1e6) == round(sizes["ens-40-6-dlcl"] / 1e6) == g["teacher-40-6"]
+    assert round(sum(sizes.values()) / 1e6) == g["ensemble"]
+
+
 def test_dlcl_adds_negligible_params():
     # Table 1 prints the same size with and without DLCL (PAPER.md:40-43)
     for name in ("student-35-6", "teacher-40-6"):
