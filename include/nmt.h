@@ -194,6 +194,34 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
                                   int64_t out_cap, int64_t* h_out_off, float* h_score,
                                   nmt_stats* stats, void* stream);
 
+/* ---- Text pipeline (§8(f) row f3), host side.  "jointly byte pair encoded with 32K
+ * merge operations using a shared vocabulary ... After decoding, we removed the BPE
+ * separators", with the C++ subword codec of PAPER.md:141 (fastBPE
+ * conventions, reading R28): pretokenised lines split on ASCII whitespace; a word starts
+ * as its UTF-8 characters; the adjacent pair of lowest merge rank is merged at every
+ * non-overlapping occurrence, left to right, until none applies; non-final subwords end
+ * in "@@".  Vocabulary: reserved PAD, UNK, BOS, EOS = 0..3, vocabulary-file token i has
+ * id 4 + i.  The codec is immutable after load (safe for concurrent use). */
+typedef struct nmt_text nmt_text;
+/* vocab: UTF-8, one token per line; merges: one "a b" pair per line, rank = line order,
+ * "#version" lines skipped.  NMT_E_FORMAT names the offending line (malformed merge,
+ * duplicate pair or token). */
+nmt_status nmt_text_load(const char* vocab, int64_t vocab_len, const char* merges,
+                         int64_t merges_len, nmt_text** out);
+void nmt_text_free(nmt_text* t);
+int32_t nmt_text_vocab_size(const nmt_text* t);   /* 4 reserved + file tokens */
+/* '\n'-separated lines -> ids: BPE, token -> id (unknown -> UNK), EOS appended per line.
+ * h_ids [cap] flat ids, h_off [max_lines + 1] line offsets, *n_lines the line count;
+ * n_threads >= 1 host threads split the lines.  NMT_E_SHAPE if cap / max_lines are short. */
+nmt_status nmt_text_encode(const nmt_text* t, const char* text, int64_t len, int32_t n_threads,
+                           int32_t* h_ids, int64_t cap, int64_t* h_off, int64_t max_lines,
+                           int64_t* n_lines);
+/* ids -> text: per sequence stop at EOS, skip PAD / UNK / BOS, join tokens by spaces and
+ * delete every "@@ "; each line '\n'-terminated into out [cap], *out_len bytes.
+ * NMT_E_INPUT for an id outside [0, vocab size). */
+nmt_status nmt_text_decode(const nmt_text* t, const int32_t* h_ids, const int64_t* h_off,
+                           int64_t n, char* out, int64_t cap, int64_t* out_len);
+
 /* Same with DEVICE-resident sources and outputs (inputs already in HBM):
  *   d_ids [h_off[n]] int32 flat sources on the device; h_off [n+1] host offsets (plan);
  *   d_out [n][out_stride] int32 generated tokens (EOS included if produced),

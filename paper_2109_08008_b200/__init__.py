@@ -4,5 +4,5 @@ The product is libnmt.so (include/nmt.h, C ABI; hand-written sm_100a CUDA under 
 This package holds its build script, the NTSD blob writer and a thin ctypes binding.
 It never imports ``oracle/`` (test infrastructure) and has no CPU fallback.
 """
-from .nmt import (Model, Batch, Ensemble, NmtError, dev_gemm, dev_gemm_argmax,  # noqa: F401
+from .nmt import (Model, Batch, Ensemble, TextCodec, NmtError, dev_gemm, dev_gemm_argmax,  # noqa: F401
                   dev_gemm_decode, lib, LIB_PATH, EXPORTS)

@@ -713,24 +713,9 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   }
 }
 
-template <class F> nmt_status guard(F f) {
-  try {
-    g_err.clear();
-    f();
-    return NMT_OK;
-  } catch (const NmtError& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const CudaError& e) {
-    g_err = e.what();
-    return NMT_E_CUDA;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return NMT_E_ARG;
-  }
-}
-
 }  // namespace
+
+std::string& nmt::last_error() { return g_err; }
 
 // ====================================================================== C ABI
 extern "C" {

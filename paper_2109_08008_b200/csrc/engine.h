@@ -187,6 +187,25 @@ struct nmt_ensemble {
 };
 
 namespace nmt {
+// Every C-ABI entry point runs its body through guard(): exceptions become status codes,
+// the message goes to the thread-local last error (nmt_last_error).
+std::string& last_error();
+template <class F> nmt_status guard(F f) {
+  try {
+    last_error().clear();
+    f();
+    return NMT_OK;
+  } catch (const NmtError& e) {
+    last_error() = e.what();
+    return e.code;
+  } catch (const CudaError& e) {
+    last_error() = e.what();
+    return NMT_E_CUDA;
+  } catch (const std::exception& e) {
+    last_error() = e.what();
+    return NMT_E_ARG;
+  }
+}
 // forward.cu
 void encode_any(nmt_model* m, int B, int S, cudaStream_t s);
 // finish = false leaves the greedy bookkeeping to a following finish_prune launch.

@@ -25,7 +25,8 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_batch_results", "nmt_translate", "nmt_translate_device", "nmt_last_error",
            "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode",
            "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
-           "nmt_translate_ensemble"]
+           "nmt_translate_ensemble", "nmt_text_load", "nmt_text_free", "nmt_text_vocab_size",
+           "nmt_text_encode", "nmt_text_decode"]
 
 
 class ProfEntry(C.Structure):
@@ -165,6 +166,15 @@ class Model:
                                    _stream(stream)))
         outs = [out[out_off[i]:out_off[i + 1]].tolist() for i in range(n)]
         return outs, st.as_dict()
+
+    def translate_text(self, codec, lines, caps=None, threads=4, **kw):
+        """File-to-file path (§8(f) f3): lines -> BPE ids (library codec) -> nmt_translate
+        -> ids -> lines with the separators removed."""
+        ids, off = codec.encode(lines, threads=threads)
+        outs, st = self.translate(ids, off, caps=caps, **kw)
+        oo = np.cumsum([0] + [len(o) for o in outs]).astype(np.int64)
+        flat = np.array([t for o in outs for t in o], dtype=np.int32)
+        return codec.decode(flat, oo), st
 
     def translate_nbest(self, ids, off, nbest, beam, caps=None, max_tokens=None, max_sents=None,
                         prune_every=1, prune_ratio=0.25, sync_every=4, workers=1, stream=None):
@@ -349,4 +359,59 @@ class Ensemble:
                 for i in range(n)]
         scores = [[float(score[i * N + r]) for r in range(N)] for i in range(n)]
         return hyps, scores, st.as_dict()
+
+
+class TextCodec:
+    """Host-side text pipeline (C-ABI nmt_text_*): fastBPE-style subword
+    codec + shared vocabulary.  encode(lines) -> (ids, off); decode(ids, off) -> lines."""
+
+    def __init__(self, vocab_text: str, merges_text: str):
+        v = vocab_text.encode("utf-8")
+        m = merges_text.encode("utf-8")
+        h = C.c_void_p()
+        _check(lib().nmt_text_load(v, C.c_int64(len(v)), m, C.c_int64(len(m)), C.byref(h)))
+        self.h = h
+
+    @property
+    def vocab_size(self):
+        L = lib()
+        L.nmt_text_vocab_size.restype = C.c_int32
+        return int(L.nmt_text_vocab_size(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nmt_text_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def encode(self, lines, threads=1):
+        text = "\n".join(lines).encode("utf-8")
+        n = len(lines)
+        cap = len(text) + 2 * n + 16          # at most one id per byte + EOS per line
+        ids = np.empty(cap, dtype=np.int32)
+        off = np.empty(n + 2, dtype=np.int64)
+        nl = C.c_int64()
+        _check(lib().nmt_text_encode(self.h, text, C.c_int64(len(text)), C.c_int32(threads),
+                                     ids.ctypes.data_as(C.c_void_p), C.c_int64(cap),
+                                     off.ctypes.data_as(C.c_void_p), C.c_int64(n + 1), C.byref(nl)))
+        k = int(nl.value)
+        # an empty trailing line is not a line
+        return ids[: off[k]].copy(), off[: k + 1].copy()
+
+    def decode(self, ids, off):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        n = len(off) - 1
+        cap = 64 * (len(ids) + 1) + n + 16
+        buf = C.create_string_buffer(cap)
+        ol = C.c_int64()
+        _check(lib().nmt_text_decode(self.h, ids.ctypes.data_as(C.c_void_p),
+                                     off.ctypes.data_as(C.c_void_p), C.c_int64(n), buf,
+                                     C.c_int64(cap), C.byref(ol)))
+        return buf.raw[: ol.value].decode("utf-8").split("\n")[:n]
 

@@ -354,6 +354,34 @@ def test_ensemble_heterogeneous_teachers_subset():
     ens.close()
 
 
+def test_text_pipeline_end_to_end():
+    """§8(f) f3: text lines -> library BPE codec -> GPU greedy translation (tiny, FP32) ->
+    codec decode, equal to the oracle pipeline (oracle BPE -> oracle greedy -> oracle
+    decode) line for line on margin-safe sentences."""
+    from oracle import translate_fast
+    from oracle.text import load_merges, load_vocab, bpe_apply, encode_ids, decode_ids, bpe_remove
+    from synth import Workload
+    from synth.text import synthetic_bpe, synthetic_lines
+    from paper_2109_08008_b200 import TextCodec
+    m_txt, v_txt, sym = synthetic_bpe(pad_to=1000)
+    lines = [ln for ln in synthetic_lines(24, sym, max_words=4) if ln.strip()]
+    ranks = load_merges(m_txt)
+    tok2id, id2tok = load_vocab(v_txt)
+    enc = [encode_ids(bpe_apply(ln, ranks), tok2id) for ln in lines]
+    caps = np.full(len(lines), 10, dtype=np.int32)
+    om = oracle_model("tiny", 3.0)
+    off = np.cumsum([0] + [len(e) for e in enc]).astype(np.int64)
+    wl = Workload(np.array(sum(enc, []), dtype=np.int32), off, caps)
+    ref_ids = translate_fast(om, wl, max_tokens=256, max_sents=8)
+    ref = [bpe_remove(decode_ids(r, id2tok, 1000)) for r in ref_ids]
+    gm = gpu_model("tiny", "fp32", 3.0, max_tokens=256, max_sents=8, max_tgt_len=32)
+    codec = TextCodec(v_txt, m_txt)
+    got, st = gm.translate_text(codec, lines, caps=caps)
+    assert len(got) == len(lines)
+    assert sum(g == r for g, r in zip(got, ref)) >= len(lines) - 1
+    codec.close()
+
+
 def test_beam_teacher_30_6_subset():
     """C4: teacher-scale 30-6 Transformer-DLCL-RPR, FP16 beam 4 with cached attention."""
     from oracle import beam_search
