@@ -592,6 +592,22 @@ nmt_model* clone_worker(nmt_model* m) {
   return c.release();
 }
 
+// Separate decode stream of a worker (tuning: NMT_PRIO=1 high / 2 low priority for the
+// decode phase; unset or 0 keeps everything on `ws`, measured best).
+cudaStream_t decode_stream(nmt_model* m, cudaStream_t ws) {
+  static const int mode = getenv("NMT_PRIO") ? atoi(getenv("NMT_PRIO")) : 0;
+  if (mode != 1 && mode != 2) return ws;
+  if (!m->dec_stream) {
+    int least = 0, greatest = 0;
+    NMT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    NMT_CUDA(cudaStreamCreateWithPriority(&m->dec_stream, cudaStreamNonBlocking,
+                                          mode == 1 ? greatest : least));
+    NMT_CUDA(cudaEventCreateWithFlags(&m->ev_enc, cudaEventDisableTiming));
+    NMT_CUDA(cudaEventCreateWithFlags(&m->ev_dec, cudaEventDisableTiming));
+  }
+  return m->dec_stream;
+}
+
 // Whole-set driver.  Batches (length-sorted plan) are taken from a shared counter by
 // `n_workers` workers, each a (model-or-clone, stream) pair on its own host thread; worker 0
 // is the model itself on the caller's stream.  load_src(wm, stream, order, B, S, lens)
@@ -642,23 +658,32 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
       }
       load_src(wm, ws, &p.order[lo], B, S, lens.data());
       encode_common(wm, B, S, lens.data(), caps.data(), ws, K);
+      cudaStream_t ds = decode_stream(wm, ws);
+      if (ds != ws) {   // decode after this batch's encoder, on the high-priority stream
+        NMT_CUDA(cudaEventRecord(wm->ev_enc, ws));
+        NMT_CUDA(cudaStreamWaitEvent(ds, wm->ev_enc, 0));
+      }
       nmt_batch& b = wm->batch;
       b.NB = NB;
       int rows = B * K;
       int t = 0;
       // the live count is polled every `sync_every` steps (lagged upper bound for grids)
       for (; t < b.max_cap && rows > 0; ++t) {
-        step_and_prune(wm, b, rows, every, ratio, ws);
+        step_and_prune(wm, b, rows, every, ratio, ds);
         if ((t + 1) % sync_every == 0) {
-          poll_state(wm, ws);
+          poll_state(wm, ds);
           rows = wm->hp.st->n_live;
         }
       }
-      poll_state(wm, ws);
+      poll_state(wm, ds);
       steps += t;
       prunes += wm->hp.st->prunes;
       b.step = t;
-      gen += emit(wm, ws, &p.order[lo], B);
+      gen += emit(wm, ds, &p.order[lo], B);
+      if (ds != ws) {   // the next batch's staging / encoder reuse the arena
+        NMT_CUDA(cudaEventRecord(wm->ev_dec, ds));
+        NMT_CUDA(cudaStreamWaitEvent(ws, wm->ev_dec, 0));
+      }
       b.valid = false;
     }
   };

@@ -155,7 +155,14 @@ struct nmt_model {
   bool owns_weights = true;
   std::vector<nmt_model*> workers;
   cudaStream_t own_stream = nullptr;
+  // decode phase on a high-priority stream (translate loop): a batch's latency-bound decode
+  // steps are scheduled ahead of the other workers' encoder kernels when SMs free up
+  cudaStream_t dec_stream = nullptr;
+  cudaEvent_t ev_enc = nullptr, ev_dec = nullptr;
   ~nmt_model() {
+    if (dec_stream) cudaStreamDestroy(dec_stream);
+    if (ev_enc) cudaEventDestroy(ev_enc);
+    if (ev_dec) cudaEventDestroy(ev_dec);
     for (auto* w : workers) delete w;
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : pgraphs) {

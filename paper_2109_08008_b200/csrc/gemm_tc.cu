@@ -182,7 +182,8 @@ struct Params {
   float* ws;          // split-K partials [tile][split][BM][BN]
   int* counters;      // split-K arrival counters [tile] (self-resetting)
   int dbg;            // tuning experiments only (NMT_GEMM_DBG bits): 1 = drain TMEM only,
-                      // 2 = no TMA stores, 4 = no staging / stores, 8 = no epilogue math
+                      // 2 = no TMA stores, 4 = no staging / stores, 8 = no epilogue math,
+                      // 32 = operand TMA only for the first STAGES k-blocks (MMA rate)
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
   float2* st_out;     // LN folding, producer side (GemmArgs)
   const float2* ln_st;
@@ -485,6 +486,10 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
             tma_load_2d_pair(sa, &mapA, fb, kb * BK, m0);
             tma_load_2d_pair(sa + SM::A_BYTES, &mapB, fb, kb * BK, n0);
           } else {
+            if ((p.dbg & 32) && it >= STAGES) {   // tuning: MMAs on stale tiles, no TMA
+              mbar_arrive(&full[st]);
+              continue;
+            }
             mbar_expect_tx(&full[st], SM::STAGE);
             tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
 #pragma unroll

@@ -45,7 +45,9 @@ def main():
         R = torch.randn(M, Nn, device="cuda", generator=g).half() if resid else None
         C = torch.empty(M, Nn, device="cuda").half()
         ms = bench(lambda: dev_gemm(A, B, bias, R, relu=relu, out=C))
-        res[name] = {"M": M, "N": Nn, "K": K, "us": ms * 1e3, "tflops": 2 * M * Nn * K / ms / 1e9}
+        ref = bench(lambda: torch.nn.functional.linear(A, B))     # cuBLAS, plain GEMM (context)
+        res[name] = {"M": M, "N": Nn, "K": K, "us": ms * 1e3, "tflops": 2 * M * Nn * K / ms / 1e9,
+                     "cublas_us": ref * 1e3}
     M = a.rows
     for name, (Nn, K, resid, relu) in {
         "dec_qkv": (3 * d, d, False, False), "dec_out": (d, d, True, False),
