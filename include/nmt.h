@@ -269,6 +269,19 @@ nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t
                                const void* d_A, int32_t lda, const void* d_B, int32_t ldb,
                                int32_t* d_next, float* d_logits, void* stream);
 
+/* Encoder RPR self-attention alone (Shaw et al. with clipped relative keys AND values,
+ * PAPER.md:23, :34; reading R7): for sentence b, head h, query i < len[b]:
+ *   e_ij = q_i . (k_j + A^K[r(i,j)]) / sqrt(dh),  r(i,j) = clip(j - i, -k, k) + k, j < len[b]
+ *   o_i  = sum_j softmax_j(e_i) (v_j + A^V[r(i,j)]);   rows i >= len[b] are written 0.
+ * d_qkv [B*S][3d] (Q | K | V, head h at columns h*dh of each third), d_len int32 [B]
+ * (device), d_relk / d_relv [2k+1][dh] (may be NULL when use_rpr = 0), d_out [B*S][d];
+ * all device memory in the precision `prec`, row-major, owned by the caller.  S <= 128.
+ * FP16: tensor-core kernel (TMA-fed pipeline for dh = 64).  Asynchronous on `stream`. */
+nmt_status nmt_dev_attn_encoder(nmt_precision prec, int32_t B, int32_t S, int32_t d, int32_t H,
+                                int32_t kclip, int32_t use_rpr, const void* d_qkv,
+                                const int32_t* d_len, const void* d_relk, const void* d_relv,
+                                void* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,4 +5,4 @@ This package holds its build script, the NTSD blob writer and a thin ctypes bind
 It never imports ``oracle/`` (test infrastructure) and has no CPU fallback.
 """
 from .nmt import (Model, Batch, Ensemble, TextCodec, NmtError, dev_gemm, dev_gemm_argmax,  # noqa: F401
-                  dev_gemm_decode, lib, LIB_PATH, EXPORTS)
+                  dev_gemm_decode, dev_attn_encoder, lib, LIB_PATH, EXPORTS)

@@ -7,6 +7,11 @@
 // Scores, masking and the softmax stay in FP32 registers; P and the bucket sums B are
 // rounded to FP16 only as MMA operands (FP16-mode tolerance).  One CTA per
 // (sentence, head), 4 warps each owning 16-query blocks; Q/K/V staged with cp.async.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -262,6 +267,375 @@ __global__ void __launch_bounds__(128) k_attn_enc_tc(const __half* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ TMA-fed pipeline (DH = 64)
+// The same arithmetic as k_attn_enc_tc (scores, relative terms, softmax, P V + B A^V, all
+// MMA operands FP16, FP32 accumulation), restructured for HBM throughput:
+//  * persistent CTAs walk the (sentence, head) items c, c + G, ...; one producer warp
+//    streams each item's Q / K / V head tiles (SP rows x 128 B, 128-B swizzle) into a ring
+//    of NSLOT shared-memory slots with three TMA loads (no per-thread copy issue), so the
+//    loads of the next items are in flight while the current ones are computed;
+//  * W consumer warps take (item, 16-query block) units round robin; a slot is released
+//    when all SP/16 units of its item have arrived on its `empty` barrier;
+//  * A^K / A^V (shared by all heads of the layer, reading R7) are staged once per CTA;
+//  * each warp stages its 16 x 64 output block in shared memory and writes full 128-B
+//    row segments.
+// Rows of the TMA box beyond the sentence (SP > S) belong to the next sentence or lie
+// beyond the tensor (zero-filled by TMA); they are masked as keys (j >= n) and never
+// written as queries (rows >= S).
+}  // namespace
+namespace tc {
+CUtensorMap make_map(const void* ptr, int rows, int cols, int ld, int box_rows, bool out);
+}
+namespace {
+
+constexpr int kEncW = 8;             // consumer warps per CTA
+constexpr int kEncMaxSlots = 16;
+constexpr int kEncWarpScratch = 16 * QLD * 4 + 16 * (RP + 8) * 2;   // q.A^K [16][33] f32 + B [16][40] f16
+constexpr int kEncTab = 2 * RP * (64 + 8) * 2;                        // A^K, A^V [32][72] f16
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  for (uint32_t i = 0;; ++i) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (ok) return;
+    if ((i & 1023) == 1023 && clock64() - t0 > 20000000000ll) __trap();   // pipeline bug
+  }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+// byte offset of the 16-B chunk `ch` (0..7) of row r in a 128-B-swizzled tile
+__device__ __forceinline__ uint32_t sw128(int r, int ch) { return r * 128 + ((ch ^ (r & 7)) << 4); }
+
+template <int NT>
+__global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_tma(
+    const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
+    const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
+    int B, int S, int d, int H, int kclip, int use_rpr, int nslot) {
+  constexpr int DH = 64, SP = NT * 8, NQ = SP / 16, LDH = DH + 8, LDB = RP + 8;
+  constexpr int TILE = SP * 128, SLOT = 3 * TILE;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* slots = sm;
+  __half* sAK = reinterpret_cast<__half*>(sm + nslot * SLOT);
+  __half* sAV = sAK + RP * LDH;
+  uint8_t* wscr = reinterpret_cast<uint8_t*>(sAV + RP * LDH);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wscr + kEncW * kEncWarpScratch);
+  uint64_t* empty = full + kEncMaxSlots;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int items = B * H, G = gridDim.x, c = blockIdx.x;
+  const int nloc = c < items ? (items - 1 - c) / G + 1 : 0;   // items of this CTA
+  const int R = 2 * kclip + 1;
+  if (tid == 0) {
+    for (int i = 0; i < nslot; ++i) {
+      mbar_init1(&full[i], 1);
+      mbar_init1(&empty[i], NQ);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mqkv)) : "memory");
+  }
+  // A^K / A^V once per CTA (rows >= R zero: finite operands for the padded MMA columns)
+  for (int idx = tid; idx < RP * (DH / 8); idx += blockDim.x) {
+    const int r = idx / (DH / 8), cc = (idx % (DH / 8)) * 8;
+    const bool ok = use_rpr && r < R;
+    cp_async16(sAK + r * LDH + cc, relk + (ok ? r * DH + cc : 0), ok ? 16 : 0);
+    cp_async16(sAV + r * LDH + cc, relv + (ok ? r * DH + cc : 0), ok ? 16 : 0);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+
+  if (warp == kEncW) {  // ---------------- producer
+    if (lane == 0) {
+      for (int k = 0; k < nloc; ++k) {
+        const int sl = k % nslot;
+        if (k >= nslot) mbar_wait1(&empty[sl], ((k / nslot) - 1) & 1);
+        const int it = c + k * G, b = it / H, h = it - b * H;
+        uint8_t* dst = slots + sl * SLOT;
+        mbar_expect(&full[sl], SLOT);
+        tma_2d(dst, &mqkv, &full[sl], h * DH, b * S);
+        tma_2d(dst + TILE, &mqkv, &full[sl], d + h * DH, b * S);
+        tma_2d(dst + 2 * TILE, &mqkv, &full[sl], 2 * d + h * DH, b * S);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  float* sQA = reinterpret_cast<float*>(wscr + warp * kEncWarpScratch);      // [16][QLD]
+  __half* sB = reinterpret_cast<__half*>(wscr + warp * kEncWarpScratch + 16 * QLD * 4);  // [16][LDB]
+  const float scale = rsqrtf((float)DH);
+  const int g = lane >> 2, tig = lane & 3, mi = lane >> 3, rr = lane & 7;
+  for (int u = warp; u < nloc * NQ; u += kEncW) {
+    const int k = u / NQ, qb = u - k * NQ, sl = k % nslot;
+    const int it = c + k * G, b = it / H, h = it - b * H;
+    const int n = len[b], m0 = qb * 16;
+    const uint32_t tQ = smem_addr(slots + sl * SLOT), tK = tQ + TILE, tV = tK + TILE;
+    mbar_wait1(&full[sl], (k / nslot) & 1);
+    float oc[DH / 8][4];
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
+    const int r0 = m0 + g, r1 = r0 + 8;
+    if (m0 < n) {
+      // zero this unit's bucket sums (band buckets without a key stay 0)
+      for (int idx = lane; idx < 16 * LDB / 8; idx += 32)
+        reinterpret_cast<uint4*>(sB)[idx] = make_uint4(0u, 0u, 0u, 0u);
+      // ---- S = Q K^T and QA = Q A^K^T
+      float sc[NT][4], qa[RP / 8][4];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+#pragma unroll
+      for (int t = 0; t < RP / 8; ++t) qa[t][0] = qa[t][1] = qa[t][2] = qa[t][3] = 0.f;
+#pragma unroll
+      for (int k0 = 0; k0 < DH; k0 += 16) {
+        uint32_t af[4];
+        {
+          const int row = m0 + rr + (mi & 1) * 8;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                       : "r"(tQ + sw128(row, k0 / 8 + (mi >> 1))));
+        }
+#pragma unroll
+        for (int t = 0; t < NT; t += 2) {
+          uint32_t bf[4];
+          const int row = (t + (mi >> 1)) * 8 + rr;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
+                       : "r"(tK + sw128(row, k0 / 8 + (mi & 1))));
+          mma16816(sc[t], af, bf[0], bf[1]);
+          mma16816(sc[t + 1], af, bf[2], bf[3]);
+        }
+#pragma unroll
+        for (int t = 0; t < RP / 8; t += 2) {
+          uint32_t bf[4];
+          ldsm_x4(bf, sAK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
+          mma16816(qa[t], af, bf[0], bf[1]);
+          mma16816(qa[t + 1], af, bf[2], bf[3]);
+        }
+      }
+      // ---- relative-key term, mask, scale, FP32 softmax (rows r0, r1; quad reductions).
+      // Branch-free: with use_rpr = 0 the staged tables are zero, so the relative terms
+      // add exact zeros.  Scores are kept in log2 units (scale * log2 e folded in).
+#pragma unroll
+      for (int t = 0; t < RP / 8; ++t) {
+        const int cc = t * 8 + 2 * tig;
+        sQA[g * QLD + cc] = qa[t][0];
+        sQA[g * QLD + cc + 1] = qa[t][1];
+        sQA[(g + 8) * QLD + cc] = qa[t][2];
+        sQA[(g + 8) * QLD + cc + 1] = qa[t][3];
+      }
+      __syncwarp();
+      const float sl2 = scale * 1.4426950408889634f;
+      const bool ok0 = r0 < n, ok1 = r1 < n;
+      const float* qa0 = sQA + g * QLD + kclip;        // indexed by clip(j - i, -k, k)
+      const float* qa1 = sQA + (g + 8) * QLD + kclip;
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool top = e < 2;
+          const int j = t * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
+          const float v = sc[t][e] + (top ? qa0 : qa1)[min(max(dj, -kclip), kclip)];
+          sc[t][e] = (j < n && (top ? ok0 : ok1)) ? v * sl2 : -INFINITY;
+          if (top) mx0 = fmaxf(mx0, sc[t][e]);
+          else mx1 = fmaxf(mx1, sc[t][e]);
+        }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
+      if (mx1 == -INFINITY) mx1 = 0.f;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = exp2f(sc[t][e] - (e < 2 ? mx0 : mx1));
+          sc[t][e] = v;
+          if (e < 2) s0 += v;
+          else s1 += v;
+        }
+      s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+      s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+      const float inv0 = s0 > 0.f ? 1.f / s0 : 0.f, inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
+      // P, and the bucket sums B[i][r] = sum_{j: r(i,j) = r} P[i][j]: the band buckets have
+      // one key each (unique writer; masked keys carry P = 0), the two clipped ends are sums
+      float lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
+      __half* sb0 = sB + g * LDB + kclip;
+      __half* sb1 = sB + (g + 8) * LDB + kclip;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool top = e < 2;
+          const int j = t * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
+          const float p = sc[t][e] * (top ? inv0 : inv1);
+          sc[t][e] = p;
+          const float pl = dj <= -kclip ? p : 0.f, ph = dj >= kclip ? p : 0.f;
+          if (top) { lo0 += pl; hi0 += ph; } else { lo1 += pl; hi1 += ph; }
+          if (dj > -kclip && dj < kclip) (top ? sb0 : sb1)[dj] = __float2half(p);
+        }
+      lo0 += __shfl_xor_sync(0xffffffffu, lo0, 1); lo0 += __shfl_xor_sync(0xffffffffu, lo0, 2);
+      hi0 += __shfl_xor_sync(0xffffffffu, hi0, 1); hi0 += __shfl_xor_sync(0xffffffffu, hi0, 2);
+      lo1 += __shfl_xor_sync(0xffffffffu, lo1, 1); lo1 += __shfl_xor_sync(0xffffffffu, lo1, 2);
+      hi1 += __shfl_xor_sync(0xffffffffu, hi1, 1); hi1 += __shfl_xor_sync(0xffffffffu, hi1, 2);
+      if (tig == 0) {
+        sb0[-kclip] = __float2half(lo0); sb0[kclip] = __float2half(hi0);
+        sb1[-kclip] = __float2half(lo1); sb1[kclip] = __float2half(hi1);
+      }
+      __syncwarp();
+      // ---- O = P V (+ B A^V)
+#pragma unroll
+      for (int kk = 0; kk < NT / 2; ++kk) {
+        uint32_t af[4];
+        af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
+        af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
+        af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+        af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 16) {
+          uint32_t bf[4];
+          const int row = kk * 16 + (mi & 1) * 8 + rr;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
+                       : "r"(tV + sw128(row, c0 / 8 + (mi >> 1))));
+          mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+          mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+        }
+      }
+      {
+#pragma unroll
+        for (int kk = 0; kk < RP / 16; ++kk) {
+          uint32_t af[4];
+          ldsm_x4(af, sB + (rr + (mi & 1) * 8) * LDB + kk * 16 + (mi >> 1) * 8);
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            uint32_t bf[4];
+            ldsm_x4_t(bf, sAV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+            mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+            mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+          }
+        }
+      }
+    }
+    // this unit no longer reads the slot: release it (the producer may refill it)
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&empty[sl]);
+    // ---- stage the 16 x 64 FP16 block (rows >= n are zero) in the q.A^K scratch
+    // (2 KB, 128-B rows, 16-B chunks XOR-swizzled by row), then full-row stores
+    uint8_t* st = reinterpret_cast<uint8_t*>(sQA);
+#pragma unroll
+    for (int t = 0; t < DH / 8; ++t) {
+      const uint32_t w0 = r0 < n ? pack_h2(oc[t][0], oc[t][1]) : 0u;
+      const uint32_t w1 = r1 < n ? pack_h2(oc[t][2], oc[t][3]) : 0u;
+      *reinterpret_cast<uint32_t*>(st + sw128(g, t) + 4 * tig) = w0;
+      *reinterpret_cast<uint32_t*>(st + sw128(g + 8, t) + 4 * tig) = w1;
+    }
+    __syncwarp();
+    __half* obase = out + ((size_t)b * S) * d + h * DH;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = i * 32 + lane, row = idx >> 3, ch = idx & 7;
+      if (m0 + row < S)
+        *reinterpret_cast<uint4*>(obase + (size_t)(m0 + row) * d + ch * 8) =
+            *reinterpret_cast<const uint4*>(st + sw128(row, ch));
+    }
+    __syncwarp();
+  }
+}
+
+struct EncTmaCfg {
+  int nslot, smem, grid_per_sm;
+};
+
+template <int NT>
+EncTmaCfg enc_tma_cfg() {
+  static EncTmaCfg cfg = [] {
+    constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
+    const int fixed = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 1024;
+    // enough slots for the items the W warps work on at once plus two being prefetched,
+    // within ~112 KB (two CTAs per SM) when possible
+    int want = std::min(kEncMaxSlots, (kEncW + NQ - 1) / NQ + 2);
+    int ns = std::min(want, (112 * 1024 - fixed) / SLOT);
+    if (ns < 2) ns = std::min(want, (220 * 1024 - fixed) / SLOT);
+    EncTmaCfg c{};
+    c.nslot = std::max(1, ns);
+    c.smem = fixed + c.nslot * SLOT;
+    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  c.smem));
+    int occ = 0;
+    NMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_attn_enc_tma<NT>,
+                                                           32 * (kEncW + 1), c.smem));
+    c.grid_per_sm = std::max(1, occ);
+    return c;
+  }();
+  return cfg;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    NMT_CUDA(cudaGetDevice(&dev));
+    NMT_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+template <int NT>
+void launch_tma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  const EncTmaCfg c = enc_tma_cfg<NT>();
+  const CUtensorMap map = tc::make_map(qkv, B * S, 3 * d, 3 * d, NT * 8, false);
+  const int grid = std::min(B * H, c.grid_per_sm * sm_count());
+  launch_k(k_attn_enc_tma<NT>, dim3(grid), dim3(32 * (kEncW + 1)), (size_t)c.smem, s, map, len, relk,
+           relv, out, B, S, d, H, kclip, use_rpr, c.nslot);
+}
+
+void launch_tma_sp(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                   __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  switch ((S + 15) / 16 * 16) {
+    case 16: launch_tma<2>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 32: launch_tma<4>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 48: launch_tma<6>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 64: launch_tma<8>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 80: launch_tma<10>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 96: launch_tma<12>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 112: launch_tma<14>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    case 128: launch_tma<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
+    default: throw CudaError("attn_encoder: S > 128");
+  }
+}
+
 template <int DH, int NT>
 void launch_nt(const __half* qkv, const int* len, const __half* relk, const __half* relv,
                __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
@@ -301,6 +675,12 @@ void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, cons
                      __half* out, int B, int S, int d, int H, int kclip, int use_rpr,
                      cudaStream_t s) {
   if (2 * kclip + 1 > RP - 1) throw CudaError("attn_encoder_tc: 2k+1 must be < 32");
+  static const bool legacy = getenv("NMT_ENC_ATTN") && atoi(getenv("NMT_ENC_ATTN")) == 0;  // A/B only
+  if (d / H == 64 && !legacy) {
+    launch_tma_sp(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s);
+    NMT_LAUNCH_CHECK();
+    return;
+  }
   switch (d / H) {
     case 16: launch_dh<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;
     case 32: launch_dh<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s); break;

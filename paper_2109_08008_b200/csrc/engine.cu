@@ -1273,4 +1273,25 @@ nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t
   });
 }
 
+nmt_status nmt_dev_attn_encoder(nmt_precision prec, int32_t B, int32_t S, int32_t d, int32_t H,
+                                int32_t kclip, int32_t use_rpr, const void* d_qkv,
+                                const int32_t* d_len, const void* d_relk, const void* d_relv,
+                                void* d_out, void* stream) {
+  return guard([&] {
+    NMT_REQUIRE(d_qkv && d_len && d_out && B > 0 && S > 0 && H > 0 && d % H == 0, NMT_E_ARG,
+                "bad attention args");
+    NMT_REQUIRE(!use_rpr || (d_relk && d_relv), NMT_E_ARG, "RPR tables missing");
+    NMT_REQUIRE(S <= 128 && 2 * kclip + 1 <= 31, NMT_E_SHAPE, "S > 128 or 2k+1 > 31");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (prec == NMT_FP16)
+      attn_encoder<__half>(static_cast<const __half*>(d_qkv), d_len,
+                           static_cast<const __half*>(d_relk), static_cast<const __half*>(d_relv),
+                           static_cast<__half*>(d_out), B, S, d, H, kclip, use_rpr, s);
+    else
+      attn_encoder<float>(static_cast<const float*>(d_qkv), d_len,
+                          static_cast<const float*>(d_relk), static_cast<const float*>(d_relv),
+                          static_cast<float*>(d_out), B, S, d, H, kclip, use_rpr, s);
+  });
+}
+
 }  // extern "C"

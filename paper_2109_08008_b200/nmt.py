@@ -26,7 +26,7 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode",
            "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
            "nmt_translate_ensemble", "nmt_text_load", "nmt_text_free", "nmt_text_vocab_size",
-           "nmt_text_encode", "nmt_text_decode"]
+           "nmt_text_encode", "nmt_text_decode", "nmt_dev_attn_encoder"]
 
 
 class ProfEntry(C.Structure):
@@ -307,6 +307,18 @@ def dev_gemm_argmax(A, B, logits=False, stream=None):
     _check(lib().nmt_dev_gemm_argmax(prec, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                                      _ptr(nxt), _ptr(lg), _stream(stream)))
     return (nxt, lg) if logits else nxt
+
+
+def dev_attn_encoder(qkv, lens, relk, relv, B, S, H, kclip, use_rpr=True, stream=None):
+    """Encoder RPR self-attention alone (C-ABI nmt_dev_attn_encoder): qkv [B*S][3d] CUDA
+    tensor (fp16 / fp32), lens int32 CUDA [B], relk / relv [2k+1][dh]; returns out [B*S][d]."""
+    import torch
+    d = qkv.shape[1] // 3
+    prec = NMT_FP16 if qkv.dtype == torch.float16 else NMT_FP32
+    out = torch.empty(B * S, d, dtype=qkv.dtype, device=qkv.device)
+    _check(lib().nmt_dev_attn_encoder(prec, B, S, d, H, kclip, int(use_rpr), _ptr(qkv), _ptr(lens),
+                                      _ptr(relk), _ptr(relv), _ptr(out), _stream(stream)))
+    return out
 
 
 class Ensemble:

@@ -93,6 +93,39 @@ def test_argmax_ties_lowest_id():
 
 
 # ------------------------------------------------------------------ model parity
+# ------------------------------------------------------------------ encoder attention unit
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("S,lens", [(5, [5, 2]), (16, [16, 9, 1]), (23, [23, 17, 8, 23]),
+                                    (32, [32, 31, 30]), (41, [41, 9]), (77, [77, 60]),
+                                    (120, [120, 64, 7])])
+def test_attn_encoder_unit(prec, S, lens):
+    """Encoder RPR self-attention through nmt_dev_attn_encoder vs the oracle's plain double
+    loop (oracle.nn.rpr_attention_loops, Shaw et al. keys and values):
+    every padded length class of the FP16 TMA pipeline (SP = 16..128), ragged lengths,
+    sentences shorter than the clip distance, query rows >= len written 0."""
+    from oracle.nn import rpr_attention_loops
+    from paper_2109_08008_b200 import dev_attn_encoder
+    rng = np.random.default_rng(1000 + S)
+    B, d, H, kc = len(lens), 512, 8, 8
+    dt = torch.float16 if prec == "fp16" else torch.float32
+    qkv = torch.from_numpy(rng.standard_normal((B * S, 3 * d))).to(dt)
+    relk = torch.from_numpy(0.5 * rng.standard_normal((2 * kc + 1, d // H))).to(dt)
+    relv = torch.from_numpy(0.5 * rng.standard_normal((2 * kc + 1, d // H))).to(dt)
+    ln = torch.tensor(lens, dtype=torch.int32)
+    out = dev_attn_encoder(qkv.cuda(), ln.cuda(), relk.cuda(), relv.cuda(), B, S, H, kc)
+    g = out.float().cpu().numpy()
+    x = qkv.double().numpy()
+    ak, av = relk.double().numpy(), relv.double().numpy()
+    for b, n in enumerate(lens):
+        rows = x[b * S:b * S + n]
+        ref = rpr_attention_loops(rows[:, :d], rows[:, d:2 * d], rows[:, 2 * d:], ak, av, H, kc,
+                                  lambda i, j: (True, i))
+        got = g[b * S:(b + 1) * S]
+        tol = 1e-4 if prec == "fp32" else 1e-2
+        assert np.abs(got[:n] - ref).max() <= tol * max(1.0, np.abs(ref).max()), (b, n)
+        assert not np.any(got[n:]), "padding query rows must be zero"
+
+
 def _teacher_forced(name, prec, srcs, forced, eos_boost=1.0):
     """Run encoder + forced decode on GPU and oracle; compare encoder out and logits."""
     cfg, _ = weights(name, eos_boost)
