@@ -2,9 +2,9 @@
 """Benchmark of the B200 hot path: FP16 greedy translation with the 35-1 Transformer-DLCL-RPR
 student (BASELINE.json configs[2], metric "target tokens/sec ... ms/decode step").
 
-A step = nmt_translate_device over one 12000-sentence chunk (4 x newstest2018) of the
+A step = nmt_translate_device over one 48000-sentence chunk (16 x newstest2018) of the
 synthetic 1M-sentence set (DESIGN.md input recipe): length sort, dynamic 32768-token /
-4096-sentence batches (the paper's rule, at a B200-sized budget), three
+4096-sentence batches (the paper's rule, at a B200-sized budget), four
 concurrent batch workers, 35-layer encoder with RPR + DLCL, cached greedy
 decoding with the fused vocab argmax, batch pruning (rho = 0.25).  Each rank/step gets a
 distinct chunk (weak scaling: sentences are independent; no collective
@@ -31,7 +31,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "target tokens/sec (FP16 greedy, 35-1 student) at 1/2/4/8 B200; ms/decode step"
 UNIT = "target tokens/s"
-CHUNK = 12000           # 4 newstest2018-sized sets (2998 sentences each)
+CHUNK = 48000           # 16 newstest2018-sized sets (2998 sentences each)
+# decode-step buckets of live rows (1-16, 17-64, 65-148, 149-512; plus the
+# larger live batches of the B200-sized budget)
+BUCKETS = [(1, 16), (17, 64), (65, 148), (149, 512), (513, 2048), (2049, 4096)]
+T_WINDOW = (12, 20)     # "at t ~ 16"
+STEP_SENTS = 12000      # sentences of the step-timing run
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # Encoder GEMMs are dense contractions at N = 16K+ rows (tensor-bound).  Other classes take
 # the binding roof of their algorithmic FLOPs and bytes (decoder GEMMs / vocab projection:
@@ -175,7 +180,7 @@ def main():
     ap.add_argument("--max-tokens", type=int, default=32768)
     ap.add_argument("--max-sents", type=int, default=4096)
     ap.add_argument("--sync-every", type=int, default=4)
-    ap.add_argument("--workers", type=int, default=3,
+    ap.add_argument("--workers", type=int, default=4,
                     help="concurrent batch workers per GPU (own arena + stream, shared weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
@@ -193,6 +198,7 @@ def main():
         return
 
     from synth import PRESETS, generate_weights, newstest_like
+    from synth.workload import FULL_SET
     cfg = PRESETS[args.config]
     W = generate_weights(cfg)
 
@@ -222,7 +228,8 @@ def main():
     n_chunks = args.warmup + args.steps
     chunks = []
     for k in range(n_chunks):
-        idx = chunk_index(k, rank, world)   # disjoint chunks per (step, rank): weak scaling
+        # disjoint chunks per (step, rank) (weak scaling), cycling through the 1M-sentence set
+        idx = chunk_index(k, rank, world) % (FULL_SET // args.chunk)
         wl = newstest_like(args.chunk, cfg.vocab_size, start=idx * args.chunk)
         chunks.append((wl, torch.from_numpy(wl.ids).cuda()))
     Tm = model.Tmax
@@ -292,8 +299,24 @@ def main():
     # ---- per-kernel-class profile of one more step (CUDA events on the launching stream)
     model.profile(2)
     st = dev_step(args.warmup, workers=1)  # per-class events need one stream
-    prof = model.profile(0)
+    prof = model.profile(-1)
+    # decode-step device times: plain step graphs bracketed by event nodes (profile mode 3)
+    # over the first STEP_SENTS sentences of the chunk, one worker
+    model.profile(3)
+    wl, _ = chunks[args.warmup]
+    sub = wl.shard(0, min(wl.n, STEP_SENTS))
+    model.translate_device(torch.from_numpy(sub.ids).cuda(), sub.off, d_out, d_len, caps=sub.caps,
+                           max_tokens=args.max_tokens, max_sents=args.max_sents,
+                           sync_every=args.sync_every, workers=1)
+    srec = model.profile_steps()   # (t, live rows, device ms) of every decode step
+    model.profile(0)
     tot = sum(v["ms"] for v in prof.values())
+    step_ms = {}
+    for lo, hi in BUCKETS:
+        v = sorted(ms for t, live, ms in srec if lo <= live <= hi and T_WINDOW[0] <= t <= T_WINDOW[1])
+        if v:
+            step_ms[f"{lo}-{hi}"] = {"median_ms": round(v[len(v) // 2], 4), "steps": len(v)}
+    mean_step = sum(ms for _, _, ms in srec) / len(srec) if srec else None
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     pk, src = peaks()
     # the binding roof of the class: the larger of FLOPs / tensor peak and bytes / HBM peak
@@ -313,7 +336,6 @@ def main():
                  "per_launch": {"flops" if roof["bound"] == "tensor" else "bytes":
                                 (dom["flops"] if roof["bound"] == "tensor" else dom["bytes"]) / dom["launches"],
                                 "ms": dom["ms"] / dom["launches"], "launches": dom["launches"]}})
-    dec_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("dec") or k in ("vocab_argmax", "bookkeeping"))
     kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                    "share": round(v["ms"] / tot, 4) if tot else None} for k, v in prof.items()}
 
@@ -328,8 +350,11 @@ def main():
                        "max_tokens": args.max_tokens, "max_sents": args.max_sents,
                        "parallelism": f"sentence-sharded x{world}",
                        "l2": "working set > L2 (262 MB FP16 weights + DLCL history)"},
-            "ms_per_decode_step": ms_max / max(1.0, steps_all / world),
-            "ms_per_decode_step_kernels": dec_ms / max(1, st["decode_steps"]),
+            # device time of one decode step (its CUDA graph bracketed by event nodes,
+            # finish/prune included), one worker, STEP_SENTS sentences of the chunk: mean over
+            # all steps and median per live-row bucket at t in T_WINDOW
+            "ms_per_decode_step": mean_step,
+            "decode_step_ms_by_live_rows": {"t_window": list(T_WINDOW), "buckets": step_ms},
             "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clocks,

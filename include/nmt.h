@@ -236,7 +236,9 @@ const char* nmt_last_error(void);   /* thread-local; valid until the next nmt_* 
 /* Per-kernel-class profile, measured with CUDA events recorded on the launching stream
  * around every launch while enabled (adds two event records per launch).
  * mode: 1 = enable, 2 = reset counters and enable, 0 = reset and disable,
- *       -1 = read only.  When `out` is non-NULL, up to `cap` entries for the classes
+ *       -1 = read only, 3 = reset the step records and time decode steps only (no
+ *       per-kernel events: each step's plain graph between two event nodes, see
+ *       nmt_profile_steps).  When `out` is non-NULL, up to `cap` entries for the classes
  * that ran are written (read happens before any reset) and *n_out is set.
  * flops / bytes are the ALGORITHMIC work of the launches.
  * Synchronises the device. */
@@ -247,6 +249,20 @@ typedef struct {
 } nmt_prof_entry;
 nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t cap,
                        int32_t* n_out);
+
+/* Decode steps run while profiling (translate paths; greedy and beam): for each step, the
+ * step counter t and live rows entering it (read back before the step) and the device time
+ * of the step as replayed in its CUDA graph, finish/prune tail included — SURVEY §8(d)
+ * "ms/decode step".  Mode 3 brackets the plain step graph with two event nodes (the
+ * production kernel-to-kernel transitions); modes 1 / 2 time the per-kernel-profiled
+ * graph (an event pair around every kernel: longer).
+ * Copies up to `cap` records in step order, sets *n_out to the number recorded since the
+ * last profile reset (nmt_profile mode 0 / 2). */
+typedef struct {
+  int32_t t, n_live;
+  float ms;
+} nmt_step_rec;
+nmt_status nmt_profile_steps(nmt_model* m, nmt_step_rec* out, int32_t cap, int32_t* n_out);
 
 /* ---- kernel-level entry points used by the unit parity tests ------------------- */
 /* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision

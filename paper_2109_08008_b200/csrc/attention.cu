@@ -342,13 +342,14 @@ struct WarpAttn {
   }
   // Keys [j0, j0 + CH) with j < n (requires j0 < n).  addr(j, kp, vp) sets the head-slice
   // pointers of key j; bias(j) is added to the scaled score; vadd(j, v) adds to v_j.
+  // Keys j < nload (>= n, readable memory) are loaded: the loads need not wait for n.
   template <class ADDR, class BIAS, class VADD>
-  __device__ __forceinline__ void chunk(int j0, int n, ADDR addr, BIAS bias, VADD vadd) {
+  __device__ __forceinline__ void chunk(int j0, int n, int nload, ADDR addr, BIAS bias, VADD vadd) {
     Raw8<T> kr[U], vr[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * KP + kq;
-      if (j < n) {
+      if (j < nload) {
         const T *kp, *vp;
         addr(j, kp, vp);
         kr[u].load(kp + sub * 8);
@@ -430,29 +431,38 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
     const int* __restrict__ dR, const int* __restrict__ anc) {
   __shared__ float s_relv[16][DH];  // A^V[0..k] (k <= 15), shared by every head
+  __shared__ float s_relk[16][DH];  // A^K[0..k]
   __shared__ float s_x[4][16];      // per warp: q . A^K[r] / sqrt(dh), r = 0..k
   using WA = WarpAttn<T, DH>;
   pdl_trigger();
   pdl_wait();
-  if (use_rpr)
-    for (int i = threadIdx.x; i < (kclip + 1) * DH; i += blockDim.x)
-      s_relv[i / DH][i % DH] = to_f(relv[i]);
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
-  if (row >= min(rows, *dR)) return;
-  const int t = *d_t;
-  const int slot = row_slot[row];
-  const T* src = qkv + (size_t)row * 3 * d + h * DH;
+  // one memory round trip for everything that does not depend on the cache slot: the
+  // device scalars, this row's slot, q / k_t / v_t (row clamped to the host bound so the
+  // loads stay in bounds) and the relative tables
+  const int nlive = *dR, t = *d_t;
+  const int rowc = min(row, rows - 1);
+  const int slot = row_slot[rowc];
+  const T* src = qkv + (size_t)rowc * 3 * d + h * DH;
   WA w;
   w.init(lane, src, rsqrtf((float)DH));
+  Raw8<T> kt, vt;
+  if (w.kq == 0) {
+    kt.load(src + d + w.sub * 8);
+    vt.load(src + 2 * d + w.sub * 8);
+  }
+  if (use_rpr)
+    for (int i = threadIdx.x; i < (kclip + 1) * DH; i += blockDim.x) {
+      s_relv[i / DH][i % DH] = to_f(relv[i]);
+      s_relk[i / DH][i % DH] = to_f(relk[i]);
+    }
+  __syncthreads();
+  if (row >= min(rows, nlive)) return;
   if (w.kq == 0) {  // KV-cache append at position t
-    Raw8<T> r;
-    r.load(src + d + w.sub * 8);
-    r.store(kc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
-    r.load(src + 2 * d + w.sub * 8);
-    r.store(vc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
+    kt.store(kc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
+    vt.store(vc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
   }
   float* x = s_x[warp];
   if (use_rpr) {
@@ -460,9 +470,8 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
       const int b = b0 + w.kq;
       float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (b <= kclip) {
-        Raw8<T> r;
-        r.load(relk + b * DH + w.sub * 8);
-        r.to_f(f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = s_relk[b][w.sub * 8 + e];
       }
       const float e = w.group_dot(f);
       if (b <= kclip && w.sub == 0) x[b] = e;
@@ -490,11 +499,11 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
 #pragma unroll
       for (int e = 0; e < 8; ++e) f[e] += rv[e];
     };
-    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
+    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, n, addr, bias, vadd);
   } else {
     auto bias = [](int) { return 0.f; };
     auto vadd = [](int, float*) {};
-    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
+    for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, n, addr, bias, vadd);
   }
   float o[8];
   w.finish(o);
@@ -538,12 +547,15 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gw = blockIdx.x * nw + warp;
   const int row = gw / H, h = gw - (gw / H) * H;
-  if (row >= min(rows, *dR)) return;
-  const int S = *dS;
+  if (row >= rows) return;
+  // round trip 1: scalars, slot, q; round trip 2: the source length together with the
+  // first key chunk (loaded up to S, the batch's padded length, and masked by n)
+  const int nlive = *dR, S = *dS;
   const int slot = row_slot[row] / beam;
-  const int n = src_len[slot];
   WA w;
   w.init(lane, qb + (size_t)row * d + h * DH, rsqrtf((float)DH));
+  if (row >= nlive) return;
+  const int n = src_len[slot];
   const T* base = ckv + (size_t)slot * S * ldkv + h * DH;
   auto addr = [&](int j, const T*& kp, const T*& vp) {
     kp = base + (size_t)j * ldkv + koff;
@@ -551,7 +563,8 @@ __global__ void __launch_bounds__(128) k_attn_cross(
   };
   auto bias = [](int) { return 0.f; };
   auto vadd = [](int, float*) {};
-  for (int j0 = 0; j0 < n; j0 += WA::CH) w.chunk(j0, n, addr, bias, vadd);
+  w.chunk(0, n, S, addr, bias, vadd);
+  for (int j0 = WA::CH; j0 < n; j0 += WA::CH) w.chunk(j0, n, n, addr, bias, vadd);
   float o[8];
   w.finish(o);
   if (w.kq == 0) store8(out + (size_t)row * d + h * DH + w.sub * 8, o);

@@ -500,14 +500,17 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
     m->eager_keys.insert(key);
     return;
   }
-  auto capture = [&](std::vector<nmt_model::ProfRec>* recs) {
+  int nodes = 0;   // kernel nodes of the captured graph
+  auto capture = [&](std::vector<nmt_model::ProfRec>* recs, nmt_model::ProfRec* bracket = nullptr) {
     b.rows_upper = bucket;
     cudaGraph_t g;
     NMT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     g_pdl = pdl_enabled();  // programmatic edges between the step's kernels
     g_prof_capture = recs;
     try {
+      if (bracket) NMT_CUDA(cudaEventRecordWithFlags(bracket->a, s, cudaEventRecordExternal));
       eager();
+      if (bracket) NMT_CUDA(cudaEventRecordWithFlags(bracket->b, s, cudaEventRecordExternal));
     } catch (...) {
       g_pdl = false;
       g_prof_capture = nullptr;
@@ -517,11 +520,43 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
     g_pdl = false;
     g_prof_capture = nullptr;
     NMT_CUDA(cudaStreamEndCapture(s, &g));
+    size_t nn = 0;
+    NMT_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> ns(nn);
+    if (nn) NMT_CUDA(cudaGraphGetNodes(g, ns.data(), &nn));
+    nodes = 0;
+    for (auto n : ns) {
+      cudaGraphNodeType ty;
+      NMT_CUDA(cudaGraphNodeGetType(n, &ty));
+      nodes += ty == cudaGraphNodeTypeKernel;
+    }
     cudaGraphExec_t ex;
     NMT_CUDA(cudaGraphInstantiate(&ex, g, 0));
     NMT_CUDA(cudaGraphDestroy(g));
     return ex;
   };
+  if (m->prof.on && m->prof.steps_only) {
+    // step-timed replay: the plain step graph between two event nodes (kernel-to-kernel
+    // transitions as in production), synchronised so t and the live rows are exact
+    auto it = m->sgraphs.find(key);
+    if (it == m->sgraphs.end()) {
+      nmt_model::ProfRec br{};
+      NMT_CUDA(cudaEventCreate(&br.a));
+      NMT_CUDA(cudaEventCreate(&br.b));
+      cudaGraphExec_t ex = capture(nullptr, &br);
+      br.cls = nodes;
+      it = m->sgraphs.emplace(key, std::make_pair(ex, br)).first;
+    }
+    poll_state(m, s);
+    const int live = m->hp.st->n_live, tt = m->hp.st->t;
+    NMT_CUDA(cudaGraphLaunch(it->second.first, s));
+    NMT_CUDA(cudaStreamSynchronize(s));
+    float sm = 0.f;
+    NMT_CUDA(cudaEventElapsedTime(&sm, it->second.second.a, it->second.second.b));
+    if (m->prof.steps.size() < (1u << 22)) m->prof.steps.push_back({tt, live, sm});
+    g_launches += it->second.second.cls;
+    return;
+  }
   if (m->prof.on) {
     // profiled replay: the same graph with an external event pair around every kernel,
     // read back after each step (timings of the kernels as they run in the graph)
@@ -531,9 +566,16 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
       cudaGraphExec_t ex = capture(&recs);
       it = m->pgraphs.emplace(key, std::make_pair(ex, std::move(recs))).first;
     }
+    poll_state(m, s);   // live rows and t entering this step (profiled steps synchronise)
+    const int live = m->hp.st->n_live, tt = m->hp.st->t;
     NMT_CUDA(cudaGraphLaunch(it->second.first, s));
     NMT_CUDA(cudaStreamSynchronize(s));
     auto& P = m->prof;
+    if (!it->second.second.empty() && P.steps.size() < (1u << 22)) {
+      float sm = 0.f;
+      NMT_CUDA(cudaEventElapsedTime(&sm, it->second.second.front().a, it->second.second.back().b));
+      P.steps.push_back({tt, live, sm});
+    }
     for (auto& r : it->second.second) {
       float ms = 0.f;
       NMT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
@@ -542,13 +584,16 @@ void step_and_prune(nmt_model* m, nmt_batch& b, int rows, int every, float ratio
       P.bytes[r.cls] += r.bytes;
       P.n[r.cls] += 1;
     }
-    g_launches += 1;
+    g_launches += it->second.second.size();
     return;
   }
   auto it = m->graphs.find(key);
-  if (it == m->graphs.end()) it = m->graphs.emplace(key, capture(nullptr)).first;
-  NMT_CUDA(cudaGraphLaunch(it->second, s));
-  g_launches += 1;
+  if (it == m->graphs.end()) {
+    cudaGraphExec_t ex = capture(nullptr);
+    it = m->graphs.emplace(key, std::make_pair(ex, nodes)).first;
+  }
+  NMT_CUDA(cudaGraphLaunch(it->second.first, s));
+  g_launches += it->second.second;   // the replay launches the graph's kernels
 }
 
 // ------------------------------------------------------------------ translate core
@@ -1201,12 +1246,27 @@ nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t 
     }
     if (mode == 2 || mode == 0) {  // reset counters
       auto& P = m->prof;
+      P.steps.clear();
       std::fill(P.ms, P.ms + 16, 0.0);
       std::fill(P.flops, P.flops + 16, 0.0);
       std::fill(P.bytes, P.bytes + 16, 0.0);
       std::fill(P.n, P.n + 16, 0ll);
     }
-    if (mode >= 0 && mode <= 2) m->prof.on = (mode != 0);
+    if (mode == 3) m->prof.steps.clear();
+    if (mode >= 0 && mode <= 3) {
+      m->prof.on = (mode != 0);
+      m->prof.steps_only = (mode == 3);
+    }
+  });
+}
+
+nmt_status nmt_profile_steps(nmt_model* m, nmt_step_rec* out, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    NMT_REQUIRE(m && n_out && (out || cap == 0), NMT_E_ARG, "null argument");
+    const auto& v = m->prof.steps;
+    const int n = (int)std::min<size_t>(v.size(), (size_t)std::max(0, cap));
+    for (int i = 0; i < n; ++i) out[i] = nmt_step_rec{v[i].t, v[i].live, v[i].ms};
+    *n_out = (int)v.size();
   });
 }
 

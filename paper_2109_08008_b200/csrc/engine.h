@@ -137,18 +137,25 @@ struct nmt_model {
   struct ProfRec { int cls; cudaEvent_t a, b; double flops, bytes; };
   struct Prof {
     bool on = false;
+    bool steps_only = false;   // mode 3: per-step device time only (no per-kernel events)
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     std::vector<ProfRec> pending;
     double ms[16] = {}, flops[16] = {}, bytes[16] = {};
     long long n[16] = {};
+    // per decode step while profiling: (t, live rows, device ms of the step's kernels)
+    struct Step { int t, live; float ms; };
+    std::vector<Step> steps;
   } prof;
-  // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits)
-  std::map<std::tuple<int, int, unsigned, int>, cudaGraphExec_t> graphs;
+  // decode-step CUDA graphs keyed by (rows bucket, prune_every, prune_ratio bits), with the
+  // number of kernel nodes each replay launches (nmt_stats.launches)
+  std::map<std::tuple<int, int, unsigned, int>, std::pair<cudaGraphExec_t, int>> graphs;
   std::set<std::tuple<int, int, unsigned, int>> eager_keys;  // configurations run eagerly once
   // profiled variants of the step graphs: the graph plus its per-launch event pairs
   std::map<std::tuple<int, int, unsigned, int>,
            std::pair<cudaGraphExec_t, std::vector<ProfRec>>> pgraphs;
+  // step-timed variants (profile mode 3): the plain step graph between two event nodes
+  std::map<std::tuple<int, int, unsigned, int>, std::pair<cudaGraphExec_t, ProfRec>> sgraphs;
   // Concurrent batch workers (the GPU analog of the paper's parallel decoding processes,
   // PAPER.md:129-131): clones sharing this model's weights, each with its own arena,
   // stream, batch state and graphs.  Created lazily by nmt_translate*(n_workers > 1).
@@ -164,13 +171,18 @@ struct nmt_model {
     if (ev_enc) cudaEventDestroy(ev_enc);
     if (ev_dec) cudaEventDestroy(ev_dec);
     for (auto* w : workers) delete w;
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
     for (auto& kv : pgraphs) {
       cudaGraphExecDestroy(kv.second.first);
       for (auto& r : kv.second.second) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
       }
+    }
+    for (auto& kv : sgraphs) {
+      cudaGraphExecDestroy(kv.second.first);
+      cudaEventDestroy(kv.second.second.a);
+      cudaEventDestroy(kv.second.second.b);
     }
     for (auto e : prof.pool) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -225,7 +237,7 @@ extern thread_local std::vector<nmt_model::ProfRec>* g_prof_capture;
 template <class F>
 void prof_run(nmt_model* m, int cls, double flops, double bytes, cudaStream_t s, F&& f) {
   auto& P = m->prof;
-  if (!P.on) {
+  if (!P.on || P.steps_only) {
     f();
     return;
   }

@@ -185,6 +185,8 @@ struct Params {
                       // 2 = no TMA stores, 4 = no staging / stores, 8 = no epilogue math,
                       // 32 = operand TMA only for the first STAGES k-blocks (MMA rate)
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
+  int nfast;          // unit order: 1 = column tiles of one row block on consecutive CTAs
+                      // (the A row block is read from DRAM once and shared through L2)
   float2* st_out;     // LN folding, producer side (GemmArgs)
   const float2* ln_st;
   const float* ln_c;
@@ -426,16 +428,10 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  pdl_trigger();
-  pdl_wait();  // PDL: operands / live-row count come from the preceding kernel
-  const int M = p.dM ? min(p.M, *p.dM) : p.M;
-  const int num_m = (M + UM - 1) / UM, num_n = (p.N + BN - 1) / BN;
-  const int units = num_m * num_n;
   const int kb_total = (p.K + BK - 1) / BK;
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const int cid = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x;   // unit-stream index
   const int ncl = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
-  if (cid >= units) return;  // uniform over the pair: nothing for it
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -469,12 +465,22 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // dependents may launch once every CTA holds its TMEM (a dependent GEMM CTA allocating
+  // on the same SM then waits for this one's dealloc, never the reverse)
+  pdl_trigger();
+  // PDL: the setup above (barriers, tensor-map prefetch, TMEM allocation) overlaps the
+  // preceding kernel; its outputs (operands, the live-row count) are read only from here
+  pdl_wait();
+  const int M = p.dM ? min(p.M, *p.dM) : p.M;
+  const int num_m = (M + UM - 1) / UM, num_n = (p.N + BN - 1) / BN;
+  const int units = num_m * num_n;   // CTAs with cid >= units skip to the teardown
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
       int it = 0;
       for (int u = cid; u < units; u += ncl) {
-        const int m0 = (u % num_m) * UM + rank * BM, n0 = (u / num_m) * BN + rank * (SM::BROWS);
+        const int mi = p.nfast ? u / num_n : u % num_m, ni = p.nfast ? u % num_n : u / num_m;
+        const int m0 = mi * UM + rank * BM, n0 = ni * BN + rank * (SM::BROWS);
         for (int kb = 0; kb < kb_total; ++kb, ++it) {
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -550,7 +556,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     const uint32_t te0 = PAIR ? mapa_u32(&tempty[0], 0) : 0u, te1 = PAIR ? mapa_u32(&tempty[1], 0) : 0u;
     int local = 0;
     for (int u = cid; u < units; u += ncl, ++local) {
-      const int m0 = (u % num_m) * UM + rank * BM, n0 = (u / num_m) * BN;
+      const int mi = p.nfast ? u / num_n : u % num_m, ni = p.nfast ? u % num_n : u / num_m;
+      const int m0 = mi * UM + rank * BM, n0 = ni * BN;
       const int acc = NACC == 2 ? (local & 1) : 0;
       const uint32_t aph = NACC == 2 ? (local >> 1) & 1 : local & 1;
       const int r = q * 32 + lane;
@@ -645,7 +652,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       }
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
     }
-    if (p.tstore && lane == 0) bulk_wait0();
+    // the staging tiles must outlive the bulk stores' shared-memory reads; the global
+    // writes complete with the grid (kernel boundary / PDL wait of the dependent)
+    if (p.tstore && lane == 0) bulk_wait_read0();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if constexpr (PAIR) cluster_sync_all();  // the peer's MMAs / remote arrives are done
@@ -972,6 +981,8 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.ln_c = a.ln_c;
   p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
+  static const bool morder = getenv("NMT_GEMM_ORDER") && getenv("NMT_GEMM_ORDER")[0] == 'm';  // A/B only
+  p.nfast = !morder;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
   const CUtensorMap mc = out_map(a, p);
@@ -1009,6 +1020,7 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   p.ln_c = a.ln_c;
   p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
+  p.nfast = 1;
   const int units = ceil_div(a.M, 2 * BM) * ceil_div(a.N, BN);
   const int pairs = std::min(units, num_sms() / 2);
   cudaLaunchConfig_t cfg{};

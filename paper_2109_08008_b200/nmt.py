@@ -26,12 +26,17 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_dev_gemm", "nmt_dev_gemm_argmax", "nmt_profile", "nmt_dev_gemm_decode",
            "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
            "nmt_translate_ensemble", "nmt_text_load", "nmt_text_free", "nmt_text_vocab_size",
-           "nmt_text_encode", "nmt_text_decode", "nmt_dev_attn_encoder"]
+           "nmt_text_encode", "nmt_text_decode", "nmt_dev_attn_encoder",
+           "nmt_profile_steps"]
 
 
 class ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
                 ("flops", C.c_double), ("bytes", C.c_double)]
+
+
+class StepRec(C.Structure):
+    _fields_ = [("t", C.c_int32), ("n_live", C.c_int32), ("ms", C.c_float)]
 
 
 class NmtError(RuntimeError):
@@ -133,6 +138,14 @@ class Model:
         return {buf[i].name.decode(): {"launches": buf[i].launches, "ms": buf[i].ms,
                                        "flops": buf[i].flops, "bytes": buf[i].bytes}
                 for i in range(n.value)}
+
+    def profile_steps(self):
+        """Decode steps recorded while profiling: list of (t, live rows, device ms)."""
+        n = C.c_int32()
+        _check(lib().nmt_profile_steps(self.h, None, 0, C.byref(n)))
+        buf = (StepRec * max(1, n.value))()
+        _check(lib().nmt_profile_steps(self.h, buf, n.value, C.byref(n)))
+        return [(buf[i].t, buf[i].n_live, buf[i].ms) for i in range(n.value)]
 
     # ---------------------------------------------------------------- step API
     def encode(self, src, src_len, tgt_cap=None, beam=1, stream=None):

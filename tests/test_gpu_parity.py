@@ -275,7 +275,7 @@ def test_translate_host_equals_device_and_steps():
     with torch.cuda.stream(side):
         out_h2, st2 = gm.translate(wl.ids, wl.off, caps=wl.caps)
     assert out_h2 == out_h
-    assert st2["launches"] < st_h["launches"]   # graphs: one launch per decode step
+    assert st2["launches"] == st_h["launches"]   # graph replays launch the same kernels
 
 
 @pytest.mark.parametrize("prec", PRECS)

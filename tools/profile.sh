@@ -6,7 +6,7 @@
 tag=${1:-r1}
 out=gpurun_out
 mkdir -p $out
-B="python bench.py --steps 1 --warmup 0 --chunk 600 --no-e2e --no-cpu-baseline --workers 1"
+B="python bench.py --steps 1 --warmup 0 --chunk ${CHUNK:-3000} --no-e2e --no-cpu-baseline --workers 1"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file $out/${tag}_launches.csv $B > $out/${tag}_launches.log 2>&1
 echo "launches rc=$?"
@@ -16,7 +16,7 @@ full() {  # name regex, skip, count
   echo "$1 rc=$?"
 }
 full dec_gemm '^k_gemm_tc$' 300 2
-full enc_gemm '^k_gemm_tc$' 4 2
+full enc_gemm '^k_gemm_tc$' 4 4
 full dlcl '^k_dlcl_vec$' 10 1
-full enc_attn '^k_attn_enc_tc$' 4 1
+full enc_attn '^k_attn_enc_tma$' 4 1
 full dec_attn '^k_attn_(dec_self|cross)$' 20 2
