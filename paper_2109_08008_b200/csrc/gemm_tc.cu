@@ -29,7 +29,8 @@ namespace tc {
 constexpr int BM = 128;       // UMMA M (cta_group::1): one TMEM lane per output row
 constexpr int BK = 64;        // 64 halves = 128 B = one swizzle-128B atom row
 constexpr int UMMA_K = 16;    // K per tcgen05.mma for 16-bit inputs
-constexpr int kThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-11: epilogue
+constexpr int kThreads = 384;
+constexpr int kBiasMax = 2048;   // bias vectors up to this length are staged whole per CTA  // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-11: epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -185,6 +186,7 @@ struct Params {
                       // 2 = no TMA stores, 4 = no staging / stores, 8 = no epilogue math,
                       // 32 = operand TMA only for the first STAGES k-blocks (MMA rate)
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
+  int rtma;           // residual 32 x 32 blocks TMA-loaded into the staging tiles (mapR)
   int nfast;          // unit order: 1 = column tiles of one row block on consecutive CTAs
                       // (the A row block is read from DRAM once and shared through L2)
   float2* st_out;     // LN folding, producer side (GemmArgs)
@@ -247,7 +249,7 @@ __device__ __forceinline__ float2 merge_stats(const float2* st, int nch, float e
   return make_float2(mu, rsqrtf(m2 / (32.f * nch) + eps));
 }
 
-template <int BN, int STAGES, bool PAIR = false, int EW = 8>
+template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1>
 struct Smem {
   static constexpr int BROWS = PAIR ? BN / 2 : BN;   // B rows staged by one CTA
   static constexpr int A_BYTES = BM * BK * 2;
@@ -256,7 +258,10 @@ struct Smem {
   // epilogue: per warp a 32 x 32 FP16 staging tile (TMA store) and its FP32 bias slice
   static constexpr int STG = 2048;
   // per epilogue warp: a 32 x 32 staging tile (TMA store) + bias and LN c[n] slices
-  static constexpr int EPI = EW * STG + 2 * 4 * BN * 4;
+  // NSTG staging tiles per warp (2: the residual of chunk i + 1 is TMA-loaded while chunk i
+  // is processed), the whole bias vector (N <= kBiasMax) and per-unit bias / LN c slices
+  static constexpr int BIAS = kBiasMax * 4;
+  static constexpr int EPI = EW * NSTG * STG + BIAS + 2 * 4 * BN * 4;
   static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -403,11 +408,12 @@ __device__ __forceinline__ void fence_async_smem() {
 // both halves on its own `full` barrier (each CTA's TMA completes on it), issues the MMAs
 // and multicasts its commits to both CTAs' `empty` / `tfull` barriers; both CTAs drain
 // their own TMEM rows and release the accumulator on the leader's `tempty`.
-template <int BN, int STAGES, bool PAIR = false, int EW = 8>
+template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-              const __grid_constant__ CUtensorMap mapC, Params p) {
-  using SM = Smem<BN, STAGES, PAIR, EW>;
+              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
+              Params p) {
+  using SM = Smem<BN, STAGES, PAIR, EW, NSTG>;
   constexpr int UM = PAIR ? 2 * BM : BM;             // output rows per unit
   constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
   // BN <= 256: two accumulators (the epilogue of unit i overlaps the MMAs of unit i+1);
@@ -426,7 +432,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;        // [EW][2] residual tile loaded (NSTG = 2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EW);
 
   const int kb_total = (p.K + BK - 1) / BK;
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
@@ -443,6 +450,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], PAIR ? 2 * EW : EW);  // one arrive per epilogue warp (both CTAs)
     }
+    for (int i = 0; i < 2 * EW; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -550,9 +558,30 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     // EW warps = 4 TMEM lane quadrants x EW/4 column parts of HALF columns each
     const int e = warp - 4, q = warp & 3, half = e >> 2;
     constexpr int HALF = BN / (EW / 4), NPF = HALF <= 128 ? HALF / 8 : 1;
-    uint8_t* stg = epi + e * SM::STG;
-    float* sb = reinterpret_cast<float*>(epi + EW * SM::STG) + e * HALF;
-    float* sc = reinterpret_cast<float*>(epi + EW * SM::STG) + EW * HALF + e * HALF;
+    uint8_t* stg0 = epi + e * NSTG * SM::STG;
+    float* sbias = reinterpret_cast<float*>(epi + EW * NSTG * SM::STG);    // [kBiasMax]
+    float* sb = sbias + kBiasMax + e * HALF;
+    float* sc = sbias + kBiasMax + EW * HALF + e * HALF;
+    // the whole bias vector once per CTA (read per unit otherwise: a global round trip)
+    const bool bias_all = p.bias && p.N <= kBiasMax;
+    if (bias_all) {
+      for (int j = threadIdx.x - 128; j < p.N; j += 32 * EW) sbias[j] = __half2float(p.bias[j]);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+    }
+    // residual through TMA (NSTG = 2, FP16 TMA-store outputs): the 32 x 32 residual block of
+    // a chunk lands in the staging tile that then carries the chunk's output (in place)
+    const bool rt = NSTG == 2 && p.rtma;
+    uint32_t kchunk = 0;   // this warp's chunk counter (staging tile kchunk & 1)
+    auto r_issue = [&](uint32_t k, int x, int y) {   // lane 0: TMA of a residual block
+      if (lane == 0) {
+        // tile k & 1 last carried chunk k - 2, whose store is the older of (at most) two
+        // outstanding bulk groups
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        uint64_t* b = &rbar[2 * e + (k & 1)];
+        mbar_expect_tx(b, SM::STG);
+        tma_load_2d(stg0 + (k & 1) * SM::STG, &mapR, b, x, y);
+      }
+    };
     const uint32_t te0 = PAIR ? mapa_u32(&tempty[0], 0) : 0u, te1 = PAIR ? mapa_u32(&tempty[1], 0) : 0u;
     int local = 0;
     for (int u = cid; u < units; u += ncl, ++local) {
@@ -566,7 +595,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       const int cb = half * HALF;
       // residual rows and the bias slice fetched while the MMAs of this unit still run
       uint4 res[NPF];
-      const bool pf = HALF <= 128 && p.R && row_ok && n0 + cb + HALF <= p.N &&
+      if (rt && n0 + cb < p.N) r_issue(kchunk, n0 + cb, m0 + q * 32);
+      const bool pf = !rt && HALF <= 128 && p.R && row_ok && n0 + cb + HALF <= p.N &&
                       ((reinterpret_cast<uintptr_t>(p.R + (size_t)m * p.ldr + n0 + cb) & 15) == 0);
       if (pf) {
         const uint4* rp = reinterpret_cast<const uint4*>(p.R + (size_t)m * p.ldr + n0 + cb);
@@ -574,7 +604,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         for (int i = 0; i < NPF; ++i) res[i] = rp[i];
       }
       __syncwarp();
-      if (p.bias)
+      if (p.bias && !bias_all)
         for (int j = lane; j < HALF; j += 32) {
           const int n = n0 + cb + j;
           sb[j] = n < p.N ? __half2float(p.bias[n]) : 0.f;
@@ -610,9 +640,22 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         } else if (p.tstore) {
           if (n0 + c0 < p.N) {  // warp-uniform
             const bool rp = p.relu && !p.st_out;   // ReLU inside the pack instruction
+            uint8_t* stg = stg0 + (NSTG == 2 ? (kchunk & 1) * SM::STG : 0);
+            const int sw = (lane >> 1) & 3;     // 64-B swizzle: 16-B chunk c at c ^ ((row >> 1) & 3)
             if (!(p.dbg & 8))
-              epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr,
-                       row_ok, sc + (c0 - cb), ln, rp);
+              epi_math(p, m, n0 + c0, v, bias_all ? sbias + n0 + c0 : sb + (c0 - cb),
+                       pf ? res + (c0 - cb) / 8 : nullptr, row_ok && !rt, sc + (c0 - cb), ln, rp);
+            if (rt) {   // + residual (same order as the register path: after bias)
+              mbar_wait(&rbar[2 * e + (kchunk & 1)], (kchunk >> 1) & 1);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const uint4 w4 = *reinterpret_cast<const uint4*>(stg + lane * 64 + ((c ^ sw) << 4));
+                add_h2(w4.x, v[8 * c + 0], v[8 * c + 1]);
+                add_h2(w4.y, v[8 * c + 2], v[8 * c + 3]);
+                add_h2(w4.z, v[8 * c + 4], v[8 * c + 5]);
+                add_h2(w4.w, v[8 * c + 6], v[8 * c + 7]);
+              }
+            }
             if (p.st_out && row_ok) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
             uint32_t h[16];
             if (rp) {
@@ -629,9 +672,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
               if (x == 0x12345678u) p.C[0] = __float2half(1.f);
               continue;
             }
-            if (lane == 0) bulk_wait_read0();   // the previous store has read the staging tile
+            if (lane == 0) {   // the store that last used this staging tile has read it
+              if constexpr (NSTG == 1) bulk_wait_read0();
+              else if (!rt) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            ++kchunk;
             __syncwarp();
-            const int sw = (lane >> 1) & 3;     // 64-B swizzle: 16-B chunk c at c ^ ((row >> 1) & 3)
 #pragma unroll
             for (int c = 0; c < 4; ++c)
               *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ sw) << 4)) =
@@ -642,10 +688,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
               tma_store_2d(&mapC, stg, n0 + c0, m0 + q * 32);
               bulk_commit();
             }
+            if (rt && c0 + 32 < cb + HALF && n0 + c0 + 32 < p.N)   // next chunk's residual block
+              r_issue(kchunk, n0 + c0 + 32, m0 + q * 32);         // (kchunk already advanced)
           }
         } else if (row_ok && n0 + c0 < p.N) {
-          epi_math(p, m, n0 + c0, v, sb + (c0 - cb), pf ? res + (c0 - cb) / 8 : nullptr, true,
-                   sc + (c0 - cb), ln);
+          epi_math(p, m, n0 + c0, v, bias_all ? sbias + n0 + c0 : sb + (c0 - cb),
+                   pf ? res + (c0 - cb) / 8 : nullptr, true, sc + (c0 - cb), ln);
           if (p.st_out) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
           epi_out(p, m, n0 + c0, v, best);
         }
@@ -951,13 +999,13 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EW = 8>
+template <int BN, int STAGES, int EW = 8, int NSTG = 1>
 void launch(const GemmArgs& a, cudaStream_t s) {
-  using SM = Smem<BN, STAGES, false, EW>;
+  using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   static bool attr = false;
   if (!attr) {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     attr = true;
   }
@@ -984,9 +1032,14 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   static const bool morder = getenv("NMT_GEMM_ORDER") && getenv("NMT_GEMM_ORDER")[0] == 'm';  // A/B only
   p.nfast = !morder;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
-  const int grid = std::min(units, num_sms());  // persistent: one CTA per SM
+  static const int cap = getenv("NMT_GEMM_GRID_CAP") ? atoi(getenv("NMT_GEMM_GRID_CAP")) : 0;  // tuning
+  const int grid = std::min(units, cap > 0 && !a.dM ? cap : num_sms());  // persistent: one CTA per SM
   const CUtensorMap mc = out_map(a, p);
-  launch_k(k_gemm_tc<BN, STAGES, false, EW>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, p);
+  static const bool no_rtma = getenv("NMT_NO_RTMA") != nullptr;   // A/B only
+  p.rtma = NSTG == 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
+           (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && !no_rtma;
+  const CUtensorMap mr = p.rtma ? make_map(a.R, a.M, a.N, a.ldr, 32, true) : CUtensorMap{};
+  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -1038,7 +1091,7 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 2 : 1;
   const CUtensorMap mc = out_map(a, p);
-  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true>, ma, mb, mc, p));
+  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true>, ma, mb, mc, CUtensorMap{}, p));
   NMT_LAUNCH_CHECK();
 }
 
@@ -1126,7 +1179,7 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   } else if (a.tile_n == 64) {
     tc::launch<64, 4>(a, s);
   } else if (a.tile_n == 128) {
-    tc::launch<128, 4>(a, s);
+    tc::launch<128, 4, 8, 2>(a, s);
   } else if (const char* e = getenv("NMT_GEMM_CFG")) {  // tuning experiments only
     const std::string c(e);
     if (c == "128x4") tc::launch<128, 4>(a, s);
@@ -1135,7 +1188,13 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "128x4w16") tc::launch<128, 4, 16>(a, s);
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
     else if (c == "512x2") tc::launch<512, 2>(a, s);
+    else if (c == "256x3d") tc::launch<256, 3, 8, 2>(a, s);
     else tc::launch<256, 4>(a, s);
+  } else if (a.R && a.K <= 512 && !a.ln_st && !a.relu) {
+    // residual GEMM with a short main loop (attention output projection): 3 stages and two
+    // staging tiles per epilogue warp, the residual blocks TMA-loaded ahead of their chunk
+    // (measured 36.1 -> 30.9 us at 32768 rows; the 4-stage kernel wins everywhere else)
+    tc::launch<256, 3, 8, 2>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
     tc::launch<256, 4>(a, s);
