@@ -37,6 +37,7 @@ CHUNK = 48000           # 16 newstest2018-sized sets (2998 sentences each, PAPER
 BUCKETS = [(1, 16), (17, 64), (65, 148), (149, 512), (513, 2048), (2049, 4096)]
 T_WINDOW = (12, 20)     # "at t ~ 16"
 STEP_SENTS = 12000      # sentences of the step-timing run
+TRAFFIC_FILE = "profiles/r1e_enc_gemm_traffic.json"
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # Encoder GEMMs are dense contractions at N = 16K+ rows (tensor-bound).  Other classes take
 # the binding roof of their algorithmic FLOPs and bytes (decoder GEMMs / vocab projection:
@@ -331,7 +332,17 @@ def main():
         ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
         peak = pk["hbm_gbs"]
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s"}
-    roof.update({"frac": ach / peak, "traffic": None, "kernel": dom_name,
+    # DRAM traffic of the dominant class from the committed ncu --set full capture of one
+    # encoder layer's GEMM launches (tools/roofline_traffic.py), per launch, beside the
+    # algorithmic bytes of the same launches
+    traffic, tinfo = None, {}
+    tf = os.path.join(ROOT, TRAFFIC_FILE)
+    if dom_name == "enc_gemm" and os.path.exists(tf):
+        t = json.load(open(tf))
+        traffic = t["dram_bytes_per_launch"]
+        tinfo = {"traffic_algorithmic": t["algorithmic_bytes_per_launch"],
+                 "traffic_source": TRAFFIC_FILE + ": " + t["source"]}
+    roof.update({"frac": ach / peak, "traffic": traffic, **tinfo, "kernel": dom_name,
                  "share_of_step": dom["ms"] / tot if tot else None, "peak_source": src,
                  "per_launch": {"flops" if roof["bound"] == "tensor" else "bytes":
                                 (dom["flops"] if roof["bound"] == "tensor" else dom["bytes"]) / dom["launches"],

@@ -158,6 +158,7 @@ void init_arena(nmt_model* m) {
       {(void**)&m->nb_cnt, L.beam > 1 ? Bm * 4 : 256},
       {(void**)&m->blogits, L.beam > 1 ? R * (size_t)c.vocab_size * 4 : 256},
       {(void**)&m->lnst, R * (d / 32) * 8},
+      {(void**)&m->dlcl_p, c.use_dlcl && dlcl_lookahead_ok((int)d) ? N * d * 4 : 256},
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
   };

@@ -124,6 +124,7 @@ struct nmt_model {
   int* nb_cnt = nullptr;      // [max_sents] list sizes
   float* blogits = nullptr;   // [R][V] FP32 logits of the step
   float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
+  float* dlcl_p = nullptr;    // [N][d] FP32 DLCL lookahead partial (kernels.h dlcl_combine)
   float* cand_v = nullptr;    // [R][2K] top log-probs per row
   int* cand_i = nullptr;      // [R][2K] their token ids
   // pinned host staging

@@ -85,10 +85,18 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
   PROF(P_EMBED, 0, 2 * row,
        embed<T>(m->src, cT<T>(m->emb), m->pe, c.use_dlcl ? o : x, N, d, S, nullptr, nullptr, sq, s));
   const EncW& w0 = m->enc[0];
+  // DLCL two-boundary lookahead (kernels.h dlcl_combine): boundary k (combination row k+1)
+  // also produces the partial of row k+2 when k is even and row k+2 <= L+1 exists; odd
+  // boundaries start from that partial
+  static const bool no_la = getenv("NMT_NO_DLCL_LA") != nullptr;   // A/B only
+  const bool la = c.use_dlcl && dlcl_lookahead_ok(d) && !no_la;
+  auto dlcl_mode = [&](int k) { return !la ? 0 : (k & 1) ? 2 : (k + 1 <= L ? 1 : 0); };
   if (c.use_dlcl) {
-    PROF(P_DLCL, 0, 4 * row,
+    const int mode = dlcl_mode(0);
+    PROF(P_DLCL, 0, 4 * row + (mode ? row * 4.0 / tb : 0.0),
          dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, cT<T>(m->dl0_g), cT<T>(m->dl0_b), c.dlcl_ln,
-                         cT<T>(w0.attn_g), cT<T>(w0.attn_b), x, u, N, d, eps, s));
+                         cT<T>(w0.attn_g), cT<T>(w0.attn_b), x, u, N, d, eps, s, mode,
+                         m->dlcl_w + 1, m->dlcl_p));
   } else {
     PROF(P_ENC_LN, 0, 2 * row,
          layernorm<T>(x, d, cT<T>(w0.attn_g), cT<T>(w0.attn_b), u, d, N, d, eps, nullptr, s));
@@ -117,10 +125,16 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
     const T* nb = last ? cT<T>(m->enc_fb) : cT<T>(m->enc[l + 1].attn_b);
     if (c.use_dlcl) {
       const int k = l + 1;  // depth of y
-      PROF(P_DLCL, 0, (1 + k + 1 + (last ? 0 : 1) + 1) * row,
+      const int mode = dlcl_mode(k);
+      // bytes: y + history rows read (none in mode 2) + z, x, u written; FP32 partial
+      // written (mode 1) or read (mode 2)
+      const double by = (1 + (mode == 2 ? 0 : k) + 1 + (last ? 0 : 1) + 1) * row +
+                        (mode ? row * 4.0 / tb : 0.0);
+      PROF(P_DLCL, 0, by,
            dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, cT<T>(w.dl_g),
                            cT<T>(w.dl_b), c.dlcl_ln, ng, nb, last ? nullptr : x,
-                           last ? enc : u, N, d, eps, s));
+                           last ? enc : u, N, d, eps, s, mode,
+                           m->dlcl_w + (size_t)(k + 2) * (k + 1) / 2, m->dlcl_p));
     } else {
       PROF(P_ENC_LN, 0, 2 * row,
            layernorm<T>(x, d, ng, nb, last ? enc : u, d, N, d, eps, nullptr, s));

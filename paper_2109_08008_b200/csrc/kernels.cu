@@ -180,7 +180,7 @@ __global__ void k_dlcl(const T* __restrict__ y, T* __restrict__ hist, size_t his
 template <class T>
 void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
-                  int d, float eps, cudaStream_t s);
+                  int d, float eps, cudaStream_t s, int mode, const float* wP, float* P);
 
 // Vectorised variant: lane owns E contiguous columns [lane*E, lane*E + E) so every row
 // access is 16-B vector loads/stores (one 1 KB row per warp-instruction pair at d = 512).
@@ -279,42 +279,80 @@ __device__ __forceinline__ void ln_contig(float* v, int d, const T* g, const T* 
   for (int i = 0; i < E; ++i) v[i] = (v[i] - mu) * rstd * gv[i] + bv[i];
 }
 
-template <class T, int E>
+// MODE (two-boundary lookahead): the history rows read at an
+// even boundary l also feed the next boundary's combination, whose weights row l + 2 is
+// known, so odd boundaries read one FP32 partial instead of l + 1 history rows:
+//   MODE 0: x = sum_{k<=l} w[k] z_k                       (every history row read)
+//   MODE 1: as 0, and P = sum_{k<=l} wP[k] z_k -> FP32 partial (wP = weights of x_{l+2})
+//   MODE 2: x = P + w[l] z_l                              (no history reads)
+// The FP32 sums run in the same k order in every mode, so x is bit-identical to MODE 0.
+template <class T, int E, int MODE>
 __global__ void __launch_bounds__(256) k_dlcl_vec(
     const T* __restrict__ y, T* __restrict__ hist, size_t hist_stride, int l,
     const float* __restrict__ w, const T* __restrict__ gdl, const T* __restrict__ bdl, int dlcl_ln,
     const T* __restrict__ g2, const T* __restrict__ b2, T* __restrict__ xout, T* __restrict__ uout,
-    int rows, float eps) {
+    int rows, float eps, const float* __restrict__ wP, float* __restrict__ P) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   constexpr int d = 32 * E;
   const size_t off = (size_t)row * d + lane * E;
-  float z[E], x[E];
+  float z[E], x[E], pa[MODE == 1 ? E : 1];
+  if constexpr (MODE == 2) {   // the partial, issued before the y row's LN
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(P + off + i);
+      x[i] = q.x; x[i + 1] = q.y; x[i + 2] = q.z; x[i + 3] = q.w;
+    }
+  }
   ldrow<T, E>(y + off, z);
   if (dlcl_ln) ln_contig<T, E>(z, d, gdl, bdl, eps, lane);
   // z_l rounded to storage precision: later combines re-read exactly this value
   strow<T, E>(hist + (size_t)l * hist_stride + off, z);
 #pragma unroll
   for (int i = 0; i < E; ++i) z[i] = to_f(from_f<T>(z[i]));
+  if constexpr (MODE != 2) {
 #pragma unroll
-  for (int i = 0; i < E; ++i) x[i] = 0.f;
-  // U history rows in flight per lane (raw 16-B loads issued before any arithmetic): the
-  // combine is bound by HBM bandwidth, not by one memory latency per history row
-  constexpr int U = sizeof(T) == 2 ? 8 : 4;
-  int k = 0;
-  for (; k + U <= l; k += U) {
-    RawRow<T, E> a[U];
+    for (int i = 0; i < E; ++i) x[i] = 0.f;
+    if constexpr (MODE == 1) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) a[u].load(hist + (size_t)(k + u) * hist_stride + off);
+      for (int i = 0; i < E; ++i) pa[i] = 0.f;
+    }
+    // U history rows in flight per lane (raw 16-B loads issued before any arithmetic): the
+    // combine is bound by HBM bandwidth, not by one memory latency per history row
+    constexpr int U = sizeof(T) == 2 ? 8 : 4;
+    int k = 0;
+    for (; k + U <= l; k += U) {
+      RawRow<T, E> a[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) a[u].fma_into(w[k + u], x);
-  }
-  for (; k < l; ++k) {
-    float a[E];
-    ldrow<T, E>(hist + (size_t)k * hist_stride + off, a);
-    const float wa = w[k];
+      for (int u = 0; u < U; ++u) a[u].load(hist + (size_t)(k + u) * hist_stride + off);
 #pragma unroll
-    for (int i = 0; i < E; ++i) x[i] = fmaf(wa, a[i], x[i]);
+      for (int u = 0; u < U; ++u) {
+        a[u].fma_into(w[k + u], x);
+        if constexpr (MODE == 1) a[u].fma_into(wP[k + u], pa);
+      }
+    }
+    for (; k < l; ++k) {
+      float a[E];
+      ldrow<T, E>(hist + (size_t)k * hist_stride + off, a);
+      const float wa = w[k];
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = fmaf(wa, a[i], x[i]);
+      if constexpr (MODE == 1) {
+        const float wb = wP[k];
+#pragma unroll
+        for (int i = 0; i < E; ++i) pa[i] = fmaf(wb, a[i], pa[i]);
+      }
+    }
+    if constexpr (MODE == 1) {
+      const float wb = wP[l];
+#pragma unroll
+      for (int i = 0; i < E; i += 4) {
+        float4 q;
+        q.x = fmaf(wb, z[i], pa[i]); q.y = fmaf(wb, z[i + 1], pa[i + 1]);
+        q.z = fmaf(wb, z[i + 2], pa[i + 2]); q.w = fmaf(wb, z[i + 3], pa[i + 3]);
+        *reinterpret_cast<float4*>(P + off + i) = q;
+      }
+    }
   }
   const float wl = w[l];
 #pragma unroll
@@ -324,20 +362,31 @@ __global__ void __launch_bounds__(256) k_dlcl_vec(
   strow<T, E>(uout + off, x);
 }
 
+bool dlcl_lookahead_ok(int d) { return d == 512 || d == 256; }
+
 template <class T>
 void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
-                  int d, float eps, cudaStream_t s) {
+                  int d, float eps, cudaStream_t s, int mode, const float* wP, float* P) {
   if (rows <= 0) return;
-  if (d == 512)
-    k_dlcl_vec<T, 16><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl,
-                                                         dlcl_ln, g2, b2, xout, uout, rows, eps);
-  else if (d == 256)
-    k_dlcl_vec<T, 8><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl,
-                                                        dlcl_ln, g2, b2, xout, uout, rows, eps);
-  else
+  if (mode != 0 && !dlcl_lookahead_ok(d)) throw CudaError("dlcl_combine: lookahead needs d = 256 / 512");
+#define NMT_DV(E, MODE)                                                                        \
+  k_dlcl_vec<T, E, MODE><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, \
+                                                           dlcl_ln, g2, b2, xout, uout, rows, eps, \
+                                                           wP, P)
+  if (d == 512) {
+    if (mode == 1) NMT_DV(16, 1);
+    else if (mode == 2) NMT_DV(16, 2);
+    else NMT_DV(16, 0);
+  } else if (d == 256) {
+    if (mode == 1) NMT_DV(8, 1);
+    else if (mode == 2) NMT_DV(8, 2);
+    else NMT_DV(8, 0);
+  } else {
     k_dlcl<T><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, dlcl_ln, g2,
                                                  b2, xout, uout, rows, d, eps);
+  }
+#undef NMT_DV
   NMT_LAUNCH_CHECK();
 }
 
@@ -711,7 +760,8 @@ void argmax_ids(unsigned long long* keys, int* ids, int rows, cudaStream_t s) {
   template void layernorm<T>(const T*, int, const T*, const T*, T*, int, int, int, float,       \
                              const int*, cudaStream_t);                                         \
   template void dlcl_combine<T>(const T*, T*, size_t, int, const float*, const T*, const T*,    \
-                                int, const T*, const T*, T*, T*, int, int, float, cudaStream_t); \
+                                int, const T*, const T*, T*, T*, int, int, float, cudaStream_t, \
+                                int, const float*, float*);                                     \
   template void to_float<T>(const T*, float*, size_t, cudaStream_t);                          \
   template void embed_dec_ln<T>(const int*, const T*, const float*, const T*, const T*, T*, T*, \
                                 int, int, float, float, const int*, const int*, cudaStream_t);

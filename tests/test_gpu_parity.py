@@ -464,6 +464,40 @@ def test_batch_invariance_fp32():
         assert o[0] == full[i]
 
 
+_LA_SNIPPET = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from gpu_common import gpu_model, pad_batch
+from synth import newstest_like
+wl = newstest_like(48, 32000, start=3000)
+src, lens = pad_batch([wl.ids[wl.off[i]:wl.off[i + 1]] for i in range(wl.n)])
+out = {{}}
+for prec in ("fp32", "fp16"):
+    gm = gpu_model("student-35-1", prec, max_tokens=src.size, max_sents=wl.n)
+    b = gm.encode(torch.from_numpy(src).cuda(), lens)
+    out[prec] = b.encoder_output().cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_dlcl_lookahead_bit_identical(tmp_path):
+    """The DLCL two-boundary lookahead (FP32 partials) changes
+    which bytes are read, not the arithmetic: the 35-layer encoder output is bit-identical
+    with NMT_NO_DLCL_LA=1 (every boundary reads its whole history), FP32 and FP16 modes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for name, env in (("la", {}), ("plain", {"NMT_NO_DLCL_LA": "1"})):
+        path = str(tmp_path / f"{name}.npz")
+        code = _LA_SNIPPET.format(root=root, tests=os.path.join(root, "tests"), path=path)
+        subprocess.run([sys.executable, "-c", code], check=True, env={**os.environ, **env})
+        res[name] = np.load(path)
+    for prec in ("fp32", "fp16"):
+        assert np.array_equal(res["la"][prec], res["plain"][prec]), prec
+
+
 def test_errors():
     from paper_2109_08008_b200 import NmtError
     gm = gpu_model("tiny", "fp16", max_tokens=64, max_sents=4, max_tgt_len=16)
