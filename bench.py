@@ -285,12 +285,14 @@ def main():
         h2d = d2h = 0
         for k in range(args.warmup, n_chunks):
             wl, _ = chunks[k]
-            outs, st = model.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=args.max_tokens,
-                                       max_sents=args.max_sents, sync_every=args.sync_every,
-                                       workers=args.workers)
+            (flat, offs), st = model.translate(wl.ids, wl.off, caps=wl.caps,
+                                               max_tokens=args.max_tokens,
+                                               max_sents=args.max_sents,
+                                               sync_every=args.sync_every, workers=args.workers,
+                                               as_arrays=True)
             g2 += st["gen_tokens"]
             h2d += wl.ids.nbytes
-            d2h += 4 * sum(len(o) for o in outs) + 4 * len(outs)
+            d2h += flat.nbytes + 4 * (len(offs) - 1)   # token ids + per-sentence lengths
         e1.record(stream)
         barrier()
         ems, g2_all = reduce_timing(e0.elapsed_time(e1), float(g2), device="cuda")

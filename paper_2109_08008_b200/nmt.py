@@ -160,8 +160,10 @@ class Model:
         return Batch(self, b, B, S)
 
     def translate(self, ids, off, caps=None, max_tokens=None, max_sents=None, prune_every=1,
-                  prune_ratio=0.25, sync_every=4, workers=1, beam=1, stream=None):
-        """Host-buffer translation (C-ABI nmt_translate). Returns (outputs, stats dict)."""
+                  prune_ratio=0.25, sync_every=4, workers=1, beam=1, stream=None, as_arrays=False):
+        """Host-buffer translation (C-ABI nmt_translate). Returns (outputs, stats dict);
+        outputs = one token list per sentence, or with as_arrays=True the library's flat
+        (ids int32 [total], offsets int64 [n+1]) buffers as returned (no per-sentence lists)."""
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         off = np.ascontiguousarray(off, dtype=np.int64)
         n = len(off) - 1
@@ -177,6 +179,8 @@ class Model:
                                    C.c_int64(n), C.byref(o), out.ctypes.data_as(C.c_void_p),
                                    C.c_int64(out_cap), out_off.ctypes.data_as(C.c_void_p), C.byref(st),
                                    _stream(stream)))
+        if as_arrays:
+            return (out[:out_off[n]], out_off), st.as_dict()
         outs = [out[out_off[i]:out_off[i + 1]].tolist() for i in range(n)]
         return outs, st.as_dict()
 

@@ -276,6 +276,8 @@ def test_translate_host_equals_device_and_steps():
         out_h2, st2 = gm.translate(wl.ids, wl.off, caps=wl.caps)
     assert out_h2 == out_h
     assert st2["launches"] == st_h["launches"]   # graph replays launch the same kernels
+    (flat, offs), _ = gm.translate(wl.ids, wl.off, caps=wl.caps, as_arrays=True)
+    assert [flat[offs[i]:offs[i + 1]].tolist() for i in range(wl.n)] == out_h
 
 
 @pytest.mark.parametrize("prec", PRECS)
