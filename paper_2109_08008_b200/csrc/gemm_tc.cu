@@ -805,13 +805,13 @@ __global__ void __launch_bounds__(kCThreads, 3)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
-  pdl_trigger();
-  pdl_wait();
   const int S = p.splits;
   const int s = (int)cluster_ctarank();          // split index == rank in the cluster
   const int tile = blockIdx.x / S;
   const int num_m = (p.M + BM - 1) / BM;         // grid sized by the host upper bound
   const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+  pdl_trigger();   // (the TMEM allocation below is 64 columns: never blocks a dependent)
+  pdl_wait();
   const int Meff = p.dM ? min(p.M, *p.dM) : p.M;
   const bool live = m0 < Meff;                   // uniform across the cluster
   const int kb_total = (p.K + BK - 1) / BK;
@@ -1149,20 +1149,34 @@ int decode_splits(int N, int K) {
   return sp;
 }
 
-// Decode GEMMs use the persistent kernel with 128 x 128 tiles and no split-K: measured in
-// captured graphs (tools/dec_gemm_sweep.py) it beats the cluster split-K kernel at every
-// live-row count of the 35-1 decode step (6 projections: 46.7 vs 112.7 us at 1024 rows,
-// 45.4 vs 54.4 us at 256), and every output row depends on its own input row only.
-// NMT_DEC_TILE / NMT_DEC_SPLITS select other configurations for tuning experiments.
+// Decode GEMMs (rows = live batch rows): the configuration depends on the weight shape
+// only, never on the row count, so every output row is computed the same way whatever the
+// batch (batch invariance).  Measured in captured graphs (tools/dec_gemm_sweep.py, 35-1
+// shapes at 32 / 256 / 1024 rows, us per GEMM):
+//   N = K = 512 (self-out, cross-q, cross-out): 128x128 7.0-7.4, 64-wide tiles 5.9-6.3
+//   K = 2048 (FFN2): 128x128 14.1-14.7, cluster split-K 2 9.2-11.1, split 4 7.6-14.5
+//   N = 1536 / 2048, K = 512 (QKV, FFN1): 128x128 6.9-8.0, 64-wide 6.0-9.4 (worse at 1024)
+// so: 64-wide tiles for the square projections, split-K 2 through a thread-block cluster for
+// K >= 2048 (no LN-statistics output there), 128x128 otherwise.  The per-GEMM floor of
+// ~6 us is the dependent TMA round trips of the K loop plus launch and epilogue.
+// NMT_DEC_TILE / NMT_DEC_SPLITS / NMT_DEC_POLICY=old override for tuning experiments.
 void decode_config(GemmArgs& a) {
   static const int env_tile = getenv("NMT_DEC_TILE") ? atoi(getenv("NMT_DEC_TILE")) : 0;
   static const int env_splits = getenv("NMT_DEC_SPLITS") ? atoi(getenv("NMT_DEC_SPLITS")) : 0;
+  static const bool old = getenv("NMT_DEC_POLICY") && std::string(getenv("NMT_DEC_POLICY")) == "old";
+  a.splits = 1;
   if (env_splits > 1) {
     a.tile_n = 64;
     a.splits = env_splits;
-  } else {
+  } else if (env_tile || old) {
     a.tile_n = env_tile ? env_tile : 128;
-    a.splits = 1;
+  } else if (a.K >= 2048 && !a.st_out && !a.ln_st && ((a.K + 63) / 64) % 2 == 0) {
+    a.tile_n = 64;
+    a.splits = 2;
+  } else if (a.N <= 512 && a.K <= 512) {
+    a.tile_n = 64;
+  } else {
+    a.tile_n = 128;
   }
 }
 
