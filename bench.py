@@ -351,6 +351,16 @@ def main():
                                 "ms": dom["ms"] / dom["launches"], "launches": dom["launches"]}})
     kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                    "share": round(v["ms"] / tot, 4) if tot else None} for k, v in prof.items()}
+    # whole-step roofline of the profiled chunk: every kernel class at the binding roof of its
+    # algorithmic FLOPs (tensor peak) and bytes (HBM peak), summed — the step time the
+    # implemented algorithm would take on a perfectly fed B200 (SURVEY §8(d) "fraction of the
+    # roofline"), against the measured step
+    t_roof = sum(max(v["flops"] / (tpeak * 1e12), v["bytes"] / (pk["hbm_gbs"] * 1e9))
+                 for v in prof.values())
+    step_roof = {"ms_per_step": 1e3 * t_roof, "tok_s": st["gen_tokens"] / t_roof if t_roof else None,
+                 "frac": 1e3 * t_roof / (ms_max / args.steps) if t_roof else None,
+                 "note": "sum over kernel classes of max(FLOP / tensor peak, bytes / HBM peak), "
+                         "profiled chunk; frac = roofline step time / measured step time"}
 
     if rank == 0:
         line = {
@@ -369,7 +379,8 @@ def main():
             "ms_per_decode_step": mean_step,
             "decode_step_ms_by_live_rows": {"t_window": list(T_WINDOW), "buckets": step_ms},
             "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "kernels": kernels,
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+            "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
