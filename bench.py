@@ -2,10 +2,10 @@
 """Benchmark of the B200 hot path: FP16 greedy translation with the 35-1 Transformer-DLCL-RPR
 student (BASELINE.json configs[2], metric "target tokens/sec ... ms/decode step").
 
-A step = nmt_translate_device over one 48000-sentence chunk (16 x newstest2018) of the
-synthetic 1M-sentence set (DESIGN.md input recipe): length sort, dynamic 32768-token /
-4096-sentence batches (the paper's rule, at a B200-sized budget), four
-concurrent batch workers, 35-layer encoder with RPR + DLCL, cached greedy
+A step = nmt_translate_device over one 96000-sentence chunk (32 x newstest2018) of the
+synthetic 1M-sentence set (DESIGN.md input recipe): length sort, dynamic 65536-token /
+8192-sentence batches (the paper's rule, at a B200-sized budget; SURVEY
+§8(d) budget sweep), four concurrent batch workers, 35-layer encoder with RPR + DLCL, cached greedy
 decoding with the fused vocab argmax, batch pruning (rho = 0.25).  Each rank/step gets a
 distinct chunk (weak scaling: sentences are independent; no collective
 on the data path).  Inputs are resident in HBM for `value`; `e2e` times nmt_translate
@@ -31,10 +31,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "target tokens/sec (FP16 greedy, 35-1 student) at 1/2/4/8 B200; ms/decode step"
 UNIT = "target tokens/s"
-CHUNK = 48000           # 16 newstest2018-sized sets (2998 sentences each)
+CHUNK = 96000           # 32 newstest2018-sized sets (2998 sentences each)
 # decode-step buckets of live rows (1-16, 17-64, 65-148, 149-512; plus the
 # larger live batches of the B200-sized budget)
-BUCKETS = [(1, 16), (17, 64), (65, 148), (149, 512), (513, 2048), (2049, 4096)]
+BUCKETS = [(1, 16), (17, 64), (65, 148), (149, 512), (513, 2048), (2049, 8192)]
 T_WINDOW = (12, 20)     # "at t ~ 16"
 STEP_SENTS = 12000      # sentences of the step-timing run
 TRAFFIC_FILE = "profiles/r1e_enc_gemm_traffic.json"
@@ -178,8 +178,8 @@ def main():
     # B200-sized dynamic-batch budget (the paper's rule, with a larger token
     # limit than its T4's 4096-ish / 512-sentence setting; --max-tokens 4096 --max-sents 512
     # reproduces that budget)
-    ap.add_argument("--max-tokens", type=int, default=32768)
-    ap.add_argument("--max-sents", type=int, default=4096)
+    ap.add_argument("--max-tokens", type=int, default=65536)
+    ap.add_argument("--max-sents", type=int, default=8192)
     ap.add_argument("--sync-every", type=int, default=4)
     ap.add_argument("--workers", type=int, default=4,
                     help="concurrent batch workers per GPU (own arena + stream, shared weights)")
