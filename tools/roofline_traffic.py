@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def first_batch(chunk, max_tokens=32768, max_sents=4096):
+def first_batch(chunk, max_tokens=65536, max_sents=8192):
     """(B, S) of the first dynamic batch of bench chunk 0 (the paper's rule, DESIGN R17)."""
     from synth import newstest_like
     wl = newstest_like(chunk, 32000, start=0)
