@@ -500,6 +500,28 @@ def test_dlcl_lookahead_bit_identical(tmp_path):
         assert np.array_equal(res["la"][prec], res["plain"][prec]), prec
 
 
+def test_step_timing_records():
+    """nmt_profile mode 3 + nmt_profile_steps (SURVEY §8(d) ms/decode step): one record per
+    graph-replayed decode step, live rows non-increasing within a batch, positive device
+    times; the translation is unchanged by the timing; a reset clears the records."""
+    wl = newstest_like(96, 32000, start=5000)
+    gm = gpu_model("student-35-1", "fp16", max_tokens=2048, max_sents=64)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        ref, st0 = gm.translate(wl.ids, wl.off, caps=wl.caps)   # eager first steps, graphs built
+        gm.profile(3)
+        out, st = gm.translate(wl.ids, wl.off, caps=wl.caps)
+        rec = gm.profile_steps()
+        gm.profile(0)
+    assert out == ref
+    assert 0 < len(rec) <= st["decode_steps"]
+    assert all(ms > 0 and live >= 1 for _, live, ms in rec)
+    for (t0, l0, _), (t1, l1, _) in zip(rec, rec[1:]):
+        if t1 == t0 + 1:            # same batch: pruning only shrinks the live set
+            assert l1 <= l0
+    assert gm.profile_steps() == []
+
+
 def test_errors():
     from paper_2109_08008_b200 import NmtError
     gm = gpu_model("tiny", "fp16", max_tokens=64, max_sents=4, max_tgt_len=16)
