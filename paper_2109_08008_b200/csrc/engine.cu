@@ -1078,6 +1078,7 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
     std::vector<float> scores((size_t)n * NB, -INFINITY);
     std::vector<const float*> lg(nm);
     for (int k = 0; k < nm; ++k) lg[k] = e->members[k]->blogits;
+    const int R = c0->lim.max_sents * c0->lim.beam;   // row capacity (graph buckets)
     int64_t steps = 0, prunes = 0, gen = 0;
     std::vector<int> lens, caps;
     for (int bi = 0; bi < nb; ++bi) {
@@ -1101,18 +1102,63 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
       c0->batch.NB = NB;
       const int* dR = &c0->st->n_live;
       int rows = B * K, t = 0;
-      for (; t < c0->batch.max_cap && rows > 0; ++t) {
+      // one ensemble step for `rr` (>= live) rows: every member's decoder on its own caches,
+      // the distribution average (R26), the beam update and pruning; all kernels read t, the
+      // live count and S from device memory, so a captured step serves every step
+      auto step = [&](int rr) {
         for (auto* c : e->members) {
-          c->batch.rows_upper = rows;
+          c->batch.rows_upper = rr;
           decode_step_any(c, &c->batch, nullptr, nullptr, s, /*finish=*/false);
         }
-        ens_combine(lg.data(), nm, V, dR, rows, e->ens, s);
-        beam_row_topk(e->ens, V, 2 * K, dR, rows, c0->cand_v, c0->cand_i, s);
+        ens_combine(lg.data(), nm, V, dR, rr, e->ens, s);
+        beam_row_topk(e->ens, V, 2 * K, dR, rr, c0->cand_v, c0->cand_i, s);
         beam_select(K, c0->cand_v, c0->cand_i, c0->bscore, c0->prev_tok, c0->done, c0->row_slot,
                     c0->tgt_cap, c0->anc, c0->htok, Tm, c0->best_score, c0->out_tok, c0->gen_len,
-                    c0->st, V, eos, rows, s, NB, c0->nb_score, c0->nb_len, c0->nb_tok, c0->nb_cnt);
-        prune_compact(c0->st, c0->row_slot, c0->prev_tok, c0->done, every, ratio, nullptr, rows, s,
+                    c0->st, V, eos, rr, s, NB, c0->nb_score, c0->nb_len, c0->nb_tok, c0->nb_cnt);
+        prune_compact(c0->st, c0->row_slot, c0->prev_tok, c0->done, every, ratio, nullptr, rr, s,
                       c0->bscore);
+      };
+      unsigned rb;
+      memcpy(&rb, &ratio, 4);
+      for (; t < c0->batch.max_cap && rows > 0; ++t) {
+        const int bucket = std::min((int)R, (rows + 31) & ~31);
+        const auto key = std::make_tuple(bucket, NB, every, rb);
+        if (s == nullptr || !e->eager_keys.count(key)) {
+          step(rows);   // legacy stream (no capture) / first use of a configuration
+          e->eager_keys.insert(key);
+        } else {
+          auto it = e->graphs.find(key);
+          if (it == e->graphs.end()) {
+            cudaGraph_t g;
+            NMT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            g_pdl = pdl_enabled();
+            try {
+              step(bucket);
+            } catch (...) {
+              g_pdl = false;
+              cudaStreamEndCapture(s, &g);
+              throw;
+            }
+            g_pdl = false;
+            NMT_CUDA(cudaStreamEndCapture(s, &g));
+            size_t nn = 0;
+            NMT_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+            std::vector<cudaGraphNode_t> ns(nn);
+            if (nn) NMT_CUDA(cudaGraphGetNodes(g, ns.data(), &nn));
+            int nodes = 0;
+            for (auto nd : ns) {
+              cudaGraphNodeType ty;
+              NMT_CUDA(cudaGraphNodeGetType(nd, &ty));
+              nodes += ty == cudaGraphNodeTypeKernel;
+            }
+            cudaGraphExec_t ex;
+            NMT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+            NMT_CUDA(cudaGraphDestroy(g));
+            it = e->graphs.emplace(key, std::make_pair(ex, nodes)).first;
+          }
+          NMT_CUDA(cudaGraphLaunch(it->second.first, s));
+          g_launches += it->second.second;
+        }
         for (auto* c : e->members) c->batch.step = t + 1;
         if ((t + 1) % sync_every == 0) {
           poll_state(c0, s);

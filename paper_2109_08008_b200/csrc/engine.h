@@ -200,7 +200,13 @@ struct nmt_model {
 struct nmt_ensemble {
   std::vector<nmt_model*> members;
   float* ens = nullptr;   // [R][V] FP32 ensemble log-probabilities of the step
+  // whole-ensemble decode steps (every member's decoder, the averaging, the beam update and
+  // pruning) as CUDA graphs keyed by (rows bucket, n-best, prune cadence, ratio bits), with
+  // their kernel-node counts; configurations run eagerly once first
+  std::map<std::tuple<int, int, int, unsigned>, std::pair<cudaGraphExec_t, int>> graphs;
+  std::set<std::tuple<int, int, int, unsigned>> eager_keys;
   ~nmt_ensemble() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
     for (auto* c : members) delete c;
     if (ens) cudaFree(ens);
   }

@@ -356,6 +356,16 @@ def test_ensemble_tiny_matches_oracle(prec):
             same += ok
         assert same >= (wl.n if prec == "fp32" else wl.n - 2), (K, N, same)
         assert st["sentences"] == wl.n and st["gen_tokens"] > 0
+    # graph-replayed ensemble steps (non-default stream) == eager steps, bit for bit
+    h_e, s_e, _ = ens.translate(wl.ids, wl.off, beam=4, nbest=3, caps=wl.caps, max_tokens=48,
+                                max_sents=4)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for _ in range(2):   # first use of a row bucket runs eagerly, then captured graphs
+            h_g, s_g, st_g = ens.translate(wl.ids, wl.off, beam=4, nbest=3, caps=wl.caps,
+                                           max_tokens=48, max_sents=4)
+    torch.cuda.synchronize()
+    assert h_g == h_e and s_g == s_e
     solo = Ensemble([g1])
     hyps, _, _ = solo.translate(wl.ids, wl.off, beam=4, caps=wl.caps, max_tokens=48, max_sents=4)
     best, _ = g1.translate(wl.ids, wl.off, caps=wl.caps, max_tokens=48, max_sents=4, beam=4)

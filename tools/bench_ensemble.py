@@ -6,7 +6,7 @@ architecture, FP16) decoding a newstest-shaped chunk with beam 4, as 1-best and 
 the ensemble's cost ratio.  Prints one JSON object (target tokens/s, wall clock around a
 synchronised call; the first call is a warm-up).
 
-Usage: python tools/bench_ensemble.py [--n 512] [--max-tokens 4096] [--max-sents 128]"""
+Usage: python tools/bench_ensemble.py [--n 512] [--max-tokens 4096] [--max-sents 128] [--eager]"""
 import argparse
 import json
 import os
@@ -36,14 +36,19 @@ def main():
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--max-tokens", type=int, default=4096)
     ap.add_argument("--max-sents", type=int, default=128)
+    ap.add_argument("--eager", action="store_true",
+                    help="legacy default stream: eager launches (no CUDA-graph decode steps)")
     a = ap.parse_args()
+    if not a.eager:   # decode steps are captured and replayed as CUDA graphs off stream 0
+        torch.cuda.set_stream(torch.cuda.Stream())
     names = ["ens-35-6", "ens-35-6-dlcl", "ens-40-6", "ens-40-6-dlcl"]
     lim = dict(max_tokens=a.max_tokens, max_sents=a.max_sents, max_tgt_len=200, beam=4)
     models = [Model(PRESETS[n], generate_weights(PRESETS[n], seed=3000 + i), precision="fp16", **lim)
               for i, n in enumerate(names)]
     wl = newstest_like(a.n, 32000, start=500_000)
     res = {"workload": f"{a.n} newstest-shaped sentences, batches {a.max_tokens} tokens / "
-                       f"{a.max_sents} sentences, beam 4, FP16, random-init teachers",
+                       f"{a.max_sents} sentences, beam 4, FP16, random-init teachers, "
+                       f"{'eager launches' if a.eager else 'CUDA-graph decode steps'}",
            "members": names}
     single = Ensemble([models[3]])
     (h, s, st), dt = timed(lambda: single.translate(wl.ids, wl.off, beam=4, caps=wl.caps))
