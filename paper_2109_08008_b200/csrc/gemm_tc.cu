@@ -166,7 +166,6 @@ __device__ __forceinline__ void load8h(const __half* p, float* f) {
     f[2 * e + 1] = x.y;
   }
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 struct Params {
   int M, N, K;
