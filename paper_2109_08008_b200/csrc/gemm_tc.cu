@@ -186,6 +186,7 @@ struct Params {
                       // 32 = operand TMA only for the first STAGES k-blocks (MMA rate)
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
   int rtma;           // residual 32 x 32 blocks TMA-loaded into the staging tiles (mapR)
+  int bpre;           // first-unit weight tiles requested before the PDL wait
   int nfast;          // unit order: 1 = column tiles of one row block on consecutive CTAs
                       // (the A row block is read from DRAM once and shared through L2)
   float2* st_out;     // LN folding, producer side (GemmArgs)
@@ -475,15 +476,43 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   // dependents may launch once every CTA holds its TMEM (a dependent GEMM CTA allocating
   // on the same SM then waits for this one's dealloc, never the reverse)
   pdl_trigger();
-  // PDL: the setup above (barriers, tensor-map prefetch, TMEM allocation) overlaps the
-  // preceding kernel; its outputs (operands, the live-row count) are read only from here
+  // Weight prefetch (B operand = weights, never written by the preceding kernels): with the
+  // n-fastest unit order the first unit's column block (cid % num_n) does not depend on the
+  // live-row count, so its first STAGES k-blocks of B are requested before the PDL wait
+  // (expect_tx only; the producer's arrive.expect_tx for A completes the phase later).
+  const int num_n = (p.N + BN - 1) / BN;
+  int npre = 0;
+  if constexpr (!PAIR) {
+    if (warp == 0 && lane == 0 && p.nfast && p.bpre && !(p.dbg & 32)) {
+      npre = kb_total < STAGES ? kb_total : STAGES;
+      const int n0 = (cid % num_n) * BN;
+      for (int st = 0; st < npre; ++st) {
+        uint8_t* sb = smem + st * SM::STAGE + SM::A_BYTES;
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                         smem_u32(&full[st])),
+                     "r"((uint32_t)SM::B_BYTES)
+                     : "memory");
+#pragma unroll
+        for (int bo = 0; bo < BN; bo += BBOX)
+          tma_load_2d(sb + bo * BK * 2, &mapB, &full[st], st * BK, n0 + bo);
+      }
+    }
+  }
+  // PDL: the setup above (barriers, tensor-map prefetch, TMEM allocation, weight prefetch)
+  // overlaps the preceding kernel; its outputs (A, the live-row count) are read from here
   pdl_wait();
   const int M = p.dM ? min(p.M, *p.dM) : p.M;
-  const int num_m = (M + UM - 1) / UM, num_n = (p.N + BN - 1) / BN;
+  const int num_m = (M + UM - 1) / UM;
   const int units = num_m * num_n;   // CTAs with cid >= units skip to the teardown
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
+      if (npre && cid >= units) {   // no work: let the prefetched weight tiles land, then exit
+        for (int st = 0; st < npre; ++st) {
+          mbar_arrive(&full[st]);
+          mbar_wait(&full[st], 0);
+        }
+      }
       int it = 0;
       for (int u = cid; u < units; u += ncl) {
         const int mi = p.nfast ? u / num_n : u % num_m, ni = p.nfast ? u % num_n : u / num_m;
@@ -501,6 +530,11 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           } else {
             if ((p.dbg & 32) && it >= STAGES) {   // tuning: MMAs on stale tiles, no TMA
               mbar_arrive(&full[st]);
+              continue;
+            }
+            if (it < npre) {   // B already requested before the PDL wait
+              mbar_expect_tx(&full[st], SM::A_BYTES);
+              tma_load_2d(sa, &mapA, &full[st], kb * BK, m0);
               continue;
             }
             mbar_expect_tx(&full[st], SM::STAGE);
@@ -1030,6 +1064,8 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
   static const bool morder = getenv("NMT_GEMM_ORDER") && getenv("NMT_GEMM_ORDER")[0] == 'm';  // A/B only
   p.nfast = !morder;
+  static const bool no_bpre = getenv("NMT_NO_BPRE") != nullptr;   // A/B only
+  p.bpre = !no_bpre;
   const int units = ceil_div(a.M, BM) * ceil_div(a.N, BN);
   static const int cap = getenv("NMT_GEMM_GRID_CAP") ? atoi(getenv("NMT_GEMM_GRID_CAP")) : 0;  // tuning
   const int grid = std::min(units, cap > 0 && !a.dM ? cap : num_sms());  // persistent: one CTA per SM
