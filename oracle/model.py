@@ -26,9 +26,17 @@ Model (readings R1-R11):
     h = LN^dec(g), logits = h E^T (tied, no bias).
 
 Parity pins (tests/test_oracle_model.py): encoder layer == torch
-TransformerEncoderLayer(norm_first) with zero RPR tables; decoder layer ==
-torch TransformerDecoderLayer(norm_first) with zero tables; O-def == O-fast;
-DLCL one-hot reductions (reading A22); parameter counts == PAPER.md Tables 1-2.
+TransformerEncoderLayer(norm_first) with zero RPR tables
+(test_encoder_equals_torch_prenorm_stack); decoder layer == torch
+TransformerDecoderLayer(norm_first) with zero tables
+(test_decoder_equals_torch_prenorm_layer); O-def == O-fast
+(test_encoder_def_equals_batched, test_cached_decoder_equals_recompute,
+test_greedy_def_equals_fast_and_prune_invariance); DLCL (encode_def's Eq. 2 sum,
+test_dlcl_eq2_against_torch_layers): uniform W -> mean of z_k, the [.5,.25,.25]
+hand sum, one-hot W with LN^dl on == plain stack + explicit LN^dl (A22 ii);
+one-hot with LN^dl off == plain stack (A22 i,
+test_dlcl_one_hot_without_ln_is_plain_stack); W = 0 -> final-LN bias;
+parameter counts == PAPER.md Tables 1-2 (tests/test_oracle_params.py).
 """
 from __future__ import annotations
 

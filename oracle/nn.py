@@ -12,8 +12,13 @@ Each function restates one definition:
     (reading R7/R24). Pinned: brute-force table.
   * rpr_attention_loops — Shaw et al. relative self-attention written as the
     plain double loop over (query i, key j); keys AND values get the clipped
-    relative embedding (reading R7). Pinned: zero tables == torch
-    scaled_dot_product_attention; n = 1 closed form; unclipped case.
+    relative embedding (reading R7). Pinned (tests/test_oracle_nn.py): zero tables ==
+    torch scaled_dot_product_attention (test_rpr_zero_tables_is_vanilla_attention);
+    constant tables == vanilla + shift (test_rpr_constant_tables_shift); n = 1 closed
+    form o = v_0 + A^V[k] (test_rpr_single_token_closed_form); the j - i DIRECTION by a
+    hand-computed asymmetric-table example, n = 3, k = 1 (test_rpr_direction_hand_example);
+    the unclipped case k >= n - 1 with distance-linear tables == SDPA on position-shifted
+    keys / values (test_rpr_unclipped_linear_tables_are_shifted_vanilla).
 """
 from __future__ import annotations
 

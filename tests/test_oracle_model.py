@@ -202,3 +202,65 @@ def test_beam_early_stop_is_sound(toy8, K):
         a = beam_search(toy8, src, 6, K=K, early_stop=True)
         b = beam_search(toy8, src, 6, K=K, early_stop=False)
         assert a[0] == b[0] and abs(a[1] - b[1]) < 1e-12
+
+
+def _torch_layer(W, cfg, l):
+    """torch.nn.TransformerEncoderLayer(norm_first) loaded with encoder layer l (zero RPR)."""
+    d = cfg.d_model
+    p = f"enc.{l}."
+    lay = torch.nn.TransformerEncoderLayer(d, cfg.n_heads, cfg.d_ffn, dropout=0.0, batch_first=True,
+                                           norm_first=True, layer_norm_eps=cfg.ln_eps).double().eval()
+    lay.self_attn.in_proj_weight.data = _t(W[p + "qkv.w"]); lay.self_attn.in_proj_bias.data = _t(W[p + "qkv.b"])
+    lay.self_attn.out_proj.weight.data = _t(W[p + "out.w"]); lay.self_attn.out_proj.bias.data = _t(W[p + "out.b"])
+    lay.linear1.weight.data = _t(W[p + "ffn1.w"]); lay.linear1.bias.data = _t(W[p + "ffn1.b"])
+    lay.linear2.weight.data = _t(W[p + "ffn2.w"]); lay.linear2.bias.data = _t(W[p + "ffn2.b"])
+    _set_ln(lay.norm1, W, p + "attn_ln"); _set_ln(lay.norm2, W, p + "ffn_ln")
+    return lay
+
+
+# DLCL weight rows W^{(m)}, m = 1..L+1 (L = 2), written out by hand
+_DLCL_CASES = {
+    # W^{(l+1)} = 1/(l+1) . 1  ->  x_{l+1} = mean of z_0..z_l (SURVEY §8(c) DLCL pins)
+    "uniform_mean": [[1.0], [0.5, 0.5], [1 / 3, 1 / 3, 1 / 3]],
+    # the [.5, .25, .25] hand sum for the encoder top: x_3 = .5 z_0 + .25 z_1 + .25 z_2
+    "hand_sum": [[0.75], [0.3, 0.7], [0.5, 0.25, 0.25]],
+    # reading A22 (ii): one-hot W^{(l+1)} = e_l with the Eq.-2 LN ON == the plain pre-norm
+    # stack with an explicit LN^dl_l inserted after every layer (and before the final LN)
+    "one_hot_ln_on": [[1.0], [0.0, 1.0], [0.0, 0.0, 1.0]],
+}
+
+
+@pytest.mark.parametrize("case", sorted(_DLCL_CASES))
+def test_dlcl_eq2_against_torch_layers(case):
+    """Eq. 1-2: z_k = LN^dl_k(y_k), x_{l+1} = sum_{k<=l} W^{(l+1)}_k z_k,
+    enc = LN^enc(sum_k W^{(L+1)}_k z_k), evaluated here step by step with torch layers and
+    F.layer_norm on hand-written weight rows (zero RPR tables so the layers are the textbook
+    pre-norm TransformerEncoderLayer)."""
+    cfg = TINY  # L = 2, DLCL on, dlcl_ln on
+    rows = _DLCL_CASES[case]
+    W = _zero_rpr({k: v.astype(np.float64) for k, v in generate_weights(cfg).items()})
+    W["enc.dlcl.w"] = np.concatenate([np.array(r, dtype=np.float64) for r in rows])
+    src = [17, 400, 5, 999, 23, 3]
+    d = cfg.d_model
+    ln = lambda x, name: torch.nn.functional.layer_norm(x, (d,), _t(W[name + ".g"]), _t(W[name + ".b"]),
+                                                        cfg.ln_eps)
+    y = _t(W["emb"][src] * math.sqrt(d) + sinusoid_pe(len(src), d)).unsqueeze(0)
+    zs = [ln(y, "enc.dlcl.ln.0")]
+    x = rows[0][0] * zs[0]
+    with torch.no_grad():
+        for l in range(cfg.enc_layers):
+            y = _torch_layer(W, cfg, l)(x)
+            zs.append(ln(y, f"enc.dlcl.ln.{l + 1}"))
+            x = sum(wk * zk for wk, zk in zip(rows[l + 1], zs))
+    ref = ln(x[0], "enc.final_ln").numpy()
+    got = OracleModel(W, cfg).encode_def(src)
+    np.testing.assert_allclose(got, ref, rtol=1e-10, atol=1e-10)
+    if case == "uniform_mean":   # the combination really is the mean of the z_k
+        np.testing.assert_allclose(x.numpy(), (sum(zs) / 3).numpy(), rtol=1e-14, atol=1e-14)
+    if case == "one_hot_ln_on":
+        # == plain stack with LN^dl between layers (no DLCL weights anywhere)
+        with torch.no_grad():
+            h = ln(_t(W["emb"][src] * math.sqrt(d) + sinusoid_pe(len(src), d)).unsqueeze(0), "enc.dlcl.ln.0")
+            for l in range(cfg.enc_layers):
+                h = ln(_torch_layer(W, cfg, l)(h), f"enc.dlcl.ln.{l + 1}")
+        np.testing.assert_allclose(got, ln(h[0], "enc.final_ln").numpy(), rtol=1e-10, atol=1e-10)

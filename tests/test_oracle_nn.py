@@ -114,3 +114,59 @@ def test_rpr_single_token_closed_form():
     ak, av = r.normal(size=(17, 8)), r.normal(size=(17, 8))
     got = rpr_attention_loops(q, k, v, ak, av, H, 8, lambda i, j: (True, i))
     np.testing.assert_allclose(got[0], v[0] + np.tile(av[8], H), rtol=1e-14)  # o = v_0 + A^V[k]
+
+
+def test_rpr_direction_hand_example():
+    """Shaw et al. (cited at PAPER.md:23): a^K_ij = w^K_clip(j-i, k), e_ij = q_i.(k_j + a^K_ij)/sqrt(dz),
+    o_i = sum_j a_ij (v_j + a^V_ij).  Hand example with an ASYMMETRIC table, so a swapped
+    clip(i-j) gather fails: n = 3, k = 1, H = 1, dh = 2, q_i = e_0, k_j = v_j = 0,
+    A^K[r] = (r - k) e_0  ->  e_ij = clip(j-i, -1, 1)/sqrt(2);
+    A^V = [[1, 0], [0, 1], [1, 1]] (bucket of distance -1, 0, +1)."""
+    s = 1.0 / math.sqrt(2.0)
+    q = np.array([[1.0, 0.0]] * 3)
+    z = np.zeros((3, 2))
+    ak = np.array([[-1.0, 0.0], [0.0, 0.0], [1.0, 0.0]])
+    av = np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])
+    got = rpr_attention_loops(q, z, z, ak, av, 1, 1, lambda i, j: (True, i))
+    E = math.exp(s)
+    Ei = math.exp(-s)
+    # i = 0: distances 0, +1, +2 -> buckets 1, 2, 2; logits 0, s, s
+    o0 = (1.0 * av[1] + 2 * E * av[2]) / (1.0 + 2 * E)
+    # i = 1: distances -1, 0, +1 -> buckets 0, 1, 2; logits -s, 0, s
+    o1 = (Ei * av[0] + 1.0 * av[1] + E * av[2]) / (Ei + 1.0 + E)
+    # i = 2: distances -2, -1, 0 -> buckets 0, 0, 1; logits -s, -s, 0
+    o2 = (2 * Ei * av[0] + 1.0 * av[1]) / (2 * Ei + 1.0)
+    np.testing.assert_allclose(got, np.array([o0, o1, o2]), rtol=1e-14, atol=1e-15)
+    # the causal (decoder) mask keeps only j <= i: row 2 is unchanged, row 0 = A^V[k]
+    got_c = rpr_attention_loops(q, z, z, ak, av, 1, 1, lambda i, j: (j <= i, i))
+    np.testing.assert_allclose(got_c[0], av[1], rtol=1e-15)
+    np.testing.assert_allclose(got_c[2], o2, rtol=1e-14)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_rpr_unclipped_linear_tables_are_shifted_vanilla(causal):
+    """Unclipped case (k >= n-1: every distance j-i has its own bucket j-i+k).  With tables
+    linear in the distance, A^K[r] = (r-k) u and A^V[r] = (r-k) w:
+      e_ij = q_i.(k_j + j u)/sqrt(dh) - i q_i.u/sqrt(dh)   (the last term is constant in j:
+                                                           softmax ignores it)
+      o_i  = sum_j a_ij (v_j + j w) - i w.
+    So RPR == torch scaled_dot_product_attention on keys k_j + j u, values v_j + j w, minus
+    i w — a library routine pin that fixes both the direction j - i and the bucket offset."""
+    r = np.random.default_rng(8)
+    n, d, H, kc = 9, 32, 4, 8
+    dh = d // H
+    q, k, v = (r.normal(size=(n, d)) for _ in range(3))
+    u, w = r.normal(size=dh) * 0.3, r.normal(size=dh)
+    dist = np.arange(2 * kc + 1) - kc
+    ak, av = dist[:, None] * u[None, :], dist[:, None] * w[None, :]
+    mask = np.tril(np.ones((n, n), bool)) if causal else np.ones((n, n), bool)
+    got = rpr_attention_loops(q, k, v, ak, av, H, kc, lambda i, j: (bool(mask[i, j]), i))
+    pos = np.arange(n)[:, None]
+    ks = k + pos * np.tile(u, H)
+    vs = v + pos * np.tile(w, H)
+    ref = _sdpa(q, ks, vs, H, mask) - pos * np.tile(w, H)
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-11)
+    # with a clip (k = 2 < n - 1) the same tables are NOT the shifted vanilla attention
+    got2 = rpr_attention_loops(q, k, v, ak[kc - 2:kc + 3], av[kc - 2:kc + 3], H, 2,
+                               lambda i, j: (bool(mask[i, j]), i))
+    assert np.abs(got2 - ref).max() > 1e-3
