@@ -228,7 +228,8 @@ def main():
     from paper_2109_08008_b200 import Model
     from paper_2109_08008_b200.dist import chunk_index
 
-    model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents)
+    model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents,
+                  workspaces=args.workers)
     # a non-default stream: decode steps are replayed as CUDA graphs (no capture on stream 0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)

@@ -63,24 +63,47 @@ typedef struct {
   float ln_eps;                   /* 1e-5 (reading R10)                                      */
 } nmt_config;
 
-/* Sizes the arena is allocated for (nmt_load_weights). */
+/* Sizes the arenas are allocated for (nmt_load_weights) — the paper's memory pool
+ * (PAPER.md:143, :154): every device buffer of the path is carved from these arenas at load. */
 typedef struct {
   int32_t max_tokens;   /* padded source tokens per batch: n_sent * s_max <= max_tokens          */
   int32_t max_sents;    /* sentences per batch (PAPER.md:138 uses 512)                           */
   int32_t max_tgt_len;  /* <= config max_tgt_len; decode steps per batch                          */
   int32_t beam;         /* 1 = greedy                                                              */
+  int32_t n_workspaces; /* arenas allocated at load (0 or 1 = one): the upper bound of
+                           nmt_translate_opts.n_workers (concurrent batch workers)                 */
 } nmt_limits;
 
 typedef struct nmt_model nmt_model;   /* opaque: device weights + arena */
 typedef struct nmt_batch nmt_batch;   /* opaque: one encoded batch living in the model's arena */
 
-/* Load an NTSD blob (host memory, `nbytes`): magic "NTSD", version 1, config block,
- * named tensors (FP16 or FP32).  Weights are converted to `prec` on the device.
- * Errors: NMT_E_FORMAT, NMT_E_INTEGRITY (no partial model is returned), NMT_E_RESOURCE. */
+/* Load an NTSD blob (host memory, `nbytes`; "stored in FP16").
+ * Two versions are read (all little endian):
+ *   v1 — the SPEC checkpoint layout: "NTSD" | u32 1 | 8 x u32 config (enc_layers,
+ *        dec_layers, d_model, n_heads, d_ffn, vocab_size, max_rel_pos, flags: bit0 use_dlcl,
+ *        bit1 shared_emb — must be set: the embedding is tied) | u32 n_tensors |
+ *        per tensor {u16 name_len, name, u8 rank, u32 dims[rank], u8 dtype (0 F32, 1 F16),
+ *        payload inline}.  Fields v1 lacks take the DESIGN.md readings: use_rpr =
+ *        (max_rel_pos > 0), dlcl_ln 1, max_src_len 120, max_tgt_len 200, max_pos 1024,
+ *        ids PAD 0 / UNK 1 / BOS 2 / EOS 3, ln_eps 1e-5.
+ *   v2 — this build's extended layout: "NTSD" | u32 2 | u32 72 | nmt_config | u32 n |
+ *        per tensor {u16 name_len, name, u8 dtype, u8 rank, u32 dims, u64 offset, u64 nbytes}
+ *        | aligned payloads.
+ * Tensor names are the canonical names of DESIGN.md / SURVEY Appendix B.  Weights are
+ * converted to `prec` on the device; every arena (limits->n_workspaces) is allocated here.
+ * Errors: NMT_E_FORMAT (magic, version, flags), NMT_E_INTEGRITY (missing / duplicate /
+ * mis-shaped tensor, truncated blob, offsets outside the blob; no partial model is
+ * returned), NMT_E_RESOURCE (device allocation). */
 nmt_status nmt_load_weights(const void* h_ntsd, size_t nbytes, int device, nmt_precision prec,
                             const nmt_limits* lim, nmt_model** out);
 nmt_status nmt_get_config(const nmt_model* m, nmt_config* out);
 void nmt_free_model(nmt_model* m);
+
+/* Parse and validate an NTSD blob on the host only (no device work): the same checks as
+ * nmt_load_weights up to the device upload.  *h_n_tensors (may be NULL) receives the
+ * tensor count, *h_version (may be NULL) the format version. */
+nmt_status nmt_ntsd_inspect(const void* h_ntsd, size_t nbytes, nmt_config* out,
+                            int64_t* h_n_tensors, int32_t* h_version);
 
 /* Encode one batch (encoder output and per-decoder-layer cross K/V
  * are computed once here and cached).
@@ -102,10 +125,18 @@ nmt_status nmt_encode(nmt_model* m, const int32_t* d_src, const int32_t* h_src_l
 nmt_status nmt_batch_encoder_output(const nmt_batch* b, float* d_dst, void* stream);
 
 /* Per-step outputs; every pointer optional (NULL = not written). Sizes are n_live rows
- * of the live batch *before* this step's pruning. */
+ * of the live batch *before* this step's pruning (beam: n_live = live sentences * K). */
 typedef struct {
-  int32_t* d_next;    /* [n_live]    argmax token per live row (ties -> lowest id)   */
-  uint8_t* d_done;    /* [n_live]    row finished (EOS or cap) at or before this step */
+  int32_t* d_next;    /* [n_live]    next token per live row (greedy: argmax, ties ->
+                                     lowest id; beam: the token of the hypothesis now in
+                                     this row)                                         */
+  int32_t* d_parent;  /* [n_live]    beam: pre-step live row this hypothesis extends
+                                     (-1: row holds no continuation / sentence finished);
+                                     greedy: the row itself                             */
+  float* d_score;     /* [n_live]    beam: cumulative log-probability of the row's
+                                     hypothesis (-inf when empty); greedy: not written  */
+  uint8_t* d_done;    /* [n_live]    row finished (EOS or cap; beam: sentence search
+                                     stopped) at or before this step                    */
   float* d_logits;    /* [n_live][V] FP32 logits (parity / debug; slows the step)      */
 } nmt_step_out;
 
@@ -117,13 +148,20 @@ typedef struct {
 nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, int32_t step,
                            const nmt_step_out* out, void* stream);
 
-/* Batch pruning (reading R18): if #done >= max(1, ceil(ratio*n_live))
- * (ratio < 0: never, except when every row is done), compact the live rows stably.
+/* Batch pruning (reading R18), after a decode step.
+ *   d_keep == NULL: if #done >= max(1, ceil(ratio*n_live)) (ratio < 0: never, except when
+ *                 every row is done), compact the live rows stably, dropping done rows.
+ *   d_keep [n_live] (device, optional; greedy batches only): the caller's mask — rows with
+ *                 d_keep[r] == 0 are removed (their outputs so far are final), rows with
+ *                 d_keep[r] != 0 stay live in their order (a finished row that is kept keeps
+ *                 its sticky done flag; its tokens are ignored); `ratio` is ignored.
  *   d_new_to_old [n_live] (optional): ascending pre-prune indices of surviving rows;
  *                 entries past the new count are -1.  Unchanged identity if no prune.
- *   h_n_live (optional): new live count — synchronises the stream when non-NULL. */
-nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_new_to_old,
-                           int32_t* h_n_live, void* stream);
+ *   h_n_live (optional): new live count — synchronises the stream when non-NULL.
+ * Errors: NMT_E_STATE (no decode step since the last prune), NMT_E_UNSUPPORTED (d_keep on a
+ * beam batch).  Never allocates. */
+nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, const uint8_t* d_keep,
+                           int32_t* d_new_to_old, int32_t* h_n_live, void* stream);
 
 /* Number of live rows (synchronises the stream). */
 nmt_status nmt_batch_live(nmt_batch* b, int32_t* h_n_live, void* stream);
@@ -131,6 +169,11 @@ nmt_status nmt_batch_live(nmt_batch* b, int32_t* h_n_live, void* stream);
 /* Results in batch order (synchronous): h_ids [n_sent][max_tgt_len] generated tokens
  * (EOS included when produced), h_len [n_sent] generated counts. */
 nmt_status nmt_batch_results(nmt_batch* b, int32_t* h_ids, int32_t* h_len, void* stream);
+
+/* Release a batch: its arena becomes free for the next nmt_encode (no device call, no
+ * free — the arena belongs to the model).  NULL is a no-op; a released or superseded batch
+ * handle is rejected by every other call with NMT_E_ARG. */
+void nmt_batch_free(nmt_batch* b);
 
 typedef struct {
   int32_t max_tokens;    /* dynamic-batch token budget, <= limits */
@@ -148,7 +191,12 @@ typedef struct {
 
 typedef struct {
   int64_t sentences, src_tokens, gen_tokens, out_tokens, decode_steps, prunes, batches, launches;
-  double ms_total;
+  int64_t truncated;            /* sources cut to max_src_len - 1 tokens + EOS (translate only) */
+  int64_t arena_system_allocs;  /* cudaMalloc / cudaMallocHost calls of the model since load
+                                   (weights + every arena); flat across translate calls      */
+  double ms_total;              /* host wall time of the call                                 */
+  double ms_encode, ms_decode;  /* device time (CUDA events on each worker's stream) summed
+                                   over batches: encoder + cross K/V, and the decode loop     */
 } nmt_stats;
 
 /* Whole translation with HOST buffers (synchronous): length sort, dynamic batches,
@@ -156,7 +204,11 @@ typedef struct {
  * with the terminating EOS stripped.
  *   h_ids [h_off[n]] int32 flat EOS-terminated sources, h_off [n+1] int64.
  *   h_out [out_cap] receives the flat outputs, h_out_off [n+1] their offsets.
- * Sources longer than max_src_len are rejected (NMT_E_INPUT). */
+ * Sources longer than min(max_src_len, max_tokens) are truncated to that many tokens with
+ * EOS last ("maximum length ... 120"; counted in stats->truncated) — a batch
+ * pipeline never aborts on one long line; empty sources (len 0) are NMT_E_INPUT.
+ * opts->n_workers must not exceed limits.n_workspaces (NMT_E_ARG): no arena is allocated
+ * here. */
 nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
                          const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
                          int64_t* h_out_off, nmt_stats* stats, void* stream);

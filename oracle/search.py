@@ -75,8 +75,10 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
     """Greedy translation of a Workload; returns list of outputs in input order.
 
     ``log`` (optional dict) receives 'prunes': [(batch, step, new_to_old)],
-    'gen_tokens', 'steps', 'batches', and 'margins': per sentence, the top1 - top2
-    logit gap at every generated position (which positions are margin-safe).
+    'gen_tokens', 'steps', 'batches', 'margins': per sentence, the top1 - top2
+    logit gap at every generated position (which positions are margin-safe), and
+    'scales': per sentence, max |logit| at every generated position (the FP32
+    tolerance scale).  Logging only: no effect on the outputs.
     """
     cfg = model.cfg
     lens = wl.lengths()
@@ -84,6 +86,7 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
     outputs = [None] * wl.n
     prunes = []
     margins = [None] * wl.n
+    scales = [None] * wl.n
     gen_tokens = 0
     steps = 0
     for bi, idx in enumerate(batches):
@@ -98,6 +101,7 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
         done = np.zeros(B, dtype=bool)
         gen = [[] for _ in range(B)]
         gaps = [[] for _ in range(B)]
+        scl = [[] for _ in range(B)]
         t = 0
         while True:
             logits = model.decoder_step(tok, t, cache, ckv, src_len)
@@ -107,6 +111,7 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
                 if not done[r]:
                     gen[s].append(int(nxt[r]))
                     gaps[s].append(float(top2[r, 1] - top2[r, 0]))
+                    scl[s].append(float(np.abs(logits[r]).max()))
                     if nxt[r] == EOS_ID or len(gen[s]) == caps[s]:
                         done[r] = True
             tok = nxt
@@ -127,8 +132,10 @@ def translate_fast(model, wl, max_tokens: int = 4096, max_sents: int = 512,
             gen_tokens += len(g)
             outputs[i] = g[:-1] if g and g[-1] == EOS_ID else g
             margins[i] = gaps[s]
+            scales[i] = scl[s]
     if log is not None:
-        log.update(prunes=prunes, gen_tokens=gen_tokens, steps=steps, batches=batches, margins=margins)
+        log.update(prunes=prunes, gen_tokens=gen_tokens, steps=steps, batches=batches, margins=margins,
+                   scales=scales)
     return outputs
 
 

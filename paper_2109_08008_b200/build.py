@@ -9,6 +9,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -17,7 +18,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas=-v"]
+         "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas=-v"]
+OBJ = os.path.join(HERE, "build")
 
 
 def sources():
@@ -39,17 +41,34 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC] + FLAGS + ["-I", INCLUDE, "-o", tmp] + sources()
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-    if r.returncode != 0:
+    # one nvcc per translation unit in parallel, then one link (no relocatable device code:
+    # kernels are launched only from host code in their own file)
+    os.makedirs(OBJ, exist_ok=True)
+    srcs = sources()
+
+    def cc(src):
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        r = subprocess.run([NVCC] + FLAGS + ["-I", INCLUDE, "-c", "-o", obj, src],
+                           capture_output=True, text=True)
+        return obj, r
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        res = list(ex.map(cc, srcs))
+    errs = "".join(r.stdout + r.stderr for _, r in res)
+    if verbose or any(r.returncode != 0 for _, r in res):
+        sys.stderr.write(errs)
+    if any(r.returncode != 0 for _, r in res):
         raise RuntimeError("nvcc failed building libnmt.so")
+    tmp = LIB + ".tmp"
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] +
+                       [o for o, _ in res] , capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed linking libnmt.so")
     os.replace(tmp, LIB)
     log = os.path.join(HERE, "build_ptxas.log")
     with open(log, "w") as f:
-        f.write(r.stderr)
+        f.write(errs)
     return LIB
 
 

@@ -238,12 +238,13 @@ void launch_enc(const T* qkv, const int* len, const T* relk, const T* relv, T* o
   size_t fl = 2 * S * (DH + 1) + S * DH + R * (DH + 1) + R * DH + S * (R + 1) + S * (S + 1) +
               S * (R + 1);
   size_t smem = fl * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  // thread-safe one-time attribute setup (C++11 static initialisation)
+  static const bool attr = [&] {
     NMT_CUDA(cudaFuncSetAttribute(k_attn_enc<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   k_attn_enc<T, DH><<<dim3(B, H), 256, smem, s>>>(qkv, len, relk, relv, out, S, d, kclip, use_rpr);
   NMT_LAUNCH_CHECK();
 }

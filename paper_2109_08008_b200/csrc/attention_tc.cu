@@ -602,12 +602,12 @@ EncTmaCfg enc_tma_cfg() {
 }
 
 int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
+  static const int n = [] {
+    int dev = 0, c = 0;
     NMT_CUDA(cudaGetDevice(&dev));
-    NMT_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
+    NMT_CUDA(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev));
+    return c;
+  }();
   return n;
 }
 
@@ -640,12 +640,13 @@ template <int DH, int NT>
 void launch_nt(const __half* qkv, const int* len, const __half* relk, const __half* relv,
                __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
   using L = EncSmem<DH, NT>;
-  static bool attr = false;
-  if (!attr) {
+  // thread-safe one-time attribute setup (C++11 static initialisation)
+  static const bool attr = [&] {
     NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tc<DH, NT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   // one warp per 16-query block up to 4: short sentences do not hold idle warps
   constexpr int threads = 32 * (NT / 2 < 4 ? NT / 2 : 4);
   k_attn_enc_tc<DH, NT><<<dim3(B, H), threads, L::BYTES, s>>>(qkv, len, relk, relv, out, S, d,

@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(128) k_beam_select(
     const int* __restrict__ cap, int* __restrict__ anc, int* __restrict__ htok, int Tmax,
     float* __restrict__ best_score, int* __restrict__ out_tok, int* __restrict__ gen_len,
     DevState* st, int V, int eos, int NB, float* __restrict__ nb_score,
-    int* __restrict__ nb_len, int* __restrict__ nb_tok, int* __restrict__ nb_cnt) {
+    int* __restrict__ nb_len, int* __restrict__ nb_tok, int* __restrict__ nb_cnt,
+    int* __restrict__ parent_out) {
   extern __shared__ int sm_i[];
   constexpr int KB = 2 * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -193,7 +194,10 @@ __global__ void __launch_bounds__(128) k_beam_select(
   const int n_live = st->n_live;
   if (grp * K >= n_live) return;
   const int r0 = grp * K;
-  if (done[r0]) return;  // finished sentence waiting to be pruned
+  if (done[r0]) {  // finished sentence waiting to be pruned
+    if (parent_out && lane < K) parent_out[r0 + lane] = -1;
+    return;
+  }
   const int t = st->t;
   const int sent = row_slot[r0] / K;
   int* s_anc = sm_i + warp * 2 * K * (Tmax + 1);
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(128) k_beam_select(
     __syncwarp();
   }
   if (sdone) {
+    if (parent_out && lane < K) parent_out[r0 + lane] = -1;
     if (lane < K) done[r0 + lane] = 1;
     if (lane == 0) atomicAdd(&st->n_done, K);
     return;
@@ -335,10 +340,12 @@ __global__ void __launch_bounds__(128) k_beam_select(
         if (t + 1 < Tmax) htok[(size_t)slot * Tmax + t + 1] = s_new[warp][i].tok;
         prev_tok[r] = s_new[warp][i].tok;
         score[r] = s_new[warp][i].v;
+        if (parent_out) parent_out[r] = r0 + s_new[warp][i].k;
       }
     } else if (lane == 0) {
       score[r] = -INFINITY;  // fewer than K continuations (tiny vocabularies)
       prev_tok[r] = eos;
+      if (parent_out) parent_out[r] = -1;
     }
   }
 }
@@ -355,7 +362,7 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
                  uint8_t* done, const int* row_slot, const int* cap, int* anc, int* htok,
                  int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st, int V,
                  int eos, int rows_upper, cudaStream_t s, int NB, float* nb_score, int* nb_len,
-                 int* nb_tok, int* nb_cnt) {
+                 int* nb_tok, int* nb_cnt, int* parent_out) {
   if (rows_upper <= 0) return;
   if (NB < 1 || NB > K) throw CudaError("beam_select: nbest must be in [1, beam]");
   const int groups = (rows_upper + K - 1) / K, nw = 4;
@@ -363,7 +370,7 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
 #define NMT_BS(KK)                                                                            \
   k_beam_select<KK><<<ceil_div(groups, nw), nw * 32, smem, s>>>(                              \
       cand_v, cand_i, score, prev_tok, done, row_slot, cap, anc, htok, Tmax, best_score,       \
-      out_tok, gen_len, st, V, eos, NB, nb_score, nb_len, nb_tok, nb_cnt)
+      out_tok, gen_len, st, V, eos, NB, nb_score, nb_len, nb_tok, nb_cnt, parent_out)
   switch (K) {
     case 1: NMT_BS(1); break;
     case 2: NMT_BS(2); break;

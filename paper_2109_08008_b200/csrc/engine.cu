@@ -168,11 +168,14 @@ void init_arena(nmt_model* m) {
   NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
               std::string("arena cudaMalloc failed: ") + cudaGetErrorString(e));
   a.cap = a.used;
+  m->sys_allocs += 1;
   for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
   NMT_CUDA(cudaMemset(a.base, 0, a.used));
+  for (auto& ev : m->ev_t) NMT_CUDA(cudaEventCreate(&ev));
   // pinned host staging (each region rounded to 64 B)
   size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 + 16 * 64;
   NMT_CUDA(cudaMallocHost(&m->pinned, pb));
+  m->sys_allocs += 1;
   char* p = (char*)m->pinned;
   auto take = [&](size_t b) { char* r = p; p += (b + 63) & ~size_t(63); return r; };
   m->hp.boff = (long long*)take(Bm * 8);
@@ -199,6 +202,7 @@ void fold_weights(nmt_model* m) {
   cudaError_t e = cudaMalloc(&m->foldbuf, wbytes + cbytes + bbytes + 1024);
   NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
               std::string("fold cudaMalloc failed: ") + cudaGetErrorString(e));
+  m->sys_allocs += 1;
   char* wp = (char*)m->foldbuf;
   float* cp = (float*)(wp + wbytes);
   char* bp = (char*)(cp + rows) + 256;
@@ -271,48 +275,125 @@ void bind_weights(nmt_model* m) {
   }
 }
 
+// NTSD parsing (host only; shared by nmt_load_weights and nmt_ntsd_inspect).  Every size
+// check is written so that no sum can wrap (a crafted blob must fail with NMT_E_INTEGRITY).
+struct Parsed {
+  nmt_config cfg{};
+  int version = 0;
+  std::unordered_map<std::string, TensorRec> recs;
+};
+
+void set_defaults(nmt_config& c) {   // fields the SPEC's v1 block does not carry
+  c.dlcl_ln = 1;
+  c.max_src_len = 120;
+  c.max_tgt_len = 200;
+  c.max_pos = 1024;
+  c.pad_id = 0; c.unk_id = 1; c.bos_id = 2; c.eos_id = 3;
+  c.ln_eps = 1e-5f;
+}
+
+Parsed parse_blob(const void* blob, size_t nbytes) {
+  NMT_REQUIRE(blob, NMT_E_ARG, "null blob");
+  Parsed P;
+  const uint8_t* p = (const uint8_t*)blob;
+  const uint8_t* end = p + nbytes;
+  NMT_REQUIRE(nbytes >= 8 && memcmp(p, "NTSD", 4) == 0, NMT_E_FORMAT, "NTSD: bad magic");
+  p += 4;
+  const uint32_t ver = rd<uint32_t>(p, end);
+  NMT_REQUIRE(ver == 1 || ver == 2, NMT_E_FORMAT, "NTSD: unsupported version " + std::to_string(ver));
+  P.version = (int)ver;
+  nmt_config& cfg = P.cfg;
+  if (ver == 1) {   // SPEC layout: 8 x u32 config, inline payloads
+    uint32_t v[8];
+    for (auto& x : v) x = rd<uint32_t>(p, end);
+    NMT_REQUIRE((v[7] & ~3u) == 0, NMT_E_FORMAT, "NTSD v1: unknown flag bits");
+    NMT_REQUIRE(v[7] & 2u, NMT_E_UNSUPPORTED, "NTSD v1: untied embeddings (shared_emb = 0) not built");
+    for (int i = 0; i < 7; ++i)
+      NMT_REQUIRE(v[i] <= (1u << 24), NMT_E_FORMAT, "NTSD v1: config field out of range");
+    cfg.enc_layers = (int)v[0]; cfg.dec_layers = (int)v[1]; cfg.d_model = (int)v[2];
+    cfg.n_heads = (int)v[3]; cfg.d_ffn = (int)v[4]; cfg.vocab_size = (int)v[5];
+    cfg.use_rpr = v[6] > 0;
+    cfg.max_rel_pos = v[6] > 0 ? (int)v[6] : 8;
+    cfg.use_dlcl = v[7] & 1u;
+    set_defaults(cfg);
+  } else {
+    const uint32_t cb = rd<uint32_t>(p, end);
+    NMT_REQUIRE(cb == sizeof(nmt_config), NMT_E_FORMAT, "NTSD: config block size mismatch");
+    NMT_REQUIRE((size_t)(end - p) >= cb, NMT_E_INTEGRITY, "NTSD: truncated config");
+    memcpy(&cfg, p, cb);
+    p += cb;
+  }
+  validate_config(cfg);
+  const uint32_t nt = rd<uint32_t>(p, end);
+  for (uint32_t i = 0; i < nt; ++i) {
+    TensorRec r;
+    const uint16_t nl = rd<uint16_t>(p, end);
+    NMT_REQUIRE((size_t)(end - p) >= nl, NMT_E_INTEGRITY, "NTSD: truncated name");
+    r.name.assign((const char*)p, nl);
+    p += nl;
+    uint8_t nd;
+    if (ver == 1) {
+      nd = rd<uint8_t>(p, end);
+      NMT_REQUIRE(nd <= 8, NMT_E_INTEGRITY, "NTSD: rank > 8 for " + r.name);
+      for (int k = 0; k < nd; ++k) r.dims.push_back(rd<uint32_t>(p, end));
+      r.dtype = rd<uint8_t>(p, end);
+    } else {
+      r.dtype = rd<uint8_t>(p, end);
+      nd = rd<uint8_t>(p, end);
+      NMT_REQUIRE(nd <= 8, NMT_E_INTEGRITY, "NTSD: rank > 8 for " + r.name);
+      for (int k = 0; k < nd; ++k) r.dims.push_back(rd<uint32_t>(p, end));
+    }
+    NMT_REQUIRE(r.dtype == 0 || r.dtype == 1, NMT_E_FORMAT, "NTSD: bad dtype for " + r.name);
+    // element count without overflow: every dim < 2^32, product capped at 2^40
+    uint64_t cnt = 1;
+    for (auto dd : r.dims) {
+      NMT_REQUIRE(dd == 0 || cnt <= (uint64_t(1) << 40) / dd, NMT_E_INTEGRITY,
+                  "NTSD: tensor too large: " + r.name);
+      cnt *= dd;
+    }
+    const uint64_t es = r.dtype == 1 ? 2 : 4;
+    if (ver == 1) {
+      const uint64_t nb = cnt * es;
+      NMT_REQUIRE(nb <= (uint64_t)(end - p), NMT_E_INTEGRITY, "NTSD: truncated tensor " + r.name);
+      r.data = p;
+      r.nbytes = nb;
+      p += nb;
+    } else {
+      const uint64_t off = rd<uint64_t>(p, end), nb = rd<uint64_t>(p, end);
+      // off + nb <= nbytes, written so that it cannot wrap
+      NMT_REQUIRE(nb <= nbytes && off <= nbytes - nb, NMT_E_INTEGRITY,
+                  "NTSD: tensor " + r.name + " outside the blob");
+      NMT_REQUIRE(nb == cnt * es, NMT_E_INTEGRITY, "NTSD: byte size mismatch for " + r.name);
+      r.data = (const uint8_t*)blob + off;
+      r.nbytes = nb;
+    }
+    NMT_REQUIRE(P.recs.count(r.name) == 0, NMT_E_INTEGRITY, "NTSD: duplicate tensor " + r.name);
+    P.recs.emplace(r.name, r);
+  }
+  auto can = canonical(cfg);
+  NMT_REQUIRE(P.recs.size() == can.size(), NMT_E_INTEGRITY,
+              "NTSD: expected " + std::to_string(can.size()) + " tensors, got " +
+                  std::to_string(P.recs.size()));
+  for (auto& kv : can) {
+    auto it = P.recs.find(kv.first);
+    NMT_REQUIRE(it != P.recs.end(), NMT_E_INTEGRITY, "NTSD: missing tensor " + kv.first);
+    NMT_REQUIRE(it->second.dims == kv.second, NMT_E_INTEGRITY, "NTSD: shape mismatch for " + kv.first);
+  }
+  return P;
+}
+
+nmt_model* clone_worker(nmt_model* m);
+
 nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
                 const nmt_limits* lim) {
   NMT_REQUIRE(blob && lim, NMT_E_ARG, "null blob or limits");
   NMT_REQUIRE(prec == NMT_FP16 || prec == NMT_FP32, NMT_E_ARG, "bad precision");
-  const uint8_t* p = (const uint8_t*)blob;
-  const uint8_t* end = p + nbytes;
-  NMT_REQUIRE(nbytes >= 12 && memcmp(p, "NTSD", 4) == 0, NMT_E_FORMAT, "NTSD: bad magic");
-  p += 4;
-  uint32_t ver = rd<uint32_t>(p, end);
-  NMT_REQUIRE(ver == 1, NMT_E_FORMAT, "NTSD: unsupported version " + std::to_string(ver));
-  uint32_t cb = rd<uint32_t>(p, end);
-  NMT_REQUIRE(cb == sizeof(nmt_config), NMT_E_FORMAT, "NTSD: config block size mismatch");
-  NMT_REQUIRE(p + cb <= end, NMT_E_INTEGRITY, "NTSD: truncated config");
-  nmt_config cfg;
-  memcpy(&cfg, p, cb);
-  p += cb;
-  validate_config(cfg);
-  uint32_t nt = rd<uint32_t>(p, end);
-  std::unordered_map<std::string, TensorRec> recs;
-  for (uint32_t i = 0; i < nt; ++i) {
-    TensorRec r;
-    uint16_t nl = rd<uint16_t>(p, end);
-    NMT_REQUIRE(p + nl <= end, NMT_E_INTEGRITY, "NTSD: truncated name");
-    r.name.assign((const char*)p, nl);
-    p += nl;
-    r.dtype = rd<uint8_t>(p, end);
-    uint8_t nd = rd<uint8_t>(p, end);
-    for (int k = 0; k < nd; ++k) r.dims.push_back(rd<uint32_t>(p, end));
-    uint64_t off = rd<uint64_t>(p, end), nb = rd<uint64_t>(p, end);
-    NMT_REQUIRE(r.dtype == 0 || r.dtype == 1, NMT_E_FORMAT, "NTSD: bad dtype for " + r.name);
-    NMT_REQUIRE(off + nb <= nbytes, NMT_E_INTEGRITY, "NTSD: truncated tensor " + r.name);
-    r.data = (const uint8_t*)blob + off;
-    r.nbytes = nb;
-    NMT_REQUIRE(recs.count(r.name) == 0, NMT_E_INTEGRITY, "NTSD: duplicate tensor " + r.name);
-    recs.emplace(r.name, r);
-  }
-  auto can = canonical(cfg);
-  NMT_REQUIRE(recs.size() == can.size(), NMT_E_INTEGRITY,
-              "NTSD: expected " + std::to_string(can.size()) + " tensors, got " +
-                  std::to_string(recs.size()));
+  Parsed P = parse_blob(blob, nbytes);
+  const nmt_config cfg = P.cfg;
+  auto& recs = P.recs;
   NMT_REQUIRE(lim->max_tokens >= 1 && lim->max_sents >= 1 && lim->max_tgt_len >= 1 &&
-                  lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1,
+                  lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1 &&
+                  lim->n_workspaces >= 0 && lim->n_workspaces <= 8,
               NMT_E_ARG, "bad limits");
   NMT_REQUIRE(lim->beam <= 4, NMT_E_UNSUPPORTED, "beam > 4 is not built");
   NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 16384, NMT_E_ARG, "max_sents*beam > 16384");
@@ -321,20 +402,18 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->cfg = cfg;
   m->prec = prec;
   m->lim = *lim;
+  m->lim.n_workspaces = std::max(1, lim->n_workspaces);
   m->device = device;
   m->tb = prec == NMT_FP16 ? 2 : 4;
   NMT_CUDA(cudaSetDevice(device));
+  auto can = canonical(cfg);
   size_t total = 0;
   std::vector<size_t> offs;
   for (auto& kv : can) {
     auto it = recs.find(kv.first);
     NMT_REQUIRE(it != recs.end(), NMT_E_INTEGRITY, "NTSD: missing tensor " + kv.first);
-    const TensorRec& r = it->second;
-    NMT_REQUIRE(r.dims == kv.second, NMT_E_INTEGRITY, "NTSD: shape mismatch for " + kv.first);
     size_t cnt = 1;
     for (auto dd : kv.second) cnt *= dd;
-    NMT_REQUIRE(r.nbytes == cnt * (r.dtype == 1 ? 2 : 4), NMT_E_INTEGRITY,
-                "NTSD: byte size mismatch for " + kv.first);
     offs.push_back(total);
     total += (cnt * m->tb + 255) & ~size_t(255);
   }
@@ -400,6 +479,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   cudaError_t e = cudaMalloc(&m->wbuf, total);
   NMT_REQUIRE(e == cudaSuccess, NMT_E_RESOURCE,
               std::string("weights cudaMalloc failed: ") + cudaGetErrorString(e));
+  m->sys_allocs += 1;
   NMT_CUDA(cudaMemcpy(m->wbuf, host.data(), total, cudaMemcpyHostToDevice));
   char* base = (char*)m->wbuf;
   for (size_t t = 0; t < can.size(); ++t) m->W[can[t].first] = base + offs[t];
@@ -410,6 +490,8 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   bind_weights(m.get());
   if (prec == NMT_FP16) fold_weights(m.get());
   init_arena(m.get());
+  // the remaining worker arenas of the memory pool: translate never allocates
+  for (int w = 1; w < m->lim.n_workspaces; ++w) m->workers.push_back(clone_worker(m.get()));
   NMT_CUDA(cudaDeviceSynchronize());
   return m.release();
 }
@@ -605,17 +687,16 @@ struct Plan {
 
 // Dynamic batching over length-sorted input, reading R17:
 // stable sort by (-len, index); b = min(max_sents, floor(max_tokens / len_first), rest).
-Plan plan_batches(const int64_t* h_off, int64_t n, int max_tokens, int max_sents) {
+// len = the (possibly truncated) source lengths.
+Plan plan_batches(const int* len, int64_t n, int max_tokens, int max_sents) {
   Plan p;
   p.order.resize(n);
   std::iota(p.order.begin(), p.order.end(), 0);
-  std::stable_sort(p.order.begin(), p.order.end(), [&](int a, int b) {
-    return (h_off[a + 1] - h_off[a]) > (h_off[b + 1] - h_off[b]);
-  });
+  std::stable_sort(p.order.begin(), p.order.end(), [&](int a, int b) { return len[a] > len[b]; });
   int64_t i = 0;
   while (i < n) {
     p.bstart.push_back((int)i);
-    int first = (int)(h_off[p.order[i] + 1] - h_off[p.order[i]]);
+    int first = len[p.order[i]];
     int64_t b = std::min<int64_t>({(int64_t)max_sents, std::max<int64_t>(1, max_tokens / first),
                                    n - i});
     i += b;
@@ -654,11 +735,29 @@ cudaStream_t decode_stream(nmt_model* m, cudaStream_t ws) {
   return m->dec_stream;
 }
 
+// Source lengths seen by the path: sources longer than min(max_src_len, max_tokens) are cut
+// to that length with EOS last (counted).  Empty sources are rejected.
+std::vector<int> effective_lengths(const nmt_model* m, const int64_t* h_off, int64_t n,
+                                   int max_tokens, int64_t* truncated) {
+  const int cut = std::min(m->cfg.max_src_len, max_tokens);
+  std::vector<int> len(n);
+  int64_t tr = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t l = h_off[i + 1] - h_off[i];
+    NMT_REQUIRE(l >= 1, NMT_E_INPUT, "empty source sentence " + std::to_string(i));
+    if (l > cut) ++tr;
+    len[i] = (int)std::min<int64_t>(l, cut);
+  }
+  if (truncated) *truncated = tr;
+  return len;
+}
+
 // Whole-set driver.  Batches (length-sorted plan) are taken from a shared counter by
 // `n_workers` workers, each a (model-or-clone, stream) pair on its own host thread; worker 0
-// is the model itself on the caller's stream.  load_src(wm, stream, order, B, S, lens)
-// stages the batch sources into wm->src; emit(wm, stream, order, B) consumes the results
-// and returns the batch's generated-token count.
+// is the model itself on the caller's stream; the worker arenas were allocated at load.
+// load_src(wm, stream, order, B, S, lens) stages the batch sources into wm->src (lens are the
+// effective lengths: a source with lens < its length is truncated, EOS last); emit(wm,
+// stream, order, B) consumes the results and returns the batch's generated-token count.
 template <class LoadF, class EmitF>
 void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_translate_opts* o,
                     LoadF load_src, EmitF emit, nmt_stats* st, cudaStream_t s) {
@@ -673,20 +772,20 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   NMT_REQUIRE(NB <= K, NMT_E_ARG, "nbest must be <= beam");
   NMT_REQUIRE(max_tokens <= m->lim.max_tokens && max_sents <= m->lim.max_sents, NMT_E_ARG,
               "translate opts exceed the model limits");
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t len = h_off[i + 1] - h_off[i];
-    NMT_REQUIRE(len >= 1, NMT_E_INPUT, "empty source sentence " + std::to_string(i));
-    NMT_REQUIRE(len <= m->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
-                "source " + std::to_string(i) + " longer than max_src_len");
-  }
-  while ((int)m->workers.size() < W - 1) m->workers.push_back(clone_worker(m));
-  Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+  NMT_REQUIRE(W <= 1 + (int)m->workers.size(), NMT_E_ARG,
+              "n_workers " + std::to_string(W) + " > limits.n_workspaces " +
+                  std::to_string(1 + m->workers.size()));
+  int64_t truncated = 0;
+  const std::vector<int> elen = effective_lengths(m, h_off, n, max_tokens, &truncated);
+  Plan p = plan_batches(elen.data(), n, max_tokens, max_sents);
   const int nb = (int)p.bstart.size() - 1;
   auto t0 = std::chrono::steady_clock::now();
   unsigned long long l0 = g_launches;
   std::atomic<int> next{0};
   std::atomic<int64_t> steps{0}, prunes{0}, gen{0};
   std::atomic<bool> failed{false};
+  std::mutex tmu;
+  double ms_enc = 0.0, ms_dec = 0.0;
 
   auto run = [&](nmt_model* wm, cudaStream_t ws) {
     std::vector<int> lens, caps;
@@ -694,16 +793,18 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
       const int bi = next++;
       if (bi >= nb || failed) break;
       const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
-      const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+      const int S = elen[p.order[lo]];
       lens.resize(B);
       caps.resize(B);
       for (int j = 0; j < B; ++j) {
         int sid = p.order[lo + j];
-        lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+        lens[j] = elen[sid];
         caps[j] = o && o->h_tgt_cap ? o->h_tgt_cap[sid] : wm->lim.max_tgt_len;
       }
+      NMT_CUDA(cudaEventRecord(wm->ev_t[0], ws));
       load_src(wm, ws, &p.order[lo], B, S, lens.data());
       encode_common(wm, B, S, lens.data(), caps.data(), ws, K);
+      NMT_CUDA(cudaEventRecord(wm->ev_t[1], ws));
       cudaStream_t ds = decode_stream(wm, ws);
       if (ds != ws) {   // decode after this batch's encoder, on the high-priority stream
         NMT_CUDA(cudaEventRecord(wm->ev_enc, ws));
@@ -721,7 +822,16 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
           rows = wm->hp.st->n_live;
         }
       }
+      NMT_CUDA(cudaEventRecord(wm->ev_t[2], ds));
       poll_state(wm, ds);
+      {
+        float e1 = 0.f, e2 = 0.f;
+        NMT_CUDA(cudaEventElapsedTime(&e1, wm->ev_t[0], wm->ev_t[1]));
+        NMT_CUDA(cudaEventElapsedTime(&e2, wm->ev_t[1], wm->ev_t[2]));
+        std::lock_guard<std::mutex> g(tmu);
+        ms_enc += e1;
+        ms_dec += e2;
+      }
       steps += t;
       prunes += wm->hp.st->prunes;
       b.step = t;
@@ -779,6 +889,11 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
     st->prunes = prunes;
     st->batches = nb;
     st->launches = (int64_t)(g_launches - l0);
+    st->truncated = truncated;
+    st->arena_system_allocs = m->sys_allocs;
+    for (auto* w : m->workers) st->arena_system_allocs += w->sys_allocs;
+    st->ms_encode = ms_enc;
+    st->ms_decode = ms_dec;
     st->ms_total =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -854,14 +969,18 @@ nmt_status nmt_decode_step(nmt_model* m, nmt_batch* b, const int32_t* d_prev, in
   });
 }
 
-nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, int32_t* d_new_to_old,
-                           int32_t* h_n_live, void* stream) {
+nmt_status nmt_prune_batch(nmt_model* m, nmt_batch* b, float ratio, const uint8_t* d_keep,
+                           int32_t* d_new_to_old, int32_t* h_n_live, void* stream) {
   return guard([&] {
     NMT_REQUIRE(m && b && b->valid && b->m == m, NMT_E_ARG, "null or invalid batch");
     NMT_REQUIRE(b->pending_step_done, NMT_E_STATE, "prune must follow a decode step");
+    NMT_REQUIRE(!(d_keep && b->K > 1), NMT_E_UNSUPPORTED, "d_keep is greedy-only");
     cudaStream_t s = (cudaStream_t)stream;
-    prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old, b->rows_upper,
-                  s, b->K > 1 ? m->bscore : nullptr);
+    if (d_keep)
+      prune_keep(m->st, m->row_slot, m->prev_tok, m->done, d_keep, d_new_to_old, b->rows_upper, s);
+    else
+      prune_compact(m->st, m->row_slot, m->prev_tok, m->done, 1, ratio, d_new_to_old,
+                    b->rows_upper, s, b->K > 1 ? m->bscore : nullptr);
     b->pending_step_done = false;
     b->step += 1;
     if (h_n_live) {
@@ -892,6 +1011,24 @@ nmt_status nmt_batch_results(nmt_batch* b, int32_t* h_ids, int32_t* h_len, void*
   });
 }
 
+void nmt_batch_free(nmt_batch* b) {
+  if (b) {
+    b->valid = false;
+    b->pending_step_done = false;
+  }
+}
+
+nmt_status nmt_ntsd_inspect(const void* h_ntsd, size_t nbytes, nmt_config* out,
+                            int64_t* h_n_tensors, int32_t* h_version) {
+  return guard([&] {
+    NMT_REQUIRE(out, NMT_E_ARG, "null out");
+    Parsed P = parse_blob(h_ntsd, nbytes);
+    *out = P.cfg;
+    if (h_n_tensors) *h_n_tensors = (int64_t)P.recs.size();
+    if (h_version) *h_version = P.version;
+  });
+}
+
 nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_off, int64_t n,
                          const nmt_translate_opts* opts, int32_t* h_out, int64_t out_cap,
                          int64_t* h_out_off, nmt_stats* stats, void* stream) {
@@ -905,9 +1042,11 @@ nmt_status nmt_translate(nmt_model* m, const int32_t* h_ids, const int64_t* h_of
                         const int* lens) {
       for (int j = 0; j < B; ++j) {
         const int32_t* src = h_ids + h_off[order[j]];
+        const bool cut = h_off[order[j] + 1] - h_off[order[j]] > lens[j];   // truncated
         for (int p = 0; p < S; ++p) {
           int v = p < lens[j] ? src[p] : wm->cfg.pad_id;
           NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          if (cut && p == lens[j] - 1) v = wm->cfg.eos_id;
           wm->hp.src[(size_t)j * S + p] = v;
         }
       }
@@ -959,9 +1098,11 @@ nmt_status nmt_translate_nbest(nmt_model* m, const int32_t* h_ids, const int64_t
                         const int* lens) {
       for (int j = 0; j < B; ++j) {
         const int32_t* src = h_ids + h_off[order[j]];
+        const bool cut = h_off[order[j] + 1] - h_off[order[j]] > lens[j];   // truncated
         for (int p = 0; p < S; ++p) {
           int v = p < lens[j] ? src[p] : wm->cfg.pad_id;
           NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          if (cut && p == lens[j] - 1) v = wm->cfg.eos_id;
           wm->hp.src[(size_t)j * S + p] = v;
         }
       }
@@ -1066,13 +1207,10 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
     const int sync_every = opts->sync_every > 0 ? opts->sync_every : 4;
     NMT_REQUIRE(max_tokens <= c0->lim.max_tokens && max_sents <= c0->lim.max_sents, NMT_E_ARG,
                 "translate opts exceed the model limits");
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t len = h_off[i + 1] - h_off[i];
-      NMT_REQUIRE(len >= 1 && len <= c0->cfg.max_src_len && len <= max_tokens, NMT_E_INPUT,
-                  "source " + std::to_string(i) + " empty or longer than max_src_len");
-    }
+    int64_t truncated = 0;
+    const std::vector<int> elen = effective_lengths(c0, h_off, n, max_tokens, &truncated);
     auto t0 = std::chrono::steady_clock::now();
-    Plan p = plan_batches(h_off, n, max_tokens, max_sents);
+    Plan p = plan_batches(elen.data(), n, max_tokens, max_sents);
     const int nb = (int)p.bstart.size() - 1;
     std::vector<std::vector<int>> outs((size_t)n * NB);
     std::vector<float> scores((size_t)n * NB, -INFINITY);
@@ -1083,17 +1221,19 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
     std::vector<int> lens, caps;
     for (int bi = 0; bi < nb; ++bi) {
       const int lo = p.bstart[bi], B = p.bstart[bi + 1] - lo;
-      const int S = (int)(h_off[p.order[lo] + 1] - h_off[p.order[lo]]);
+      const int S = elen[p.order[lo]];
       lens.resize(B);
       caps.resize(B);
       for (int j = 0; j < B; ++j) {
         const int sid = p.order[lo + j];
-        lens[j] = (int)(h_off[sid + 1] - h_off[sid]);
+        lens[j] = elen[sid];
         caps[j] = opts->h_tgt_cap ? opts->h_tgt_cap[sid] : Tm;
         const int32_t* src = h_ids + h_off[sid];
+        const bool cut = h_off[sid + 1] - h_off[sid] > lens[j];
         for (int q = 0; q < S; ++q) {
-          const int v = q < lens[j] ? src[q] : c0->cfg.pad_id;
+          int v = q < lens[j] ? src[q] : c0->cfg.pad_id;
           NMT_REQUIRE(v >= 0 && v < V, NMT_E_INPUT, "token id out of range");
+          if (cut && q == lens[j] - 1) v = c0->cfg.eos_id;
           c0->hp.src[(size_t)j * S + q] = v;
         }
       }
@@ -1221,6 +1361,8 @@ nmt_status nmt_translate_ensemble(nmt_ensemble* e, const int32_t* h_ids, const i
       stats->decode_steps = steps;
       stats->prunes = prunes;
       stats->batches = nb;
+      stats->truncated = truncated;
+      for (auto* c : e->members) stats->arena_system_allocs += c->sys_allocs;
       stats->ms_total = std::chrono::duration<double, std::milli>(
                             std::chrono::steady_clock::now() - t0).count();
     }
@@ -1242,11 +1384,13 @@ nmt_status nmt_translate_device(nmt_model* m, const int32_t* d_ids, const int64_
                         const int* lens) {
       for (int j = 0; j < B; ++j) {
         wm->hp.boff[j] = h_off[order[j]];
-        wm->hp.blen[j] = lens[j];
+        const bool cut = h_off[order[j] + 1] - h_off[order[j]] > lens[j];
+        wm->hp.blen[j] = cut ? -lens[j] : lens[j];   // negative: truncated, EOS last
       }
       NMT_CUDA(cudaMemcpyAsync(wm->boff, wm->hp.boff, B * 8, cudaMemcpyHostToDevice, ws));
       NMT_CUDA(cudaMemcpyAsync(wm->blen, wm->hp.blen, B * 4, cudaMemcpyHostToDevice, ws));
-      pack_sources(d_ids, wm->boff, wm->blen, B, S, wm->src, wm->cfg.vocab_size, wm->bad, ws);
+      pack_sources(d_ids, wm->boff, wm->blen, B, S, wm->src, wm->cfg.vocab_size, wm->bad,
+                   wm->cfg.eos_id, ws);
     };
     auto emit = [&](nmt_model* wm, cudaStream_t ws, const int* order, int B) -> int64_t {
       for (int j = 0; j < B; ++j) wm->hp.sent[j] = order[j];

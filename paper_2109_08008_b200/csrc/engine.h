@@ -159,7 +159,7 @@ struct nmt_model {
   std::map<std::tuple<int, int, unsigned, int>, std::pair<cudaGraphExec_t, ProfRec>> sgraphs;
   // Concurrent batch workers (the GPU analog of the paper's parallel decoding processes,
   // PAPER.md:129-131): clones sharing this model's weights, each with its own arena,
-  // stream, batch state and graphs.  Created lazily by nmt_translate*(n_workers > 1).
+  // stream, batch state and graphs.  Allocated at load (nmt_limits.n_workspaces - 1 clones).
   bool owns_weights = true;
   std::vector<nmt_model*> workers;
   cudaStream_t own_stream = nullptr;
@@ -167,7 +167,14 @@ struct nmt_model {
   // steps are scheduled ahead of the other workers' encoder kernels when SMs free up
   cudaStream_t dec_stream = nullptr;
   cudaEvent_t ev_enc = nullptr, ev_dec = nullptr;
+  // memory-pool accounting (nmt_stats.arena_system_allocs): cudaMalloc / cudaMallocHost calls
+  int64_t sys_allocs = 0;
+  // per-batch device timing of the translate loop (nmt_stats.ms_encode / ms_decode):
+  // before encode, after encode, after the decode loop
+  cudaEvent_t ev_t[3] = {nullptr, nullptr, nullptr};
   ~nmt_model() {
+    for (auto e : ev_t)
+      if (e) cudaEventDestroy(e);
     if (dec_stream) cudaStreamDestroy(dec_stream);
     if (ev_enc) cudaEventDestroy(ev_enc);
     if (ev_dec) cudaEventDestroy(ev_dec);

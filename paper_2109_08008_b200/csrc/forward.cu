@@ -244,11 +244,15 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
     GemmArgs a = vocab_args();
     a.argmax = m->keys; a.logits = out ? out->d_logits : nullptr;
     PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
-    if (finish)
+    if (finish) {
       PROF(P_BOOK, 0, 0,
            greedy_finish(m->keys, nullptr, m->prev_tok, m->done, m->row_slot, m->tgt_cap,
                          m->out_tok, Tm, m->gen_len, m->st, R, c.eos_id,
                          out ? out->d_next : nullptr, out ? out->d_done : nullptr, s));
+      if (out && out->d_parent)
+        step_outputs(m->st, m->prev_tok, nullptr, m->done, nullptr, nullptr, nullptr, R, s,
+                     out->d_parent);
+    }
     return;
   }
   // beam: FP32 logits -> per-row LSE + top-2K -> per-sentence select
@@ -265,7 +269,11 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   PROF(P_BOOK, 0, 0,
        beam_select(K, m->cand_v, m->cand_i, m->bscore, m->prev_tok, m->done, m->row_slot,
                    m->tgt_cap, m->anc, m->htok, Tm, m->best_score, m->out_tok, m->gen_len, m->st,
-                   V, c.eos_id, R, s, b->NB, m->nb_score, m->nb_len, m->nb_tok, m->nb_cnt));
+                   V, c.eos_id, R, s, b->NB, m->nb_score, m->nb_len, m->nb_tok, m->nb_cnt,
+                   out ? out->d_parent : nullptr));
+  if (out)   // step-drivable beam (nmt_step_out): next tokens, cumulative scores, done flags
+    step_outputs(m->st, m->prev_tok, m->bscore, m->done, out->d_next, out->d_score, out->d_done,
+                 R, s);
 }
 
 }  // namespace

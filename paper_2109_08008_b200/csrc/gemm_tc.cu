@@ -1023,12 +1023,12 @@ CUtensorMap out_map(const GemmArgs& a, Params& p) {
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
+  static const int n = [] {
+    int dev = 0, c = 0;
     NMT_CUDA(cudaGetDevice(&dev));
-    NMT_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
+    NMT_CUDA(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev));
+    return c;
+  }();
   return n;
 }
 
@@ -1036,12 +1036,13 @@ template <int BN, int STAGES, int EW = 8, int NSTG = 1>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
-  static bool attr = false;
-  if (!attr) {
+  // thread-safe one-time attribute setup (C++11 static initialisation)
+  static const bool attr = [&] {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   if (a.splits > 1) throw CudaError("gemm_tc: persistent kernel has no split-K (use the cluster path)");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN > 256 ? 256 : BN);
@@ -1083,12 +1084,13 @@ template <int BN, int STAGES>
 void launch_pair(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, true>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
-  static bool attr = false;
-  if (!attr) {
+  // thread-safe one-time attribute setup (C++11 static initialisation)
+  static const bool attr = [&] {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN / 2);
   Params p{};
@@ -1134,14 +1136,15 @@ void launch_cluster(const GemmArgs& a, cudaStream_t s) {
   constexpr int STAGES = 3;
   using SM = Smem<64, STAGES>;
   const int bytes = SM::BYTES;
-  static bool attr = false;
-  if (!attr) {
+  // thread-safe one-time attribute setup (C++11 static initialisation)
+  static const bool attr = [&] {
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc_cluster<STAGES>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc_cluster<STAGES>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   const int S = a.splits;
   if (((a.K + BK - 1) / BK) % S || BM % S) throw CudaError("gemm_tc: bad cluster split");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);

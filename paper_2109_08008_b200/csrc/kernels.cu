@@ -662,6 +662,86 @@ void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, in
   NMT_LAUNCH_CHECK();
 }
 
+// Caller-driven pruning (nmt_prune_batch with d_keep, greedy): rows with keep[r] == 0 leave
+// the live batch, the others stay in order with their sticky done flags.
+__global__ void __launch_bounds__(1024) k_prune_keep(DevState* st, int* row_slot, int* prev_tok,
+                                                     uint8_t* done, const uint8_t* keep,
+                                                     int* new_to_old) {
+  __shared__ int s_total, s_done;
+  const int n = st->n_live, t = st->t;
+  if (threadIdx.x == 0) s_done = 0;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(n, lo + per);
+  int r_slot[kPrunePer], r_tok[kPrunePer];
+  unsigned keepmask = 0, donemask = 0;
+  int kept = 0, kdone = 0;
+#pragma unroll
+  for (int k = 0; k < kPrunePer; ++k) {
+    const int i = lo + k;
+    if (i < hi) {
+      r_slot[k] = row_slot[i];
+      r_tok[k] = prev_tok[i];
+      if (keep[i]) {
+        keepmask |= 1u << k;
+        ++kept;
+        if (done[i]) { donemask |= 1u << k; ++kdone; }
+      }
+    }
+  }
+  const int base = block_excl_scan(kept, &s_total);
+  if (kdone) atomicAdd(&s_done, kdone);
+  __syncthreads();
+  int o = base;
+#pragma unroll
+  for (int k = 0; k < kPrunePer; ++k) {
+    if (keepmask & (1u << k)) {
+      row_slot[o] = r_slot[k];
+      prev_tok[o] = r_tok[k];
+      done[o] = (donemask >> k) & 1u;
+      if (new_to_old) new_to_old[o] = lo + k;
+      ++o;
+    }
+  }
+  __syncthreads();
+  const int nn = s_total;
+  if (new_to_old)
+    for (int i = nn + threadIdx.x; i < n; i += blockDim.x) new_to_old[i] = -1;
+  if (threadIdx.x == 0) {
+    if (nn < n) st->prunes += 1;
+    st->n_live = nn;
+    st->n_done = s_done;
+    st->t = t + 1;
+  }
+}
+
+void prune_keep(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, const uint8_t* keep,
+                int* new_to_old, int rows_upper, cudaStream_t s) {
+  if (rows_upper > kPruneMaxRows) throw CudaError("prune_keep: too many rows");
+  k_prune_keep<<<1, 1024, 0, s>>>(st, row_slot, prev_tok, done, keep, new_to_old);
+  NMT_LAUNCH_CHECK();
+}
+
+// Per-row step outputs of a beam step (nmt_step_out): next token, cumulative score, done.
+__global__ void k_step_outputs(const DevState* st, const int* prev_tok, const float* score,
+                               const uint8_t* done, int* d_next, float* d_score,
+                               uint8_t* d_done, int* d_parent_id) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= st->n_live) return;
+  if (d_next) d_next[r] = prev_tok[r];
+  if (d_score) d_score[r] = score[r];
+  if (d_done) d_done[r] = done[r];
+  if (d_parent_id) d_parent_id[r] = r;
+}
+
+void step_outputs(const DevState* st, const int* prev_tok, const float* score, const uint8_t* done,
+                  int* d_next, float* d_score, uint8_t* d_done, int rows_upper, cudaStream_t s,
+                  int* d_parent_identity) {
+  if (rows_upper <= 0 || (!d_next && !d_score && !d_done && !d_parent_identity)) return;
+  k_step_outputs<<<ceil_div(rows_upper, 128), 128, 0, s>>>(st, prev_tok, score, done, d_next,
+                                                           d_score, d_done, d_parent_identity);
+  NMT_LAUNCH_CHECK();
+}
+
 __global__ void k_batch_init(int* row_slot, int* prev_tok, uint8_t* done, int* gen_len,
                              DevState* st, int B, int S, int bos) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -708,12 +788,14 @@ void scatter_outputs(const int* out_tok, int out_stride, const int* gen_len, con
 
 __global__ void k_pack(const int* __restrict__ ids, const long long* __restrict__ boff,
                        const int* __restrict__ blen, int S, int* __restrict__ out, int vocab,
-                       int* bad) {
+                       int* bad, int eos) {
   const int b = blockIdx.x;
   const long long o = boff[b];
-  const int n = blen[b];
+  const int nb = blen[b];
+  const bool cut = nb < 0;            // truncated source: keep |blen| - 1 ids, then EOS
+  const int n = cut ? -nb : nb;
   for (int p = threadIdx.x; p < S; p += blockDim.x) {
-    int v = p < n ? ids[o + p] : 0;
+    int v = p < n ? ((cut && p == n - 1) ? eos : ids[o + p]) : 0;
     if (v < 0 || v >= vocab) {
       atomicOr(bad, 1);
       v = 0;
@@ -723,9 +805,9 @@ __global__ void k_pack(const int* __restrict__ ids, const long long* __restrict_
 }
 
 void pack_sources(const int* ids, const long long* boff, const int* blen, int B, int S, int* out,
-                  int vocab, int* bad, cudaStream_t s) {
+                  int vocab, int* bad, int eos, cudaStream_t s) {
   if (B <= 0) return;
-  k_pack<<<B, 128, 0, s>>>(ids, boff, blen, S, out, vocab, bad);
+  k_pack<<<B, 128, 0, s>>>(ids, boff, blen, S, out, vocab, bad, eos);
   NMT_LAUNCH_CHECK();
 }
 

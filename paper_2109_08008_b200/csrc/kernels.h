@@ -125,7 +125,7 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
                  int Tmax, float* best_score, int* out_tok, int* gen_len, DevState* st,
                  int V, int eos, int rows_upper, cudaStream_t s, int NB = 1,
                  float* nb_score = nullptr, int* nb_len = nullptr, int* nb_tok = nullptr,
-                 int* nb_cnt = nullptr);
+                 int* nb_cnt = nullptr, int* parent_out = nullptr);
 // Teacher ensemble (reading R26): ens[r][v] = logsumexp_m(log_softmax(logits_m[r])[v]) - log M.
 void ens_combine(const float* const* logits, int nm, int V, const int* dR, int rows_upper,
                  float* ens, cudaStream_t s);
@@ -164,6 +164,16 @@ void prune_compact(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, in
                    float ratio, int* new_to_old, int rows_upper, cudaStream_t s,
                    float* score = nullptr /* beam: per-row scores compacted alongside */);
 
+// Caller-mask compaction (nmt_prune_batch d_keep): rows with keep[r] == 0 are removed,
+// survivors keep their order and sticky done flags; n_done is recounted.  Advances st->t.
+void prune_keep(DevState* st, int* row_slot, int* prev_tok, uint8_t* done, const uint8_t* keep,
+                int* new_to_old, int rows_upper, cudaStream_t s);
+// Step outputs for rows < n_live: d_next = prev_tok, d_score = score, d_done = done (beam);
+// d_parent_identity[r] = r (greedy: every row extends itself).  Null pointers are skipped.
+void step_outputs(const DevState* st, const int* prev_tok, const float* score, const uint8_t* done,
+                  int* d_next, float* d_score, uint8_t* d_done, int rows_upper, cudaStream_t s,
+                  int* d_parent_identity = nullptr);
+
 // greedy_finish + prune_compact fused into one single-CTA launch (translate loop).
 void finish_prune(unsigned long long* keys, int* prev_tok, uint8_t* done, int* row_slot,
                   const int* cap, int* out_tok, int out_stride, int* gen_len, DevState* st,
@@ -180,8 +190,9 @@ void scatter_outputs(const int* out_tok, int out_stride, const int* gen_len, con
 
 // Pack flat EOS-terminated device sources into padded [B][S]: row b copies blen[b]
 // ids from ids + boff[b]; PAD elsewhere.  Ids outside [0, V) set *bad |= 1.
+// blen[b] < 0 marks a truncated source: |blen[b]| - 1 ids, then `eos`.
 void pack_sources(const int* ids, const long long* boff, const int* blen, int B, int S, int* out,
-                  int vocab, int* bad, cudaStream_t s);
+                  int vocab, int* bad, int eos, cudaStream_t s);
 
 // Convert a [rows][d] T buffer to FP32 (debug / parity output).
 template <class T> void to_float(const T* in, float* out, size_t n, cudaStream_t s);

@@ -27,7 +27,7 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
            "nmt_translate_ensemble", "nmt_text_load", "nmt_text_free", "nmt_text_vocab_size",
            "nmt_text_encode", "nmt_text_decode", "nmt_dev_attn_encoder",
-           "nmt_profile_steps"]
+           "nmt_profile_steps", "nmt_batch_free", "nmt_ntsd_inspect"]
 
 
 class ProfEntry(C.Structure):
@@ -47,11 +47,22 @@ class NmtError(RuntimeError):
 
 class Limits(C.Structure):
     _fields_ = [("max_tokens", C.c_int32), ("max_sents", C.c_int32), ("max_tgt_len", C.c_int32),
-                ("beam", C.c_int32)]
+                ("beam", C.c_int32), ("n_workspaces", C.c_int32)]
+
+
+class Config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "enc_layers", "dec_layers", "d_model", "n_heads", "d_ffn", "vocab_size", "max_rel_pos",
+        "use_dlcl", "use_rpr", "dlcl_ln", "max_src_len", "max_tgt_len", "max_pos", "pad_id",
+        "unk_id", "bos_id", "eos_id")] + [("ln_eps", C.c_float)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
 
 
 class StepOut(C.Structure):
-    _fields_ = [("d_next", C.c_void_p), ("d_done", C.c_void_p), ("d_logits", C.c_void_p)]
+    _fields_ = [("d_next", C.c_void_p), ("d_parent", C.c_void_p), ("d_score", C.c_void_p),
+                ("d_done", C.c_void_p), ("d_logits", C.c_void_p)]
 
 
 class TranslateOpts(C.Structure):
@@ -62,8 +73,9 @@ class TranslateOpts(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("sentences", "src_tokens", "gen_tokens", "out_tokens",
-                                         "decode_steps", "prunes", "batches", "launches")] + \
-               [("ms_total", C.c_double)]
+                                         "decode_steps", "prunes", "batches", "launches",
+                                         "truncated", "arena_system_allocs")] + \
+               [("ms_total", C.c_double), ("ms_encode", C.c_double), ("ms_decode", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -91,6 +103,16 @@ def _check(code):
         raise NmtError(code, lib().nmt_last_error().decode())
 
 
+def ntsd_inspect(blob: bytes):
+    """Host-only NTSD parse + validation (C-ABI nmt_ntsd_inspect; no device needed).
+    Returns (config dict, tensor count, version)."""
+    cfg = Config()
+    nt = C.c_int64()
+    ver = C.c_int32()
+    _check(lib().nmt_ntsd_inspect(blob, C.c_size_t(len(blob)), C.byref(cfg), C.byref(nt), C.byref(ver)))
+    return cfg.as_dict(), nt.value, ver.value
+
+
 def _ptr(t):
     return C.c_void_p(0 if t is None else t.data_ptr())
 
@@ -106,7 +128,7 @@ class Model:
 
     def __init__(self, cfg, weights: dict, precision: str = "fp16", max_tokens: int = 4096,
                  max_sents: int = 512, max_tgt_len: int | None = None, device: int = 0,
-                 beam: int = 1):
+                 beam: int = 1, workspaces: int = 1, ntsd_version=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libnmt needs a CUDA device (no CPU fallback)")
@@ -115,8 +137,8 @@ class Model:
         self.device = device
         self.V = cfg.vocab_size
         self.Tmax = max_tgt_len or cfg.max_tgt_len
-        blob = ntsd.pack(cfg, weights)
-        lim = Limits(max_tokens, max_sents, self.Tmax, beam)
+        blob = ntsd.pack(cfg, weights, version=ntsd_version)
+        lim = Limits(max_tokens, max_sents, self.Tmax, beam, workspaces)
         h = C.c_void_p()
         torch.cuda.set_device(device)
         _check(lib().nmt_load_weights(blob, C.c_size_t(len(blob)), device, self.prec, C.byref(lim),
@@ -252,29 +274,40 @@ class Batch:
         return out
 
     def decode_step(self, prev=None, logits=False, n_live=None, stream=None):
-        """One step; returns dict of CUDA tensors next / done (/ logits) for the live rows."""
+        """One step; returns dict of CUDA tensors next / parent / score / done (/ logits) for
+        the live rows (score: beam only)."""
         import torch
         rows = n_live if n_live is not None else self.live(stream)
         nxt = torch.empty(max(rows, 1), dtype=torch.int32, device="cuda")
+        par = torch.empty(max(rows, 1), dtype=torch.int32, device="cuda")
+        sc = torch.full((max(rows, 1),), float("nan"), dtype=torch.float32, device="cuda")
         done = torch.empty(max(rows, 1), dtype=torch.uint8, device="cuda")
         lg = torch.empty(max(rows, 1), self.model.V, dtype=torch.float32, device="cuda") if logits else None
-        so = StepOut(nxt.data_ptr(), done.data_ptr(), 0 if lg is None else lg.data_ptr())
+        so = StepOut(nxt.data_ptr(), par.data_ptr(), sc.data_ptr(), done.data_ptr(),
+                     0 if lg is None else lg.data_ptr())
         _check(lib().nmt_decode_step(self.model.h, self.h, _ptr(prev), self.step, C.byref(so),
                                      _stream(stream)))
-        r = {"next": nxt[:rows], "done": done[:rows]}
+        r = {"next": nxt[:rows], "parent": par[:rows], "score": sc[:rows], "done": done[:rows]}
         if lg is not None:
             r["logits"] = lg[:rows]
         return r
 
-    def prune(self, ratio=0.25, want_map=True, stream=None):
+    def prune(self, ratio=0.25, want_map=True, keep=None, stream=None):
+        """nmt_prune_batch: ratio rule, or the caller's keep mask (uint8 CUDA tensor [n_live])."""
         import torch
         rows = self.live(stream)
         m = torch.empty(max(rows, 1), dtype=torch.int32, device="cuda") if want_map else None
         n = C.c_int32()
-        _check(lib().nmt_prune_batch(self.model.h, self.h, C.c_float(ratio), _ptr(m), C.byref(n),
-                                     _stream(stream)))
+        _check(lib().nmt_prune_batch(self.model.h, self.h, C.c_float(ratio), _ptr(keep), _ptr(m),
+                                     C.byref(n), _stream(stream)))
         self.step += 1
         return n.value, (m[:rows] if m is not None else None)
+
+    def free(self):
+        """nmt_batch_free: the arena is released for the next encode; the handle is dead."""
+        if self.h:
+            lib().nmt_batch_free(self.h)
+            self.h = None
 
     def live(self, stream=None):
         n = C.c_int32()
