@@ -43,6 +43,13 @@ FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1
 # the binding roof of their algorithmic FLOPs and bytes (decoder GEMMs / vocab projection:
 # tensor-bound once the live batch exceeds ~250 rows, the ridge).
 TENSOR_CLASSES = {"enc_gemm"}
+ENC_CLASSES = {"enc_gemm", "enc_rpr_attn", "dlcl_combine", "enc_layernorm"}
+# SURVEY §8(d) whole-run roofline model of C3/C5 at the 65536 / 8192 budget (encoder GEMMs at
+# the tensor peak, DLCL and decode steps at the HBM peak, B_live shrinking under pruning):
+# 4.06M target tok/s per GPU with the measured burst peaks (1.64 PF, 6.55 TB/s), 3.71M with
+# the sustained tensor peak; at the paper's 4096 / 512 budget 3.15M.
+MODEL_TOK_S = {"65536/8192": {"burst": 4.06e6, "sustained": 3.71e6},
+               "4096/512": {"burst": 3.15e6}}
 
 
 def peaks():
@@ -129,6 +136,62 @@ def oracle_timed(cfg, W, wl, workers, max_tokens=4096, max_sents=512):
     return sum(toks), dt, len(jobs)
 
 
+def padded_tokens(lengths, max_tokens, max_sents):
+    """Padded source tokens sum(B * S) of the dynamic batch plan (reading R17):
+    stable sort by (-len, index), b = min(max_sents, max_tokens // len_first, rest)."""
+    L = np.sort(np.asarray(lengths))[::-1]
+    i, tot = 0, 0
+    while i < len(L):
+        b = min(max_sents, max(1, max_tokens // int(L[i])), len(L) - i)
+        tot += b * int(L[i])
+        i += b
+    return tot
+
+
+def enc_flops_per_token(cfg):
+    """Algorithmic encoder GEMM FLOPs per (real) source token: L x 2(4d^2 + 2dF) for the
+    layers (QKV, output, FFN1, FFN2) + Ld x 2(2d^2) for the cross K/V."""
+    d, F = cfg.d_model, cfg.d_ffn
+    return cfg.enc_layers * 2 * (4 * d * d + 2 * d * F) + cfg.dec_layers * 2 * (2 * d * d)
+
+
+def host_info():
+    """CPU model / BLAS vendor of the oracle baseline (SURVEY §8(d) asks for both)."""
+    cpu = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')}"
+    except Exception:
+        pass
+    return {"cpu_model": cpu, "blas": blas, "logical_cpus": os.cpu_count()}
+
+
+def odef_timing(cfg, W, wl, n=1, cap=4):
+    """O-def (FP64, plain loops, no cache) on n sentences with a small target cap — the
+    definitional oracle's speed, for honesty; bounded to a few seconds."""
+    from oracle import OracleModel, greedy_def
+    om = OracleModel(W, cfg)
+    t0 = time.perf_counter()
+    toks = 0
+    for i in range(n):
+        src = wl.sentence(i)[-8:]
+        out = greedy_def(om, list(src), cap)
+        toks += len(out) + (1 if len(out) < cap else 0)
+    dt = time.perf_counter() - t0
+    return {"value": toks / dt, "unit": UNIT, "sample": f"{n} sentence(s) (last 8 source tokens), "
+                                                        f"cap {cap}, FP64, 1 process, {dt:.1f} s"}
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -190,8 +253,11 @@ def main():
                     help="concurrent batch workers per GPU (own arena + stream, shared weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
+    ap.add_argument("--no-paper-tok-s", action="store_true",
+                    help="skip the tok/s run at the paper's 4096 / 512 budget")
     ap.add_argument("--ref-sents-per-worker", type=int, default=12)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-odef", action="store_true", help="skip the O-def timing of the cpu baseline")
     ap.add_argument("--no-paper-budget", action="store_true",
                     help="skip the decode-step timing at the paper's 4096 / 512 batch budget")
     ap.add_argument("--cap-clip", type=int, default=0,
@@ -213,12 +279,19 @@ def main():
     # CPU baseline first (forked NumPy workers; before CUDA is initialised)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # O-fast FP32 as it stands, the paper's CPU scheme (contiguous shards, one process
+        # per core, one BLAS thread each) with the paper's batch plan
+        # (4096 tokens / 512 sentences), on a bounded slice of the same
+        # synthetic set (the 2,998-sentence subset takes minutes: --cpu-sents-per-worker)
         workers = min(cpu_cores(), 64)
         wl = newstest_like(workers * args.cpu_sents_per_worker, cfg.vocab_size, start=900_000)
-        t, dt, used = oracle_timed(cfg, W, wl, workers, args.max_tokens, args.max_sents)
+        t, dt, used = oracle_timed(cfg, W, wl, workers, 4096, 512)
         cpu = {"value": t / dt, "unit": UNIT, "cores": used, "kind": "oracle",
                "sample": f"{wl.n} sentences (sentences 900000.. of the synthetic 1M set), "
-                         f"{used} processes x 1 BLAS thread, O-fast FP32, {dt:.1f} s"}
+                         f"{used} processes x 1 BLAS thread, O-fast FP32, batch plan 4096 / 512, "
+                         f"{dt:.1f} s", **host_info()}
+        if not args.no_odef:
+            cpu["odef"] = odef_timing(cfg, W, wl)
 
     import torch
     torch.cuda.set_device(local)
@@ -267,12 +340,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)
-    gen = steps = launches = 0
+    gen = steps = launches = sents = 0
     for k in range(args.warmup, n_chunks):
         st = dev_step(k)
         gen += st["gen_tokens"]
         steps += st["decode_steps"]
         launches += st["launches"]
+        sents += st["sentences"]
     ev1.record(stream)
     barrier()
     clocks = clk.stop()
@@ -282,6 +356,14 @@ def main():
     ms_max, gen_all = reduce_timing(ms, float(gen), device="cuda")   # max over ranks / sum
     _, steps_all = reduce_timing(ms, float(steps), device="cuda")
     value = gen_all / (ms_max / 1000.0)
+    # output tokens exclude the terminating EOS (A14): count them from the last timed chunk's
+    # device outputs (every chunk's outputs are written to d_out / d_len)
+    _, sents_all = reduce_timing(ms, float(sents), device="cuda")
+    sents_s = sents_all / (ms_max / 1000.0)
+    dl = d_len.cpu().numpy()
+    last = d_out.cpu().numpy()[np.arange(len(dl)), np.maximum(dl - 1, 0)]
+    eos_frac = float(((dl > 0) & (last == 3)).sum()) / max(1.0, float(dl.sum()))
+    out_tok_s = value * (1.0 - eos_frac)
 
     # ---- e2e through the host-buffer C-ABI call (H2D + D2H inside the timed region)
     e2e = None
@@ -334,8 +416,26 @@ def main():
     mean_step = sum(ms for _, _, ms in srec) / len(srec) if srec else None
     # the same at the paper's batch budget (C3: 4096 tokens / 512 sentences)
     paper_steps = None
+    paper_tok_s = None
     if not args.no_paper_budget:
-        pm = Model(cfg, W, precision="fp16", max_tokens=4096, max_sents=512)
+        pm = Model(cfg, W, precision="fp16", max_tokens=4096, max_sents=512, workspaces=args.workers)
+        if not args.no_paper_tok_s:
+            # whole-chunk throughput at the paper's budget (C3: 4096 tokens / 512 sentences,
+            # PAPER.md:121, :138), same chunk, same workers, device-resident (one warm run)
+            wl_p, d_ids_p = chunks[args.warmup]
+            for rep in range(2):
+                barrier()
+                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                p0.record(stream)
+                stp = pm.translate_device(d_ids_p, wl_p.off, d_out, d_len, caps=wl_p.caps,
+                                          sync_every=args.sync_every, workers=args.workers)
+                p1.record(stream)
+                barrier()
+            paper_tok_s = {"value": stp["gen_tokens"] / (p0.elapsed_time(p1) / 1e3), "unit": UNIT,
+                           "max_tokens": 4096, "max_sents": 512, "workers": args.workers,
+                           "sentences": wl_p.n, "decode_steps": stp["decode_steps"],
+                           "whole_run_frac": None}
+            paper_tok_s["whole_run_frac"] = paper_tok_s["value"] / MODEL_TOK_S["4096/512"]["burst"]
         pm.translate_device(torch.from_numpy(sub.ids).cuda(), sub.off, d_out, d_len, caps=sub.caps,
                             sync_every=args.sync_every, workers=1)   # warm (graphs)
         pm.profile(3)
@@ -347,6 +447,20 @@ def main():
         paper_steps = {"max_tokens": 4096, "max_sents": 512, "t_window": list(T_WINDOW),
                        "buckets": bucketed(prec_),
                        "mean_ms": sum(ms for _, _, ms in prec_) / len(prec_) if prec_ else None}
+    # The library counts the encoder classes' work on PADDED rows (B * S per batch); the
+    # method's algorithmic work is on real source tokens.  Scale those classes by
+    # real / padded tokens of the profiled chunk's plan (enc_gemm exactly: real tokens x
+    # enc_flops_per_token).
+    wl_prof = chunks[args.warmup][0]
+    real_tok = int(wl_prof.lengths().sum())
+    pad_tok = padded_tokens(wl_prof.lengths(), args.max_tokens, args.max_sents)
+    for k, v in prof.items():
+        if k in ENC_CLASSES:
+            v["flops_implemented"], v["bytes_implemented"] = v["flops"], v["bytes"]
+            v["flops"] = v["flops"] * real_tok / pad_tok
+            v["bytes"] = v["bytes"] * real_tok / pad_tok
+    if "enc_gemm" in prof:
+        prof["enc_gemm"]["flops"] = real_tok * enc_flops_per_token(cfg)
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     pk, src = peaks()
     # the binding roof of the class: the larger of FLOPs / tensor peak and bytes / HBM peak
@@ -372,12 +486,27 @@ def main():
         tinfo = {"traffic_algorithmic": t["algorithmic_bytes_per_launch"],
                  "traffic_source": TRAFFIC_FILE + ": " + t["source"]}
     roof.update({"frac": ach / peak, "traffic": traffic, **tinfo, "kernel": dom_name,
+                 "algorithmic": (f"real source tokens {real_tok} x {enc_flops_per_token(cfg)} FLOP "
+                                 f"(SURVEY §8(d)); padded tokens {pad_tok} not counted")
+                                if dom_name == "enc_gemm" else "library-counted",
                  "share_of_step": dom["ms"] / tot if tot else None, "peak_source": src,
                  "per_launch": {"flops" if roof["bound"] == "tensor" else "bytes":
                                 (dom["flops"] if roof["bound"] == "tensor" else dom["bytes"]) / dom["launches"],
                                 "ms": dom["ms"] / dom["launches"], "launches": dom["launches"]}})
-    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
-                   "share": round(v["ms"] / tot, 4) if tot else None} for k, v in prof.items()}
+    def class_roof(v):
+        tt = v["flops"] / (tpeak * 1e12) if v["flops"] else 0.0
+        th = v["bytes"] / (pk["hbm_gbs"] * 1e9) if v["bytes"] else 0.0
+        return ("tensor" if tt > th else "hbm"), max(tt, th)
+    kernels = {}
+    for k, v in prof.items():
+        bnd, troof = class_roof(v)
+        kernels[k] = {"ms": round(v["ms"], 3), "launches": v["launches"],
+                      "share": round(v["ms"] / tot, 4) if tot else None, "bound": bnd,
+                      "roof_ms": round(1e3 * troof, 3),
+                      "frac": round(1e3 * troof / v["ms"], 4) if v["ms"] else None,
+                      "achieved": (round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if bnd == "tensor"
+                                   else round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)),
+                      "unit": "TFLOP/s" if bnd == "tensor" else "GB/s"}
     # whole-step roofline of the profiled chunk: every kernel class at the binding roof of its
     # algorithmic FLOPs (tensor peak) and bytes (HBM peak), summed — the step time the
     # implemented algorithm would take on a perfectly fed B200 (SURVEY §8(d) "fraction of the
@@ -406,6 +535,12 @@ def main():
             "ms_per_decode_step": mean_step,
             "decode_step_ms_by_live_rows": {"t_window": list(T_WINDOW), "buckets": step_ms},
             "decode_step_ms_paper_budget": paper_steps,
+            "paper_budget_tok_s": paper_tok_s,
+            # achieved tok/s / SURVEY §8(d)'s whole-run roofline model at this budget
+            "whole_run_frac": ({k: value / v for k, v in
+                                MODEL_TOK_S[f"{args.max_tokens}/{args.max_sents}"].items()}
+                               if f"{args.max_tokens}/{args.max_sents}" in MODEL_TOK_S else None),
+            "out_tokens_per_s": out_tok_s, "sentences_per_s": sents_s,
             "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
             "step_roofline": step_roof, "kernels": kernels,
