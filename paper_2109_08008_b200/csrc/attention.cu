@@ -12,6 +12,7 @@
 // each, buckets 0 and 2k the tails j <= i-k and j >= i+k.
 #include "common.cuh"
 #include "kernels.h"
+#include "warp_attn.cuh"
 
 namespace nmt {
 
@@ -276,150 +277,6 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
 // of a dependent chain per key.  Softmax is online over chunks (running max and sum,
 // FP32, rescaled per chunk).  The RPR value term is folded per key, v_j + A^V[r(j)], which
 // is the same sum as the bucket form sum_r (sum_{j in r} a_j) A^V[r] above.
-template <class T> struct Raw8;   // 8 consecutive elements in their storage type
-template <> struct Raw8<__half> {
-  uint4 u;
-  __device__ __forceinline__ void load(const __half* p) { u = *reinterpret_cast<const uint4*>(p); }
-  __device__ __forceinline__ void store(__half* p) const { *reinterpret_cast<uint4*>(p) = u; }
-  __device__ __forceinline__ void zero() { u = make_uint4(0u, 0u, 0u, 0u); }
-  __device__ __forceinline__ void to_f(float* f) const {
-    const __half2* h = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 x = __half22float2(h[e]);
-      f[2 * e] = x.x;
-      f[2 * e + 1] = x.y;
-    }
-  }
-};
-template <> struct Raw8<float> {
-  float4 a, b;
-  __device__ __forceinline__ void load(const float* p) {
-    a = reinterpret_cast<const float4*>(p)[0];
-    b = reinterpret_cast<const float4*>(p)[1];
-  }
-  __device__ __forceinline__ void store(float* p) const {
-    reinterpret_cast<float4*>(p)[0] = a;
-    reinterpret_cast<float4*>(p)[1] = b;
-  }
-  __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ __forceinline__ void to_f(float* f) const {
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-  }
-};
-
-template <class T, int DH>
-struct WarpAttn {
-  static constexpr int G = DH / 8, KP = 32 / G;
-  static constexpr int U = sizeof(T) == 2 ? G : (G >= 2 ? G / 2 : 1);
-  static constexpr int CH = KP * U;
-  int sub, kq;
-  float q[8], m, l, acc[8];
-
-  // q (this lane's 8 channels) pre-multiplied by 1/sqrt(dh)
-  __device__ __forceinline__ void init(int lane, const T* qhead, float scale) {
-    sub = lane % G;
-    kq = lane / G;
-    Raw8<T> r;
-    r.load(qhead + sub * 8);
-    r.to_f(q);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) q[e] *= scale, acc[e] = 0.f;
-    m = -INFINITY;
-    l = 0.f;
-  }
-  // q . x over the head, x given as this lane's 8 channels (all lanes must call)
-  __device__ __forceinline__ float group_dot(const float* x) const {
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      s0 = fmaf(q[e], x[e], s0);
-      s1 = fmaf(q[e + 1], x[e + 1], s1);
-    }
-    float s = s0 + s1;
-#pragma unroll
-    for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    return s;
-  }
-  // Keys [j0, j0 + CH) with j < n (requires j0 < n).  addr(j, kp, vp) sets the head-slice
-  // pointers of key j; bias(j) is added to the scaled score; vadd(j, v) adds to v_j.
-  // Keys j < nload (>= n, readable memory) are loaded: the loads need not wait for n.
-  template <class ADDR, class BIAS, class VADD>
-  __device__ __forceinline__ void chunk(int j0, int n, int nload, ADDR addr, BIAS bias, VADD vadd) {
-    Raw8<T> kr[U], vr[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * KP + kq;
-      if (j < nload) {
-        const T *kp, *vp;
-        addr(j, kp, vp);
-        kr[u].load(kp + sub * 8);
-        vr[u].load(vp + sub * 8);
-      } else {
-        kr[u].zero();
-        vr[u].zero();
-      }
-    }
-    float s[U], cm = -INFINITY;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * KP + kq;
-      float f[8];
-      kr[u].to_f(f);
-      const float e = group_dot(f);
-      s[u] = j < n ? e + bias(j) : -INFINITY;
-      cm = fmaxf(cm, s[u]);
-    }
-#pragma unroll
-    for (int off = G; off < 32; off <<= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
-    const float mn = fmaxf(m, cm);
-    const float corr = __expf(m - mn);
-    l *= corr;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] *= corr;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * KP + kq;
-      if (j < n) {
-        const float p = __expf(s[u] - mn);
-        float f[8];
-        vr[u].to_f(f);
-        vadd(j, f);
-        l += p;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = fmaf(p, f[e], acc[e]);
-      }
-    }
-    m = mn;
-  }
-  // Sum over the KP key groups; every lane ends with the normalised output of its channels.
-  __device__ __forceinline__ void finish(float* o) {
-#pragma unroll
-    for (int off = G; off < 32; off <<= 1) {
-      l += __shfl_xor_sync(0xffffffffu, l, off);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
-    }
-    const float inv = 1.f / l;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = acc[e] * inv;
-  }
-};
-
-template <class T>
-__device__ __forceinline__ void store8(T* p, const float* o) {
-  if constexpr (sizeof(T) == 2) {
-    uint4 u;
-    __half2* h = reinterpret_cast<__half2*>(&u);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = __floats2half2_rn(o[2 * e], o[2 * e + 1]);
-    *reinterpret_cast<uint4*>(p) = u;
-  } else {
-    reinterpret_cast<float4*>(p)[0] = make_float4(o[0], o[1], o[2], o[3]);
-    reinterpret_cast<float4*>(p)[1] = make_float4(o[4], o[5], o[6], o[7]);
-  }
-}
-
 // ----------------------------------------------------------------- decoder self-attention
 // Step t = *d_t: k_t, v_t are appended to the row's cache slot and
 // positions 0..t attended; key t is taken from the fresh projection.  Only buckets

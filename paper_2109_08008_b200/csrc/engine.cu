@@ -161,6 +161,7 @@ void init_arena(nmt_model* m) {
       {(void**)&m->dlcl_p, c.use_dlcl && dlcl_lookahead_ok((int)d) ? N * d * 4 : 256},
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
+      {(void**)&m->fused_ctr, fused_counter_ints() * 4},
   };
   std::vector<size_t> offs;
   for (auto& it : items) offs.push_back(a.take(it.second));
@@ -405,6 +406,8 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->lim.n_workspaces = std::max(1, lim->n_workspaces);
   m->device = device;
   m->tb = prec == NMT_FP16 ? 2 : 4;
+  m->fuse_rows = getenv("NMT_NO_FUSE") ? -1
+                 : getenv("NMT_FUSE_ROWS") ? atoi(getenv("NMT_FUSE_ROWS")) : 1024;
   NMT_CUDA(cudaSetDevice(device));
   auto can = canonical(cfg);
   size_t total = 0;
@@ -714,6 +717,7 @@ nmt_model* clone_worker(nmt_model* m) {
   c->enc_fb = m->enc_fb; c->dec_fg = m->dec_fg; c->dec_fb = m->dec_fb;
   c->ckv_w = m->ckv_w; c->ckv_b = m->ckv_b; c->dlcl_w = m->dlcl_w; c->pe = m->pe;
   c->foldbuf = m->foldbuf; c->fold = m->fold;
+  c->fuse_rows = m->fuse_rows;
   init_arena(c.get());
   NMT_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   return c.release();

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <memory>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -13,6 +14,7 @@
 
 #include "../../include/nmt.h"
 #include "common.cuh"
+#include "decode_fused.h"
 #include "kernels.h"
 
 namespace nmt {
@@ -58,7 +60,7 @@ struct DecW {
 
 enum ProfClass {
   P_ENC_GEMM = 0, P_ENC_ATTN, P_DLCL, P_ENC_LN, P_EMBED, P_DEC_GEMM, P_VOCAB, P_DEC_SELF,
-  P_DEC_CROSS, P_DEC_LN, P_BOOK, P_NCLS
+  P_DEC_CROSS, P_DEC_LN, P_BOOK, P_DEC_FUSED, P_NCLS
 };
 extern const char* kProfNames[P_NCLS];
 
@@ -125,6 +127,11 @@ struct nmt_model {
   float* blogits = nullptr;   // [R][V] FP32 logits of the step
   float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
   float* dlcl_p = nullptr;    // [N][d] FP32 DLCL lookahead partial (kernels.h dlcl_combine)
+  int* fused_ctr = nullptr;   // fused decode step: item / completion counters (decode_fused.cu)
+  // fused decode step policy, read at load: live rows up to which one launch runs every
+  // phase (env NMT_FUSE_ROWS, default 1024); -1 = unfused step (env NMT_NO_FUSE, A/B only)
+  int fuse_rows = 1024;
+  std::unique_ptr<nmt::FusedParams> fused;   // its parameter block (built on first use)
   float* cand_v = nullptr;    // [R][2K] top log-probs per row
   int* cand_i = nullptr;      // [R][2K] their token ids
   // pinned host staging

@@ -18,13 +18,15 @@
 //   sticky done flags, outputs per slot                                               [finish]
 #include <cmath>
 
+#include "decode_fused.h"
 #include "engine.h"
+#include "tc_dev.cuh"
 
 namespace nmt {
 
 const char* kProfNames[P_NCLS] = {"enc_gemm",  "enc_rpr_attn", "dlcl_combine", "enc_layernorm",
                                   "embed",     "dec_gemm",     "vocab_argmax", "dec_self_attn",
-                                  "dec_cross_attn", "dec_layernorm", "bookkeeping"};
+                                  "dec_cross_attn", "dec_layernorm", "bookkeeping", "dec_fused"};
 
 void prof_flush(nmt_model* m) {
   auto& P = m->prof;
@@ -145,6 +147,127 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
   PROF(P_ENC_GEMM, gemm_flops(a), gemm_bytes(a, tb), gemm<T>(a, s));
 }
 
+// ---------------------------------------------------------------- fused decode step
+// Live-row threshold of the single fused launch (embedding ... final LN in one persistent
+// kernel, decode_fused.cu); above it the attention phases run as the standalone kernels
+// (more warps in flight per SM for the latency-bound KV reads) between fused GEMM segments.
+// (NMT_FUSE_ROWS / NMT_NO_FUSE are read when the model is loaded: nmt_model::fuse_rows)
+bool fused_enabled(const nmt_model* m) {
+  const nmt_config& c = m->cfg;
+  return m->fuse_rows >= 0 && m->prec == NMT_FP16 && !m->fold.empty() && m->fused_ctr &&
+         fused_supported(c.d_model, c.n_heads, c.d_ffn, c.dec_layers);
+}
+
+// Parameter block of the fused step (every buffer and weight is fixed after load): the six
+// projections of each decoder layer with the unfused path's operands, LN folding and shape
+// policy (gemm_tc.cu decode_config), their TMA descriptors over the row capacity.
+const FusedParams& fused_params(nmt_model* m) {
+  if (m->fused) return *m->fused;
+  const nmt_config& c = m->cfg;
+  const int d = c.d_model, F = c.d_ffn, Ld = c.dec_layers;
+  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
+  const int Tm = m->lim.max_tgt_len;
+  std::unique_ptr<FusedParams> P(new FusedParams());
+  memset(P.get(), 0, sizeof(FusedParams));
+  auto H = [](const void* p) { return static_cast<const __half*>(p); };
+  auto Hm = [](void* p) { return static_cast<__half*>(p); };
+  for (int l = 0; l < Ld; ++l) {
+    const DecW& w = m->dec[l];
+    const DecFold& f = m->fold[l];
+    FusedLayer& L = P->L[l];
+    auto set = [&](int slot, const void* A, int K, const void* B, int N, const void* bias,
+                   const void* R, void* C, int ldc, int relu, float2* st_out,
+                   const float2* ln_st, const float* ln_c) {
+      GemmPhase& G = L.g[slot];
+      G.N = N; G.K = K; G.relu = relu; G.ldc = ldc;
+      G.bias = H(bias); G.R = H(R); G.C = Hm(C);
+      G.st_out = st_out; G.ln_st = ln_st; G.ln_c = ln_c;
+      // decode_config: split-K 2 for K >= 2048 without LN statistics, 64-wide tiles for the
+      // d x d projections, 128-wide otherwise
+      G.split = (K >= 2048 && !st_out && !ln_st && ((K + 63) / 64) % 2 == 0) ? 1 : 0;
+      G.bn = G.split ? 64 : (N <= 512 && K <= 512) ? 64 : 128;
+      if (N % G.bn || K % 64) throw CudaError("fused decode: projection shape not tileable");
+      G.nt = N / G.bn;
+      L.ma[slot] = tc::make_map(A, Rmax, K, K, 128);
+      L.mb[slot] = tc::make_map(B, N, K, K, G.bn);
+    };
+    if (l == 0)
+      set(0, m->du, d, w.qkv_w, 3 * d, w.qkv_b, nullptr, m->dqkv, 3 * d, 0, nullptr, nullptr, nullptr);
+    else
+      set(0, m->g, d, f.qkv.w, 3 * d, f.qkv.b, nullptr, m->dqkv, 3 * d, 0, nullptr, m->lnst, f.qkv.c);
+    set(1, m->dout, d, w.so_w, d, w.so_b, m->g, m->g, d, 0, m->lnst, nullptr, nullptr);
+    set(2, m->g, d, f.cq.w, d, f.cq.b, nullptr, m->dq, d, 0, nullptr, m->lnst, f.cq.c);
+    set(3, m->dout, d, w.co_w, d, w.co_b, m->g, m->g, d, 0, m->lnst, nullptr, nullptr);
+    set(4, m->g, d, f.w1.w, F, f.w1.b, nullptr, m->dh, F, 1, nullptr, m->lnst, f.w1.c);
+    set(5, m->dh, F, w.w2, d, w.b2, m->g, m->g, d, 0, l + 1 < Ld ? m->lnst : nullptr, nullptr, nullptr);
+    L.relk = H(w.relk);
+    L.relv = H(w.relv);
+    L.kc = Hm(m->kc) + (size_t)l * Rmax * Tm * d;
+    L.vc = Hm(m->vc) + (size_t)l * Rmax * Tm * d;
+    L.koff = l * 2 * d;
+    L.voff = l * 2 * d + d;
+  }
+  P->Ld = Ld; P->Tmax = Tm; P->kclip = c.max_rel_pos; P->use_rpr = c.use_rpr;
+  P->ldkv = Ld * 2 * d;
+  P->eps = c.ln_eps; P->scale = std::sqrt((float)d);
+  P->emb = H(m->emb); P->ln0_g = H(m->dec[0].self_g); P->ln0_b = H(m->dec[0].self_b);
+  P->lnf_g = H(m->dec_fg); P->lnf_b = H(m->dec_fb); P->pe = m->pe;
+  P->g = Hm(m->g); P->u = Hm(m->du); P->qkv = Hm(m->dqkv); P->attn_out = Hm(m->dout); P->q = Hm(m->dq);
+  P->row_slot = m->row_slot; P->src_len = m->src_len; P->ckv = H(m->ckv); P->st = m->st;
+  P->ctr = m->fused_ctr;
+  m->fused = std::move(P);
+  return *m->fused;
+}
+
+// The decoder of one step (embedding ... final LN into du) through the fused kernel: one
+// launch over every phase when the live rows are few (latency-bound step), else fused GEMM
+// segments with the standalone attention kernels between them.
+template <class T>
+void decoder_fused(nmt_model* m, nmt_batch* b, const int* d_prev, cudaStream_t s) {
+  const nmt_config& c = m->cfg;
+  const int d = c.d_model, H = c.n_heads, Ld = c.dec_layers, F = c.d_ffn;
+  const int R = b->rows_upper;
+  const int Tm = m->lim.max_tgt_len;
+  const int Rmax = m->lim.max_sents * std::max(1, m->lim.beam);
+  const int nph = 2 + 8 * Ld;
+  FusedParams p = fused_params(m);
+  p.ids = d_prev ? d_prev : m->prev_tok;
+  p.beam = b->K;
+  p.anc = b->K > 1 ? m->anc : nullptr;
+  const int* dR = &m->st->n_live;
+  const int* dt = &m->st->t;
+  const double wbytes = 2.0 * ((double)Ld * (4.0 * d * d + 2.0 * d * F + 3.0 * d * d));
+  const double fl = 2.0 * R * ((double)Ld * (6.0 * d * d + 2.0 * d * F));
+  auto launch = [&](int p0, int p1, double flops, double bytes) {
+    p.pbeg = p0;
+    p.pend = p1;
+    PROF(P_DEC_FUSED, flops, bytes, decode_fused(p, d / 32, s));
+  };
+  if (R <= m->fuse_rows) {
+    launch(0, nph, fl, wbytes + 8.0 * R * d * 2);
+    return;
+  }
+  int p0 = 0;
+  for (int l = 0; l < Ld; ++l) {
+    T* kc = (T*)m->kc + (size_t)l * Rmax * Tm * d;
+    T* vc = (T*)m->vc + (size_t)l * Rmax * Tm * d;
+    const DecW& w = m->dec[l];
+    const int a1 = 1 + 8 * l + 1, a2 = 1 + 8 * l + 4;
+    launch(p0, a1, 2.0 * R * 3 * d * d, 2.0 * 3 * d * d);
+    PROF(P_DEC_SELF, 4.0 * R * (b->step + 1) * d, (2.0 * (b->step + 1) + 6) * R * d * 2,
+         attn_decoder_self<T>((const T*)m->dqkv, kc, vc, Tm, m->row_slot, (const T*)w.relk,
+                              (const T*)w.relv, (T*)m->dout, R, d, H, c.max_rel_pos, c.use_rpr, dt,
+                              dR, b->K > 1 ? m->anc : nullptr, s));
+    launch(a1 + 1, a2, 2.0 * R * 2 * d * d, 2.0 * 2 * d * d);
+    PROF(P_DEC_CROSS, 4.0 * R * b->S * d, (2.0 * b->S + 2) * R * d * 2,
+         attn_cross<T>((const T*)m->dq, (const T*)m->ckv, Ld * 2 * d, l * 2 * d, l * 2 * d + d,
+                       &m->st->S, c.max_src_len, m->src_len, m->row_slot, (T*)m->dout, R, d, H,
+                       dR, b->K, s));
+    p0 = a2 + 1;
+  }
+  launch(p0, nph, 2.0 * R * (d * d + 2.0 * d * F), 2.0 * (d * d + 2.0 * d * F));
+}
+
 template <class T>
 void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
                       cudaStream_t s, bool finish) {
@@ -161,6 +284,11 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   const double row = (double)R * d * tb;
   T *g = (T*)m->g, *du = (T*)m->du, *dqkv = (T*)m->dqkv, *dout = (T*)m->dout, *dq = (T*)m->dq,
     *dh = (T*)m->dh;
+  if (sizeof(T) == 2 && fused_enabled(m)) {
+    decoder_fused<T>(m, b, d_prev, s);   // embedding ... final LN -> du (decode_fused.cu)
+    goto vocab;
+  }
+  {
   // g = sqrt(d) E[w_t] + PE(t) fused with the first layer's pre-norm
   PROF(P_EMBED, 0, 3 * row,
        embed_dec_ln<T>(d_prev ? d_prev : m->prev_tok, cT<T>(m->emb), m->pe,
@@ -233,6 +361,8 @@ void decode_step_impl(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_s
   // row tile) would pay the folded-LN epilogue once per unit (measured +40% vocab time).
   PROF(P_DEC_LN, 0, 2 * row,
        layernorm<T>(g, d, cT<T>(m->dec_fg), cT<T>(m->dec_fb), du, d, R, d, eps, dR, s));
+  }
+vocab:
   // the tied vocab projection behind the final LN
   auto vocab_args = [&]() {
     GemmArgs v = mk(R, c.vocab_size, d, du, d, m->emb, d, nullptr, nullptr, 0);

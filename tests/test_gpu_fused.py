@@ -1,0 +1,90 @@
+"""-m gpu tests of the fused FP16 decode step (csrc/decode_fused.cu): one persistent kernel
+for embedding ... final LN (or fused GEMM segments around the standalone attention kernels
+above NMT_FUSE_ROWS live rows) must be bit-identical to the unfused 11-launch step, whose
+arithmetic it reproduces (tile shapes, split-K association, epilogue order), for greedy
+and beam search, one and six decoder layers; the oracle parity of the fused step itself
+is covered by every FP16 d = 512 test of test_gpu_parity.py / test_gpu_fullsize.py (the
+fused path is the default there)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from synth import newstest_like
+from gpu_common import weights
+
+pytestmark = pytest.mark.gpu
+
+
+def _model(name, env, **lim):
+    from paper_2109_08008_b200 import Model
+    cfg, W = weights(name)
+    old = {k: os.environ.get(k) for k in ("NMT_NO_FUSE", "NMT_FUSE_ROWS")}
+    try:
+        for k in old:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        return Model(cfg, W, precision="fp16", **lim)   # the policy is read at load
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+MODES = {"unfused": {"NMT_NO_FUSE": "1"}, "one_launch": {"NMT_FUSE_ROWS": "100000"},
+         "segments": {"NMT_FUSE_ROWS": "0"}, "default": {}}
+
+
+@pytest.mark.parametrize("name,n,lim,beam", [
+    ("student-35-1", 600, dict(max_tokens=8192, max_sents=512), 1),
+    ("student-6-1", 300, dict(max_tokens=2048, max_sents=128), 1),
+    ("teacher-30-6", 24, dict(max_tokens=1024, max_sents=16, max_tgt_len=24, beam=4), 4),
+])
+def test_fused_step_bit_identical(name, n, lim, beam):
+    wl = newstest_like(n, 32000, start=5000)
+    caps = np.minimum(wl.caps, lim.get("max_tgt_len", 200))
+    outs = {}
+    side = torch.cuda.Stream()     # graph-replayed steps (first use of a bucket runs eagerly)
+    for mode, env in MODES.items():
+        m = _model(name, env, **lim)
+        with torch.cuda.stream(side):
+            o1, st = m.translate(wl.ids, wl.off, caps=caps, beam=beam)
+            o2, _ = m.translate(wl.ids, wl.off, caps=caps, beam=beam)
+        torch.cuda.synchronize()
+        assert o1 == o2, mode
+        outs[mode] = (o1, st["gen_tokens"], st["decode_steps"])
+        del m
+    ref = outs["unfused"]
+    for mode, got in outs.items():
+        diff = [i for i in range(wl.n) if got[0][i] != ref[0][i]]
+        assert not diff, (mode, len(diff), diff[:5])
+        assert got[1:] == ref[1:], mode
+
+
+def test_fused_teacher_forced_logits_identical():
+    """Step API with teacher forcing and FP32 logits: fused and unfused steps give the same
+    logits bit for bit at every step (35-1, 40 sentences, 14 steps across the clip boundary)."""
+    from synth import random_tokens, BOS_ID
+    from gpu_common import pad_batch
+    wl = newstest_like(40, 32000, start=777)
+    srcs = [wl.sentence(i) for i in range(wl.n)]
+    src, lens = pad_batch(srcs)
+    T = 14
+    forced = np.concatenate([np.full((wl.n, 1), BOS_ID), random_tokens(wl.n, T - 1, 32000, seed=8)], 1)
+    res = {}
+    for mode in ("unfused", "one_launch", "segments"):
+        m = _model("student-35-1", MODES[mode], max_tokens=8192, max_sents=64, max_tgt_len=32)
+        b = m.encode(torch.from_numpy(src).cuda(), lens)
+        lg = []
+        for t in range(T):
+            r = b.decode_step(prev=torch.from_numpy(forced[:, t].astype(np.int32)).cuda(), logits=True,
+                              n_live=wl.n)
+            lg.append(r["logits"].cpu().numpy())
+            b.prune(ratio=-1.0, want_map=False)
+        res[mode] = np.stack(lg)
+        del m
+    assert np.array_equal(res["unfused"], res["one_launch"])
+    assert np.array_equal(res["unfused"], res["segments"])
