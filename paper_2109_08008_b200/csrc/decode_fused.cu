@@ -304,12 +304,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
     const int mt = threadIdx.x - 32 * MW0;   // 0..255
     uint32_t ng = 0;
     auto signal = [&](int p, int rb) {      // this item's outputs are visible gpu-wide
-      fence_proxy_async_global();
+      fence_proxy_async_global();           // generic-proxy stores -> later TMA (async) reads
+      __threadfence();
       asm volatile("bar.sync 1, %0;" ::"r"(32 * NMW) : "memory");
-      if (mt == 0) {
-        __threadfence();
-        atomicAdd(done + p * kMaxRB + rb, 1);
-      }
+      if (mt == 0) atomicAdd(done + p * kMaxRB + rb, 1);
     };
     for (int k = 0;; ++k) {
       const int slot = k & 1;
@@ -332,10 +330,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
         const bool row_ok = m < R;
         const int wcols = G.bn / 2;                 // columns of this warp: 32 or 64
         const int cb = hf * wcols;
-        float2 ln = make_float2(0.f, 0.f);
-        if (G.ln_st && row_ok) ln = merge_stats_cg<E>(G.ln_st + (size_t)m * (G.K / 32), P.eps);
+        // the accumulator is ready only after the producer saw this row block's inputs
+        // complete: everything this launch wrote (statistics, residual) is read after it
         mbar_wait(&S.tfull[acc], aph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float2 ln = make_float2(0.f, 0.f);
+        if (G.ln_st && row_ok) ln = merge_stats_cg<E>(G.ln_st + (size_t)m * (G.K / 32), P.eps);
         const uint32_t tb = tmem + acc * 128 + ((uint32_t)(q * 32) << 16);
         for (int c0 = cb; c0 < cb + wcols; c0 += 32) {
           float v[32];
