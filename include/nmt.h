@@ -316,6 +316,13 @@ typedef struct {
 } nmt_step_rec;
 nmt_status nmt_profile_steps(nmt_model* m, nmt_step_rec* out, int32_t cap, int32_t* n_out);
 
+/* Debug timeline of the model's last fused decode-step launch (models loaded with the
+ * environment variable NMT_FUSED_TRACE set; tools/fused_trace.py): per work item 4 x u64
+ * {phase << 40 | row block << 20 | CTA, received, inputs ready, done} (globaltimer ns) at
+ * index 4 * item, then one start time per CTA at 4 * 65536 + CTA.  Synchronises the device.
+ * NMT_E_STATE when the model was loaded without the variable. */
+nmt_status nmt_debug_fused_trace(nmt_model* m, uint64_t* h_out, int64_t cap);
+
 /* ---- kernel-level entry points used by the unit parity tests ------------------- */
 /* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision
  * (FP16: tcgen05/TMEM/TMA tensor-core GEMM; FP32: SIMT), all pointers device, row-major

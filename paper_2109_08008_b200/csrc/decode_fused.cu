@@ -59,6 +59,11 @@ __device__ __forceinline__ int gemm_slot(int p) {
   return r == 0 ? 0 : r == 2 ? 1 : r == 3 ? 2 : r == 5 ? 3 : r == 6 ? 4 : 5;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -67,15 +72,19 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Bounded spin on a completion counter (a scheduling bug traps instead of hanging the GPU).
+// Bounded spin on a completion counter (a scheduling bug traps instead of hanging the GPU):
+// tight polling first (the producer is usually a few hundred ns away), then backing off.
 __device__ __forceinline__ void wait_count(const int* c, int target) {
   if (ld_acquire(c) >= target) return;
   const long long t0 = clock64();
-  for (;;) {
-    __nanosleep(32);
+  for (uint32_t i = 1;; ++i) {
+    if (i > 256) __nanosleep(64);
     if (ld_acquire(c) >= target) return;
-    if (clock64() - t0 > 20000000000ll) __trap();
+    if ((i & 255) == 0 && clock64() - t0 > 20000000000ll) __trap();
   }
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ float2 ld_cg_f2x2(const float2* p, float2& b) {
   float4 v;
@@ -196,6 +205,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem;
   const int R = S.R, total = S.total;
+  if (P.trace && threadIdx.x == 0) P.trace[4 * 65536 + blockIdx.x] = gtimer();
   int* done = P.ctr + 2;   // [phase][row block] completion counters
 
   // item -> (phase, row block, index within the row block)
@@ -233,17 +243,21 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
         decode(item, p, rb, j);
         if (phase_kind(p, nph) != K_GEMM) continue;
         const GemmPhase& G = P.L[phase_layer(p)].g[gemm_slot(p)];
-        const CUtensorMap* ma = &P.L[phase_layer(p)].ma[gemm_slot(p)];
+        const int n0 = j * G.bn, m0 = rb * kRB;
+        // a row block with few live rows loads 32-row A boxes (rows beyond are never stored)
+        const bool small = R - m0 <= 32;
+        const CUtensorMap* ma = small ? &P.L[phase_layer(p)].ma32[gemm_slot(p)]
+                                      : &P.L[phase_layer(p)].ma[gemm_slot(p)];
         const CUtensorMap* mb = &P.L[phase_layer(p)].mb[gemm_slot(p)];
         const int kbt = G.K / BK;
         const uint32_t bbytes = (uint32_t)G.bn * BK * 2;
-        const int n0 = j * G.bn, m0 = rb * kRB;
+        const uint32_t abytes = small ? 32 * BK * 2 : A_BYTES;
         const int npre = min(kbt, NST);
         // weights first: they never depend on this launch's work
         for (int kb = 0; kb < npre; ++kb) {
           const uint32_t q = it + kb, st = q % NST;
           mbar_wait(&S.empty[st], ((q / NST) & 1) ^ 1);
-          mbar_expect_tx(&S.full[st], A_BYTES + bbytes);
+          mbar_expect_tx(&S.full[st], abytes + bbytes);
           tma_load_2d(stages + st * STAGE + A_BYTES, mb, &S.full[st], kb * BK, n0);
         }
         if (p > P.pbeg) {   // the activation rows of rb are ready (previous phase complete)
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
           const uint32_t q = it + kb, st = q % NST;
           if (kb >= npre) {
             mbar_wait(&S.empty[st], ((q / NST) & 1) ^ 1);
-            mbar_expect_tx(&S.full[st], A_BYTES + bbytes);
+            mbar_expect_tx(&S.full[st], abytes + bbytes);
             tma_load_2d(stages + st * STAGE + A_BYTES, mb, &S.full[st], kb * BK, n0);
           }
           tma_load_2d(stages + st * STAGE, ma, &S.full[st], kb * BK, m0);
@@ -303,11 +317,23 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
     const int w = warp - MW0;
     const int mt = threadIdx.x - 32 * MW0;   // 0..255
     uint32_t ng = 0;
+    unsigned long long t_recv = 0, t_ready = 0;
+    int cur_item = 0;
     auto signal = [&](int p, int rb) {      // this item's outputs are visible gpu-wide
       fence_proxy_async_global();           // generic-proxy stores -> later TMA (async) reads
-      __threadfence();
       asm volatile("bar.sync 1, %0;" ::"r"(32 * NMW) : "memory");
-      if (mt == 0) atomicAdd(done + p * kMaxRB + rb, 1);
+      if (mt == 0) {
+        // the CTA barrier orders every math thread's stores before this release (the
+        // CUTLASS generic-barrier pattern: __syncthreads, then one red.release.gpu)
+        red_release_add(done + p * kMaxRB + rb, 1);
+        if (P.trace) {   // debug timeline: (phase, rb, cta), received, inputs ready, done
+          unsigned long long* tr = P.trace + 4 * (size_t)cur_item;
+          tr[0] = ((unsigned long long)p << 40) | ((unsigned long long)rb << 20) | blockIdx.x;
+          tr[1] = t_recv;
+          tr[2] = t_ready;
+          tr[3] = gtimer();
+        }
+      }
     };
     for (int k = 0;; ++k) {
       const int slot = k & 1;
@@ -316,6 +342,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.rempty[slot]);
       if (item < 0) break;
+      if (P.trace) t_recv = gtimer();
+      cur_item = item;
       int p, rb, j;
       decode(item, p, rb, j);
       const int kind = phase_kind(p, nph);
@@ -334,6 +362,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
         // complete: everything this launch wrote (statistics, residual) is read after it
         mbar_wait(&S.tfull[acc], aph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (P.trace) t_ready = gtimer();
         float2 ln = make_float2(0.f, 0.f);
         if (G.ln_st && row_ok) ln = merge_stats_cg<E>(G.ln_st + (size_t)m * (G.K / 32), P.eps);
         const uint32_t tb = tmem + acc * 128 + ((uint32_t)(q * 32) << 16);
@@ -410,6 +439,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_cons
         if (lane == 0) wait_count(done + (p - 1) * kMaxRB + rb, expected(p - 1, rb));
         __syncwarp();
       }
+      if (P.trace) t_ready = gtimer();
       const int t = S.t;
       if (kind == K_EMB || kind == K_LN) {
         // one warp per row (kernels.cu k_embed_dec_ln_vec / k_layernorm_vec)

@@ -29,6 +29,7 @@ struct GemmPhase {
 
 struct FusedLayer {
   CUtensorMap ma[6], mb[6];   // QKV, self-out, cross-q, cross-out, FFN1, FFN2
+  CUtensorMap ma32[6];        // A with 32-row boxes: a row block with <= 32 live rows
   GemmPhase g[6];
   const __half *relk, *relv;
   __half *kc, *vc;            // this layer's self-attention cache [slot][Tmax][d]
@@ -48,6 +49,7 @@ struct FusedParams {
   const __half* ckv;
   DevState* st;
   int* ctr;                   // [0] next item, [1] CTAs done, [2..] (phase, row block) counters
+  unsigned long long* trace;  // optional timeline (nmt_debug_fused_trace): per item 4 x u64
 };
 
 size_t fused_counter_ints();

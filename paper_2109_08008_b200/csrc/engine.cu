@@ -408,6 +408,11 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->tb = prec == NMT_FP16 ? 2 : 4;
   m->fuse_rows = getenv("NMT_NO_FUSE") ? -1
                  : getenv("NMT_FUSE_ROWS") ? atoi(getenv("NMT_FUSE_ROWS")) : 1024;
+  if (getenv("NMT_FUSED_TRACE")) {   // debug timeline of the fused decode step (not the product path)
+    NMT_CUDA(cudaMalloc(&m->fused_trace, (4 * 65536 + 1024) * 8));
+    NMT_CUDA(cudaMemset(m->fused_trace, 0, (4 * 65536 + 1024) * 8));
+    m->sys_allocs += 1;
+  }
   NMT_CUDA(cudaSetDevice(device));
   auto can = canonical(cfg);
   size_t total = 0;
@@ -1452,6 +1457,16 @@ nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t 
       m->prof.on = (mode != 0);
       m->prof.steps_only = (mode == 3);
     }
+  });
+}
+
+nmt_status nmt_debug_fused_trace(nmt_model* m, uint64_t* h_out, int64_t cap) {
+  return guard([&] {
+    NMT_REQUIRE(m && h_out, NMT_E_ARG, "null argument");
+    NMT_REQUIRE(m->fused_trace, NMT_E_STATE, "load with NMT_FUSED_TRACE set to record the trace");
+    NMT_CUDA(cudaDeviceSynchronize());
+    const int64_t n = std::min<int64_t>(cap, 4 * 65536 + 1024);
+    NMT_CUDA(cudaMemcpy(h_out, m->fused_trace, n * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -131,6 +131,7 @@ struct nmt_model {
   // fused decode step policy, read at load: live rows up to which one launch runs every
   // phase (env NMT_FUSE_ROWS, default 1024); -1 = unfused step (env NMT_NO_FUSE, A/B only)
   int fuse_rows = 1024;
+  unsigned long long* fused_trace = nullptr;   // NMT_FUSED_TRACE: timeline of the last fused launch
   std::unique_ptr<nmt::FusedParams> fused;   // its parameter block (built on first use)
   float* cand_v = nullptr;    // [R][2K] top log-probs per row
   int* cand_i = nullptr;      // [R][2K] their token ids
@@ -204,6 +205,7 @@ struct nmt_model {
     if (wbuf && owns_weights) cudaFree(wbuf);
     if (foldbuf && owns_weights) cudaFree(foldbuf);
     if (ar.base) cudaFree(ar.base);
+    if (fused_trace) cudaFree(fused_trace);
     if (pinned) cudaFreeHost(pinned);
   }
 };

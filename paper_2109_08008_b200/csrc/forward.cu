@@ -189,6 +189,7 @@ const FusedParams& fused_params(nmt_model* m) {
       if (N % G.bn || K % 64) throw CudaError("fused decode: projection shape not tileable");
       G.nt = N / G.bn;
       L.ma[slot] = tc::make_map(A, Rmax, K, K, 128);
+      L.ma32[slot] = tc::make_map(A, Rmax, K, K, 32);
       L.mb[slot] = tc::make_map(B, N, K, K, G.bn);
     };
     if (l == 0)
@@ -215,6 +216,7 @@ const FusedParams& fused_params(nmt_model* m) {
   P->g = Hm(m->g); P->u = Hm(m->du); P->qkv = Hm(m->dqkv); P->attn_out = Hm(m->dout); P->q = Hm(m->dq);
   P->row_slot = m->row_slot; P->src_len = m->src_len; P->ckv = H(m->ckv); P->st = m->st;
   P->ctr = m->fused_ctr;
+  P->trace = m->fused_trace;
   m->fused = std::move(P);
   return *m->fused;
 }
