@@ -406,8 +406,11 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   m->lim.n_workspaces = std::max(1, lim->n_workspaces);
   m->device = device;
   m->tb = prec == NMT_FP16 ? 2 : 4;
+  // fused decode step (decode_fused.cu): opt-in (NMT_FUSE_ROWS = live-row threshold of the
+  // single launch) — measured slower than the graph-replayed unfused step at every live-row
+  // count on B200 (profiles/r2g_*), so the product default is unfused
   m->fuse_rows = getenv("NMT_NO_FUSE") ? -1
-                 : getenv("NMT_FUSE_ROWS") ? atoi(getenv("NMT_FUSE_ROWS")) : 1024;
+                 : getenv("NMT_FUSE_ROWS") ? atoi(getenv("NMT_FUSE_ROWS")) : -1;
   if (getenv("NMT_FUSED_TRACE")) {   // debug timeline of the fused decode step (not the product path)
     NMT_CUDA(cudaMalloc(&m->fused_trace, (4 * 65536 + 1024) * 8));
     NMT_CUDA(cudaMemset(m->fused_trace, 0, (4 * 65536 + 1024) * 8));

@@ -129,8 +129,9 @@ struct nmt_model {
   float* dlcl_p = nullptr;    // [N][d] FP32 DLCL lookahead partial (kernels.h dlcl_combine)
   int* fused_ctr = nullptr;   // fused decode step: item / completion counters (decode_fused.cu)
   // fused decode step policy, read at load: live rows up to which one launch runs every
-  // phase (env NMT_FUSE_ROWS, default 1024); -1 = unfused step (env NMT_NO_FUSE, A/B only)
-  int fuse_rows = 1024;
+  // phase (env NMT_FUSE_ROWS; above it fused GEMM segments around the standalone attention
+  // kernels); -1 = the unfused step (default, and env NMT_NO_FUSE)
+  int fuse_rows = -1;
   unsigned long long* fused_trace = nullptr;   // NMT_FUSED_TRACE: timeline of the last fused launch
   std::unique_ptr<nmt::FusedParams> fused;   // its parameter block (built on first use)
   float* cand_v = nullptr;    // [R][2K] top log-probs per row

@@ -3,8 +3,8 @@ for embedding ... final LN (or fused GEMM segments around the standalone attenti
 above NMT_FUSE_ROWS live rows) must be bit-identical to the unfused 11-launch step, whose
 arithmetic it reproduces (tile shapes, split-K association, epilogue order), for greedy
 and beam search, one and six decoder layers; the oracle parity of the fused step itself
-is covered by every FP16 d = 512 test of test_gpu_parity.py / test_gpu_fullsize.py (the
-fused path is the default there)."""
+follows from this equality and the oracle parity of the unfused step (the fused step is
+opt-in: NMT_FUSE_ROWS; measured slower than the graph-replayed unfused step on B200)."""
 import os
 
 import numpy as np
@@ -35,7 +35,7 @@ def _model(name, env, **lim):
 
 
 MODES = {"unfused": {"NMT_NO_FUSE": "1"}, "one_launch": {"NMT_FUSE_ROWS": "100000"},
-         "segments": {"NMT_FUSE_ROWS": "0"}, "default": {}}
+         "segments": {"NMT_FUSE_ROWS": "0"}, "mixed": {"NMT_FUSE_ROWS": "64"}, "default": {}}
 
 
 @pytest.mark.parametrize("name,n,lim,beam", [
