@@ -234,6 +234,79 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- C5 whole-set mode
+def run_whole_set(args, rank, world, local):
+    """C5 as SURVEY §8(e) writes it: the synthetic set (1M sentences by default) split into
+    contiguous shards over the W ranks ("split the input ... merge ... in
+    the original order"); each rank translates its shard with nmt_translate_device
+    (device-resident, 4 batch workers), the outputs are gathered to rank 0 in rank order
+    (NCCL all_gather of the compacted tokens), and rank 0 prints tok/s (total generated
+    tokens / max-over-ranks device time: strong scaling) and the SHA-256 of the merged
+    outputs — equal across world sizes when the path is batch invariant."""
+    import torch
+    from synth import PRESETS, generate_weights, newstest_like
+    from paper_2109_08008_b200 import Model
+    from paper_2109_08008_b200.dist import (shard_range, reduce_timing, gather_device_outputs,
+                                            outputs_digest)
+    cfg = PRESETS[args.config]
+    W = generate_weights(cfg)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    full = newstest_like(args.set_size, cfg.vocab_size, start=0)
+    lo, hi = shard_range(full.n, rank, world)
+    wl = full.shard(lo, hi)
+    model = Model(cfg, W, precision="fp16", max_tokens=args.max_tokens, max_sents=args.max_sents,
+                  workspaces=args.workers)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    d_ids = torch.from_numpy(wl.ids).cuda()
+    d_out = torch.empty(wl.n, model.Tmax, dtype=torch.int32, device="cuda")
+    d_len = torch.empty(wl.n, dtype=torch.int32, device="cuda")
+    warm = wl.shard(0, min(wl.n, 24000))      # graphs / caches of every row bucket
+    model.translate_device(torch.from_numpy(warm.ids).cuda(), warm.off, d_out, d_len,
+                           caps=warm.caps, max_tokens=args.max_tokens, max_sents=args.max_sents,
+                           workers=args.workers)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+    barrier()
+    clk = Clocks(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    st = model.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps,
+                                max_tokens=args.max_tokens, max_sents=args.max_sents,
+                                sync_every=args.sync_every, workers=args.workers)
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms_max, gen_all = reduce_timing(e0.elapsed_time(e1), float(st["gen_tokens"]), device="cuda")
+    _, sent_all = reduce_timing(0.0, float(st["sentences"]), device="cuda")
+    merged = gather_device_outputs(d_out, d_len, device="cuda")
+    if rank == 0:
+        flat, lens = merged
+        assert len(lens) == full.n and int(lens.sum()) == int(gen_all)
+        line = {"metric": METRIC, "value": gen_all / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+                "steps": 1, "warmup": 1, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+                "config": {"workload": f"C5: whole synthetic {full.n}-sentence set, contiguous shards "
+                                       f"over {world} ranks, {args.config} FP16 greedy, pruning "
+                                       f"rho=0.25, {args.workers} batch workers per GPU",
+                           "max_tokens": args.max_tokens, "max_sents": args.max_sents,
+                           "parallelism": f"sentence-sharded x{world} (no data-path collective)"},
+                "sentences": int(sent_all), "gen_tokens": int(gen_all),
+                "sentences_per_s": sent_all / (ms_max / 1e3),
+                "outputs_sha256": outputs_digest(flat, lens), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 # ----------------------------------------------------------------- product arm
 def main():
     ap = argparse.ArgumentParser()
@@ -260,6 +333,10 @@ def main():
     ap.add_argument("--no-odef", action="store_true", help="skip the O-def timing of the cpu baseline")
     ap.add_argument("--no-paper-budget", action="store_true",
                     help="skip the decode-step timing at the paper's 4096 / 512 batch budget")
+    ap.add_argument("--whole-set", action="store_true",
+                    help="C5: translate the whole synthetic set sharded over the ranks (strong "
+                         "scaling), gather the outputs to rank 0, print tok/s and their digest")
+    ap.add_argument("--set-size", type=int, default=1_000_000)
     ap.add_argument("--cap-clip", type=int, default=0,
                     help="analysis only: clip target caps (1 = encoder-dominated run); not a bench value")
     args = ap.parse_args()
@@ -269,6 +346,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.whole_set:
+        run_whole_set(args, rank, world, local)
         return
 
     from synth import PRESETS, generate_weights, newstest_like

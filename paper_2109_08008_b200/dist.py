@@ -72,3 +72,50 @@ def gather_outputs(outs: list, device=None):
             merged.append(toks[off:off + L].tolist())
             off += L
     return merged
+
+
+def gather_device_outputs(d_out, d_len, device=None):
+    """Whole-set merge (C5, "merge ... in the original order"): every rank
+    holds its contiguous shard's outputs as d_out [n_r][stride] int32 (EOS included when
+    produced) and d_len [n_r]; the tokens are compacted on the rank's device, gathered with
+    the process group's all_gather (NCCL on GPUs: padded to the largest shard) and
+    concatenated in rank order on rank 0.  Returns (flat int32 tokens, lengths int32) as
+    NumPy arrays on rank 0, None elsewhere; without a process group the local arrays."""
+    import torch
+    import torch.distributed as dist
+    n_r, stride = d_out.shape
+    dev = d_out.device if device is None else device
+    lens = d_len.to(torch.int64)
+    keep = torch.arange(stride, device=d_out.device)[None, :] < lens[:, None]
+    flat = d_out[keep].to(torch.int32)            # row-major: sentence by sentence
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return flat.cpu().numpy(), d_len.to(torch.int32).cpu().numpy()
+    world, rank = dist.get_world_size(), dist.get_rank()
+    meta = torch.tensor([n_r, flat.numel()], dtype=torch.int64, device=dev)
+    metas = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(metas, meta)
+    n_max = int(max(int(m[0]) for m in metas))
+    t_max = max(1, int(max(int(m[1]) for m in metas)))
+    pl = torch.zeros(n_max, dtype=torch.int32, device=dev)
+    pl[:n_r] = d_len.to(torch.int32).to(dev)
+    pt = torch.zeros(t_max, dtype=torch.int32, device=dev)
+    pt[:flat.numel()] = flat.to(dev)
+    al = [torch.zeros_like(pl) for _ in range(world)]
+    at = [torch.zeros_like(pt) for _ in range(world)]
+    dist.all_gather(al, pl)
+    dist.all_gather(at, pt)
+    if rank != 0:
+        return None
+    toks = [at[r][:int(metas[r][1])].cpu().numpy() for r in range(world)]
+    ls = [al[r][:int(metas[r][0])].cpu().numpy() for r in range(world)]
+    return np.concatenate(toks).astype(np.int32), np.concatenate(ls).astype(np.int32)
+
+
+def outputs_digest(flat: np.ndarray, lens: np.ndarray) -> str:
+    """SHA-256 over (lengths, tokens) little-endian int32: byte-identical merged outputs
+    across world sizes have equal digests (SURVEY §8(e) check)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(lens, dtype="<i4").tobytes())
+    h.update(np.ascontiguousarray(flat, dtype="<i4").tobytes())
+    return h.hexdigest()
