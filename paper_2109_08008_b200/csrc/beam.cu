@@ -109,6 +109,69 @@ __global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__
   }
 }
 
+// ------------------------------------------------------------------ beam epilogue merge
+// One warp per live row over the nseg partial records of the vocab GEMM's beam epilogue
+// (tc_dev.cuh BeamAcc): LSE from the segment (max, sum) pairs, then KB rounds of warp
+// argmax over the segments' sorted top-8 lists (each lane owns every 32nd segment).
+__global__ void __launch_bounds__(128) k_beam_merge(const float* __restrict__ part, int nseg, int KB,
+                                                    const int* __restrict__ dR,
+                                                    float* __restrict__ cand_v,
+                                                    int* __restrict__ cand_i) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= *dR) return;
+  const float* pr = part + (size_t)row * nseg * (2 + 2 * kKB);
+  float mm = -INFINITY;
+  for (int g = lane; g < nseg; g += 32) mm = fmaxf(mm, pr[(size_t)g * (2 + 2 * kKB)]);
+  float M = mm;
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float ss = 0.f;
+  for (int g = lane; g < nseg; g += 32) {
+    const float* r = pr + (size_t)g * (2 + 2 * kKB);
+    if (r[0] > -INFINITY) ss += r[1] * __expf(r[0] - M);
+  }
+  ss = warp_sum(ss);
+  const float lse = M + __logf(ss);
+  constexpr int kMaxSeg = 16;   // segments per lane (nseg <= 512: V <= 65536)
+  int ptr[kMaxSeg];
+#pragma unroll
+  for (int q = 0; q < kMaxSeg; ++q) ptr[q] = 0;
+  for (int k = 0; k < KB; ++k) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff, bq = -1;
+#pragma unroll
+    for (int q = 0; q < kMaxSeg; ++q) {
+      const int g = lane + 32 * q;
+      if (g < nseg && ptr[q] < kKB) {
+        const float* r = pr + (size_t)g * (2 + 2 * kKB);
+        const float v = r[2 + ptr[q]];
+        const int id = __float_as_int(r[2 + kKB + ptr[q]]);
+        if (cand_better(v, id, bv, bi)) { bv = v; bi = id; bq = q; }
+      }
+    }
+    float wv = bv;
+    int wi = bi;
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+      if (cand_better(ov, oi, wv, wi)) { wv = ov; wi = oi; }
+    }
+    if (bq >= 0 && bi == wi && bv == wv) ptr[bq]++;
+    if (lane == 0) {
+      cand_v[(size_t)row * KB + k] = wv - lse;
+      cand_i[(size_t)row * KB + k] = wi;
+    }
+  }
+}
+
+void beam_merge(const float* part, int nseg, int KB, const int* dR, int rows_upper, float* cand_v,
+                int* cand_i, cudaStream_t s) {
+  if (rows_upper <= 0) return;
+  if (KB > kKB || nseg > 32 * 16) throw CudaError("beam_merge: 2K > 8 or V > 65536");
+  k_beam_merge<<<ceil_div(rows_upper, 4), 128, 0, s>>>(part, nseg, KB, dR, cand_v, cand_i);
+  NMT_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ teacher ensemble
 // "a simple ensemble strategy", reading R26: per row the members' next-token
 // distributions are averaged, ens[v] = logsumexp_m(x_m[v] - LSE_m) - log M (FP32).  One

@@ -162,6 +162,8 @@ void init_arena(nmt_model* m) {
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->fused_ctr, fused_counter_ints() * 4},
+      {(void**)&m->bpart, L.beam > 1 && m->prec == NMT_FP16
+                              ? R * (size_t)((c.vocab_size + 127) / 128) * 18 * 4 : 256},
   };
   std::vector<size_t> offs;
   for (auto& it : items) offs.push_back(a.take(it.second));
@@ -173,6 +175,7 @@ void init_arena(nmt_model* m) {
   for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
   NMT_CUDA(cudaMemset(a.base, 0, a.used));
   for (auto& ev : m->ev_t) NMT_CUDA(cudaEventCreate(&ev));
+  m->beam_epi = L.beam > 1 && m->prec == NMT_FP16 && getenv("NMT_NO_BEAM_EPI") == nullptr;
   // pinned host staging (each region rounded to 64 B)
   size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 + 16 * 64;
   NMT_CUDA(cudaMallocHost(&m->pinned, pb));

@@ -387,17 +387,31 @@ vocab:
     }
     return;
   }
-  // beam: FP32 logits -> per-row LSE + top-2K -> per-sentence select
+  // beam
   const int K = b->K, V = c.vocab_size;
   GemmArgs a = vocab_args();
-  a.logits = m->blogits;
-  PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) + (double)R * V * 4, gemm<T>(a, s));
-  if (out && out->d_logits)
-    NMT_CUDA(cudaMemcpyAsync(out->d_logits, m->blogits, (size_t)R * V * 4,
-                             cudaMemcpyDeviceToDevice, s));
-  if (!finish) return;
-  PROF(P_BOOK, 0, (double)R * V * 4,
-       beam_row_topk(m->blogits, V, 2 * K, dR, R, m->cand_v, m->cand_i, s));
+  if (sizeof(T) == 2 && finish && !(out && out->d_logits) && m->beam_epi) {
+    // FP16: the vocab GEMM epilogue keeps per (row, 128-column segment) the log-sum-exp
+    // partial and the top-8 candidates — the R x V logits are never written (SURVEY §2.6
+    // K17) — and one warp per row merges them into the LSE and the top-2K log-probs
+    const int nseg = (V + 127) / 128;
+    a.beam_part = m->bpart;
+    PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) - (double)R * V * tb + (double)R * nseg * 72,
+         gemm<T>(a, s));
+    PROF(P_BOOK, 0, (double)R * nseg * 72,
+         beam_merge(m->bpart, nseg, 2 * K, dR, R, m->cand_v, m->cand_i, s));
+  } else {
+    // FP32 logits -> per-row LSE + top-2K (FP32 mode, logits dumps, and the ensemble's
+    // members, whose distributions are averaged before the top-2K)
+    a.logits = m->blogits;
+    PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) + (double)R * V * 4, gemm<T>(a, s));
+    if (out && out->d_logits)
+      NMT_CUDA(cudaMemcpyAsync(out->d_logits, m->blogits, (size_t)R * V * 4,
+                               cudaMemcpyDeviceToDevice, s));
+    if (!finish) return;
+    PROF(P_BOOK, 0, (double)R * V * 4,
+         beam_row_topk(m->blogits, V, 2 * K, dR, R, m->cand_v, m->cand_i, s));
+  }
   PROF(P_BOOK, 0, 0,
        beam_select(K, m->cand_v, m->cand_i, m->bscore, m->prev_tok, m->done, m->row_slot,
                    m->tgt_cap, m->anc, m->htok, Tm, m->best_score, m->out_tok, m->gen_len, m->st,

@@ -282,6 +282,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
       unsigned long long best = 0ull;
+      BeamAcc bacc;
+      if (p.bpart) bacc.init();
 #pragma unroll
       for (int c0 = cb; c0 < cb + HALF; c0 += 32) {
         float v[32];
@@ -355,10 +357,15 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           epi_math(p, m, n0 + c0, v, bias_all ? sbias + n0 + c0 : sb + (c0 - cb),
                    pf ? res + (c0 - cb) / 8 : nullptr, true, sc + (c0 - cb), ln);
           if (p.st_out) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
-          epi_out(p, m, n0 + c0, v, best);
+          if (p.bpart) bacc.add(v, n0 + c0, min(32, p.N - (n0 + c0)));
+          else epi_out(p, m, n0 + c0, v, best);
         }
       }
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
+      if (p.bpart && row_ok && n0 + cb < p.N) {   // this thread's segment of the row
+        const int nseg = (p.N + HALF - 1) / HALF;
+        bacc.store(p.bpart + ((size_t)m * nseg + (n0 + cb) / HALF) * kBeamRec);
+      }
     }
     // the staging tiles must outlive the bulk stores' shared-memory reads; the global
     // writes complete with the grid (kernel boundary / PDL wait of the dependent)
@@ -684,6 +691,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.dM = a.dM;
   p.argmax = a.argmax;
   p.logits = a.logits;
+  p.bpart = a.beam_part;
   p.splits = 1;
   p.st_out = a.st_out;
   p.ln_st = a.ln_st;
@@ -731,6 +739,7 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   p.dM = a.dM;
   p.argmax = a.argmax;
   p.logits = a.logits;
+  p.bpart = a.beam_part;
   p.splits = 1;
   p.st_out = a.st_out;
   p.ln_st = a.ln_st;
@@ -847,6 +856,11 @@ void decode_config(GemmArgs& a) {
 
 void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
+  if (a.beam_part) {   // beam epilogue: 128 x 256 units, 128-column segments per thread
+    if (a.logits || a.argmax || a.C || a.bias || a.R) throw CudaError("gemm_tc: beam epilogue is exclusive");
+    tc::launch<256, 4>(a, s);
+    return;
+  }
   if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||
       (reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
     throw CudaError("gemm_tc: K / leading dims must be multiples of 8 and 16-B aligned");

@@ -163,6 +163,8 @@ struct Params {
   const int* dM;
   unsigned long long* argmax;
   float* logits;
+  float* bpart;       // beam epilogue (logits never stored): per (row, HALF-column segment)
+                      // {max, sum exp(x - max), top-8 values, top-8 ids} (kBeamRec floats)
   int splits;         // split-K factor (kb_total % splits == 0)
   float* ws;          // split-K partials [tile][split][BM][BN]
   int* counters;      // split-K arrival counters [tile] (self-resetting)
@@ -385,6 +387,66 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+
+// ---- beam epilogue: online log-sum-exp and the top-8
+// (value desc, id asc) of one row's segment of logits, kept in registers across chunks
+constexpr int kBeamKB = 8;
+constexpr int kBeamRec = 2 + 2 * kBeamKB;
+struct BeamAcc {
+  float mx, sum;
+  float tv[kBeamKB];
+  int ti[kBeamKB];
+  __device__ __forceinline__ void init() {
+    mx = -INFINITY;
+    sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kBeamKB; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
+  }
+  __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
+    return a > b || (a == b && ia < ib);
+  }
+  // 32 columns nb..nb+31 of the row, nv of them valid
+  __device__ __forceinline__ void add(const float* v, int nb, int nv) {
+    float cm = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) cm = fmaxf(cm, v[j]);
+    float cs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) cs += __expf(v[j] - cm);
+    if (cm > mx) {
+      sum = sum * __expf(mx - cm) + cs;
+      mx = cm;
+    } else {
+      sum += cs * __expf(cm - mx);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < nv && better(v[j], nb + j, tv[kBeamKB - 1], ti[kBeamKB - 1])) {
+        float cv = v[j];
+        int ci = nb + j;
+#pragma unroll
+        for (int k = 0; k < kBeamKB; ++k) {
+          if (better(cv, ci, tv[k], ti[k])) {
+            const float t1 = tv[k];
+            const int t2 = ti[k];
+            tv[k] = cv; ti[k] = ci; cv = t1; ci = t2;
+          }
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void store(float* rec) const {
+    rec[0] = mx;
+    rec[1] = sum;
+#pragma unroll
+    for (int k = 0; k < kBeamKB; ++k) {
+      rec[2 + k] = tv[k];
+      rec[2 + kBeamKB + k] = __int_as_float(ti[k]);
+    }
+  }
+};
 
 // Host: TMA descriptor (cached) of a row-major FP16 [rows][cols] matrix with leading dim ld:
 // operand maps box {BK, box_rows}, 128-B swizzle; output maps (out) box {32, 32}, 64-B swizzle.

@@ -88,3 +88,44 @@ def test_fused_teacher_forced_logits_identical():
         del m
     assert np.array_equal(res["unfused"], res["one_launch"])
     assert np.array_equal(res["unfused"], res["segments"])
+
+
+@pytest.mark.parametrize("name,n,lim", [
+    ("tiny", 10, dict(max_tokens=256, max_sents=8, max_tgt_len=32, beam=4)),
+    ("teacher-30-6", 16, dict(max_tokens=1024, max_sents=16, max_tgt_len=20, beam=4)),
+])
+def test_beam_epilogue_matches_logits_path(name, n, lim):
+    """FP16 beam: the vocab GEMM's fused epilogue (per 128-column segment LSE partial and
+    top-8, merged per row; logits never written) selects the same hypotheses as the FP32-
+    logits path (materialised logits + row top-2K); scores agree to FP32 rounding of the
+    LSE association."""
+    from synth import tiny_workload
+    from paper_2109_08008_b200 import Model
+    from gpu_common import weights
+    if name == "tiny":
+        wl = tiny_workload(n=n, seed=11, max_cap=12)
+        cfg, W = weights("tiny", 3.0)
+    else:
+        wl = newstest_like(n, 32000, start=313)
+        cfg, W = weights(name)
+    caps = np.minimum(wl.caps, lim["max_tgt_len"])
+    res = {}
+    for mode in ("logits", "epilogue"):
+        old = os.environ.pop("NMT_NO_BEAM_EPI", None)
+        if mode == "logits":
+            os.environ["NMT_NO_BEAM_EPI"] = "1"
+        try:
+            m = Model(cfg, W, precision="fp16", **lim)
+        finally:
+            os.environ.pop("NMT_NO_BEAM_EPI", None)
+            if old is not None:
+                os.environ["NMT_NO_BEAM_EPI"] = old
+        hyps, scores, _ = m.translate_nbest(wl.ids, wl.off, 2, 4, caps=caps)
+        res[mode] = (hyps, scores)
+        del m
+    (h0, s0), (h1, s1) = res["logits"], res["epilogue"]
+    same = sum(a == b for a, b in zip(h0, h1))
+    assert same == len(h0), (same, len(h0))
+    for a, b in zip(s0, s1):
+        for x, y in zip(a, b):
+            assert abs(x - y) <= 1e-4 * max(1.0, abs(x)), (x, y)
