@@ -234,6 +234,54 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- C4 beam measurement
+def c4_measure(args, reps=3):
+    import torch
+    from synth import PRESETS, generate_weights, newstest_like
+    from paper_2109_08008_b200 import Model
+    cfg = PRESETS["teacher-30-6"]
+    W = generate_weights(cfg)
+    m = Model(cfg, W, precision="fp16", max_tokens=4096, max_sents=128, beam=4)
+    wl = newstest_like(512, cfg.vocab_size, start=0)
+    d_ids = torch.from_numpy(wl.ids).cuda()
+    d_out = torch.empty(wl.n, m.Tmax, dtype=torch.int32, device="cuda")
+    d_len = torch.empty(wl.n, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4)   # graphs
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    gen = steps = 0
+    for _ in range(reps):
+        st = m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4)
+        gen += st["gen_tokens"]
+        steps += st["decode_steps"]
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    m.profile(2)
+    m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4)
+    prof = m.profile(-1)
+    m.profile(0)
+    pk, _ = peaks()
+    tpeak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    kern = {}
+    tot = sum(v["ms"] for v in prof.values())
+    for k, v in prof.items():
+        tt = v["flops"] / (tpeak * 1e12) if v["flops"] else 0.0
+        th = v["bytes"] / (pk["hbm_gbs"] * 1e9) if v["bytes"] else 0.0
+        kern[k] = {"ms": round(v["ms"], 3), "share": round(v["ms"] / tot, 4) if tot else None,
+                   "bound": "tensor" if tt > th else "hbm",
+                   "frac": round(1e3 * max(tt, th) / v["ms"], 4) if v["ms"] else None}
+    del m
+    return {"value": gen / reps / (ms / 1e3), "unit": UNIT, "model": "teacher-30-6 DLCL+RPR FP16",
+            "beam": 4, "sentences": wl.n, "max_tokens": 4096, "max_sents": 128,
+            "ms_per_pass": ms, "decode_steps_per_pass": steps // reps,
+            "ms_per_decode_step": ms / max(1, steps // reps),
+            "epilogue": "fused beam epilogue (no logits)" if not os.environ.get("NMT_NO_BEAM_EPI")
+                        else "logits + row top-2K", "kernels": kern}
+
+
 # ----------------------------------------------------------------- C5 whole-set mode
 def run_whole_set(args, rank, world, local):
     """C5 as SURVEY §8(e) writes it: the synthetic set (1M sentences by default) split into
@@ -333,6 +381,7 @@ def main():
     ap.add_argument("--no-odef", action="store_true", help="skip the O-def timing of the cpu baseline")
     ap.add_argument("--no-paper-budget", action="store_true",
                     help="skip the decode-step timing at the paper's 4096 / 512 batch budget")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (30-6 beam 4) measurement")
     ap.add_argument("--whole-set", action="store_true",
                     help="C5: translate the whole synthetic set sharded over the ranks (strong "
                          "scaling), gather the outputs to rank 0, print tok/s and their digest")
@@ -541,6 +590,12 @@ def main():
             v["bytes"] = v["bytes"] * real_tok / pad_tok
     if "enc_gemm" in prof:
         prof["enc_gemm"]["flops"] = real_tok * enc_flops_per_token(cfg)
+    # ---- C4 (BASELINE configs[3]): teacher-scale 30-6 DLCL+RPR, FP16 beam 4 with cached
+    # attention: the first 512 sentences, 4096 source tokens / 128 sentences
+    # (512 hypothesis rows) per batch; device-resident, one worker; per-class profile
+    c4 = None
+    if not args.no_c4 and rank == 0:
+        c4 = c4_measure(args)
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     pk, src = peaks()
     # the binding roof of the class: the larger of FLOPs / tensor peak and bytes / HBM peak
@@ -624,6 +679,7 @@ def main():
             "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
             "step_roofline": step_roof, "kernels": kernels,
+            "c4_beam": c4,
             "cpu_baseline": cpu, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
