@@ -391,10 +391,10 @@ vocab:
   const int K = b->K, V = c.vocab_size;
   GemmArgs a = vocab_args();
   if (sizeof(T) == 2 && finish && !(out && out->d_logits) && m->beam_epi) {
-    // FP16: the vocab GEMM epilogue keeps per (row, 128-column segment) the log-sum-exp
+    // FP16: the vocab GEMM epilogue keeps per (row, 256-column segment) the log-sum-exp
     // partial and the top-8 candidates — the R x V logits are never written (SURVEY §2.6
     // K17) — and one warp per row merges them into the LSE and the top-2K log-probs
-    const int nseg = (V + 127) / 128;
+    const int nseg = (V + 255) / 256;   // one segment per 256-column unit (gemm_tc.cu)
     a.beam_part = m->bpart;
     PROF(P_VOCAB, gemm_flops(a), gemm_bytes(a, tb) - (double)R * V * tb + (double)R * nseg * 72,
          gemm<T>(a, s));

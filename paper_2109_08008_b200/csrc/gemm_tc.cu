@@ -35,7 +35,7 @@ namespace tc {
 // both halves on its own `full` barrier (each CTA's TMA completes on it), issues the MMAs
 // and multicasts its commits to both CTAs' `empty` / `tfull` barriers; both CTAs drain
 // their own TMEM rows and release the accumulator on the leader's `tempty`.
-template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1>
+template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1, bool BEAM = false>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
       unsigned long long best = 0ull;
       BeamAcc bacc;
-      if (p.bpart) bacc.init();
+      if constexpr (BEAM) bacc.init();
 #pragma unroll
       for (int c0 = cb; c0 < cb + HALF; c0 += 32) {
         float v[32];
@@ -357,12 +357,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           epi_math(p, m, n0 + c0, v, bias_all ? sbias + n0 + c0 : sb + (c0 - cb),
                    pf ? res + (c0 - cb) / 8 : nullptr, true, sc + (c0 - cb), ln);
           if (p.st_out) p.st_out[(size_t)m * (p.N / 32) + (n0 + c0) / 32] = chunk_stats(v);
-          if (p.bpart) bacc.add(v, n0 + c0, min(32, p.N - (n0 + c0)));
+          if constexpr (BEAM) bacc.add(v, n0 + c0, min(32, p.N - (n0 + c0)));
           else epi_out(p, m, n0 + c0, v, best);
         }
       }
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
-      if (p.bpart && row_ok && n0 + cb < p.N) {   // this thread's segment of the row
+      if (BEAM && row_ok && n0 + cb < p.N) {   // this thread's segment of the row
         const int nseg = (p.N + HALF - 1) / HALF;
         bacc.store(p.bpart + ((size_t)m * nseg + (n0 + cb) / HALF) * kBeamRec);
       }
@@ -666,13 +666,13 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EW = 8, int NSTG = 1>
+template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
@@ -710,7 +710,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.rtma = NSTG == 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
            (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && !no_rtma;
   const CUtensorMap mr = p.rtma ? make_map(a.R, a.M, a.N, a.ldr, 32, true) : CUtensorMap{};
-  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
+  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -856,9 +856,11 @@ void decode_config(GemmArgs& a) {
 
 void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
-  if (a.beam_part) {   // beam epilogue: 128 x 256 units, 128-column segments per thread
+  if (a.beam_part) {   // beam epilogue: 128 x 256 units, one 256-column segment per row
     if (a.logits || a.argmax || a.C || a.bias || a.R) throw CudaError("gemm_tc: beam epilogue is exclusive");
-    tc::launch<256, 4>(a, s);
+    // 4 epilogue warps: 256-column segments per thread, and the registers of a 256-thread
+    // CTA keep the running top-8 without spills
+    tc::launch<256, 4, 4, 1, true>(a, s);
     return;
   }
   if ((a.K % 8) || (a.lda % 8) || (a.ldb % 8) ||

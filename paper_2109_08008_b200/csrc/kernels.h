@@ -27,8 +27,8 @@ struct GemmArgs {
   const int* dM = nullptr;
   unsigned long long* argmax = nullptr;
   float* logits = nullptr;
-  // beam epilogue (FP16 tcgen05 path): per (row, 128-column segment) log-sum-exp partial and
-  // top-8 candidates instead of logits, [M][ceil(N/128)][2 + 16] floats (beam_merge)
+  // beam epilogue (FP16 tcgen05 path): per (row, 256-column segment) log-sum-exp partial and
+  // top-8 candidates instead of logits, [M][ceil(N/256)][2 + 16] floats (beam_merge)
   float* beam_part = nullptr;
   // tcgen05 path only: output tile width (128, or 64 for decode-size GEMMs) and a
   // deterministic split-K factor with its FP32 workspace / self-resetting counters.
@@ -130,7 +130,7 @@ void beam_select(int K, const float* cand_v, const int* cand_i, float* score, in
                  float* nb_score = nullptr, int* nb_len = nullptr, int* nb_tok = nullptr,
                  int* nb_cnt = nullptr, int* parent_out = nullptr);
 // Merge of the vocab GEMM's beam epilogue partials (GemmArgs::beam_part, nseg segments of
-// 128 columns per row): per row LSE = M + log sum_i s_i exp(m_i - M) and the top-KB
+// 256 columns per row): per row LSE = M + log sum_i s_i exp(m_i - M) and the top-KB
 // candidates (value desc, id asc) as log-probabilities -> cand_v / cand_i (= beam_row_topk).
 void beam_merge(const float* part, int nseg, int KB, const int* dR, int rows_upper, float* cand_v,
                 int* cand_i, cudaStream_t s);

@@ -405,7 +405,9 @@ struct BeamAcc {
   __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
     return a > b || (a == b && ia < ib);
   }
-  // 32 columns nb..nb+31 of the row, nv of them valid
+  // 32 columns nb..nb+31 of the row, nv of them valid.  The chunk maximum decides whether
+  // the chunk can enter the top-8 at all (after the first chunks it rarely can), so the
+  // per-element work is one exp and one add.
   __device__ __forceinline__ void add(const float* v, int nb, int nv) {
     float cm = -INFINITY;
 #pragma unroll
@@ -421,19 +423,18 @@ struct BeamAcc {
     } else {
       sum += cs * __expf(cm - mx);
     }
+    if (!(cm >= tv[kBeamKB - 1])) return;   // nothing of this chunk enters the top-8
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < nv && better(v[j], nb + j, tv[kBeamKB - 1], ti[kBeamKB - 1])) {
-        float cv = v[j];
-        int ci = nb + j;
+    for (int j = 0; j < 32; ++j)
+      if (j < nv && better(v[j], nb + j, tv[kBeamKB - 1], ti[kBeamKB - 1])) insert(v[j], nb + j);
+  }
+  __device__ __forceinline__ void insert(float cv, int ci) {
 #pragma unroll
-        for (int k = 0; k < kBeamKB; ++k) {
-          if (better(cv, ci, tv[k], ti[k])) {
-            const float t1 = tv[k];
-            const int t2 = ti[k];
-            tv[k] = cv; ti[k] = ci; cv = t1; ci = t2;
-          }
-        }
+    for (int k = 0; k < kBeamKB; ++k) {
+      if (better(cv, ci, tv[k], ti[k])) {
+        const float t1 = tv[k];
+        const int t2 = ti[k];
+        tv[k] = cv; ti[k] = ci; cv = t1; ci = t2;
       }
     }
   }
