@@ -278,8 +278,8 @@ def c4_measure(args, reps=3):
             "beam": 4, "sentences": wl.n, "max_tokens": 4096, "max_sents": 128,
             "ms_per_pass": ms, "decode_steps_per_pass": steps // reps,
             "ms_per_decode_step": ms / max(1, steps // reps),
-            "epilogue": "fused beam epilogue (no logits)" if not os.environ.get("NMT_NO_BEAM_EPI")
-                        else "logits + row top-2K", "kernels": kern}
+            "epilogue": "fused beam epilogue (no logits)" if os.environ.get("NMT_BEAM_EPI")
+                        else "FP32 logits + two-pass row top-2K", "kernels": kern}
 
 
 # ----------------------------------------------------------------- C5 whole-set mode

@@ -26,6 +26,13 @@ __device__ __forceinline__ bool cand_better(float a, int ia, float b, int ib) {
   return a > b || (a == b && ia < ib);
 }
 
+// Two passes over the row (L2-resident after the first): pass 1 keeps per thread only the
+// running (max, sum exp) and its maximum's id — no per-element insertion, no divergence; the
+// KB-th largest of the 256 thread maxima is a lower bound tau on the row's KB-th largest
+// value, so pass 2 appends the few elements >= tau to shared memory and warp 0 selects the
+// top-KB (value desc, id asc) from them.  Rows with more than kCandCap elements >= tau
+// (massive ties) fall back to a block-wide selection over the whole row.
+constexpr int kCandCap = 1024;
 __global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__ logits, int V,
                                                        int KB, const int* __restrict__ dR,
                                                        float* __restrict__ cand_v,
@@ -33,42 +40,26 @@ __global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__
   const int row = blockIdx.x;
   if (row >= *dR) return;
   const float* x = logits + (size_t)row * V;
-  float tv[kKB];
-  int ti[kKB];
-#pragma unroll
-  for (int k = 0; k < kKB; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
   float m = -INFINITY, s = 0.f;
   for (int v = threadIdx.x; v < V; v += blockDim.x) {
     const float f = x[v];
     if (f > m) { s = s * __expf(m - f) + 1.f; m = f; }
     else s += __expf(f - m);
-    if (cand_better(f, v, tv[kKB - 1], ti[kKB - 1])) {  // sorted insertion
-      float cv = f; int ci = v;
-#pragma unroll
-      for (int k = 0; k < kKB; ++k) {
-        if (cand_better(cv, ci, tv[k], ti[k])) {
-          const float t1 = tv[k]; const int t2 = ti[k];
-          tv[k] = cv; ti[k] = ci; cv = t1; ci = t2;
-        }
-      }
-    }
   }
-  // block LSE
-  __shared__ float sm_m[8], sm_s[8];
-  __shared__ float sv[256 * kKB];
-  __shared__ int si[256 * kKB];
+  __shared__ float sm_m[8], sm_s[8], s_tmax[256];
+  __shared__ float s_cv[kCandCap];
+  __shared__ int s_ci[kCandCap];
+  __shared__ int s_n;
+  __shared__ float s_tau, s_lse;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  s_tmax[threadIdx.x] = m;
+  if (threadIdx.x == 0) s_n = 0;
   {
     float mm = m;
     for (int o = 16; o; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
     float ss = (m == -INFINITY) ? 0.f : s * __expf(m - mm);
     ss = warp_sum(ss);
     if (lane == 0) { sm_m[warp] = mm; sm_s[warp] = ss; }
-  }
-#pragma unroll
-  for (int k = 0; k < kKB; ++k) {
-    sv[threadIdx.x * kKB + k] = tv[k];
-    si[threadIdx.x * kKB + k] = ti[k];
   }
   __syncthreads();
   if (warp == 0) {
@@ -77,35 +68,98 @@ __global__ void __launch_bounds__(256) k_beam_row_topk(const float* __restrict__
     for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float ss = (lane < 8 && mm > -INFINITY) ? sm_s[lane] * __expf(mm - M) : 0.f;
     ss = warp_sum(ss);
-    const float lse = M + __logf(ss);
-    // merge 256 x KB candidates: each lane scans 8 threads' sorted lists, then KB rounds
-    // of warp argmax (value desc, id asc)
-    int ptr[8];
+    // tau = KB-th largest thread maximum: KB rounds of warp max over 8 maxima per lane
+    float t[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) ptr[q] = 0;
+    for (int q = 0; q < 8; ++q) t[q] = s_tmax[lane * 8 + q];
+    float tau = -INFINITY;
     for (int k = 0; k < KB; ++k) {
-      float bv = -INFINITY; int bi = 0x7fffffff, bq = -1;
+      float bv = -INFINITY;
+      int bq = -1;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int th = lane * 8 + q;
-        if (ptr[q] < kKB) {
-          const float v = sv[th * kKB + ptr[q]];
-          const int id = si[th * kKB + ptr[q]];
-          if (cand_better(v, id, bv, bi)) { bv = v; bi = id; bq = q; }
+      for (int q = 0; q < 8; ++q)
+        if (t[q] > bv) { bv = t[q]; bq = q; }
+      float wv = bv;
+      for (int o = 16; o; o >>= 1) wv = fmaxf(wv, __shfl_xor_sync(0xffffffffu, wv, o));
+      // remove one instance of the maximum (lowest lane holding it)
+      const unsigned own = __ballot_sync(0xffffffffu, bq >= 0 && bv == wv);
+      if (own && lane == __ffs(own) - 1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q == bq) t[q] = -INFINITY;
+      }
+      tau = wv;
+    }
+    if (lane == 0) { s_tau = tau; s_lse = M + __logf(ss); }
+  }
+  __syncthreads();
+  const float tau = s_tau;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float f = x[v];
+    if (f >= tau) {
+      const int at = atomicAdd(&s_n, 1);
+      if (at < kCandCap) { s_cv[at] = f; s_ci[at] = v; }
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  const float lse = s_lse;
+  if (n <= kCandCap) {
+    if (warp == 0) {   // KB rounds of warp argmax (value desc, id asc) over the candidates
+      for (int k = 0; k < KB; ++k) {
+        float bv = -INFINITY;
+        int bi = 0x7fffffff, bj = -1;
+        for (int j = lane; j < n; j += 32)
+          if (cand_better(s_cv[j], s_ci[j], bv, bi)) { bv = s_cv[j]; bi = s_ci[j]; bj = j; }
+        float wv = bv;
+        int wi = bi;
+        for (int o = 16; o; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+          if (cand_better(ov, oi, wv, wi)) { wv = ov; wi = oi; }
+        }
+        if (bj >= 0 && bi == wi && bv == wv) s_cv[bj] = -INFINITY, s_ci[bj] = 0x7fffffff;
+        __syncwarp();
+        if (lane == 0) {
+          cand_v[(size_t)row * KB + k] = wv - lse;        // log_softmax value
+          cand_i[(size_t)row * KB + k] = wi;
         }
       }
-      float wv = bv; int wi = bi;
-      for (int o = 16; o; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
-        if (cand_better(ov, oi, wv, wi)) { wv = ov; wi = oi; }
-      }
-      if (bq >= 0 && bi == wi && bv == wv) ptr[bq]++;  // the owning lane advances
-      if (lane == 0) {
-        cand_v[(size_t)row * KB + k] = wv - lse;        // log_softmax value
-        cand_i[(size_t)row * KB + k] = wi;
-      }
     }
+    return;
+  }
+  // fallback (more than kCandCap elements >= tau): KB rounds of block argmax over the row
+  __shared__ float s_wv[8];
+  __shared__ int s_wi[8];
+  float last_v = INFINITY;
+  int last_i = -1;
+  for (int k = 0; k < KB; ++k) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      const float f = x[v];
+      // strictly after (last_v, last_i) in (value desc, id asc) order
+      const bool after = f < last_v || (f == last_v && v > last_i);
+      if (after && cand_better(f, v, bv, bi)) { bv = f; bi = v; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (cand_better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { s_wv[warp] = bv; s_wi[warp] = bi; }
+    __syncthreads();
+    float wv = s_wv[0];
+    int wi = s_wi[0];
+    for (int w = 1; w < 8; ++w)
+      if (cand_better(s_wv[w], s_wi[w], wv, wi)) { wv = s_wv[w]; wi = s_wi[w]; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cand_v[(size_t)row * KB + k] = wv - lse;
+      cand_i[(size_t)row * KB + k] = wi;
+    }
+    last_v = wv;
+    last_i = wi;
   }
 }
 

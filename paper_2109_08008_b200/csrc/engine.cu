@@ -175,7 +175,9 @@ void init_arena(nmt_model* m) {
   for (size_t i = 0; i < items.size(); ++i) *items[i].first = a.base + offs[i];
   NMT_CUDA(cudaMemset(a.base, 0, a.used));
   for (auto& ev : m->ev_t) NMT_CUDA(cudaEventCreate(&ev));
-  m->beam_epi = L.beam > 1 && m->prec == NMT_FP16 && getenv("NMT_NO_BEAM_EPI") == nullptr;
+  // fused beam epilogue (logits never written): opt-in, NMT_BEAM_EPI=1 — measured slower
+  // than the logits + two-pass row top-K path on B200
+  m->beam_epi = L.beam > 1 && m->prec == NMT_FP16 && getenv("NMT_BEAM_EPI") != nullptr;
   // pinned host staging (each region rounded to 64 B)
   size_t pb = N * 4 + Bm * 4 * 2 + Bm * 8 + Bm * 4 * 2 + Bm * Tm * 4 + Bm * 4 + 64 + 64 + 16 * 64;
   NMT_CUDA(cudaMallocHost(&m->pinned, pb));

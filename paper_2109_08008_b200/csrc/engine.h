@@ -126,7 +126,7 @@ struct nmt_model {
   int* nb_cnt = nullptr;      // [max_sents] list sizes
   float* blogits = nullptr;   // [R][V] FP32 logits of the step
   float* bpart = nullptr;     // [R][ceil(V/256)][18] beam-epilogue partials (FP16 beam)
-  bool beam_epi = false;      // FP16 beam steps use the fused epilogue (env NMT_NO_BEAM_EPI: off)
+  bool beam_epi = false;      // FP16 beam steps use the fused epilogue (opt-in: env NMT_BEAM_EPI)
   float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
   float* dlcl_p = nullptr;    // [N][d] FP32 DLCL lookahead partial (kernels.h dlcl_combine)
   int* fused_ctr = nullptr;   // fused decode step: item / completion counters (decode_fused.cu)

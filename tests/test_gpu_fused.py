@@ -111,15 +111,15 @@ def test_beam_epilogue_matches_logits_path(name, n, lim):
     caps = np.minimum(wl.caps, lim["max_tgt_len"])
     res = {}
     for mode in ("logits", "epilogue"):
-        old = os.environ.pop("NMT_NO_BEAM_EPI", None)
-        if mode == "logits":
-            os.environ["NMT_NO_BEAM_EPI"] = "1"
+        old = os.environ.pop("NMT_BEAM_EPI", None)
+        if mode == "epilogue":
+            os.environ["NMT_BEAM_EPI"] = "1"
         try:
             m = Model(cfg, W, precision="fp16", **lim)
         finally:
-            os.environ.pop("NMT_NO_BEAM_EPI", None)
+            os.environ.pop("NMT_BEAM_EPI", None)
             if old is not None:
-                os.environ["NMT_NO_BEAM_EPI"] = old
+                os.environ["NMT_BEAM_EPI"] = old
         hyps, scores, _ = m.translate_nbest(wl.ids, wl.off, 2, 4, caps=caps)
         res[mode] = (hyps, scores)
         del m
