@@ -676,7 +676,15 @@ void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, cons
                      __half* out, int B, int S, int d, int H, int kclip, int use_rpr,
                      cudaStream_t s) {
   if (2 * kclip + 1 > RP - 1) throw CudaError("attn_encoder_tc: 2k+1 must be < 32");
-  static const bool legacy = getenv("NMT_ENC_ATTN") && atoi(getenv("NMT_ENC_ATTN")) == 0;  // A/B only
+  // NMT_ENC_ATTN (read per call; A/B and tests): 0 = one CTA per item (cp.async), 2 = the
+  // tcgen05 / TMEM kernel (attention_umma.cu), unset = the TMA-fed mma.sync pipeline
+  const char* ea = getenv("NMT_ENC_ATTN");
+  const int mode = ea ? atoi(ea) : 1;
+  if (mode == 2 && d / H == 64 && use_rpr && kclip <= 8 && relk && relv) {
+    attn_encoder_umma(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
+    return;
+  }
+  const bool legacy = mode == 0;
   if (d / H == 64 && !legacy) {
     launch_tma_sp(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s);
     NMT_LAUNCH_CHECK();
