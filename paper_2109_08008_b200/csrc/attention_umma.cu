@@ -123,42 +123,52 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
     }
   } else if (warp == 1) {
     if (lane == 0) {   // ------------------------------------------------ MMA issuer
-      auto qk = [&](int k) {   // S = Q K^T, QA = Q A^K^T of local tile k
-        const int sl = k & 1, bf = k & 1;
-        mbar_wait(&U.full[sl], (k >> 1) & 1);
-        mbar_wait(&U.tfree[bf], ((k >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* base = slots + sl * SLOT;
-        const uint32_t tS = tmem + bf * 256, tQA = tS + 128;
+      // Two independent streams: QK^T of tile kq (needs its Q / K / V slot loaded and its
+      // TMEM buffer drained) and P V of tile kp (needs its softmax done).  A blocking wait
+      // on one would stall the other (P V of tile k behind the TMA latency of tile k + 2),
+      // so the issuer polls both and issues whichever is ready.
+      int kq = 0, kp = 0;
+      while (kp < nloc) {
+        bool did = false;
+        if (kq < nloc && kq < kp + 2) {
+          const int sl = kq & 1;
+          if (mbar_try(&U.full[sl], (kq >> 1) & 1) && mbar_try(&U.tfree[sl], ((kq >> 1) & 1) ^ 1)) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint8_t* base = slots + sl * SLOT;
+            const uint32_t tS = tmem + sl * 256, tQA = tS + 128;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t dq = make_desc_sw128(base) + 2 * kk;
-          mma_f16(tS, dq, make_desc_sw128(base + TILE) + 2 * kk, idesc(128, 0), kk > 0);
-          mma_f16(tQA, dq, make_desc_sw128(sAK) + 2 * kk, idesc(32, 0), kk > 0);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t dq = make_desc_sw128(base) + 2 * kk;
+              mma_f16(tS, dq, make_desc_sw128(base + TILE) + 2 * kk, idesc(128, 0), kk > 0);
+              mma_f16(tQA, dq, make_desc_sw128(sAK) + 2 * kk, idesc(32, 0), kk > 0);
+            }
+            mma_commit(&U.sfull[sl]);
+            ++kq;
+            did = true;
+          }
         }
-        mma_commit(&U.sfull[bf]);
-      };
-      if (nloc > 0) qk(0);
-      for (int k = 0; k < nloc; ++k) {
-        if (k + 1 < nloc) qk(k + 1);
-        const int sl = k & 1, bf = k & 1;
-        mbar_wait(&U.pfull[bf], (k >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tO = tmem + bf * 256 + 160;
-        const uint8_t* vb = slots + sl * SLOT + 2 * TILE;
-        // O = P V: K = 128 keys; P K-major (two 64-key atom columns), V MN-major (8-key
-        // groups 1024 B apart: +2048 B per 16 keys)
+        if (kp < kq && mbar_try(&U.pfull[kp & 1], (kp >> 1) & 1)) {
+          const int sl = kp & 1, bf = kp & 1;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t tO = tmem + bf * 256 + 160;
+          const uint8_t* vb = slots + sl * SLOT + 2 * TILE;
+          // O = P V: K = 128 keys; P K-major (two 64-key atom columns), V MN-major (8-key
+          // groups 1024 B apart: +2048 B per 16 keys)
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_f16(tO, make_desc_sw128(sP + bf * PT + (kk >> 2) * TILE) + 2 * (kk & 3),
-                  make_desc_sw128(vb + kk * 2048), idesc(64, 1), kk > 0);
-        // O += B A^V: K = 32 buckets
+          for (int kk = 0; kk < 8; ++kk)
+            mma_f16(tO, make_desc_sw128(sP + bf * PT + (kk >> 2) * TILE) + 2 * (kk & 3),
+                    make_desc_sw128(vb + kk * 2048), idesc(64, 1), kk > 0);
+          // O += B A^V: K = 32 buckets
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-          mma_f16(tO, make_desc_sw128(sB + bf * BT) + 2 * kk, make_desc_sw128(sAV + kk * 2048),
-                  idesc(64, 1), 1u);
-        mma_commit(&U.ofull[bf]);
-        mma_commit(&U.empty[sl]);   // Q / K / V of this slot fully consumed
+          for (int kk = 0; kk < 2; ++kk)
+            mma_f16(tO, make_desc_sw128(sB + bf * BT) + 2 * kk, make_desc_sw128(sAV + kk * 2048),
+                    idesc(64, 1), 1u);
+          mma_commit(&U.ofull[bf]);
+          mma_commit(&U.empty[sl]);   // Q / K / V of this slot fully consumed
+          ++kp;
+          did = true;
+        }
+        if (!did) __nanosleep(20);
       }
     }
   } else if (warp >= 4) {   // ------------------------------------------------ softmax + epilogue
@@ -187,12 +197,12 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
 #pragma unroll 1
       for (int c0 = 0; c0 < SPP; c0 += 32) {
         float v[32];
-        tmem_ld32(trow + a * SPP + c0, v);
+        tmem_ld32(trow + ((a * SPP + c0) & ~31), v);   // SPP < 32: the item's keys within
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
-          const int j = c0 + jj;
+          const int j = c0 + jj - ((a * SPP) & 31);   // key index within the item
           const float s = (v[jj] + qa[min(max(j - i, -kclip), kclip) + kclip]) * sl2;
-          if (j < n) mx = fmaxf(mx, s);
+          if (j >= 0 && j < n) mx = fmaxf(mx, s);
         }
       }
       if (!row_ok) mx = 0.f;
@@ -211,18 +221,19 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
           *reinterpret_cast<uint4*>(prow + (kc >> 3) * TILE + swz(r, kc & 7)) = make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll 1
-      for (int c0 = 0; c0 < SPP; c0 += 32) {
+      for (int c0 = 0; c0 < (SPP < 32 ? 32 : SPP); c0 += 32) {
         float v[32];
-        tmem_ld32(trow + a * SPP + c0, v);
+        const int cb = (a * SPP + c0) & ~31;           // first tile column of this window
+        tmem_ld32(trow + cb, v);
         uint32_t hp[16];
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 2) {
           float p2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int j = c0 + jj + e, dj = j - i;
+            const int j = c0 + jj + e - ((a * SPP) & 31), dj = j - i;
             const float s = (v[jj + e] + qa[min(max(dj, -kclip), kclip) + kclip]) * sl2;
-            const float p = (row_ok && j < n) ? exp2f(s - mx) : 0.f;
+            const float p = (row_ok && j >= 0 && j < n) ? exp2f(s - mx) : 0.f;
             p2[e] = p;
             sum += p;
             lo += dj <= -kclip ? p : 0.f;
@@ -230,10 +241,10 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
           }
           hp[jj / 2] = pack_half2_sat(p2[0], p2[1]);
         }
-        // FP16 P into the K-major SW128 tile: key = a*SPP + c0 + 8*u + e
+        // FP16 P into the K-major SW128 tile: tile key = cb + 8*u + e
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int kc = (a * SPP + c0) / 8 + u;
+          const int kc = cb / 8 + u;
           *reinterpret_cast<uint4*>(prow + (kc >> 3) * TILE + swz(r, kc & 7)) =
               make_uint4(hp[4 * u], hp[4 * u + 1], hp[4 * u + 2], hp[4 * u + 3]);
         }
@@ -315,7 +326,9 @@ void attn_encoder_umma(const __half* qkv, const int* len, const __half* relk, co
                        __half* out, int B, int S, int d, int H, int kclip, cudaStream_t s) {
   if (d / H != 64 || S > 128 || kclip > 8 || kclip < 1 || !relk || !relv)
     throw CudaError("attn_encoder_umma: needs dh = 64, S <= 128, 1 <= k <= 8 and RPR tables");
-  if (S <= 32) ua::launch<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
+  if (S <= 8) ua::launch<8>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
+  else if (S <= 16) ua::launch<16>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
+  else if (S <= 32) ua::launch<32>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
   else if (S <= 64) ua::launch<64>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
   else ua::launch<128>(qkv, len, relk, relv, out, B, S, d, H, kclip, s);
   NMT_LAUNCH_CHECK();
