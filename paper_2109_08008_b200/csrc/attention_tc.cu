@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_
   constexpr int DH = 64, SP = NT * 8, NQ = SP / 16, LDH = DH + 8, LDB = RP + 8;
   constexpr int TILE = SP * 128, SLOT = 3 * TILE;
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on the __shared__ array (an integer round trip
+  // would hide the address space: generic LD/ST instead of LDS/STS)
+  uint8_t* sm = smraw + ((1024u - (smem_addr(smraw) & 1023u)) & 1023u);
   uint8_t* slots = sm;
   __half* sAK = reinterpret_cast<__half*>(sm + nslot * SLOT);
   __half* sAV = sAK + RP * LDH;

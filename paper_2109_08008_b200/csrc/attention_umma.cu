@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
     int B, int S, int d, int H, int kclip) {
   constexpr int IPT = 128 / SPP;         // items per tile
   extern __shared__ uint8_t smraw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);   // keeps the shared address space
   uint8_t* slots = sm;                             // [2][Q | K | V]
   uint8_t* sP = slots + 2 * SLOT;                  // [2][P]
   uint8_t* sB = sP + 2 * PT;                       // [2][B]

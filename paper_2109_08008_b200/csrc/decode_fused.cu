@@ -150,8 +150,7 @@ __device__ __forceinline__ int rows_per_item(int kind, int H) {
 template <int E, int DH>
 __global__ void __launch_bounds__(kThreadsF, 1) k_decode_fused(const __grid_constant__ FusedParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+  uint8_t* stages = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // shared address space kept
   Smem& S = *reinterpret_cast<Smem*>(stages + NST * STAGE);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nph = 2 + 8 * P.Ld;

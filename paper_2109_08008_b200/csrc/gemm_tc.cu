@@ -52,8 +52,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   constexpr int BBOX = BN > 256 ? 256 : BN;         // TMA box rows of B (<= 256)
   static_assert(!(PAIR && BN > 256), "pair units use BN <= 256");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on the __shared__ array: an integer round trip
+  // would hide the address space (generic LD/ST instead of LDS/STS in the epilogue)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi = smem + STAGES * SM::STAGE;   // 1024-B aligned (STAGE is a multiple of 1024)
   uint64_t* full = reinterpret_cast<uint64_t*>(epi + SM::EPI);
   uint64_t* empty = full + STAGES;
@@ -462,8 +463,9 @@ __global__ void __launch_bounds__(kCThreads, 3)
   using SM = Smem<BN, STAGES>;
   constexpr int LDP = BN + 4;  // padded FP32 partial row (conflict-light float4 stores)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on the __shared__ array: an integer round trip
+  // would hide the address space (generic LD/ST instead of LDS/STS in the epilogue)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // [BM][LDP] FP32 partial, written after the last MMA has drained every stage buffer
   float* part = reinterpret_cast<float*>(smem);
   static_assert(BM * LDP * 4 <= STAGES * SM::STAGE, "partial must fit in the stage buffers");
