@@ -33,7 +33,10 @@ constexpr int kThreadsU = 384;           // warps: 0 TMA, 1 MMA, 2 TMEM, 3 idle,
 constexpr uint32_t kTmemCols = 512;      // two buffers x (S 128 + QA 32 + O 64, padded to 256)
 
 struct USmem {
-  uint64_t full[2], empty[2], sfull[2], pfull[2], ofull[2], tfree[2];
+  // Q / K and V of a slot are loaded and released separately: Q / K are consumed by the
+  // QK^T MMA (released early, so the next tile's loads overlap this tile's softmax), V by
+  // P V
+  uint64_t full[2], empty[2], vfull[2], vempty[2], sfull[2], pfull[2], ofull[2], tfree[2];
   uint32_t tmem;
   float qa[2][128][17];                  // per group: q . A^K rows (FP32, bucket-indexed)
 };
@@ -71,6 +74,8 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
     for (int i = 0; i < 2; ++i) {
       mbar_init(&U.full[i], 1);
       mbar_init(&U.empty[i], 1);
+      mbar_init(&U.vfull[i], 1);
+      mbar_init(&U.vempty[i], 1);
       mbar_init(&U.sfull[i], 1);
       mbar_init(&U.pfull[i], 4);
       mbar_init(&U.ofull[i], 1);
@@ -104,21 +109,44 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
 
   if (warp == 0) {
     if (lane == 0) {   // ------------------------------------------------ TMA producer
-      for (int k = 0; k < nloc; ++k) {
-        const int sl = k & 1, t = c + k * G;
-        mbar_wait(&U.empty[sl], ((k >> 1) & 1) ^ 1);
-        mbar_expect_tx(&U.full[sl], IPT * 3 * SPP * 128);
-        uint8_t* dst = slots + sl * SLOT;
-#pragma unroll
-        for (int a = 0; a < IPT; ++a) {
-          const int it = t * IPT + a;
-          // a missing item (last tile) loads rows past the tensor: zero-filled by TMA
-          const int b = it < items ? it / H : B + 2, h = it < items ? it % H : 0;
-          const int y = it < items ? b * S : B * S + 256;
-          tma_load_2d(dst + a * SPP * 128, &mqkv, &U.full[sl], h * 64, y);
-          tma_load_2d(dst + TILE + a * SPP * 128, &mqkv, &U.full[sl], d + h * 64, y);
-          tma_load_2d(dst + 2 * TILE + a * SPP * 128, &mqkv, &U.full[sl], 2 * d + h * 64, y);
+      // two streams (Q / K of tile kq, V of tile kv), issued as their slots free up
+      auto src_row = [&](int t, int a, int& h) {
+        const int it = t * IPT + a;
+        // a missing item (last tile) loads rows past the tensor: zero-filled by TMA
+        h = it < items ? it % H : 0;
+        return it < items ? (it / H) * S : B * S + 256;
+      };
+      int kq = 0, kv = 0;
+      while (kv < nloc) {
+        bool did = false;
+        if (kq < nloc && kq < kv + 2 && mbar_try(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
+          const int sl = kq & 1, t = c + kq * G;
+          mbar_expect_tx(&U.full[sl], IPT * 2 * SPP * 128);
+          uint8_t* dst = slots + sl * SLOT;
+#pragma unroll 1
+          for (int a = 0; a < IPT; ++a) {
+            int h;
+            const int y = src_row(t, a, h);
+            tma_load_2d(dst + a * SPP * 128, &mqkv, &U.full[sl], h * 64, y);
+            tma_load_2d(dst + TILE + a * SPP * 128, &mqkv, &U.full[sl], d + h * 64, y);
+          }
+          ++kq;
+          did = true;
         }
+        if (kv < kq && mbar_try(&U.vempty[kv & 1], ((kv >> 1) & 1) ^ 1)) {
+          const int sl = kv & 1, t = c + kv * G;
+          mbar_expect_tx(&U.vfull[sl], IPT * SPP * 128);
+          uint8_t* dst = slots + sl * SLOT + 2 * TILE;
+#pragma unroll 1
+          for (int a = 0; a < IPT; ++a) {
+            int h;
+            const int y = src_row(t, a, h);
+            tma_load_2d(dst + a * SPP * 128, &mqkv, &U.vfull[sl], 2 * d + h * 64, y);
+          }
+          ++kv;
+          did = true;
+        }
+        if (!did) __nanosleep(20);
       }
     }
   } else if (warp == 1) {
@@ -143,11 +171,13 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
               mma_f16(tQA, dq, make_desc_sw128(sAK) + 2 * kk, idesc(32, 0), kk > 0);
             }
             mma_commit(&U.sfull[sl]);
+            mma_commit(&U.empty[sl]);   // Q / K consumed: the next tile's Q / K may load
             ++kq;
             did = true;
           }
         }
-        if (kp < kq && mbar_try(&U.pfull[kp & 1], (kp >> 1) & 1)) {
+        if (kp < kq && mbar_try(&U.pfull[kp & 1], (kp >> 1) & 1) &&
+            mbar_try(&U.vfull[kp & 1], (kp >> 1) & 1)) {
           const int sl = kp & 1, bf = kp & 1;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t tO = tmem + bf * 256 + 160;
@@ -164,7 +194,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
             mma_f16(tO, make_desc_sw128(sB + bf * BT) + 2 * kk, make_desc_sw128(sAV + kk * 2048),
                     idesc(64, 1), 1u);
           mma_commit(&U.ofull[bf]);
-          mma_commit(&U.empty[sl]);   // Q / K / V of this slot fully consumed
+          mma_commit(&U.vempty[sl]);   // V of this slot consumed
           ++kp;
           did = true;
         }
