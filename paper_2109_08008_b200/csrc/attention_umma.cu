@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       int kq = 0, kv = 0;
       while (kv < nloc) {
         bool did = false;
-        if (kq < nloc && kq < kv + 2 && mbar_try(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
+        if (kq < nloc && kq < kv + 2 && mbar_test(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
           const int sl = kq & 1, t = c + kq * G;
           mbar_expect_tx(&U.full[sl], IPT * 2 * SPP * 128);
           uint8_t* dst = slots + sl * SLOT;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
           ++kq;
           did = true;
         }
-        if (kv < kq && mbar_try(&U.vempty[kv & 1], ((kv >> 1) & 1) ^ 1)) {
+        if (kv < kq && mbar_test(&U.vempty[kv & 1], ((kv >> 1) & 1) ^ 1)) {
           const int sl = kv & 1, t = c + kv * G;
           mbar_expect_tx(&U.vfull[sl], IPT * SPP * 128);
           uint8_t* dst = slots + sl * SLOT + 2 * TILE;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
         bool did = false;
         if (kq < nloc && kq < kp + 2) {
           const int sl = kq & 1;
-          if (mbar_try(&U.full[sl], (kq >> 1) & 1) && mbar_try(&U.tfree[sl], ((kq >> 1) & 1) ^ 1)) {
+          if (mbar_test(&U.full[sl], (kq >> 1) & 1) && mbar_test(&U.tfree[sl], ((kq >> 1) & 1) ^ 1)) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint8_t* base = slots + sl * SLOT;
             const uint32_t tS = tmem + sl * 256, tQA = tS + 128;
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
             did = true;
           }
         }
-        if (kp < kq && mbar_try(&U.pfull[kp & 1], (kp >> 1) & 1) &&
-            mbar_try(&U.vfull[kp & 1], (kp >> 1) & 1)) {
+        if (kp < kq && mbar_test(&U.pfull[kp & 1], (kp >> 1) & 1) &&
+            mbar_test(&U.vfull[kp & 1], (kp >> 1) & 1)) {
           const int sl = kp & 1, bf = kp & 1;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t tO = tmem + bf * 256 + 160;
