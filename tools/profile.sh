@@ -6,7 +6,7 @@
 tag=${1:-r1}
 out=gpurun_out
 mkdir -p $out
-B="python bench.py --steps 1 --warmup 0 --chunk ${CHUNK:-3000} --no-e2e --no-cpu-baseline --workers 1"
+B="python bench.py --steps 1 --warmup 0 --chunk ${CHUNK:-3000} --no-e2e --no-cpu-baseline --no-paper-budget --no-c4 --workers 1"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${NLAUNCH:-3000} --csv \
   --log-file $out/${tag}_launches.csv $B > $out/${tag}_launches.log 2>&1
 echo "launches rc=$?"
