@@ -107,18 +107,19 @@ _WL = None
 
 
 def _oracle_worker(args):
-    lo, hi, mt, ms = args
+    lo, hi, mt, ms, nth = args
     from threadpoolctl import threadpool_limits
     from oracle import translate_fast
-    with threadpool_limits(1):
+    with threadpool_limits(nth):
         log = {}
         translate_fast(_OM, _WL.shard(lo, hi), mt, ms, prune_ratio=0.25, log=log)
     return log["gen_tokens"]
 
 
-def oracle_timed(cfg, W, wl, workers, max_tokens=4096, max_sents=512):
+def oracle_timed(cfg, W, wl, workers, max_tokens=4096, max_sents=512, threads=1):
     """O-fast (FP32 NumPy, cached + batched + pruned) as it stands, `workers` processes with
-    one BLAS thread each on contiguous shards (the paper's CPU scheme)."""
+    `threads` BLAS threads each on contiguous shards (the paper's CPU scheme, PAPER.md:129-131;
+    its CPU track ran 24 processes x 2 MKL threads with 64-sentence batches)."""
     global _OM, _WL
     import multiprocessing as mp
     from oracle import OracleModel
@@ -126,8 +127,8 @@ def oracle_timed(cfg, W, wl, workers, max_tokens=4096, max_sents=512):
     _WL = wl
     n = wl.n
     bounds = np.linspace(0, n, workers + 1).astype(int)
-    jobs = [(int(bounds[i]), int(bounds[i + 1]), max_tokens, max_sents) for i in range(workers)
-            if bounds[i + 1] > bounds[i]]
+    jobs = [(int(bounds[i]), int(bounds[i + 1]), max_tokens, max_sents, threads)
+            for i in range(workers) if bounds[i + 1] > bounds[i]]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(len(jobs)) as pool:
@@ -374,6 +375,8 @@ def main():
                     help="concurrent batch workers per GPU (own arena + stream, shared weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sents-per-worker", type=int, default=40)
+    ap.add_argument("--cpu-threads", type=int, default=0, help="BLAS threads per oracle process")
+    ap.add_argument("--cpu-max-sents", type=int, default=0, help="oracle batch cap (sentences)")
     ap.add_argument("--no-paper-tok-s", action="store_true",
                     help="skip the tok/s run at the paper's 4096 / 512 budget")
     ap.add_argument("--ref-sents-per-worker", type=int, default=12)
@@ -412,13 +415,18 @@ def main():
         # per core, one BLAS thread each) with the paper's batch plan
         # (4096 tokens / 512 sentences), on a bounded slice of the same
         # synthetic set (the 2,998-sentence subset takes minutes: --cpu-sents-per-worker)
-        workers = min(cpu_cores(), 64)
-        wl = newstest_like(workers * args.cpu_sents_per_worker, cfg.vocab_size, start=900_000)
-        t, dt, used = oracle_timed(cfg, W, wl, workers, 4096, 512)
-        cpu = {"value": t / dt, "unit": UNIT, "cores": used, "kind": "oracle",
+        # the CPU-track model (9-1-tiny, §8(f) f4) runs the paper's CPU scheme: 2 BLAS threads
+        # per process, 64-sentence batches
+        tiny = args.config == "student-9-1-tiny"
+        nth = args.cpu_threads or (2 if tiny else 1)
+        cms = args.cpu_max_sents or (64 if tiny else 512)
+        workers = max(1, min(cpu_cores(), 64) // nth)
+        wl = newstest_like(workers * args.cpu_sents_per_worker * nth, cfg.vocab_size, start=900_000)
+        t, dt, used = oracle_timed(cfg, W, wl, workers, 4096, cms, nth)
+        cpu = {"value": t / dt, "unit": UNIT, "cores": used * nth, "kind": "oracle",
                "sample": f"{wl.n} sentences (sentences 900000.. of the synthetic 1M set), "
-                         f"{used} processes x 1 BLAS thread, O-fast FP32, batch plan 4096 / 512, "
-                         f"{dt:.1f} s", **host_info()}
+                         f"{used} processes x {nth} BLAS thread(s), O-fast FP32, batch plan "
+                         f"4096 / {cms}, {dt:.1f} s", **host_info()}
         if not args.no_odef:
             cpu["odef"] = odef_timing(cfg, W, wl)
 
@@ -564,7 +572,8 @@ def main():
                            "max_tokens": 4096, "max_sents": 512, "workers": args.workers,
                            "sentences": wl_p.n, "decode_steps": stp["decode_steps"],
                            "whole_run_frac": None}
-            paper_tok_s["whole_run_frac"] = paper_tok_s["value"] / MODEL_TOK_S["4096/512"]["burst"]
+            if args.config == "student-35-1":
+                paper_tok_s["whole_run_frac"] = paper_tok_s["value"] / MODEL_TOK_S["4096/512"]["burst"]
         pm.translate_device(torch.from_numpy(sub.ids).cuda(), sub.off, d_out, d_len, caps=sub.caps,
                             sync_every=args.sync_every, workers=1)   # warm (graphs)
         pm.profile(3)
@@ -674,7 +683,8 @@ def main():
             # achieved tok/s / SURVEY §8(d)'s whole-run roofline model at this budget
             "whole_run_frac": ({k: value / v for k, v in
                                 MODEL_TOK_S[f"{args.max_tokens}/{args.max_sents}"].items()}
-                               if f"{args.max_tokens}/{args.max_sents}" in MODEL_TOK_S else None),
+                               if f"{args.max_tokens}/{args.max_sents}" in MODEL_TOK_S
+                               and args.config == "student-35-1" else None),
             "out_tokens_per_s": out_tok_s, "sentences_per_s": sents_s,
             "decode_steps": int(steps_all), "gen_tokens": int(gen_all),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,

@@ -64,6 +64,11 @@ PRESETS = {
     "student-35-6": ModelConfig(enc_layers=35, dec_layers=6),
     "student-18-1": ModelConfig(enc_layers=18, dec_layers=1),
     "student-9-1": ModelConfig(enc_layers=9, dec_layers=1),
+    # §8(f) row f4, the CPU-track model 9-1-tiny: "the same
+    # settings as the 9-1 model except that the model size is 256" — reading R30: d = 256,
+    # F = 4d = 1024, the 9-1's 8 heads (dh = 32), DLCL + RPR, tied E: 16.4M parameters
+    # (the "90%" reduction vs 35-6, and Table 3's 67 MiB as FP32)
+    "student-9-1-tiny": ModelConfig(enc_layers=9, dec_layers=1, d_model=256, n_heads=8, d_ffn=1024),
     "teacher-40-6": ModelConfig(enc_layers=40, dec_layers=6),
     # the four ensemble teachers (Table 1), §8(f) row f1
     "ens-35-6": ModelConfig(enc_layers=35, dec_layers=6, use_dlcl=False),

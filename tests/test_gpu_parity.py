@@ -168,7 +168,7 @@ def test_tiny_teacher_forced(prec):
 
 
 @pytest.mark.parametrize("prec", PRECS)
-@pytest.mark.parametrize("name", ["student-6-1", "student-35-1"])
+@pytest.mark.parametrize("name", ["student-6-1", "student-35-1", "student-9-1-tiny"])
 def test_base_teacher_forced(prec, name):
     wl = newstest_like(24, 32000)
     srcs = [wl.sentence(i) for i in range(wl.n)]
@@ -250,10 +250,12 @@ def test_prune_maps_bit_exact(prec):
 
 
 @pytest.mark.parametrize("prec", PRECS)
-def test_35_1_free_running_subset(prec):
+@pytest.mark.parametrize("name", ["student-35-1", "student-9-1-tiny"])
+def test_35_1_free_running_subset(prec, name):
+    """Free-running greedy with pruning vs O-fast: 35-1 (C3) and the CPU-track 9-1-tiny
+    (§8(f) f4, d = 256, dh = 32, the CPU batch cap of 64 sentences scaled to 16 here)."""
     wl = newstest_like(40, 32000)
-    n_cmp, st, log = _free_running("student-35-1", prec, wl, eos_boost=1.0, max_tokens=512,
-                                   max_sents=16)
+    n_cmp, st, log = _free_running(name, prec, wl, eos_boost=1.0, max_tokens=512, max_sents=16)
     assert n_cmp > 0
 
 

@@ -59,3 +59,18 @@ def test_ffn_width_is_2048():
     # F=2048 is the only power-of-two width reproducing 131M for 35-1
     hits = [F for F in (1024, 2048, 4096) if round(param_count(PRESETS["student-35-1"].replace(d_ffn=F), False) / 1e6) == 131]
     assert hits == [2048]
+
+
+def test_tiny_cpu_model_reading():
+    """Reading R30 for 9-1-tiny: 16.4M parameters reproduce the printed ~90%
+    reduction vs 35-6 and Table 3's 67 MiB as an FP32 file (within 3%, the other Table 3
+    rows are within 1.2% as FP16); the 25M of Table 2 is the contradicting statement."""
+    g = _golden()
+    n = param_count(PRESETS["student-9-1-tiny"], False)
+    red = 1.0 - n / param_count(PRESETS["student-35-6"], False)
+    assert abs(red - g["reduction:student-9-1-tiny"]) < 0.015, red
+    mb32 = n * 4 / 1e6
+    assert 0 <= g["fp32_mib:student-9-1-tiny"] - mb32 <= 0.03 * g["fp32_mib:student-9-1-tiny"], mb32
+    # the other widths do not: F = 2048 gives 21.6M (86 MB FP32), 86% reduction
+    wide = param_count(PRESETS["student-9-1-tiny"].replace(d_ffn=2048), False)
+    assert wide * 4 / 1e6 > 80
