@@ -884,6 +884,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "256x3w16") tc::launch<256, 3, 16>(a, s);
     else if (c == "128x4w16") tc::launch<128, 4, 16>(a, s);
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
+    else if (c == "pair256x5") tc::launch_pair<256, 5>(a, s);
+    else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
     else if (c == "512x2") tc::launch<512, 2>(a, s);
     else if (c == "256x3d") tc::launch<256, 3, 8, 2>(a, s);
     else tc::launch<256, 4>(a, s);
