@@ -18,7 +18,8 @@ PRECS = ["fp32", "fp16"]
 # ------------------------------------------------------------------ GEMM units
 @pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (3, 512, 512), (148, 1536, 512), (300, 2048, 512),
-                                   (129, 512, 2048), (4096, 512, 512), (77, 1000, 64), (512, 32000, 512)])
+                                   (129, 512, 2048), (4096, 512, 512), (77, 1000, 64), (512, 32000, 512),
+                                   (4099, 512, 2048)])
 def test_gemm_unit(prec, M, N, K):
     from paper_2109_08008_b200 import dev_gemm
     g = torch.Generator().manual_seed(M * 7 + N + K)
