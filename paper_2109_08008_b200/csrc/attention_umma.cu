@@ -30,13 +30,15 @@ constexpr int SLOT = 3 * TILE;           // Q, K, V
 constexpr int PT = 2 * TILE;             // P [128 rows][128 keys] = two SW128 atoms columns
 constexpr int BT = TILE;                 // bucket sums [128][64] (32 used)
 constexpr int kThreadsU = 384;           // warps: 0 TMA, 1 MMA, 2 TMEM, 3 idle, 4-11 softmax
-constexpr uint32_t kTmemCols = 512;      // two buffers x (S 128 + QA 32 + O 64, padded to 256)
+constexpr uint32_t kTmemCols = 512;      // three buffers x (S / O 128 + QA 32) = 480
+constexpr int NTB = 3;                   // TMEM buffers: tiles in flight between QK^T and the epilogue
+constexpr uint32_t TBC = 160;            // columns per TMEM buffer: S [0,128), O aliases S [64,128), QA [128,160)
 
 struct USmem {
   // Q / K and V of a slot are loaded and released separately: Q / K are consumed by the
   // QK^T MMA (released early, so the next tile's loads overlap this tile's softmax), V by
   // P V
-  uint64_t full[2], empty[2], vfull[2], vempty[2], sfull[2], pfull[2], ofull[2], tfree[2];
+  uint64_t full[2], empty[2], vfull[2], vempty[2], pfull[2], sfull[NTB], ofull[NTB], tfree[NTB];
   uint32_t tmem;
   float qa[2][128][17];                  // per group: q . A^K rows (FP32, bucket-indexed)
 };
@@ -76,8 +78,10 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       mbar_init(&U.empty[i], 1);
       mbar_init(&U.vfull[i], 1);
       mbar_init(&U.vempty[i], 1);
-      mbar_init(&U.sfull[i], 1);
       mbar_init(&U.pfull[i], 4);
+    }
+    for (int i = 0; i < NTB; ++i) {
+      mbar_init(&U.sfull[i], 1);
       mbar_init(&U.ofull[i], 1);
       mbar_init(&U.tfree[i], 4);
     }
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       int kq = 0, kv = 0;
       while (kv < nloc) {
         bool did = false;
-        if (kq < nloc && kq < kv + 2 && mbar_test(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
+        if (kq < nloc && mbar_test(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
           const int sl = kq & 1, t = c + kq * G;
           mbar_expect_tx(&U.full[sl], IPT * 2 * SPP * 128);
           uint8_t* dst = slots + sl * SLOT;
@@ -158,19 +162,19 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       int kq = 0, kp = 0;
       while (kp < nloc) {
         bool did = false;
-        if (kq < nloc && kq < kp + 2) {
-          const int sl = kq & 1;
-          if (mbar_test(&U.full[sl], (kq >> 1) & 1) && mbar_test(&U.tfree[sl], ((kq >> 1) & 1) ^ 1)) {
+        if (kq < nloc && kq < kp + NTB) {
+          const int sl = kq & 1, tb = kq % NTB;
+          if (mbar_test(&U.full[sl], (kq >> 1) & 1) && mbar_test(&U.tfree[tb], ((kq / NTB) & 1) ^ 1)) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint8_t* base = slots + sl * SLOT;
-            const uint32_t tS = tmem + sl * 256, tQA = tS + 128;
+            const uint32_t tS = tmem + tb * TBC, tQA = tS + 128;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t dq = make_desc_sw128(base) + 2 * kk;
               mma_f16(tS, dq, make_desc_sw128(base + TILE) + 2 * kk, idesc(128, 0), kk > 0);
               mma_f16(tQA, dq, make_desc_sw128(sAK) + 2 * kk, idesc(32, 0), kk > 0);
             }
-            mma_commit(&U.sfull[sl]);
+            mma_commit(&U.sfull[tb]);
             mma_commit(&U.empty[sl]);   // Q / K consumed: the next tile's Q / K may load
             ++kq;
             did = true;
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
             mbar_test(&U.vfull[kp & 1], (kp >> 1) & 1)) {
           const int sl = kp & 1, bf = kp & 1;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t tO = tmem + bf * 256 + 160;
+          const uint32_t tO = tmem + (kp % NTB) * TBC + 64;   // aliases S: read before pfull
           const uint8_t* vb = slots + sl * SLOT + 2 * TILE;
           // O = P V: K = 128 keys; P K-major (two 64-key atom columns), V MN-major (8-key
           // groups 1024 B apart: +2048 B per 16 keys)
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
           for (int kk = 0; kk < 2; ++kk)
             mma_f16(tO, make_desc_sw128(sB + bf * BT) + 2 * kk, make_desc_sw128(sAV + kk * 2048),
                     idesc(64, 1), 1u);
-          mma_commit(&U.ofull[bf]);
+          mma_commit(&U.ofull[kp % NTB]);
           mma_commit(&U.vempty[sl]);   // V of this slot consumed
           ++kp;
           did = true;
@@ -212,9 +216,10 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       const int b = item_ok ? it / H : 0, h = item_ok ? it % H : 0;
       const int n = item_ok ? len[b] : 0;
       const bool row_ok = i < n;
-      mbar_wait(&U.sfull[bf], (k >> 1) & 1);
+      const int tb = k % NTB;
+      mbar_wait(&U.sfull[tb], (k / NTB) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t trow = tmem + bf * 256 + ((uint32_t)(q * 32) << 16);
+      const uint32_t trow = tmem + tb * TBC + ((uint32_t)(q * 32) << 16);
       float* qa = U.qa[grp][r];
       {
         float v[32];
@@ -303,14 +308,14 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       if (lane == 0) mbar_arrive(&U.pfull[bf]);
       // epilogue: O / sum -> FP16 (query rows in [n, S) written as 0; rows >= S belong to
       // the next sentence)
-      mbar_wait(&U.ofull[bf], (k >> 1) & 1);
+      mbar_wait(&U.ofull[tb], (k / NTB) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float o[64];
-      tmem_ld32(trow + 160, o);
-      tmem_ld32(trow + 192, o + 32);
+      tmem_ld32(trow + 64, o);
+      tmem_ld32(trow + 96, o + 32);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&U.tfree[bf]);
+      if (lane == 0) mbar_arrive(&U.tfree[tb]);
       if (item_ok && i < S) {
         const float inv = row_ok && sum > 0.f ? 1.f / sum : 0.f;
         uint4* orow = reinterpret_cast<uint4*>(out + ((size_t)b * S + i) * d + h * 64);
