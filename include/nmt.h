@@ -323,6 +323,12 @@ nmt_status nmt_profile_steps(nmt_model* m, nmt_step_rec* out, int32_t cap, int32
  * NMT_E_STATE when the model was loaded without the variable. */
 nmt_status nmt_debug_fused_trace(nmt_model* m, uint64_t* h_out, int64_t cap);
 
+/* Debug timeline of the last tcgen05 encoder-attention launch (NMT_ENC_ATTN=2 with the
+ * environment variable NMT_ATTN_TRACE set at the first launch): CTA 0, per local tile k < 64,
+ * 8 globaltimer stamps {Q/K TMA, V TMA, QK^T issued, S seen, P ready, P V issued, O seen,
+ * TMEM freed} at h_out[8k + e].  Synchronises the device. */
+nmt_status nmt_debug_attn_trace(uint64_t* h_out, int64_t cap);
+
 /* ---- kernel-level entry points used by the unit parity tests ------------------- */
 /* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision
  * (FP16: tcgen05/TMEM/TMA tensor-core GEMM; FP32: SIMT), all pointers device, row-major

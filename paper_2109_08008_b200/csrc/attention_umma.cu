@@ -43,6 +43,18 @@ struct USmem {
   float qa[2][128][17];                  // per group: q . A^K rows (FP32, bucket-indexed)
 };
 
+// debug timeline of CTA 0 (nmt_debug_attn_trace): per local tile k < 64, 8 globaltimer
+// stamps {Q/K TMA issued, V TMA issued, QK^T issued, S seen by softmax, P ready,
+// P V issued, O seen by epilogue, TMEM freed}
+__device__ unsigned long long g_ua_trace[64 * 8];
+__device__ __forceinline__ unsigned long long ua_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define UA_TR(k, e) \
+  do { if (trace && blockIdx.x == 0 && (k) < 64) g_ua_trace[(k) * 8 + (e)] = ua_now(); } while (0)
+
 __device__ __forceinline__ uint32_t swz(int r, int chunk) {   // SW128 byte offset of (row, 16-B chunk)
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4));
 }
@@ -56,7 +68,7 @@ template <int SPP>
 __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
     const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
     const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
-    int B, int S, int d, int H, int kclip) {
+    int B, int S, int d, int H, int kclip, int trace) {
   constexpr int IPT = 128 / SPP;         // items per tile
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);   // keeps the shared address space
@@ -125,6 +137,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
         bool did = false;
         if (kq < nloc && mbar_test(&U.empty[kq & 1], ((kq >> 1) & 1) ^ 1)) {
           const int sl = kq & 1, t = c + kq * G;
+          UA_TR(kq, 0);
           mbar_expect_tx(&U.full[sl], IPT * 2 * SPP * 128);
           uint8_t* dst = slots + sl * SLOT;
 #pragma unroll 1
@@ -139,6 +152,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
         }
         if (kv < kq && mbar_test(&U.vempty[kv & 1], ((kv >> 1) & 1) ^ 1)) {
           const int sl = kv & 1, t = c + kv * G;
+          UA_TR(kv, 1);
           mbar_expect_tx(&U.vfull[sl], IPT * SPP * 128);
           uint8_t* dst = slots + sl * SLOT + 2 * TILE;
 #pragma unroll 1
@@ -175,6 +189,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
               mma_f16(tQA, dq, make_desc_sw128(sAK) + 2 * kk, idesc(32, 0), kk > 0);
             }
             mma_commit(&U.sfull[tb]);
+            UA_TR(kq, 2);
             mma_commit(&U.empty[sl]);   // Q / K consumed: the next tile's Q / K may load
             ++kq;
             did = true;
@@ -198,6 +213,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
             mma_f16(tO, make_desc_sw128(sB + bf * BT) + 2 * kk, make_desc_sw128(sAV + kk * 2048),
                     idesc(64, 1), 1u);
           mma_commit(&U.ofull[kp % NTB]);
+          UA_TR(kp, 5);
           mma_commit(&U.vempty[sl]);   // V of this slot consumed
           ++kp;
           did = true;
@@ -218,6 +234,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       const bool row_ok = i < n;
       const int tb = k % NTB;
       mbar_wait(&U.sfull[tb], (k / NTB) & 1);
+      if (r == 0) UA_TR(k, 3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + tb * TBC + ((uint32_t)(q * 32) << 16);
       float* qa = U.qa[grp][r];
@@ -306,9 +323,11 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&U.pfull[bf]);
+      if (r == 0) UA_TR(k, 4);
       // epilogue: O / sum -> FP16 (query rows in [n, S) written as 0; rows >= S belong to
       // the next sentence)
       mbar_wait(&U.ofull[tb], (k / NTB) & 1);
+      if (r == 0) UA_TR(k, 6);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float o[64];
       tmem_ld32(trow + 64, o);
@@ -316,6 +335,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&U.tfree[tb]);
+      if (r == 0) UA_TR(k, 7);
       if (item_ok && i < S) {
         const float inv = row_ok && sum > 0.f ? 1.f / sum : 0.f;
         uint4* orow = reinterpret_cast<uint4*>(out + ((size_t)b * S + i) * d + h * 64);
@@ -350,11 +370,17 @@ void launch(const __half* qkv, const int* len, const __half* relk, const __half*
   const CUtensorMap map = make_map(qkv, B * S, 3 * d, 3 * d, SPP);
   const int tiles = (B * H + (128 / SPP) - 1) / (128 / SPP);
   const int grid = std::min(tiles, num_sms());
+  static const int trace = getenv("NMT_ATTN_TRACE") ? 1 : 0;   // debug timeline (CTA 0)
   launch_k(k_attn_enc_umma<SPP>, dim3(grid), dim3(kThreadsU), smem_bytes(), s, map, len, relk, relv,
-           out, B, S, d, H, kclip);
+           out, B, S, d, H, kclip, trace);
 }
 
 }  // namespace ua
+
+void attn_umma_trace(unsigned long long* h_out, int cap) {
+  NMT_CUDA(cudaDeviceSynchronize());
+  NMT_CUDA(cudaMemcpyFromSymbol(h_out, ua::g_ua_trace, sizeof(unsigned long long) * std::min(cap, 64 * 8)));
+}
 
 // FP16, dh = 64, S <= 128, RPR on (the tables are required: zero tables give vanilla attention).
 void attn_encoder_umma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
