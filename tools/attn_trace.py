@@ -21,11 +21,11 @@ relk = torch.randn(17, 64, dtype=torch.float16, device="cuda") * 0.5
 relv = torch.randn(17, 64, dtype=torch.float16, device="cuda") * 0.5
 for _ in range(3):
     dev_attn_encoder(qkv, ln, relk, relv, B, S, H, kc)
-buf = (C.c_uint64 * 512)()
-_check(lib().nmt_debug_attn_trace(buf, 512))
-a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(64, 8)
+buf = (C.c_uint64 * 1024)()
+_check(lib().nmt_debug_attn_trace(buf, 1024))
+a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64).reshape(64, 16)[:, :13]
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
-print("tile  qkTMA  vTMA  QKiss  Sseen  Pready  PViss  Oseen  Tfree   (us from first TMA)")
+print("tile  qkTMA  vTMA  QKiss  Sseen  Pready  PViss  Oseen  Tfree  qa_dn  p1_dn  p2_dn  bnd_dn fence_dn")
 for k, r in enumerate(a[:20]):
     print(f"{k:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in r))
