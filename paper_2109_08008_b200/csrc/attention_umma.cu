@@ -314,15 +314,6 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
             hi += dj >= kclip ? p : 0.f;
           }
           hp[jj / 2] = pack_half2_sat(p2[0], p2[1]);
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {   // band buckets (FP16 values equal to P's)
-            const int j = 32 * ch + jj + e - off, dj = j - i;
-            if (row_ok && j >= 0 && j < n && dj > -kclip && dj < kclip) {
-              const int bk = dj + kclip;
-              *reinterpret_cast<uint16_t*>(brow + swz(r, bk >> 3) + (bk & 7) * 2) =
-                  (uint16_t)(e ? hp[jj / 2] >> 16 : hp[jj / 2] & 0xffffu);
-            }
-          }
         }
         // FP16 P into the K-major SW128 tile: tile key = cb0 + 32 ch + 8 u + e
 #pragma unroll
@@ -353,6 +344,25 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
         }
       }
       if (r == 0) UA_TR(k, 10);
+      if (row_ok) {
+        // band buckets: one key each, B[r][j - i + k] = the FP16 P_ij the MMA uses (read back
+        // from this thread's P row; static offsets: the loads are issued together)
+        __half bv[15];
+#pragma unroll
+        for (int dd = -7; dd <= 7; ++dd) {
+          const int j = i + dd, key = a * SPP + j;
+          bv[dd + 7] = (dd > -kclip && dd < kclip && j >= 0 && j < n)
+                           ? *reinterpret_cast<const __half*>(prow + (key >> 6) * TILE +
+                                                              swz(r, (key >> 3) & 7) + (key & 7) * 2)
+                           : __half();
+        }
+#pragma unroll
+        for (int dd = -7; dd <= 7; ++dd) {
+          const int bk = dd + kclip;
+          if (dd > -kclip && dd < kclip)
+            *reinterpret_cast<__half*>(brow + swz(r, bk >> 3) + (bk & 7) * 2) = bv[dd + 7];
+        }
+      }
       if (row_ok) {   // the clipped ends
         *reinterpret_cast<__half*>(brow + swz(r, 0)) = __float2half(lo);
         *reinterpret_cast<__half*>(brow + swz(r, (2 * kclip) >> 3) + ((2 * kclip) & 7) * 2) =
