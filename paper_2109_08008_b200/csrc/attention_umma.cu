@@ -255,6 +255,11 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       tmem_touch(v[0]);
 #pragma unroll
       for (int e = 0; e < 17; ++e) qa[e] = __uint_as_float(vq[e]);
+      // the clipped ends in registers; only band keys (|j - i| < k) look the table up
+      const float qlo = __uint_as_float(vq[0]), qhi = qa[2 * kclip];
+      auto rel = [&](int dj) {
+        return dj <= -kclip ? qlo : dj >= kclip ? qhi : qa[dj + kclip];
+      };
       if (r == 0) UA_TR(k, 8);
       // pass 1: row maximum of the scaled scores over this item's keys j < n
       float mx = -INFINITY;
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const int j = 32 * ch + jj - off;      // key index within the item
-          const float sc = (__uint_as_float(vv[jj]) + qa[min(max(j - i, -kclip), kclip) + kclip]) * sl2;
+          const float sc = (__uint_as_float(vv[jj]) + rel(j - i)) * sl2;
           if (j >= 0 && j < n) mx = fmaxf(mx, sc);
         }
       };
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 32 * ch + jj + e - off, dj = j - i;
-            const float sc = (__uint_as_float(vv[jj + e]) + qa[min(max(dj, -kclip), kclip) + kclip]) * sl2;
+            const float sc = (__uint_as_float(vv[jj + e]) + rel(dj)) * sl2;
             const float p = (row_ok && j >= 0 && j < n) ? exp2f(sc - mx) : 0.f;
             p2[e] = p;
             sum += p;
