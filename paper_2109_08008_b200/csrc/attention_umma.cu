@@ -238,81 +238,56 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + tb * TBC + ((uint32_t)(q * 32) << 16);
       float* qa = U.qa[grp][r];
-      uint8_t* prow = sP + bf * PT;
-      uint8_t* brow = sB + bf * BT;
-      // S windows of this row's item: NCH chunks of 32 tile columns (SPP < 32: the window
-      // holding the item).  TMEM loads are asynchronous until tcgen05.wait::ld: the QA row
-      // and the first S chunk are issued together, each later chunk before the previous one
-      // is processed; SPP <= 32 keeps its chunk in registers for the second pass.
-      constexpr int NCH = SPP < 32 ? 1 : SPP / 32;
-      constexpr bool KEEP = NCH == 1;
-      const int off = (a * SPP) & 31;            // item's first key inside its first window
-      const int cb0 = (a * SPP) & ~31;           // first tile column of the item's windows
-      uint32_t vq[32], v[2][32];
-      tmem_ld32_nw(trow + 128, vq);
-      tmem_ld32_nw(trow + cb0, v[0]);
-      tmem_wait_ld(vq);
-      tmem_touch(v[0]);
+      {
+        float v[32];
+        tmem_ld32(trow + 128, v);
 #pragma unroll
-      for (int e = 0; e < 17; ++e) qa[e] = __uint_as_float(vq[e]);
-      // the clipped ends in registers; only band keys (|j - i| < k) look the table up
-      const float qlo = __uint_as_float(vq[0]), qhi = qa[2 * kclip];
-      auto rel = [&](int dj) {
-        return dj <= -kclip ? qlo : dj >= kclip ? qhi : qa[dj + kclip];
-      };
+        for (int e = 0; e < 17; ++e) qa[e] = v[e];
+      }
       if (r == 0) UA_TR(k, 8);
       // pass 1: row maximum of the scaled scores over this item's keys j < n
       float mx = -INFINITY;
-      auto max_chunk = [&](const uint32_t* vv, int ch) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < SPP; c0 += 32) {
+        float v[32];
+        tmem_ld32(trow + ((a * SPP + c0) & ~31), v);   // SPP < 32: the item's keys within
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
-          const int j = 32 * ch + jj - off;      // key index within the item
-          const float sc = (__uint_as_float(vv[jj]) + rel(j - i)) * sl2;
-          if (j >= 0 && j < n) mx = fmaxf(mx, sc);
-        }
-      };
-      // chunk pairs (static register buffers v[0] / v[1]); the next chunk's load is in flight
-      // while one is processed
-#pragma unroll 1
-      for (int ch = 0; ch < NCH; ch += 2) {
-        if (ch + 1 < NCH) tmem_ld32_nw(trow + cb0 + 32 * (ch + 1), v[1]);
-        max_chunk(v[0], ch);
-        if (ch + 1 < NCH) {
-          tmem_wait_ld(v[1]);
-          tmem_touch(v[0]);
-          if (ch + 2 < NCH) tmem_ld32_nw(trow + cb0 + 32 * (ch + 2), v[0]);
-          max_chunk(v[1], ch + 1);
-          if (ch + 2 < NCH) {
-            tmem_wait_ld(v[0]);
-            tmem_touch(v[1]);
-          }
+          const int j = c0 + jj - ((a * SPP) & 31);   // key index within the item
+          const float s = (v[jj] + qa[min(max(j - i, -kclip), kclip) + kclip]) * sl2;
+          if (j >= 0 && j < n) mx = fmaxf(mx, s);
         }
       }
       if (!row_ok) mx = 0.f;
       if (r == 0) UA_TR(k, 9);
-      // pass 2: P = exp2(s - max) (0 for masked keys / rows), sums, the clipped-end bucket
-      // sums, band buckets (one key each: B[r][j - i + k] = the FP16 P_ij the MMA uses), P row
+      // pass 2: P = exp2(s - max) (0 for masked keys / rows), sums, bucket sums, FP16 P row
+      uint8_t* prow = sP + bf * PT;
       float sum = 0.f, lo = 0.f, hi = 0.f;
+      uint8_t* brow = sB + bf * BT;
 #pragma unroll
-      for (int c2 = 0; c2 < 8; ++c2)   // zero this row's bucket sums
-        *reinterpret_cast<uint4*>(brow + swz(r, c2)) = make_uint4(0u, 0u, 0u, 0u);
+      for (int ch = 0; ch < 8; ++ch)   // zero this row's bucket sums
+        *reinterpret_cast<uint4*>(brow + swz(r, ch)) = make_uint4(0u, 0u, 0u, 0u);
       // other items' key columns of this row are zero
 #pragma unroll
       for (int kc = 0; kc < 16; ++kc) {
         const int key0 = kc * 8;
-        if (key0 < cb0 || key0 >= cb0 + 32 * NCH)
+        if (key0 < a * SPP || key0 >= (a + 1) * SPP)
           *reinterpret_cast<uint4*>(prow + (kc >> 3) * TILE + swz(r, kc & 7)) = make_uint4(0u, 0u, 0u, 0u);
       }
-      auto p_chunk = [&](const uint32_t* vv, int ch) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < (SPP < 32 ? 32 : SPP); c0 += 32) {
+        float v[32];
+        const int cb = (a * SPP + c0) & ~31;           // first tile column of this window
+        tmem_ld32(trow + cb, v);
         uint32_t hp[16];
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 2) {
           float p2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int j = 32 * ch + jj + e - off, dj = j - i;
-            const float sc = (__uint_as_float(vv[jj + e]) + rel(dj)) * sl2;
-            const float p = (row_ok && j >= 0 && j < n) ? exp2f(sc - mx) : 0.f;
+            const int j = c0 + jj + e - ((a * SPP) & 31), dj = j - i;
+            const float s = (v[jj + e] + qa[min(max(dj, -kclip), kclip) + kclip]) * sl2;
+            const float p = (row_ok && j >= 0 && j < n) ? exp2f(s - mx) : 0.f;
             p2[e] = p;
             sum += p;
             lo += dj <= -kclip ? p : 0.f;
@@ -320,55 +295,29 @@ __global__ void __launch_bounds__(kThreadsU, 1) k_attn_enc_umma(
           }
           hp[jj / 2] = pack_half2_sat(p2[0], p2[1]);
         }
-        // FP16 P into the K-major SW128 tile: tile key = cb0 + 32 ch + 8 u + e
+        // FP16 P into the K-major SW128 tile: tile key = cb + 8*u + e
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int kc = (cb0 + 32 * ch) / 8 + u;
+          const int kc = cb / 8 + u;
           *reinterpret_cast<uint4*>(prow + (kc >> 3) * TILE + swz(r, kc & 7)) =
               make_uint4(hp[4 * u], hp[4 * u + 1], hp[4 * u + 2], hp[4 * u + 3]);
         }
-      };
-      if constexpr (KEEP) {   // the chunks are still in registers
-        p_chunk(v[0], 0);
-        if (NCH > 1) p_chunk(v[1], 1);
-      } else {
-        tmem_ld32_nw(trow + cb0, v[0]);
-        tmem_wait_ld(v[0]);
-#pragma unroll 1
-        for (int ch = 0; ch < NCH; ch += 2) {
-          tmem_ld32_nw(trow + cb0 + 32 * (ch + 1), v[1]);
-          p_chunk(v[0], ch);
-          tmem_wait_ld(v[1]);
-          tmem_touch(v[0]);
-          if (ch + 2 < NCH) tmem_ld32_nw(trow + cb0 + 32 * (ch + 2), v[0]);
-          p_chunk(v[1], ch + 1);
-          if (ch + 2 < NCH) {
-            tmem_wait_ld(v[0]);
-            tmem_touch(v[1]);
-          }
-        }
       }
       if (r == 0) UA_TR(k, 10);
+      // band buckets: one key each (j = i + r - k for |r - k| < k), ends: the clipped sums
       if (row_ok) {
-        // band buckets: one key each, B[r][j - i + k] = the FP16 P_ij the MMA uses (read back
-        // from this thread's P row; static offsets: the loads are issued together)
-        __half bv[15];
-#pragma unroll
-        for (int dd = -7; dd <= 7; ++dd) {
-          const int j = i + dd, key = a * SPP + j;
-          bv[dd + 7] = (dd > -kclip && dd < kclip && j >= 0 && j < n)
-                           ? *reinterpret_cast<const __half*>(prow + (key >> 6) * TILE +
-                                                              swz(r, (key >> 3) & 7) + (key & 7) * 2)
-                           : __half();
-        }
-#pragma unroll
-        for (int dd = -7; dd <= 7; ++dd) {
+        __half* bh = nullptr;
+        for (int dd = -kclip + 1; dd < kclip; ++dd) {
+          const int j = i + dd;
+          if (j < 0 || j >= n) continue;
+          // P_ij again from the stored FP16 tile (the value the P V product uses)
+          const int key = a * SPP + j;
+          const __half pv = *reinterpret_cast<const __half*>(prow + (key >> 6) * TILE +
+                                                              swz(r, (key >> 3) & 7) + (key & 7) * 2);
           const int bk = dd + kclip;
-          if (dd > -kclip && dd < kclip)
-            *reinterpret_cast<__half*>(brow + swz(r, bk >> 3) + (bk & 7) * 2) = bv[dd + 7];
+          bh = reinterpret_cast<__half*>(brow + swz(r, bk >> 3) + (bk & 7) * 2);
+          *bh = pv;
         }
-      }
-      if (row_ok) {   // the clipped ends
         *reinterpret_cast<__half*>(brow + swz(r, 0)) = __float2half(lo);
         *reinterpret_cast<__half*>(brow + swz(r, (2 * kclip) >> 3) + ((2 * kclip) & 7) * 2) =
             __float2half(hi);
