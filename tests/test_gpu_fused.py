@@ -40,6 +40,8 @@ MODES = {"unfused": {"NMT_NO_FUSE": "1"}, "one_launch": {"NMT_FUSE_ROWS": "10000
 
 @pytest.mark.parametrize("name,n,lim,beam", [
     ("student-35-1", 600, dict(max_tokens=8192, max_sents=512), 1),
+    # the bench budget: live batches up to 8192 rows, 64 row blocks per fused launch
+    ("student-35-1", 12000, dict(max_tokens=65536, max_sents=8192, workspaces=4), 1),
     ("student-6-1", 300, dict(max_tokens=2048, max_sents=128), 1),
     ("teacher-30-6", 24, dict(max_tokens=1024, max_sents=16, max_tgt_len=24, beam=4), 4),
 ])
@@ -50,9 +52,10 @@ def test_fused_step_bit_identical(name, n, lim, beam):
     side = torch.cuda.Stream()     # graph-replayed steps (first use of a bucket runs eagerly)
     for mode, env in MODES.items():
         m = _model(name, env, **lim)
+        wk = lim.get("workspaces", 1)
         with torch.cuda.stream(side):
-            o1, st = m.translate(wl.ids, wl.off, caps=caps, beam=beam)
-            o2, _ = m.translate(wl.ids, wl.off, caps=caps, beam=beam)
+            o1, st = m.translate(wl.ids, wl.off, caps=caps, beam=beam, workers=wk)
+            o2, _ = m.translate(wl.ids, wl.off, caps=caps, beam=beam, workers=wk)
         torch.cuda.synchronize()
         assert o1 == o2, mode
         outs[mode] = (o1, st["gen_tokens"], st["decode_steps"])
