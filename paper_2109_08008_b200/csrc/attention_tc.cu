@@ -333,7 +333,7 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
 __device__ __forceinline__ uint32_t sw128(int r, int ch) { return r * 128 + ((ch ^ (r & 7)) << 4); }
 
 template <int NT>
-__global__ void __maxnreg__(112) k_attn_enc_tma(
+__global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_tma(
     const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
     const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
     int B, int S, int d, int H, int kclip, int use_rpr, int nslot) {
@@ -403,173 +403,109 @@ __global__ void __maxnreg__(112) k_attn_enc_tma(
 #pragma unroll
     for (int t = 0; t < DH / 8; ++t) oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
     const int r0 = m0 + g, r1 = r0 + 8;
-    float inv0 = 0.f, inv1 = 0.f;
     if (m0 < n) {
       // zero this unit's bucket sums (band buckets without a key stay 0)
       for (int idx = lane; idx < 16 * LDB / 8; idx += 32)
         reinterpret_cast<uint4*>(sB)[idx] = make_uint4(0u, 0u, 0u, 0u);
-      // Q fragment of the 16-query block for 16-wide k-step ks (re-read from shared memory
-      // by every key chunk: registers are the occupancy limit)
-      auto qfrag = [&](uint32_t* af, int ks) {
-        const int row = m0 + rr + (mi & 1) * 8;
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
-                     : "r"(tQ + sw128(row, 2 * ks + (mi >> 1))));
-      };
-      // ---- QA = Q A^K^T -> the warp's q.A^K scratch (indexed by bucket below)
-      {
-        float qa[RP / 8][4];
+      // ---- S = Q K^T and QA = Q A^K^T
+      float sc[NT][4], qa[RP / 8][4];
 #pragma unroll
-        for (int t = 0; t < RP / 8; ++t) qa[t][0] = qa[t][1] = qa[t][2] = qa[t][3] = 0.f;
+      for (int t = 0; t < NT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-          uint32_t af[4];
-          qfrag(af, ks);
+      for (int t = 0; t < RP / 8; ++t) qa[t][0] = qa[t][1] = qa[t][2] = qa[t][3] = 0.f;
 #pragma unroll
-          for (int t = 0; t < RP / 8; t += 2) {
-            uint32_t bf[4];
-            ldsm_x4(bf, sAK + ((t + (mi >> 1)) * 8 + rr) * LDH + 16 * ks + (mi & 1) * 8);
-            mma16816(qa[t], af, bf[0], bf[1]);
-            mma16816(qa[t + 1], af, bf[2], bf[3]);
-          }
+      for (int k0 = 0; k0 < DH; k0 += 16) {
+        uint32_t af[4];
+        {
+          const int row = m0 + rr + (mi & 1) * 8;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                       : "r"(tQ + sw128(row, k0 / 8 + (mi >> 1))));
         }
 #pragma unroll
-        for (int t = 0; t < RP / 8; ++t) {
-          const int cc = t * 8 + 2 * tig;
-          sQA[g * QLD + cc] = qa[t][0];
-          sQA[g * QLD + cc + 1] = qa[t][1];
-          sQA[(g + 8) * QLD + cc] = qa[t][2];
-          sQA[(g + 8) * QLD + cc + 1] = qa[t][3];
+        for (int t = 0; t < NT; t += 2) {
+          uint32_t bf[4];
+          const int row = (t + (mi >> 1)) * 8 + rr;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
+                       : "r"(tK + sw128(row, k0 / 8 + (mi & 1))));
+          mma16816(sc[t], af, bf[0], bf[1]);
+          mma16816(sc[t + 1], af, bf[2], bf[3]);
         }
-        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < RP / 8; t += 2) {
+          uint32_t bf[4];
+          ldsm_x4(bf, sAK + ((t + (mi >> 1)) * 8 + rr) * LDH + k0 + (mi & 1) * 8);
+          mma16816(qa[t], af, bf[0], bf[1]);
+          mma16816(qa[t + 1], af, bf[2], bf[3]);
+        }
       }
+      // ---- relative-key term, mask, scale, FP32 softmax (rows r0, r1; quad reductions).
+      // Branch-free: with use_rpr = 0 the staged tables are zero, so the relative terms
+      // add exact zeros.  Scores are kept in log2 units (scale * log2 e folded in).
+#pragma unroll
+      for (int t = 0; t < RP / 8; ++t) {
+        const int cc = t * 8 + 2 * tig;
+        sQA[g * QLD + cc] = qa[t][0];
+        sQA[g * QLD + cc + 1] = qa[t][1];
+        sQA[(g + 8) * QLD + cc] = qa[t][2];
+        sQA[(g + 8) * QLD + cc + 1] = qa[t][3];
+      }
+      __syncwarp();
       const float sl2 = scale * 1.4426950408889634f;
       const bool ok0 = r0 < n, ok1 = r1 < n;
       const float* qa0 = sQA + g * QLD + kclip;        // indexed by clip(j - i, -k, k)
       const float* qa1 = sQA + (g + 8) * QLD + kclip;
-      // Scores of key tiles t0 .. t0 + CT - 1 (8 keys each): Q K^T + the relative-key term,
-      // masked, in log2 units.  Branch-free: with use_rpr = 0 the tables are zero.
-      auto scores = [&](auto& sc, int t0) {
-        constexpr int CT = sizeof(sc) / sizeof(sc[0]);
-#pragma unroll
-        for (int t = 0; t < CT; ++t) sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-          uint32_t af[4];
-          qfrag(af, ks);
-#pragma unroll
-          for (int t = 0; t < CT; t += 2) {
-            uint32_t bf[4];
-            const int row = (t0 + t + (mi >> 1)) * 8 + rr;
-            asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
-                         : "r"(tK + sw128(row, 2 * ks + (mi & 1))));
-            mma16816(sc[t], af, bf[0], bf[1]);
-            mma16816(sc[t + 1], af, bf[2], bf[3]);
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < CT; ++t)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool top = e < 2;
-            const int j = (t0 + t) * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
-            const float v = sc[t][e] + (top ? qa0 : qa1)[min(max(dj, -kclip), kclip)];
-            sc[t][e] = (j < n && (top ? ok0 : ok1)) ? v * sl2 : -INFINITY;
-          }
-      };
       float mx0 = -INFINITY, mx1 = -INFINITY;
-      auto rowmax = [&](const auto& sc) {
-        constexpr int CT = sizeof(sc) / sizeof(sc[0]);
 #pragma unroll
-        for (int t = 0; t < CT; ++t) {
-          mx0 = fmaxf(mx0, fmaxf(sc[t][0], sc[t][1]));
-          mx1 = fmaxf(mx1, fmaxf(sc[t][2], sc[t][3]));
-        }
-      };
-      // P = exp2(s - max) UNNORMALISED (the output is divided by the row sum at the end, so
-      // every key-chunking of a row gives the same arithmetic: batch invariance across
-      // padded lengths), the sums, the bucket sums B (band: one key each, unique writer;
-      // clipped ends: sums) and O += P V over the chunk's keys
-      float s0 = 0.f, s1 = 0.f, lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
-      __half* sb0 = sB + g * LDB + kclip;
-      __half* sb1 = sB + (g + 8) * LDB + kclip;
-      auto expv = [&](auto& sc, int t0) {
-        constexpr int CT = sizeof(sc) / sizeof(sc[0]);
+      for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int t = 0; t < CT; ++t)
+        for (int e = 0; e < 4; ++e) {
+          const bool top = e < 2;
+          const int j = t * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
+          const float v = sc[t][e] + (top ? qa0 : qa1)[min(max(dj, -kclip), kclip)];
+          sc[t][e] = (j < n && (top ? ok0 : ok1)) ? v * sl2 : -INFINITY;
+          if (top) mx0 = fmaxf(mx0, sc[t][e]);
+          else mx1 = fmaxf(mx1, sc[t][e]);
+        }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
+      if (mx1 == -INFINITY) mx1 = 0.f;
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool top = e < 2;
-            const int j = (t0 + t) * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
-            const float p = exp2f(sc[t][e] - (top ? mx0 : mx1));
-            sc[t][e] = p;
-            const float pl = dj <= -kclip ? p : 0.f, ph = dj >= kclip ? p : 0.f;
-            if (top) { s0 += p; lo0 += pl; hi0 += ph; } else { s1 += p; lo1 += pl; hi1 += ph; }
-            if (dj > -kclip && dj < kclip) (top ? sb0 : sb1)[dj] = __float2half(p);
-          }
+      for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int kk = 0; kk < CT / 2; ++kk) {
-          uint32_t af[4];
-          af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
-          af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
-          af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-          af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
-#pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 16) {
-            uint32_t bf[4];
-            const int row = (t0 / 2 + kk) * 16 + (mi & 1) * 8 + rr;
-            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
-                         : "r"(tV + sw128(row, c0 / 8 + (mi >> 1))));
-            mma16816(oc[c0 / 8], af, bf[0], bf[1]);
-            mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
-          }
+        for (int e = 0; e < 4; ++e) {
+          const float v = exp2f(sc[t][e] - (e < 2 ? mx0 : mx1));
+          sc[t][e] = v;
+          if (e < 2) s0 += v;
+          else s1 += v;
         }
-      };
-      auto quad_max = [&] {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-        if (mx0 == -INFINITY) mx0 = 0.f;  // padding query rows
-        if (mx1 == -INFINITY) mx1 = 0.f;
-      };
-      if constexpr (NT <= 8) {   // one key chunk: the scores stay in registers
-        float sc[NT][4];
-        scores(sc, 0);
-        rowmax(sc);
-        quad_max();
-        expv(sc, 0);
-      } else {   // two chunks (8 + NT - 8 key tiles): scores recomputed in the second pass
-        {
-          float sc[8][4];
-          scores(sc, 0);
-          rowmax(sc);
-        }
-        {
-          float sc[NT - 8][4];
-          scores(sc, 8);
-          rowmax(sc);
-        }
-        quad_max();
-        {
-          float sc[8][4];
-          scores(sc, 0);
-          expv(sc, 0);
-        }
-        {
-          float sc[NT - 8][4];
-          scores(sc, 8);
-          expv(sc, 8);
-        }
-      }
       s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
       s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
       s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
       s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-      inv0 = s0 > 0.f ? 1.f / s0 : 0.f;
-      inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
+      const float inv0 = s0 > 0.f ? 1.f / s0 : 0.f, inv1 = s1 > 0.f ? 1.f / s1 : 0.f;
+      // P, and the bucket sums B[i][r] = sum_{j: r(i,j) = r} P[i][j]: the band buckets have
+      // one key each (unique writer; masked keys carry P = 0), the two clipped ends are sums
+      float lo0 = 0.f, hi0 = 0.f, lo1 = 0.f, hi1 = 0.f;
+      __half* sb0 = sB + g * LDB + kclip;
+      __half* sb1 = sB + (g + 8) * LDB + kclip;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool top = e < 2;
+          const int j = t * 8 + 2 * tig + (e & 1), dj = j - (top ? r0 : r1);
+          const float p = sc[t][e] * (top ? inv0 : inv1);
+          sc[t][e] = p;
+          const float pl = dj <= -kclip ? p : 0.f, ph = dj >= kclip ? p : 0.f;
+          if (top) { lo0 += pl; hi0 += ph; } else { lo1 += pl; hi1 += ph; }
+          if (dj > -kclip && dj < kclip) (top ? sb0 : sb1)[dj] = __float2half(p);
+        }
       lo0 += __shfl_xor_sync(0xffffffffu, lo0, 1); lo0 += __shfl_xor_sync(0xffffffffu, lo0, 2);
       hi0 += __shfl_xor_sync(0xffffffffu, hi0, 1); hi0 += __shfl_xor_sync(0xffffffffu, hi0, 2);
       lo1 += __shfl_xor_sync(0xffffffffu, lo1, 1); lo1 += __shfl_xor_sync(0xffffffffu, lo1, 2);
@@ -579,17 +515,37 @@ __global__ void __maxnreg__(112) k_attn_enc_tma(
         sb1[-kclip] = __float2half(lo1); sb1[kclip] = __float2half(hi1);
       }
       __syncwarp();
-      // ---- O += B A^V
+      // ---- O = P V (+ B A^V)
 #pragma unroll
-      for (int kk = 0; kk < RP / 16; ++kk) {
+      for (int kk = 0; kk < NT / 2; ++kk) {
         uint32_t af[4];
-        ldsm_x4(af, sB + (rr + (mi & 1) * 8) * LDB + kk * 16 + (mi >> 1) * 8);
+        af[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
+        af[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
+        af[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+        af[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
 #pragma unroll
         for (int c0 = 0; c0 < DH; c0 += 16) {
           uint32_t bf[4];
-          ldsm_x4_t(bf, sAV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+          const int row = kk * 16 + (mi & 1) * 8 + rr;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
+                       : "r"(tV + sw128(row, c0 / 8 + (mi >> 1))));
           mma16816(oc[c0 / 8], af, bf[0], bf[1]);
           mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+        }
+      }
+      {
+#pragma unroll
+        for (int kk = 0; kk < RP / 16; ++kk) {
+          uint32_t af[4];
+          ldsm_x4(af, sB + (rr + (mi & 1) * 8) * LDB + kk * 16 + (mi >> 1) * 8);
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            uint32_t bf[4];
+            ldsm_x4_t(bf, sAV + (kk * 16 + (mi & 1) * 8 + rr) * LDH + c0 + (mi >> 1) * 8);
+            mma16816(oc[c0 / 8], af, bf[0], bf[1]);
+            mma16816(oc[c0 / 8 + 1], af, bf[2], bf[3]);
+          }
         }
       }
     }
@@ -601,8 +557,8 @@ __global__ void __maxnreg__(112) k_attn_enc_tma(
     uint8_t* st = reinterpret_cast<uint8_t*>(sQA);
 #pragma unroll
     for (int t = 0; t < DH / 8; ++t) {
-      const uint32_t w0 = r0 < n ? pack_h2(oc[t][0] * inv0, oc[t][1] * inv0) : 0u;
-      const uint32_t w1 = r1 < n ? pack_h2(oc[t][2] * inv1, oc[t][3] * inv1) : 0u;
+      const uint32_t w0 = r0 < n ? pack_h2(oc[t][0], oc[t][1]) : 0u;
+      const uint32_t w1 = r1 < n ? pack_h2(oc[t][2], oc[t][3]) : 0u;
       *reinterpret_cast<uint32_t*>(st + sw128(g, t) + 4 * tig) = w0;
       *reinterpret_cast<uint32_t*>(st + sw128(g + 8, t) + 4 * tig) = w1;
     }
