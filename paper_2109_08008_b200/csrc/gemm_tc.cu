@@ -889,7 +889,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "512x2") tc::launch<512, 2>(a, s);
     else if (c == "256x3d") tc::launch<256, 3, 8, 2>(a, s);
     else tc::launch<256, 4>(a, s);
-  } else if (a.R && a.K >= 2048 && !a.ln_st && !a.st_out && !a.relu && !a.dM) {
+  } else if (a.R && a.K >= 2048 && !a.ln_st && !a.st_out && !a.relu && !a.dM &&
+             !getenv("NMT_NO_PAIR_FFN2")) {
     // encoder FFN2 (K = 2048, residual): 256 x 256 units over a CTA pair (cta_group::2, each
     // CTA stages half of the B tile), 5 stages: 129 -> 121 us at M = 65520
     // (tools/gemm_bench.py); chosen from the weight shape only (batch invariance)
