@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas=-v"]
+# NMT_EXTRA_NVCC: extra flags for a diagnostic build, e.g. "-DNMT_TRAP_DIAG"
+FLAGS += os.environ.get("NMT_EXTRA_NVCC", "").split()
 OBJ = os.path.join(HERE, "build")
 
 

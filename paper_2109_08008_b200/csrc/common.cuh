@@ -77,6 +77,25 @@ __device__ __forceinline__ int unpack_argmax_id(unsigned long long k) {
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// ---- bounded-wait timeout -------------------------------------------------------------
+// A pipeline or scheduling bug traps (a clean launch failure) instead of hanging the GPU.
+// Built with -DNMT_TRAP_DIAG (NMT_EXTRA_NVCC), the trapping thread first prints where it
+// was waiting (the printf buffer is flushed when the launch failure is reported).
+#ifdef NMT_TRAP_DIAG
+#define NMT_TRAP(tag, a, b)                                                                  \
+  do {                                                                                       \
+    unsigned smid_;                                                                          \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                       \
+    printf("NMT_TRAP %s:%d %s block (%d,%d) of (%d,%d) thread %d of %d sm %u a=%u b=%u\n",  \
+           __FILE__, __LINE__, tag, (int)blockIdx.x, (int)blockIdx.y, (int)gridDim.x,        \
+           (int)gridDim.y, (int)threadIdx.x, (int)blockDim.x, smid_, (unsigned)(a),          \
+           (unsigned)(b));                                                                   \
+    __trap();                                                                                \
+  } while (0)
+#else
+#define NMT_TRAP(tag, a, b) __trap()
+#endif
+
 // ---- programmatic dependent launch (PDL) -----------------------------------------------
 // Decode-step kernels are launched with programmatic stream serialisation while a step is
 // captured into a CUDA graph: the next kernel's CTAs are scheduled while the previous

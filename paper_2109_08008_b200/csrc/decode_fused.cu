@@ -80,7 +80,8 @@ __device__ __forceinline__ void wait_count(const int* c, int target) {
   for (uint32_t i = 1;; ++i) {
     if (i > 256) __nanosleep(64);
     if (ld_acquire(c) >= target) return;
-    if ((i & 255) == 0 && clock64() - t0 > 20000000000ll) __trap();
+    if ((i & 255) == 0 && clock64() - t0 > 20000000000ll)
+      NMT_TRAP("wait_count", ld_acquire(c), target);
   }
 }
 __device__ __forceinline__ void red_release_add(int* p, int v) {

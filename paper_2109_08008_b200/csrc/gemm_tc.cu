@@ -479,34 +479,37 @@ __global__ void __launch_bounds__(kCThreads, 3)
   const int tile = blockIdx.x / S;
   const int num_m = (p.M + BM - 1) / BM;         // grid sized by the host upper bound
   const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
-  pdl_trigger();   // (the TMEM allocation below is 64 columns: never blocks a dependent)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Barriers and the TMEM allocation come BEFORE the PDL trigger, in every CTA: a dependent
+  // launched after the trigger may allocate all 512 columns on this SM and then block in its
+  // griddepcontrol.wait for this grid, so allocating after the trigger can deadlock.
+  if (warp == 0 && lane == 0) {
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_trigger();
   pdl_wait();
   const int Meff = p.dM ? min(p.M, *p.dM) : p.M;
   const bool live = m0 < Meff;                   // uniform across the cluster
   const int kb_total = (p.K + BK - 1) / BK;
   const int kps = kb_total / S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (live) {
-    if (warp == 0 && lane == 0) {
-      for (int st = 0; st < STAGES; ++st) {
-        mbar_init(&full[st], 1);
-        mbar_init(&empty[st], 1);
-      }
-      mbar_init(tfull, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-    }
-    if (warp == 2) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "r"(64));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (warp == 0) {
       if (lane == 0) {
@@ -577,7 +580,7 @@ __global__ void __launch_bounds__(kCThreads, 3)
     }
   }
   cluster_sync_all();  // keep shared memory alive until every CTA has read it
-  if (live && warp == 2) {
+  if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot),
                  "r"(64));

@@ -61,7 +61,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   for (uint32_t i = 1;; ++i) {
     if (mbar_try(bar, parity)) return;
-    if ((i & 1023) == 0 && clock64() - t0 > 20000000000ll) __trap();
+    if ((i & 1023) == 0 && clock64() - t0 > 20000000000ll)
+      NMT_TRAP("mbar_wait", smem_u32(bar) & 0xFFFFF, parity);
   }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
