@@ -319,7 +319,24 @@ __device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
         : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
         : "memory");
     if (ok) return;
-    if ((i & 1023) == 1023 && clock64() - t0 > 20000000000ll) __trap();   // pipeline bug
+    if ((i & 1023) == 1023 && clock64() - t0 > 20000000000ll)   // pipeline bug
+      NMT_TRAP("attn_mbar", smem_addr(bar) & 0xFFFFF, parity);
+  }
+}
+// Item hand-off counter: the producer publishes "items 0..k issued" after arming slot k's
+// barrier.  A consumer warp waits for it before the parity wait on full[k % nslot], because
+// a warp does not visit every round of a slot (units go round robin over the warps, so with
+// e.g. nslot = 3 and 4 units per item a warp sees each slot every second round): the 1-bit
+// parity wait alone would accept the completion of the round before the one it wants.  Once
+// item k is issued, round k / nslot - 1 of the slot has been consumed (so loaded) and round
+// k / nslot + 1 cannot be loaded before this warp's unit is done: the parity is exact.
+__device__ __forceinline__ void wait_issued(const int* issued, int k) {
+  int v;
+  const long long t0 = clock64();
+  for (uint32_t i = 0;; ++i) {
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(issued)) : "memory");
+    if (v > k) return;
+    if ((i & 1023) == 1023 && clock64() - t0 > 20000000000ll) NMT_TRAP("attn_issued", v, k);
   }
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
@@ -349,6 +366,7 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_
   uint8_t* wscr = reinterpret_cast<uint8_t*>(sAV + RP * LDH);
   uint64_t* full = reinterpret_cast<uint64_t*>(wscr + kEncW * kEncWarpScratch);
   uint64_t* empty = full + kEncMaxSlots;
+  int* issued = reinterpret_cast<int*>(empty + kEncMaxSlots);   // items issued by the producer
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int items = B * H, G = gridDim.x, c = blockIdx.x;
@@ -359,6 +377,7 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_
       mbar_init1(&full[i], 1);
       mbar_init1(&empty[i], NQ);
     }
+    *issued = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mqkv)) : "memory");
   }
@@ -384,6 +403,8 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_
         tma_2d(dst, &mqkv, &full[sl], h * DH, b * S);
         tma_2d(dst + TILE, &mqkv, &full[sl], d + h * DH, b * S);
         tma_2d(dst + 2 * TILE, &mqkv, &full[sl], 2 * d + h * DH, b * S);
+        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(issued)), "r"(k + 1)
+                     : "memory");
       }
     }
     return;
@@ -398,6 +419,7 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_
     const int it = c + k * G, b = it / H, h = it - b * H;
     const int n = len[b], m0 = qb * 16;
     const uint32_t tQ = smem_addr(slots + sl * SLOT), tK = tQ + TILE, tV = tK + TILE;
+    wait_issued(issued, k);
     mbar_wait1(&full[sl], (k / nslot) & 1);
     float oc[DH / 8][4];
 #pragma unroll
@@ -583,7 +605,7 @@ template <int NT>
 EncTmaCfg enc_tma_cfg() {
   static EncTmaCfg cfg = [] {
     constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
-    const int fixed = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 1024;
+    const int fixed = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 16 + 1024;
     // enough slots for the items the W warps work on at once plus two being prefetched,
     // within ~112 KB (two CTAs per SM) when possible
     int want = std::min(kEncMaxSlots, (kEncW + NQ - 1) / NQ + 2);

@@ -128,6 +128,53 @@ def test_attn_encoder_unit(prec, S, lens):
         assert not np.any(got[n:]), "padding query rows must be zero"
 
 
+@pytest.mark.parametrize("pattern", ["random", "block37", "block18"])
+@pytest.mark.parametrize("S", [32, 48, 64])
+def test_attn_encoder_slot_handoff(S, pattern):
+    """FP16 encoder attention at batch scale with sentence lengths mixing 1 and S: the
+    persistent CTAs walk ~50 (sentence, head) items each through a ring of shared-memory
+    slots, units round robin over the consumer warps, so warps whose items are short run
+    rounds ahead of the warps on long items -- the slot hand-off must still give every unit
+    its own item (csrc/attention_tc.cu, wait_issued).  The batch result is bit-identical to
+    launches of 30 sentences (at most one item per CTA: no slot reuse) and across repeats,
+    padding rows are zero, and sampled sentences match the oracle's double loop.  block37 /
+    block18 alternate long and short runs of sentences so that a CTA's consecutive items
+    (G = 296 / 148 CTAs apart, 8 heads) alternate long and short."""
+    from oracle.nn import rpr_attention_loops
+    from paper_2109_08008_b200 import dev_attn_encoder
+    rng = np.random.default_rng(77 + S)
+    B, d, H, kc = 2000, 512, 8, 8
+    if pattern == "random":
+        lens = np.where(rng.random(B) < 0.5, 1, S).astype(np.int32)
+        mid = rng.random(B) < 0.2
+        lens[mid] = rng.integers(1, S + 1, size=int(mid.sum()))
+    else:
+        blk = int(pattern[5:])
+        lens = np.where((np.arange(B) // blk) % 2 == 1, S, 1).astype(np.int32)
+    qkv = torch.from_numpy(rng.standard_normal((B * S, 3 * d))).to(torch.float16).cuda()
+    relk = torch.from_numpy(0.5 * rng.standard_normal((2 * kc + 1, d // H))).to(torch.float16).cuda()
+    relv = torch.from_numpy(0.5 * rng.standard_normal((2 * kc + 1, d // H))).to(torch.float16).cuda()
+    ln = torch.from_numpy(lens).cuda()
+    outs = [dev_attn_encoder(qkv, ln, relk, relv, B, S, H, kc) for _ in range(3)]
+    ref = torch.cat([dev_attn_encoder(qkv[b0 * S:min(B, b0 + 30) * S].contiguous(), ln[b0:b0 + 30].contiguous(),
+                                      relk, relv, min(30, B - b0), S, H, kc) for b0 in range(0, B, 30)])
+    torch.cuda.synchronize()
+    for o in outs:
+        bad = (o != ref).reshape(B, -1).any(1).nonzero().flatten().tolist()
+        assert not bad, (len(bad), bad[:8])
+    g = outs[0].float().cpu().numpy().reshape(B, S, d)
+    pad = np.arange(S)[None, :] >= lens[:, None]
+    assert not np.any(g[pad]), "padding query rows must be zero"
+    x = qkv.double().cpu().numpy()
+    ak, av = relk.double().cpu().numpy(), relv.double().cpu().numpy()
+    for b in rng.choice(np.nonzero(lens > 1)[0], 8, replace=False):
+        n = int(lens[b])
+        rows = x[b * S:b * S + n]
+        want = rpr_attention_loops(rows[:, :d], rows[:, d:2 * d], rows[:, 2 * d:], ak, av, H, kc,
+                                   lambda i, j: (True, i))
+        assert np.abs(g[b, :n] - want).max() <= 1e-2 * max(1.0, np.abs(want).max()), (b, n)
+
+
 def _teacher_forced(name, prec, srcs, forced, eos_boost=1.0):
     """Run encoder + forced decode on GPU and oracle; compare encoder out and logits."""
     cfg, _ = weights(name, eos_boost)
