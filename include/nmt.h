@@ -340,7 +340,7 @@ nmt_status nmt_dev_gemm(nmt_precision prec, int32_t M, int32_t N, int32_t K, con
                         void* stream);
 /* Same GEMM in the decode-step configuration (FP16 only): 64-wide tiles and the
  * deterministic split-K factor the decoder uses for this (N, K) (partials reduced in split
- * order by the last-arriving CTA).  Uses a library-owned workspace; M <= 4096. */
+ * order by the last-arriving CTA).  Uses a library-owned workspace; M <= 16384. */
 nmt_status nmt_dev_gemm_decode(int32_t M, int32_t N, int32_t K, const void* d_A, int32_t lda,
                                const void* d_B, int32_t ldb, const void* d_bias, const void* d_R,
                                int32_t ldr, void* d_C, int32_t ldc, int32_t relu, void* stream);

@@ -1514,7 +1514,7 @@ nmt_status nmt_dev_gemm_decode(int32_t M, int32_t N, int32_t K, const void* d_A,
                                const void* d_B, int32_t ldb, const void* d_bias, const void* d_R,
                                int32_t ldr, void* d_C, int32_t ldc, int32_t relu, void* stream) {
   return guard([&] {
-    NMT_REQUIRE(d_A && d_B && d_C && M > 0 && M <= 4096 && N > 0 && K > 0, NMT_E_ARG,
+    NMT_REQUIRE(d_A && d_B && d_C && M > 0 && M <= 16384 && N > 0 && K > 0, NMT_E_ARG,
                 "bad gemm args");
     NMT_REQUIRE(K % 16 == 0, NMT_E_SHAPE, "K must be a multiple of 16");
     static float* ws = nullptr;   // test hook scratch (not on the product path)

@@ -35,20 +35,25 @@ namespace tc {
 // both halves on its own `full` barrier (each CTA's TMA completes on it), issues the MMAs
 // and multicasts its commits to both CTAs' `empty` / `tfull` barriers; both CTAs drain
 // their own TMEM rows and release the accumulator on the leader's `tempty`.
-template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1, bool BEAM = false>
+// KS = 2: the split-K arithmetic of the cluster kernel below inside one persistent unit (two
+// TMEM accumulators per unit over the two K halves, reduced (0 + p0) + p1 in FP32 before the
+// epilogue): the large-row decode FFN2 keeps the association its small-row launches use.
+template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1, bool BEAM = false,
+          int KS = 1>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
               Params p) {
   using SM = Smem<BN, STAGES, PAIR, EW, NSTG>;
   constexpr int UM = PAIR ? 2 * BM : BM;             // output rows per unit
-  constexpr uint32_t ACC_COLS = BN;                 // one accumulator = BN FP32 columns
+  constexpr uint32_t ACC_COLS = KS * BN;            // one accumulator = KS x BN FP32 columns
   // BN <= 256: two accumulators (the epilogue of unit i overlaps the MMAs of unit i+1);
   // BN = 512 fills TMEM with one (full-row tiles for the N = 512 projections: half the
   // units of BN = 256, so M = 16K..32K rows fit one or two waves of 148 SMs)
-  constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
-  constexpr uint32_t TMEM_COLS = NACC * BN <= 32 ? 32 : NACC * BN <= 64 ? 64
-                                 : NACC * BN <= 128 ? 128 : NACC * BN <= 256 ? 256 : 512;
+  constexpr int NACC = 2 * KS * BN <= 512 ? 2 : 1;
+  constexpr int TC = NACC * KS * BN;
+  constexpr uint32_t TMEM_COLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
+  static_assert(KS == 1 || (!PAIR && !BEAM && KS == 2 && KS * BN <= 512), "KS = 2: single-CTA units");
   constexpr int BBOX = BN > 256 ? 256 : BN;         // TMA box rows of B (<= 256)
   static_assert(!(PAIR && BN > 256), "pair units use BN <= 256");
   extern __shared__ uint8_t smem_raw[];
@@ -60,8 +65,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
-  uint64_t* rbar = tempty + 2;        // [EW][2] residual tile loaded (NSTG = 2)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EW);
+  constexpr int NRB = NSTG > 2 ? NSTG : 2;
+  uint64_t* rbar = tempty + 2;        // [EW][NRB] residual tile loaded (NSTG >= 2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + NRB * EW);
 
   const int kb_total = (p.K + BK - 1) / BK;
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
@@ -78,7 +84,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], PAIR ? 2 * EW : EW);  // one arrive per epilogue warp (both CTAs)
     }
-    for (int i = 0; i < 2 * EW; ++i) mbar_init(&rbar[i], 1);
+    for (int i = 0; i < NRB * EW; ++i) mbar_init(&rbar[i], 1);
+
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -186,8 +193,11 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         const uint32_t aph = NACC == 2 ? (local >> 1) & 1 : local & 1;
         mbar_wait(&tempty[acc], aph ^ 1);   // epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + acc * ACC_COLS;
+        const uint32_t d0 = tmem + acc * ACC_COLS;
+        const int kps = kb_total / KS;   // KS = 2: k-blocks [0, kps) -> d0, [kps, 2 kps) -> d0 + BN
         for (int kb = 0, first = 1; kb < kb_total; ++kb, ++it, first = 0) {
+          if (KS == 2 && kb == kps) first = 1;
+          const uint32_t d = d0 + (KS == 2 && kb >= kps ? BN : 0);
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[st], ph);
@@ -231,7 +241,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     }
     // residual through TMA (NSTG = 2, FP16 TMA-store outputs): the 32 x 32 residual block of
     // a chunk lands in the staging tile that then carries the chunk's output (in place)
-    const bool rt = NSTG == 2 && p.rtma;
+    // NSTG = 4 (= the warp's chunks per unit): every residual block of the unit is requested
+    // when the unit starts, so the loads overlap its main loop instead of one chunk each
+    const bool rt = NSTG >= 2 && p.rtma;
+    constexpr bool RALL = NSTG >= 4;
+    static_assert(!RALL || BN / (EW / 4) / 32 <= NSTG, "one staging tile per chunk of the unit");
+    uint32_t rph = 0;      // RALL: phase bit of each rbar of this warp
     uint32_t kchunk = 0;   // this warp's chunk counter (staging tile kchunk & 1)
     auto r_issue = [&](uint32_t k, int x, int y) {   // lane 0: TMA of a residual block
       if (lane == 0) {
@@ -256,7 +271,18 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       const int cb = half * HALF;
       // residual rows and the bias slice fetched while the MMAs of this unit still run
       uint4 res[NPF];
-      if (rt && n0 + cb < p.N) r_issue(kchunk, n0 + cb, m0 + q * 32);
+      if constexpr (RALL) {
+        if (rt && lane == 0) {
+          bulk_wait_read0();   // the previous unit's stores have read every staging tile
+          for (int j = 0; j * 32 < HALF && n0 + cb + j * 32 < p.N; ++j) {
+            uint64_t* b = &rbar[NSTG * e + j];
+            mbar_expect_tx(b, SM::STG);
+            tma_load_2d(stg0 + j * SM::STG, &mapR, b, n0 + cb + j * 32, m0 + q * 32);
+          }
+        }
+      } else if (rt && n0 + cb < p.N) {
+        r_issue(kchunk, n0 + cb, m0 + q * 32);
+      }
       const bool pf = !rt && HALF <= 128 && p.R && row_ok && n0 + cb + HALF <= p.N &&
                       ((reinterpret_cast<uintptr_t>(p.R + (size_t)m * p.ldr + n0 + cb) & 15) == 0);
       if (pf) {
@@ -290,6 +316,15 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         float v[32];
         __syncwarp();
         tmem_ld32(tbase + c0, v);
+        if constexpr (KS == 2) {   // the cluster kernel's reduction order: (0 + p0) + p1
+          float v2[32];
+          tmem_ld32(tbase + BN + c0, v2);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = 0.f + v[j];
+            v[j] += v2[j];
+          }
+        }
         if (c0 + 32 >= cb + HALF) {  // this warp's columns read: release the accumulator
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -303,13 +338,19 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         } else if (p.tstore) {
           if (n0 + c0 < p.N) {  // warp-uniform
             const bool rp = p.relu && !p.st_out;   // ReLU inside the pack instruction
-            uint8_t* stg = stg0 + (NSTG == 2 ? (kchunk & 1) * SM::STG : 0);
+            const int jc = (c0 - cb) >> 5;      // chunk of this warp's columns
+            uint8_t* stg = stg0 + (RALL ? jc * SM::STG : NSTG == 2 ? (kchunk & 1) * SM::STG : 0);
             const int sw = (lane >> 1) & 3;     // 64-B swizzle: 16-B chunk c at c ^ ((row >> 1) & 3)
             if (!(p.dbg & 8))
               epi_math(p, m, n0 + c0, v, bias_all ? sbias + n0 + c0 : sb + (c0 - cb),
                        pf ? res + (c0 - cb) / 8 : nullptr, row_ok && !rt, sc + (c0 - cb), ln, rp);
             if (rt) {   // + residual (same order as the register path: after bias)
-              mbar_wait(&rbar[2 * e + (kchunk & 1)], (kchunk >> 1) & 1);
+              if constexpr (RALL) {
+                mbar_wait(&rbar[NSTG * e + jc], (rph >> jc) & 1);
+                rph ^= 1u << jc;
+              } else {
+                mbar_wait(&rbar[2 * e + (kchunk & 1)], (kchunk >> 1) & 1);
+              }
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const uint4 w4 = *reinterpret_cast<const uint4*>(stg + lane * 64 + ((c ^ sw) << 4));
@@ -351,7 +392,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
               tma_store_2d(&mapC, stg, n0 + c0, m0 + q * 32);
               bulk_commit();
             }
-            if (rt && c0 + 32 < cb + HALF && n0 + c0 + 32 < p.N)   // next chunk's residual block
+            if (!RALL && rt && c0 + 32 < cb + HALF && n0 + c0 + 32 < p.N)   // next chunk's residual
               r_issue(kchunk, n0 + c0 + 32, m0 + q * 32);         // (kchunk already advanced)
           }
         } else if (row_ok && n0 + c0 < p.N) {
@@ -671,18 +712,19 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false>
+template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false, int KS = 1>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
   (void)attr;
-  if (a.splits > 1) throw CudaError("gemm_tc: persistent kernel has no split-K (use the cluster path)");
+  if (a.splits != KS) throw CudaError("gemm_tc: split count / kernel mismatch");
+  if (KS > 1 && ((a.K + BK - 1) / BK) % KS) throw CudaError("gemm_tc: k-blocks not divisible by the splits");
   CUtensorMap ma = make_map(a.A, a.M, a.K, a.lda, BM);
   CUtensorMap mb = make_map(a.B, a.N, a.K, a.ldb, BN > 256 ? 256 : BN);
   Params p{};
@@ -712,10 +754,10 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   const int grid = std::min(units, cap > 0 && !a.dM ? cap : num_sms());  // persistent: one CTA per SM
   const CUtensorMap mc = out_map(a, p);
   static const bool no_rtma = getenv("NMT_NO_RTMA") != nullptr;   // A/B only
-  p.rtma = NSTG == 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
+  p.rtma = NSTG >= 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
            (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && !no_rtma;
   const CUtensorMap mr = p.rtma ? make_map(a.R, a.M, a.N, a.ldr, 32, true) : CUtensorMap{};
-  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
+  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -838,6 +880,13 @@ int decode_splits(int N, int K) {
 // so: 64-wide tiles for the square projections, split-K 2 through a thread-block cluster for
 // K >= 2048 (no LN-statistics output there), 128x128 otherwise.  The per-GEMM floor of
 // ~6 us is the dependent TMA round trips of the K loop plus launch and epilogue.
+// Above 2048 rows (the host bound of the launch: the graph bucket) the tiles widen
+// (graph-timed at 4096 / 8192 rows: QKV 13.9 -> 13.2 / 22.2 -> 17.4, FFN1 17.0 -> 13.6 /
+// 26.2 -> 20.5, square 9.9 -> 8.0 (128) / 15.7 -> 10.4 (256), FFN2 25.4 / 49.0 in the
+// cluster kernel): the output tile shape does not change any result (each output element
+// is the same K-ordered MMA accumulation in every tile; tools/tile_identity.py checks it
+// bit for bit), and FFN2 keeps its split-K association in the persistent kernel's KS = 2
+// units, so batch invariance holds across the switch.
 // NMT_DEC_TILE / NMT_DEC_SPLITS / NMT_DEC_POLICY=old override for tuning experiments.
 void decode_config(GemmArgs& a) {
   static const int env_tile = getenv("NMT_DEC_TILE") ? atoi(getenv("NMT_DEC_TILE")) : 0;
@@ -850,12 +899,12 @@ void decode_config(GemmArgs& a) {
   } else if (env_tile || old) {
     a.tile_n = env_tile ? env_tile : 128;
   } else if (a.K >= 2048 && !a.st_out && !a.ln_st && ((a.K + 63) / 64) % 2 == 0) {
-    a.tile_n = 64;
+    a.tile_n = a.M > 2048 ? 256 : 64;
     a.splits = 2;
   } else if (a.N <= 512 && a.K <= 512) {
-    a.tile_n = 64;
+    a.tile_n = a.M > 4096 ? 256 : a.M > 2048 ? 128 : 64;
   } else {
-    a.tile_n = 128;
+    a.tile_n = a.M >= 2048 ? 256 : 128;
   }
 }
 
@@ -874,7 +923,11 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   if ((a.st_out && a.N % 32) || (a.ln_st && (a.K % 32 || !a.ln_c)) ||
       ((a.st_out || a.ln_st) && a.splits > 1))
     throw CudaError("gemm_tc: LN folding needs N, K % 32 == 0 and the persistent kernel");
-  if (a.tile_n == 64 && a.splits > 1) {
+  if (a.tile_n == 256 && a.splits == 2) {
+    tc::launch<256, 4, 8, 1, false, 2>(a, s);   // split-K association in persistent units
+  } else if (a.splits > 1 && a.tile_n != 64) {
+    throw CudaError("gemm_tc: split-K needs 64-wide cluster tiles or 256-wide KS = 2 units");
+  } else if (a.tile_n == 64 && a.splits > 1) {
     tc::launch_cluster(a, s);   // split-K reduced through distributed shared memory
   } else if (a.tile_n == 64) {
     tc::launch<64, 4>(a, s);
@@ -901,8 +954,11 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   } else if (a.R && a.K <= 512 && !a.ln_st && !a.relu) {
     // residual GEMM with a short main loop (attention output projection): 3 stages and two
     // staging tiles per epilogue warp, the residual blocks TMA-loaded ahead of their chunk
-    // (measured 36.1 -> 30.9 us at 32768 rows; the 4-stage kernel wins everywhere else)
-    tc::launch<256, 3, 8, 2>(a, s);
+    // (measured 36.1 -> 30.9 us at 32768 rows; the 4-stage kernel wins everywhere else);
+    // four staging tiles per warp: all four residual blocks of a unit requested at its start
+    static const bool r2 = getenv("NMT_OUT_NSTG2") != nullptr;   // A/B only
+    if (r2) tc::launch<256, 3, 8, 2>(a, s);
+    else tc::launch<256, 3, 8, 4>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
     tc::launch<256, 4>(a, s);

@@ -286,7 +286,7 @@ struct Smem {
   // is processed), the whole bias vector (N <= kBiasMax) and per-unit bias / LN c slices
   static constexpr int BIAS = kBiasMax * 4;
   static constexpr int EPI = EW * NSTG * STG + BIAS + 2 * 4 * BN * 4;
-  static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align slack*/ + 512 /*barriers*/;
 };
 
 // Epilogue math on 32 consecutive columns nb..nb+31 of row m (v = FP32 accumulators):
