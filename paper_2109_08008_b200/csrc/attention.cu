@@ -282,14 +282,16 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
 // positions 0..t attended; key t is taken from the fresh projection.  Only buckets
 // r = clip(j - t, -k, k) + k in 0..k occur (j <= t).  Beam rows read their ancestors'
 // cached positions j < t through the ancestry table (no K/V copies).
+// Occupancy: 6 CTAs (24 warps) per SM; a warp's keys are short dependent load chains, so
+// the step time at thousands of rows is the number of warp waves times that latency.  The
+// relative tables are read per lane from global memory (L1-resident, 2 x (k+1) x dh
+// elements): no per-CTA staging barrier.
 template <class T, int DH>
-__global__ void __launch_bounds__(128) k_attn_dec_self(
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 6 : 4) k_attn_dec_self(
     const T* __restrict__ qkv, T* __restrict__ kc, T* __restrict__ vc, int Tmax,
     const int* __restrict__ row_slot, const T* __restrict__ relk, const T* __restrict__ relv,
     T* __restrict__ out, int rows, int d, int H, int kclip, int use_rpr, const int* __restrict__ d_t,
     const int* __restrict__ dR, const int* __restrict__ anc) {
-  __shared__ float s_relv[16][DH];  // A^V[0..k] (k <= 15), shared by every head
-  __shared__ float s_relk[16][DH];  // A^K[0..k]
   __shared__ float s_x[4][16];      // per warp: q . A^K[r] / sqrt(dh), r = 0..k
   using WA = WarpAttn<T, DH>;
   pdl_trigger();
@@ -311,12 +313,6 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
     kt.load(src + d + w.sub * 8);
     vt.load(src + 2 * d + w.sub * 8);
   }
-  if (use_rpr)
-    for (int i = threadIdx.x; i < (kclip + 1) * DH; i += blockDim.x) {
-      s_relv[i / DH][i % DH] = to_f(relv[i]);
-      s_relk[i / DH][i % DH] = to_f(relk[i]);
-    }
-  __syncthreads();
   if (row >= min(rows, nlive)) return;
   if (w.kq == 0) {  // KV-cache append at position t
     kt.store(kc + ((size_t)slot * Tmax + t) * d + h * DH + w.sub * 8);
@@ -328,8 +324,9 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
       const int b = b0 + w.kq;
       float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (b <= kclip) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = s_relk[b][w.sub * 8 + e];
+        Raw8<T> r;
+        r.load(relk + b * DH + w.sub * 8);
+        r.to_f(f);
       }
       const float e = w.group_dot(f);
       if (b <= kclip && w.sub == 0) x[b] = e;
@@ -353,7 +350,10 @@ __global__ void __launch_bounds__(128) k_attn_dec_self(
   if (use_rpr) {
     auto bias = [&](int j) { return x[max(j - t, -kclip) + kclip]; };
     auto vadd = [&](int j, float* f) {
-      const float* rv = s_relv[max(j - t, -kclip) + kclip] + w.sub * 8;
+      Raw8<T> r;
+      r.load(relv + (max(j - t, -kclip) + kclip) * DH + w.sub * 8);
+      float rv[8];
+      r.to_f(rv);
 #pragma unroll
       for (int e = 0; e < 8; ++e) f[e] += rv[e];
     };
@@ -394,7 +394,7 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
 // S = *dS (device) so a captured step graph serves every batch.  Beam rows share their
 // sentence's K/V (slot = row slot / beam).
 template <class T, int DH>
-__global__ void __launch_bounds__(128) k_attn_cross(
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 6 : 4) k_attn_cross(
     const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv, int koff, int voff,
     const int* __restrict__ dS, const int* __restrict__ src_len,
     const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,

@@ -55,7 +55,9 @@ template <> struct Raw8<float> {
 template <class T, int DH, bool CG = false>
 struct WarpAttn {
   static constexpr int G = DH / 8, KP = 32 / G;
-  static constexpr int U = sizeof(T) == 2 ? G : (G >= 2 ? G / 2 : 1);
+  // keys per lane per chunk: 4 for FP16 dh = 64 (16 keys in flight per warp, 32 registers of
+  // raw K / V), small enough for 6 CTAs (24 warps) per SM
+  static constexpr int U = sizeof(T) == 2 ? (G >= 2 ? G / 2 : 1) : (G >= 2 ? G / 2 : 1);
   static constexpr int CH = KP * U;
   int sub, kq;
   float q[8], m, l, acc[8];
