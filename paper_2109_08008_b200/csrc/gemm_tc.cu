@@ -377,8 +377,13 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
               continue;
             }
             if (lane == 0) {   // the store that last used this staging tile has read it
-              if constexpr (NSTG == 1) bulk_wait_read0();
-              else if (!rt) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              if constexpr (NSTG == 1) {
+                bulk_wait_read0();
+              } else if constexpr (RALL) {   // tile jc: last written NSTG chunks (groups) ago
+                if (!rt) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NSTG - 1) : "memory");
+              } else if (!rt) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              }
             }
             ++kchunk;
             __syncwarp();
@@ -403,6 +408,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           else epi_out(p, m, n0 + c0, v, best);
         }
       }
+      // RALL: a unit that stored fewer than NSTG chunks (N edge) drains its stores, so every
+      // staging tile is again last written NSTG groups back
+      if (RALL && p.tstore && !rt && lane == 0 && n0 + cb + HALF > p.N) bulk_wait_read0();
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
       if (BEAM && row_ok && n0 + cb < p.N) {   // this thread's segment of the row
         const int nseg = (p.N + HALF - 1) / HALF;
@@ -944,6 +952,8 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
     else if (c == "512x2") tc::launch<512, 2>(a, s);
     else if (c == "256x3d") tc::launch<256, 3, 8, 2>(a, s);
+    else if (c == "256x3q") tc::launch<256, 3, 8, 4>(a, s);
+    else if (c == "256x2q") tc::launch<256, 2, 8, 4>(a, s);
     else tc::launch<256, 4>(a, s);
   } else if (a.R && a.K >= 2048 && !a.ln_st && !a.st_out && !a.relu && !a.dM &&
              !getenv("NMT_NO_PAIR_FFN2")) {
