@@ -350,7 +350,7 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
 __device__ __forceinline__ uint32_t sw128(int r, int ch) { return r * 128 + ((ch ^ (r & 7)) << 4); }
 
 template <int NT>
-__global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 8 ? 2 : 1) k_attn_enc_tma(
+__global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 2 ? 3 : NT <= 8 ? 2 : 1) k_attn_enc_tma(
     const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
     const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
     int B, int S, int d, int H, int kclip, int use_rpr, int nslot) {
@@ -607,9 +607,12 @@ EncTmaCfg enc_tma_cfg() {
     constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
     const int fixed = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 16 + 1024;
     // enough slots for the items the W warps work on at once plus two being prefetched,
-    // within ~112 KB (two CTAs per SM) when possible
+    // within ~112 KB (two CTAs per SM) when possible; S <= 16: three CTAs per SM (the
+    // kernel is latency-bound: 24 consumer warps instead of 16; measured 37.0 -> 35.6 us at
+    // S = 16, slower at S = 32: 37.6 -> 39.9), so ~74 KB
     int want = std::min(kEncMaxSlots, (kEncW + NQ - 1) / NQ + 2);
-    int ns = std::min(want, (112 * 1024 - fixed) / SLOT);
+    const int budget = NT <= 2 ? 74 * 1024 : 112 * 1024;
+    int ns = std::min(want, (budget - fixed) / SLOT);
     if (ns < 2) ns = std::min(want, (220 * 1024 - fixed) / SLOT);
     EncTmaCfg c{};
     c.nslot = std::max(1, ns);
