@@ -349,11 +349,14 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
 // byte offset of the 16-B chunk `ch` (0..7) of row r in a 128-B-swizzled tile
 __device__ __forceinline__ uint32_t sw128(int r, int ch) { return r * 128 + ((ch ^ (r & 7)) << 4); }
 
-template <int NT>
+// KC > 0: the clip distance as a compile-time constant (the models' k = 8): the per-element
+// relative-bucket clamps and band tests fold to immediates (KC = 0: runtime kclip_rt).
+template <int NT, int KC>
 __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 2 ? 3 : NT <= 8 ? 2 : 1) k_attn_enc_tma(
     const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
     const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
-    int B, int S, int d, int H, int kclip, int use_rpr, int nslot) {
+    int B, int S, int d, int H, int kclip_rt, int use_rpr, int nslot) {
+  const int kclip = KC > 0 ? KC : kclip_rt;
   constexpr int DH = 64, SP = NT * 8, NQ = SP / 16, LDH = DH + 8, LDB = RP + 8;
   constexpr int TILE = SP * 128, SLOT = 3 * TILE;
   extern __shared__ uint8_t smraw[];
@@ -601,7 +604,7 @@ struct EncTmaCfg {
   int nslot, smem, grid_per_sm;
 };
 
-template <int NT>
+template <int NT, int KC>
 EncTmaCfg enc_tma_cfg() {
   static EncTmaCfg cfg = [] {
     constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
@@ -617,10 +620,10 @@ EncTmaCfg enc_tma_cfg() {
     EncTmaCfg c{};
     c.nslot = std::max(1, ns);
     c.smem = fixed + c.nslot * SLOT;
-    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tma<NT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   c.smem));
     int occ = 0;
-    NMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_attn_enc_tma<NT>,
+    NMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_attn_enc_tma<NT, KC>,
                                                            32 * (kEncW + 1), c.smem));
     c.grid_per_sm = std::max(1, occ);
     return c;
@@ -638,14 +641,23 @@ int sm_count() {
   return n;
 }
 
+template <int NT, int KC>
+void launch_tma_kc(const __half* qkv, const int* len, const __half* relk, const __half* relv,
+                   __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
+  const EncTmaCfg c = enc_tma_cfg<NT, KC>();
+  const CUtensorMap map = tc::make_map(qkv, B * S, 3 * d, 3 * d, NT * 8, false);
+  const int grid = std::min(B * H, c.grid_per_sm * sm_count());
+  launch_k(k_attn_enc_tma<NT, KC>, dim3(grid), dim3(32 * (kEncW + 1)), (size_t)c.smem, s, map, len,
+           relk, relv, out, B, S, d, H, kclip, use_rpr, c.nslot);
+}
+
 template <int NT>
 void launch_tma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
                 __half* out, int B, int S, int d, int H, int kclip, int use_rpr, cudaStream_t s) {
-  const EncTmaCfg c = enc_tma_cfg<NT>();
-  const CUtensorMap map = tc::make_map(qkv, B * S, 3 * d, 3 * d, NT * 8, false);
-  const int grid = std::min(B * H, c.grid_per_sm * sm_count());
-  launch_k(k_attn_enc_tma<NT>, dim3(grid), dim3(32 * (kEncW + 1)), (size_t)c.smem, s, map, len, relk,
-           relv, out, B, S, d, H, kclip, use_rpr, c.nslot);
+  if (kclip == 8)   // every preset's clip distance: compile-time k
+    launch_tma_kc<NT, 8>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s);
+  else
+    launch_tma_kc<NT, 0>(qkv, len, relk, relv, out, B, S, d, H, kclip, use_rpr, s);
 }
 
 void launch_tma_sp(const __half* qkv, const int* len, const __half* relk, const __half* relv,
