@@ -345,7 +345,7 @@ nmt_status nmt_dev_gemm_decode(int32_t M, int32_t N, int32_t K, const void* d_A,
                                const void* d_B, int32_t ldb, const void* d_bias, const void* d_R,
                                int32_t ldr, void* d_C, int32_t ldc, int32_t relu, void* stream);
 /* Fused vocab projection + argmax: d_next[m] = argmax_n (A[m] . B[n]) with ties to the
- * lowest n, FP32 accumulation; optional FP32 logits dump. */
+ * lowest n, FP32 accumulation; optional FP32 logits dump.  M <= 16384. */
 nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t K,
                                const void* d_A, int32_t lda, const void* d_B, int32_t ldb,
                                int32_t* d_next, float* d_logits, void* stream);

@@ -1544,10 +1544,10 @@ nmt_status nmt_dev_gemm_argmax(nmt_precision prec, int32_t M, int32_t N, int32_t
                                int32_t* d_next, float* d_logits, void* stream) {
   return guard([&] {
     NMT_REQUIRE(d_A && d_B && d_next && M > 0 && N > 0 && K > 0, NMT_E_ARG, "bad gemm args");
-    NMT_REQUIRE(K % 16 == 0 && M <= 4096, NMT_E_SHAPE, "K % 16 != 0 or M > 4096");
+    NMT_REQUIRE(K % 16 == 0 && M <= 16384, NMT_E_SHAPE, "K % 16 != 0 or M > 16384");
     cudaStream_t s = (cudaStream_t)stream;
     static unsigned long long* keys = nullptr;  // test hook scratch (not on the product path)
-    if (!keys) NMT_CUDA(cudaMalloc(&keys, 4096 * 8));
+    if (!keys) NMT_CUDA(cudaMalloc(&keys, 16384 * 8));
     NMT_CUDA(cudaMemsetAsync(keys, 0, (size_t)M * 8, s));
     GemmArgs a;
     a.M = M; a.N = N; a.K = K; a.A = d_A; a.lda = lda; a.B = d_B; a.ldb = ldb;
