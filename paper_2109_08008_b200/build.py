@@ -62,8 +62,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if any(r.returncode != 0 for _, r in res):
         raise RuntimeError("nvcc failed building libnmt.so")
     tmp = LIB + ".tmp"
-    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] +
-                       [o for o, _ in res] , capture_output=True, text=True)
+    # -z defs: an unresolved symbol fails the link here instead of the dlopen on the GPU box
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                        "-Xlinker", "-z,defs", "-o", tmp] + [o for o, _ in res],
+                       capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking libnmt.so")

@@ -20,6 +20,16 @@ std::atomic<unsigned long long> g_launches{0};
 thread_local bool g_pdl = false;
 thread_local std::vector<nmt_model::ProfRec>* g_prof_capture = nullptr;
 thread_local std::string g_err;
+int dlcl_blocks(const nmt_config& c, int d) {
+  static const int blk = [] {
+    if (getenv("NMT_NO_DLCL_LA")) return 1;
+    const char* e = getenv("NMT_DLCL_LA");
+    const int v = e ? atoi(e) : kDlclBlock;
+    return v < 1 ? 1 : v > 4 ? 4 : v;
+  }();
+  return c.use_dlcl && dlcl_lookahead_ok(d) ? blk : 1;
+}
+
 }  // namespace nmt
 
 using namespace nmt;
@@ -158,7 +168,7 @@ void init_arena(nmt_model* m) {
       {(void**)&m->nb_cnt, L.beam > 1 ? Bm * 4 : 256},
       {(void**)&m->blogits, L.beam > 1 ? R * (size_t)c.vocab_size * 4 : 256},
       {(void**)&m->lnst, R * (d / 32) * 8},
-      {(void**)&m->dlcl_p, c.use_dlcl && dlcl_lookahead_ok((int)d) ? N * d * 4 : 256},
+      {(void**)&m->dlcl_p, dlcl_blocks(c, (int)d) > 1 ? (dlcl_blocks(c, (int)d) - 1) * N * d * 4 : 256},
       {(void**)&m->cand_v, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->cand_i, L.beam > 1 ? R * 8 * 4 : 256},
       {(void**)&m->fused_ctr, fused_counter_ints() * 4},

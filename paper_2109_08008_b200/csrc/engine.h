@@ -128,7 +128,7 @@ struct nmt_model {
   float* bpart = nullptr;     // [R][ceil(V/256)][18] beam-epilogue partials (FP16 beam)
   bool beam_epi = false;      // FP16 beam steps use the fused epilogue (opt-in: env NMT_BEAM_EPI)
   float2* lnst = nullptr;     // [R][d/32] row-chunk (mean, M2) of the decoder residual stream
-  float* dlcl_p = nullptr;    // [N][d] FP32 DLCL lookahead partial (kernels.h dlcl_combine)
+  float* dlcl_p = nullptr;    // [blk-1][N][d] FP32 DLCL lookahead partials (kernels.h dlcl_combine)
   int* fused_ctr = nullptr;   // fused decode step: item / completion counters (decode_fused.cu)
   // fused decode step policy, read at load: live rows up to which one launch runs every
   // phase (env NMT_FUSE_ROWS; above it fused GEMM segments around the standalone attention
@@ -257,6 +257,10 @@ void encode_any(nmt_model* m, int B, int S, cudaStream_t s);
 void decode_step_any(nmt_model* m, nmt_batch* b, const int* d_prev, const nmt_step_out* out,
                      cudaStream_t s, bool finish = true);
 void prof_flush(nmt_model* m);
+// DLCL lookahead block size (kernels.h dlcl_combine): 1 = none (no DLCL, d not 256 / 512,
+// or NMT_NO_DLCL_LA); NMT_DLCL_LA = 1..4 overrides the default for A/B runs.
+constexpr int kDlclBlock = 4;   // measured: 2 -> 513 ms, 3 -> 597 ms, 4 -> 475 ms DLCL per 192000-sentence chunk
+int dlcl_blocks(const nmt_config& c, int d);
 // While a profiled decode step is being captured, its event pairs are recorded as external
 // event nodes of the graph (replayed and read after every launch of that graph).
 extern thread_local std::vector<nmt_model::ProfRec>* g_prof_capture;

@@ -87,18 +87,34 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
   PROF(P_EMBED, 0, 2 * row,
        embed<T>(m->src, cT<T>(m->emb), m->pe, c.use_dlcl ? o : x, N, d, S, nullptr, nullptr, sq, s));
   const EncW& w0 = m->enc[0];
-  // DLCL two-boundary lookahead (kernels.h dlcl_combine): boundary k (combination row k+1)
-  // also produces the partial of row k+2 when k is even and row k+2 <= L+1 exists; odd
-  // boundaries start from that partial
-  static const bool no_la = getenv("NMT_NO_DLCL_LA") != nullptr;   // A/B only
-  const bool la = c.use_dlcl && dlcl_lookahead_ok(d) && !no_la;
-  auto dlcl_mode = [&](int k) { return !la ? 0 : (k & 1) ? 2 : (k + 1 <= L ? 1 : 0); };
+  // DLCL lookahead in blocks of `la` boundaries (kernels.h dlcl_combine): the first boundary
+  // k0 of a block (combination row k0+1) also produces the partials of rows k0+2 ..
+  // k0+la (those <= L+1 exist); boundary k0+i starts from partial i and the i-1 history rows
+  // written since k0.  la = 1: no lookahead (NMT_NO_DLCL_LA, A/B); NMT_DLCL_LA overrides.
+  const int la = dlcl_blocks(c, d);
+  struct DlclStep { int mode, arg; float* P; };
+  auto dlcl_step = [&](int k) -> DlclStep {
+    if (la <= 1) return {0, 0, nullptr};
+    const int k0 = k / la * la, i = k - k0;
+    if (i == 0) {
+      const int np = std::min(la - 1, L - k);   // partial i targets row k+1+i <= L+1
+      return np > 0 ? DlclStep{1, np, m->dlcl_p} : DlclStep{0, 0, nullptr};
+    }
+    return {2, i - 1, m->dlcl_p + (size_t)(i - 1) * hs};
+  };
+  // bytes: y + history rows read (mode 2: arg rows) + z, x, u written; FP32 partials written
+  // (mode 1: arg of them) or read (mode 2: one)
+  auto dlcl_bytes = [&](int k, const DlclStep& st, bool last) {
+    const int rd = st.mode == 2 ? st.arg : st.mode == 1 ? k : k;
+    const int np = st.mode == 1 ? st.arg : st.mode == 2 ? 1 : 0;
+    return (1 + rd + 1 + (last ? 0 : 1) + 1) * row + np * row * 4.0 / tb;
+  };
   if (c.use_dlcl) {
-    const int mode = dlcl_mode(0);
-    PROF(P_DLCL, 0, 4 * row + (mode ? row * 4.0 / tb : 0.0),
+    const DlclStep st = dlcl_step(0);
+    PROF(P_DLCL, 0, dlcl_bytes(0, st, false),
          dlcl_combine<T>(o, hist, hs, 0, m->dlcl_w, cT<T>(m->dl0_g), cT<T>(m->dl0_b), c.dlcl_ln,
-                         cT<T>(w0.attn_g), cT<T>(w0.attn_b), x, u, N, d, eps, s, mode,
-                         m->dlcl_w + 1, m->dlcl_p));
+                         cT<T>(w0.attn_g), cT<T>(w0.attn_b), x, u, N, d, eps, s, st.mode,
+                         m->dlcl_w, st.P, st.arg));
   } else {
     PROF(P_ENC_LN, 0, 2 * row,
          layernorm<T>(x, d, cT<T>(w0.attn_g), cT<T>(w0.attn_b), u, d, N, d, eps, nullptr, s));
@@ -127,16 +143,11 @@ void encode_impl(nmt_model* m, int B, int S, cudaStream_t s) {
     const T* nb = last ? cT<T>(m->enc_fb) : cT<T>(m->enc[l + 1].attn_b);
     if (c.use_dlcl) {
       const int k = l + 1;  // depth of y
-      const int mode = dlcl_mode(k);
-      // bytes: y + history rows read (none in mode 2) + z, x, u written; FP32 partial
-      // written (mode 1) or read (mode 2)
-      const double by = (1 + (mode == 2 ? 0 : k) + 1 + (last ? 0 : 1) + 1) * row +
-                        (mode ? row * 4.0 / tb : 0.0);
-      PROF(P_DLCL, 0, by,
+      const DlclStep st = dlcl_step(k);
+      PROF(P_DLCL, 0, dlcl_bytes(k, st, last),
            dlcl_combine<T>(x, hist, hs, k, m->dlcl_w + (size_t)(k + 1) * k / 2, cT<T>(w.dl_g),
                            cT<T>(w.dl_b), c.dlcl_ln, ng, nb, last ? nullptr : x,
-                           last ? enc : u, N, d, eps, s, mode,
-                           m->dlcl_w + (size_t)(k + 2) * (k + 1) / 2, m->dlcl_p));
+                           last ? enc : u, N, d, eps, s, st.mode, m->dlcl_w, st.P, st.arg));
     } else {
       PROF(P_ENC_LN, 0, 2 * row,
            layernorm<T>(x, d, ng, nb, last ? enc : u, d, N, d, eps, nullptr, s));

@@ -183,24 +183,33 @@ void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
                   int d, float eps, cudaStream_t s, int mode, const float* wP, float* P);
 
-// MODE (two-boundary lookahead): the history rows read at an
-// even boundary l also feed the next boundary's combination, whose weights row l + 2 is
-// known, so odd boundaries read one FP32 partial instead of l + 1 history rows:
-//   MODE 0: x = sum_{k<=l} w[k] z_k                       (every history row read)
-//   MODE 1: as 0, and P = sum_{k<=l} wP[k] z_k -> FP32 partial (wP = weights of x_{l+2})
-//   MODE 2: x = P + w[l] z_l                              (no history reads)
+// MODE (m-boundary lookahead): boundaries are taken in blocks of
+// m; the block's first boundary l reads every history row once and also accumulates, from
+// the same rows, the FP32 partials of the block's later combinations (their weight rows
+// l + 1 + i are known), so the later boundaries read one partial plus the few history rows
+// written since the block started instead of l + 1 rows:
+//   MODE 0: x = sum_{k<=l} w[k] z_k                                 (every history row read)
+//   MODE 1: as 0, and P_i = sum_{k<=l} W^(l+1+i)[k] z_k -> FP32 partial i, i = 1..NP
+//   MODE 2: x = P + sum_{k=l-nx}^{l-1} w[k] z_k + w[l] z_l           (P: this boundary's partial)
 // The FP32 sums run in the same k order in every mode, so x is bit-identical to MODE 0.
-template <class T, int E, int MODE>
+template <class T, int E, int MODE, int NP>
 __global__ void __launch_bounds__(256) k_dlcl_vec(
     const T* __restrict__ y, T* __restrict__ hist, size_t hist_stride, int l,
     const float* __restrict__ w, const T* __restrict__ gdl, const T* __restrict__ bdl, int dlcl_ln,
     const T* __restrict__ g2, const T* __restrict__ b2, T* __restrict__ xout, T* __restrict__ uout,
-    int rows, float eps, const float* __restrict__ wP, float* __restrict__ P) {
+    int rows, float eps, const float* __restrict__ wall, float* __restrict__ P, int nx) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   constexpr int d = 32 * E;
+  constexpr int NPA = MODE == 1 ? NP : 1;
   const size_t off = (size_t)row * d + lane * E;
-  float z[E], x[E], pa[MODE == 1 ? E : 1];
+  const size_t pstride = (size_t)rows * d;   // partial i at P + (i - 1) * rows * d
+  float z[E], x[E], pa[NPA][E];
+  const float* wp[NPA];
+  if constexpr (MODE == 1) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) wp[i] = wall + (size_t)(l + 2 + i) * (l + 1 + i) / 2;   // row l+1+(i+1)
+  }
   if constexpr (MODE == 2) {   // the partial, issued before the y row's LN
 #pragma unroll
     for (int i = 0; i < E; i += 4) {
@@ -219,11 +228,13 @@ __global__ void __launch_bounds__(256) k_dlcl_vec(
     for (int i = 0; i < E; ++i) x[i] = 0.f;
     if constexpr (MODE == 1) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) pa[i] = 0.f;
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int i = 0; i < E; ++i) pa[q][i] = 0.f;
     }
     // U history rows in flight per lane (raw 16-B loads issued before any arithmetic): the
     // combine is bound by HBM bandwidth, not by one memory latency per history row
-    constexpr int U = sizeof(T) == 2 ? 8 : 4;
+    constexpr int U = sizeof(T) == 2 ? (NP >= 2 && MODE == 1 ? 4 : 8) : 4;
     int k = 0;
     for (; k + U <= l; k += U) {
       RawRow<T, E> a[U];
@@ -232,7 +243,10 @@ __global__ void __launch_bounds__(256) k_dlcl_vec(
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         a[u].fma_into(w[k + u], x);
-        if constexpr (MODE == 1) a[u].fma_into(wP[k + u], pa);
+        if constexpr (MODE == 1) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) a[u].fma_into(wp[q][k + u], pa[q]);
+        }
       }
     }
     for (; k < l; ++k) {
@@ -242,21 +256,37 @@ __global__ void __launch_bounds__(256) k_dlcl_vec(
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = fmaf(wa, a[i], x[i]);
       if constexpr (MODE == 1) {
-        const float wb = wP[k];
 #pragma unroll
-        for (int i = 0; i < E; ++i) pa[i] = fmaf(wb, a[i], pa[i]);
+        for (int q = 0; q < NP; ++q) {
+          const float wb = wp[q][k];
+#pragma unroll
+          for (int i = 0; i < E; ++i) pa[q][i] = fmaf(wb, a[i], pa[q][i]);
+        }
       }
     }
     if constexpr (MODE == 1) {
-      const float wb = wP[l];
 #pragma unroll
-      for (int i = 0; i < E; i += 4) {
-        float4 q;
-        q.x = fmaf(wb, z[i], pa[i]); q.y = fmaf(wb, z[i + 1], pa[i + 1]);
-        q.z = fmaf(wb, z[i + 2], pa[i + 2]); q.w = fmaf(wb, z[i + 3], pa[i + 3]);
-        *reinterpret_cast<float4*>(P + off + i) = q;
+      for (int q = 0; q < NP; ++q) {
+        const float wb = wp[q][l];
+#pragma unroll
+        for (int i = 0; i < E; i += 4) {
+          float4 o;
+          o.x = fmaf(wb, z[i], pa[q][i]); o.y = fmaf(wb, z[i + 1], pa[q][i + 1]);
+          o.z = fmaf(wb, z[i + 2], pa[q][i + 2]); o.w = fmaf(wb, z[i + 3], pa[q][i + 3]);
+          *reinterpret_cast<float4*>(P + q * pstride + off + i) = o;
+        }
       }
     }
+  } else {
+    // the rows written since the block's partial was formed (k = l - nx .. l - 1, nx <= 2),
+    // all loads in flight before the in-order FMAs
+    RawRow<T, E> a[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (u < nx) a[u].load(hist + (size_t)(l - nx + u) * hist_stride + off);
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (u < nx) a[u].fma_into(w[l - nx + u], x);
   }
   const float wl = w[l];
 #pragma unroll
@@ -271,25 +301,30 @@ bool dlcl_lookahead_ok(int d) { return d == 512 || d == 256; }
 template <class T>
 void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
-                  int d, float eps, cudaStream_t s, int mode, const float* wP, float* P) {
+                  int d, float eps, cudaStream_t s, int mode, const float* wall, float* P, int arg) {
   if (rows <= 0) return;
   if (mode != 0 && !dlcl_lookahead_ok(d)) throw CudaError("dlcl_combine: lookahead needs d = 256 / 512");
-#define NMT_DV(E, MODE)                                                                        \
-  k_dlcl_vec<T, E, MODE><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, \
-                                                           dlcl_ln, g2, b2, xout, uout, rows, eps, \
-                                                           wP, P)
+  if ((mode == 1 && (arg < 1 || arg > 3)) || (mode == 2 && (arg < 0 || arg > 2)))
+    throw CudaError("dlcl_combine: 1..3 partials, 0..2 extra rows");
+#define NMT_DV(E, MODE, NP)                                                                     \
+  k_dlcl_vec<T, E, MODE, NP><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl,   \
+                                                               bdl, dlcl_ln, g2, b2, xout, uout, \
+                                                               rows, eps, wall, P, arg)
+#define NMT_DVE(E)                                       \
+  if (mode == 1 && arg == 1) NMT_DV(E, 1, 1);            \
+  else if (mode == 1 && arg == 2) NMT_DV(E, 1, 2);       \
+  else if (mode == 1) NMT_DV(E, 1, 3);                   \
+  else if (mode == 2) NMT_DV(E, 2, 1);                   \
+  else NMT_DV(E, 0, 1);
   if (d == 512) {
-    if (mode == 1) NMT_DV(16, 1);
-    else if (mode == 2) NMT_DV(16, 2);
-    else NMT_DV(16, 0);
+    NMT_DVE(16)
   } else if (d == 256) {
-    if (mode == 1) NMT_DV(8, 1);
-    else if (mode == 2) NMT_DV(8, 2);
-    else NMT_DV(8, 0);
+    NMT_DVE(8)
   } else {
     k_dlcl<T><<<ceil_div(rows, 8), 256, 0, s>>>(y, hist, hist_stride, l, w, gdl, bdl, dlcl_ln, g2,
                                                  b2, xout, uout, rows, d, eps);
   }
+#undef NMT_DVE
 #undef NMT_DV
   NMT_LAUNCH_CHECK();
 }
@@ -747,7 +782,7 @@ void argmax_ids(unsigned long long* keys, int* ids, int rows, cudaStream_t s) {
                              const int*, cudaStream_t);                                         \
   template void dlcl_combine<T>(const T*, T*, size_t, int, const float*, const T*, const T*,    \
                                 int, const T*, const T*, T*, T*, int, int, float, cudaStream_t, \
-                                int, const float*, float*);                                     \
+                                int, const float*, float*, int);                                \
   template void to_float<T>(const T*, float*, size_t, cudaStream_t);                          \
   template void embed_dec_ln<T>(const int*, const T*, const float*, const T*, const T*, T*, T*, \
                                 int, int, float, float, const int*, const int*, cudaStream_t);

@@ -74,15 +74,18 @@ void layernorm(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, in
 // DLCL combine (Eq. 1-2), one launch per layer boundary l:
 //   z_l = LN^dl_l(y_l) -> hist[l];  x = sum_{k<=l} w[k] z_k;  (x -> xout, LN(x; g2,b2) -> uout)
 // dlcl_ln = 0: z_l = y_l (reading A22 test switch).
-// mode 1 also writes the FP32 partial P = sum_{k<=l} wP[k] z_k of the next boundary's
-// combination (wP = its weights row); mode 2 computes x = P + w[l] z_l without reading the
-// history (d = 256 / 512 only: dlcl_lookahead_ok).  x is the same in every mode.
+// Lookahead in blocks of boundaries (d = 256 / 512 only: dlcl_lookahead_ok; x is the same
+// in every mode): mode 1 (a block's first boundary) also writes the FP32 partials
+// P_i = sum_{k<=l} W^(l+1+i)[k] z_k, i = 1..arg (arg <= 3), at P + (i-1)*rows*d (wall = the
+// packed weight rows, row r at r(r-1)/2); mode 2 (a later boundary of the block) computes
+// x = P + sum_{k=l-arg}^{l-1} w[k] z_k + w[l] z_l from its partial and the arg history rows
+// written since the block started.
 bool dlcl_lookahead_ok(int d);
 template <class T>
 void dlcl_combine(const T* y, T* hist, size_t hist_stride, int l, const float* w, const T* gdl,
                   const T* bdl, int dlcl_ln, const T* g2, const T* b2, T* xout, T* uout, int rows,
-                  int d, float eps, cudaStream_t s, int mode = 0, const float* wP = nullptr,
-                  float* P = nullptr);
+                  int d, float eps, cudaStream_t s, int mode = 0, const float* wall = nullptr,
+                  float* P = nullptr, int arg = 0);
 
 // ---------------------------------------------------------------- attention
 // Encoder RPR self-attention (Shaw et al.) per (sentence, head):

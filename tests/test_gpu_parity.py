@@ -571,21 +571,27 @@ np.savez({path!r}, **out)
 
 
 def test_dlcl_lookahead_bit_identical(tmp_path):
-    """The DLCL two-boundary lookahead (FP32 partials) changes
-    which bytes are read, not the arithmetic: the 35-layer encoder output is bit-identical
-    with NMT_NO_DLCL_LA=1 (every boundary reads its whole history), FP32 and FP16 modes."""
+    """The DLCL lookahead (blocks of 2, 3 or 4 boundaries sharing one history read through
+    FP32 partials) changes which bytes are read, not the
+    arithmetic: the 35-layer encoder output is bit-identical with NMT_NO_DLCL_LA=1 (every
+    boundary reads its whole history), FP32 and FP16 modes, for the default block and each
+    block size (35 + 1 boundaries: blocks of 3 and 4 end on partial blocks)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for name, env in (("la", {}), ("plain", {"NMT_NO_DLCL_LA": "1"})):
+    modes = (("la", {}), ("plain", {"NMT_NO_DLCL_LA": "1"}), ("la2", {"NMT_DLCL_LA": "2"}),
+             ("la3", {"NMT_DLCL_LA": "3"}), ("la4", {"NMT_DLCL_LA": "4"}))
+    for name, env in modes:
         path = str(tmp_path / f"{name}.npz")
         code = _LA_SNIPPET.format(root=root, tests=os.path.join(root, "tests"), path=path)
-        subprocess.run([sys.executable, "-c", code], check=True, env={**os.environ, **env})
+        e = {k: v for k, v in os.environ.items() if k not in ("NMT_NO_DLCL_LA", "NMT_DLCL_LA")}
+        subprocess.run([sys.executable, "-c", code], check=True, env={**e, **env})
         res[name] = np.load(path)
-    for prec in ("fp32", "fp16"):
-        assert np.array_equal(res["la"][prec], res["plain"][prec]), prec
+    for name, _ in modes[2:] + modes[:1]:
+        for prec in ("fp32", "fp16"):
+            assert np.array_equal(res[name][prec], res["plain"][prec]), (name, prec)
 
 
 def test_step_timing_records():
