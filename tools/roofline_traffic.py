@@ -4,7 +4,8 @@ ncu --set full: layer 1's QKV / out-projection / FFN1 / FFN2 launches of the fir
 chunk 0) next to their algorithmic bytes, written to profiles/<tag>_enc_gemm_traffic.json
 for bench.py's roofline `traffic` field.
 
-Usage: python tools/roofline_traffic.py gpurun_out/<tag>_enc_gemm.ncu-rep <tag> [chunk]"""
+Usage: python tools/roofline_traffic.py gpurun_out/<tag>_enc_gemm.ncu-rep <tag> [chunk] [max_tokens max_sents]
+(the batch budget defaults to bench.py's)"""
 import csv
 import io
 import json
@@ -16,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def first_batch(chunk, max_tokens=65536, max_sents=8192):
+def first_batch(chunk, max_tokens=131072, max_sents=16384):
     """(B, S) of the first dynamic batch of bench chunk 0 (the paper's rule, DESIGN R17)."""
     from synth import newstest_like
     wl = newstest_like(chunk, 32000, start=0)
@@ -28,7 +29,7 @@ def first_batch(chunk, max_tokens=65536, max_sents=8192):
 def main():
     rep, tag = sys.argv[1], sys.argv[2]
     chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 1500
-    B, S = first_batch(chunk)
+    B, S = first_batch(chunk, *[int(x) for x in sys.argv[4:6]]) if len(sys.argv) > 5 else first_batch(chunk)
     M, d, F = B * S, 512, 2048
     # (name, N, K, residual): the launch order of one encoder layer (forward.cu)
     shapes = [("qkv", 3 * d, d, False), ("out", d, d, True), ("ffn1", F, d, False),
