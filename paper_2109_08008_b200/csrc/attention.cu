@@ -393,8 +393,10 @@ void attn_decoder_self(const T* qkv, T* kc, T* vc, int Tmax, const int* row_slot
 // keys at ckv + (slot*S + j)*ldkv + koff + h*dh, values at + voff; mask j < src_len[slot].
 // S = *dS (device) so a captured step graph serves every batch.  Beam rows share their
 // sentence's K/V (slot = row slot / beam).
+// 8 CTAs per SM (64 registers): at 8192 rows 110 -> 98 us per step; the self-attention keeps
+// 6 (at 8 its long-history steps slow down: 319 -> 385 us at t = 56..120)
 template <class T, int DH>
-__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 6 : 4) k_attn_cross(
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) k_attn_cross(
     const T* __restrict__ qb, const T* __restrict__ ckv, int ldkv, int koff, int voff,
     const int* __restrict__ dS, const int* __restrict__ src_len,
     const int* __restrict__ row_slot, T* __restrict__ out, int rows, int d, int H,
