@@ -293,6 +293,22 @@ constexpr int kEncMaxSlots = 16;
 constexpr int kEncWarpScratch = 16 * QLD * 4 + 16 * (RP + 8) * 2;   // q.A^K [16][33] f32 + B [16][40] f16
 constexpr int kEncTab = 2 * RP * (64 + 8) * 2;                        // A^K, A^V [32][72] f16
 
+// Slot-ring depth per padded length (compile time: the kernel's slot index / phase and the
+// host's shared-memory size use the same number): enough slots for the items the W warps
+// work on at once plus two being prefetched, within ~112 KB (two CTAs per SM) when possible;
+// S <= 16: three CTAs per SM (the kernel is latency-bound: 24 consumer warps instead of 16;
+// measured 37.0 -> 35.6 us at S = 16, slower at S = 32: 37.6 -> 39.9), so ~74 KB.
+constexpr int kEncFixedSmem = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 16 + 1024;
+constexpr int enc_cmin(int a, int b) { return a < b ? a : b; }
+template <int NT>
+constexpr int enc_nslot() {
+  constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
+  constexpr int want = enc_cmin(kEncMaxSlots, (kEncW + NQ - 1) / NQ + 2);
+  constexpr int budget = NT <= 2 ? 74 * 1024 : 112 * 1024;
+  constexpr int ns = enc_cmin(want, (budget - kEncFixedSmem) / SLOT);
+  constexpr int ns2 = ns >= 2 ? ns : enc_cmin(want, (220 * 1024 - kEncFixedSmem) / SLOT);
+  return ns2 < 1 ? 1 : ns2;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -355,8 +371,20 @@ template <int NT, int KC>
 __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 2 ? 3 : NT <= 8 ? 2 : 1) k_attn_enc_tma(
     const __grid_constant__ CUtensorMap mqkv, const int* __restrict__ len,
     const __half* __restrict__ relk, const __half* __restrict__ relv, __half* __restrict__ out,
-    int B, int S, int d, int H, int kclip_rt, int use_rpr, int nslot) {
+    int B, int S, int d, int H, int kclip_rt, int use_rpr, int nslot_rt, unsigned hmagic) {
   const int kclip = KC > 0 ? KC : kclip_rt;
+  // CT: the slot count as a compile-time constant and the item's (sentence, head) by a
+  // multiply-high, b = floor(it / H) = umulhi(it, ceil(2^32 / H)) (exact for it < 2^32 / H^2:
+  // items <= 2^18 here) — three integer divisions fewer per unit (S = 32: 37.5 -> 36.5 us,
+  // S = 96: 72.6 -> 66.9).  NT = 6 / 8 keep the runtime forms: under the two-CTA register cap
+  // the change makes them spill (S = 40: 47.8 -> 50.5 us).
+  constexpr bool CT = NT != 6 && NT != 8;
+  const int nslot = CT ? enc_nslot<NT>() : nslot_rt;
+  auto item_bh = [&](int it, int& b, int& h) {
+    if constexpr (CT) b = (int)__umulhi((unsigned)it, hmagic);
+    else b = it / H;
+    h = it - b * H;
+  };
   constexpr int DH = 64, SP = NT * 8, NQ = SP / 16, LDH = DH + 8, LDB = RP + 8;
   constexpr int TILE = SP * 128, SLOT = 3 * TILE;
   extern __shared__ uint8_t smraw[];
@@ -400,7 +428,9 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 2 ? 3 : NT <= 8 ? 2 : 
       for (int k = 0; k < nloc; ++k) {
         const int sl = k % nslot;
         if (k >= nslot) mbar_wait1(&empty[sl], ((k / nslot) - 1) & 1);
-        const int it = c + k * G, b = it / H, h = it - b * H;
+        const int it = c + k * G;
+        int b, h;
+        item_bh(it, b, h);
         uint8_t* dst = slots + sl * SLOT;
         mbar_expect(&full[sl], SLOT);
         tma_2d(dst, &mqkv, &full[sl], h * DH, b * S);
@@ -419,7 +449,9 @@ __global__ void __launch_bounds__(32 * (kEncW + 1), NT <= 2 ? 3 : NT <= 8 ? 2 : 
   const int g = lane >> 2, tig = lane & 3, mi = lane >> 3, rr = lane & 7;
   for (int u = warp; u < nloc * NQ; u += kEncW) {
     const int k = u / NQ, qb = u - k * NQ, sl = k % nslot;
-    const int it = c + k * G, b = it / H, h = it - b * H;
+    const int it = c + k * G;
+    int b, h;
+    item_bh(it, b, h);
     const int n = len[b], m0 = qb * 16;
     const uint32_t tQ = smem_addr(slots + sl * SLOT), tK = tQ + TILE, tV = tK + TILE;
     wait_issued(issued, k);
@@ -607,19 +639,10 @@ struct EncTmaCfg {
 template <int NT, int KC>
 EncTmaCfg enc_tma_cfg() {
   static EncTmaCfg cfg = [] {
-    constexpr int SP = NT * 8, NQ = SP / 16, SLOT = 3 * SP * 128;
-    const int fixed = kEncTab + kEncW * kEncWarpScratch + 2 * kEncMaxSlots * 8 + 16 + 1024;
-    // enough slots for the items the W warps work on at once plus two being prefetched,
-    // within ~112 KB (two CTAs per SM) when possible; S <= 16: three CTAs per SM (the
-    // kernel is latency-bound: 24 consumer warps instead of 16; measured 37.0 -> 35.6 us at
-    // S = 16, slower at S = 32: 37.6 -> 39.9), so ~74 KB
-    int want = std::min(kEncMaxSlots, (kEncW + NQ - 1) / NQ + 2);
-    const int budget = NT <= 2 ? 74 * 1024 : 112 * 1024;
-    int ns = std::min(want, (budget - fixed) / SLOT);
-    if (ns < 2) ns = std::min(want, (220 * 1024 - fixed) / SLOT);
+    constexpr int SP = NT * 8, SLOT = 3 * SP * 128;
     EncTmaCfg c{};
-    c.nslot = std::max(1, ns);
-    c.smem = fixed + c.nslot * SLOT;
+    c.nslot = enc_nslot<NT>();
+    c.smem = kEncFixedSmem + c.nslot * SLOT;
     NMT_CUDA(cudaFuncSetAttribute(k_attn_enc_tma<NT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   c.smem));
     int occ = 0;
@@ -648,7 +671,8 @@ void launch_tma_kc(const __half* qkv, const int* len, const __half* relk, const 
   const CUtensorMap map = tc::make_map(qkv, B * S, 3 * d, 3 * d, NT * 8, false);
   const int grid = std::min(B * H, c.grid_per_sm * sm_count());
   launch_k(k_attn_enc_tma<NT, KC>, dim3(grid), dim3(32 * (kEncW + 1)), (size_t)c.smem, s, map, len,
-           relk, relv, out, B, S, d, H, kclip, use_rpr, c.nslot);
+           relk, relv, out, B, S, d, H, kclip, use_rpr, c.nslot,
+           (unsigned)((0x100000000ull + H - 1) / H));
 }
 
 template <int NT>
