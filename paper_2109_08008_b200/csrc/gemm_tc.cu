@@ -38,8 +38,10 @@ namespace tc {
 // KS = 2: the split-K arithmetic of the cluster kernel below inside one persistent unit (two
 // TMEM accumulators per unit over the two K halves, reduced (0 + p0) + p1 in FP32 before the
 // epilogue): the large-row decode FFN2 keeps the association its small-row launches use.
+// AM: the vocab argmax epilogue by chunk maxima (its own instantiation: the extra arrays
+// would push the shared encoder-GEMM instantiation into spills).
 template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1, bool BEAM = false,
-          int KS = 1>
+          int KS = 1, bool AM = false>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
@@ -309,6 +311,66 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
       unsigned long long best = 0ull;
+      if constexpr (AM) {
+        // vocab argmax: per 32-column chunk only its maximum (independent max ops), the
+        // earliest chunk holding the row's maximum kept; then that chunk is read again from
+        // TMEM for the lowest column equal to the maximum — the same (value, lowest id) as a
+        // scan of every column, at about a third of the epilogue instructions
+        float bestv = 0.f;
+        int bestc = -1;
+#pragma unroll
+        for (int c0 = cb; c0 < cb + HALF; c0 += 32) {
+          if (n0 + c0 >= p.N) break;   // warp-uniform
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          const int nv = min(32, p.N - (n0 + c0));
+          float mx = v[0];
+          if (nv == 32) {
+            float m4[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) m4[j] = fmaxf(fmaxf(v[4 * j], v[4 * j + 1]), fmaxf(v[4 * j + 2], v[4 * j + 3]));
+            mx = fmaxf(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])),
+                       fmaxf(fmaxf(m4[4], m4[5]), fmaxf(m4[6], m4[7])));
+          } else {
+#pragma unroll
+            for (int j = 1; j < 32; ++j)
+              if (j < nv) mx = fmaxf(mx, v[j]);
+          }
+          if (bestc < 0 || mx > bestv) {
+            bestv = mx;
+            bestc = c0;
+          }
+        }
+        if (bestc >= 0) {   // warp-uniform (bestc >= 0 iff the warp's first chunk is inside N)
+          // tcgen05.ld addresses are per warp: re-read every chunk some lane of this warp won
+          // (usually one or two) and search it in the lanes that won it
+          int bj = 0;
+#pragma unroll 1
+          for (int c0 = cb; c0 < cb + HALF; c0 += 32) {
+            if (n0 + c0 >= p.N) break;
+            if (!__ballot_sync(0xffffffffu, bestc == c0)) continue;
+            float w[32];
+            __syncwarp();
+            tmem_ld32(tbase + c0, w);
+            if (bestc == c0) {
+              bj = 31;
+#pragma unroll
+              for (int j = 31; j >= 0; --j)
+                if (w[j] == bestv) bj = j;
+            }
+          }
+          best = pack_argmax(bestv, n0 + bestc + bj);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(acc ? te1 : te0);
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (row_ok && best) atomicMax(p.argmax + m, best);
+        continue;
+      }
       BeamAcc bacc;
       if constexpr (BEAM) bacc.init();
 #pragma unroll
@@ -720,13 +782,13 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false, int KS = 1>
+template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false, int KS = 1, bool AM = false>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
@@ -765,7 +827,7 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.rtma = NSTG >= 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
            (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && !no_rtma;
   const CUtensorMap mr = p.rtma ? make_map(a.R, a.M, a.N, a.ldr, 32, true) : CUtensorMap{};
-  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
+  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
   NMT_LAUNCH_CHECK();
 }
 
@@ -969,6 +1031,11 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const bool r2 = getenv("NMT_OUT_NSTG2") != nullptr;   // A/B only
     if (r2) tc::launch<256, 3, 8, 2>(a, s);
     else tc::launch<256, 3, 8, 4>(a, s);
+  } else if (a.argmax && !a.logits && !a.C && !a.bias && !a.R && !a.ln_st &&
+             !getenv("NMT_ARGMAX_SCAN")) {
+    // vocab projection + argmax: the chunk-maximum epilogue (NMT_ARGMAX_SCAN: per-column
+    // scan, A/B only)
+    tc::launch<256, 4, 8, 1, false, 1, true>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
     tc::launch<256, 4>(a, s);
