@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--no-paper-budget", action="store_true",
                     help="skip the decode-step timing at the paper's 4096 / 512 batch budget")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (30-6 beam 4) measurement")
-    ap.add_argument("--paper-workers", type=int, default=4,
+    ap.add_argument("--paper-workers", type=int, default=8,
                     help="batch workers of the paper-budget (4096 / 512) throughput leg")
     ap.add_argument("--whole-set", action="store_true",
                     help="C5: translate the whole synthetic set sharded over the ranks (strong "
@@ -568,7 +568,8 @@ def main():
         if not args.no_paper_tok_s:
             # whole-chunk throughput at the paper's budget (C3: 4096 tokens / 512 sentences,
             # PAPER.md:121, :138), same chunk, device-resident (one warm run); its own worker
-            # count (small batches: 4 concurrent batches fill the GPU best)
+            # count (small batches: 8 concurrent batches, tools/paper_workers.sh: 4 -> 1.09M,
+            # 6 -> 1.16M, 8 -> 1.21M)
             wl_p, d_ids_p = chunks[args.warmup]
             for rep in range(2):
                 barrier()
