@@ -594,6 +594,24 @@ def test_dlcl_lookahead_bit_identical(tmp_path):
             assert np.array_equal(res[name][prec], res["plain"][prec]), (name, prec)
 
 
+def test_decode_gemm_tile_and_split_invariance():
+    """The decode GEMM's output tile widens with the launch's row bound and FFN2's split-K
+    moves from the cluster kernel to persistent KS = 2 units above 2048 rows (gemm_tc.cu
+    decode_config): neither may change a result.  tools/tile_identity.py runs the 35-1 decoder
+    projections at 100 / 1000 / 3000 / 8000 rows with tiles 64 / 128 / 256 forced, and the
+    library policy against the cluster kernel forced, in child processes (the policy
+    switches are read once per process); every output must be bit-identical."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "tile_identity.py"), "100", "1000",
+                        "3000", "8000"], capture_output=True, text=True, check=True)
+    lines = [l for l in r.stdout.splitlines() if "IDENTICAL" in l or "DIFFER" in l]
+    assert len(lines) == 4 * 4 + 4, r.stdout[-2000:]
+    assert not [l for l in lines if "DIFFER" in l], r.stdout[-2000:]
+
+
 def test_step_timing_records():
     """nmt_profile mode 3 + nmt_profile_steps (SURVEY §8(d) ms/decode step): one record per
     graph-replayed decode step, live rows non-increasing within a batch, positive device
