@@ -229,12 +229,15 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            # same model, metric and synthetic 1M newstest-shaped set as the product arm; a
-            # bounded slice of it per step, batched at the paper's CPU budget
-            "config": {"workload": f"{args.config} greedy, bounded slice of the product arm's "
-                                   f"synthetic newstest-shaped set, oracle O-fast (FP32 NumPy)",
-                       "max_tokens": 4096, "max_sents": 512,
-                       "parallelism": f"sentence-sharded x{used} CPU processes"},
+            # the product arm's config (same model, metric and synthetic 1M newstest-shaped
+            # set); per step a bounded slice of it, which each oracle process batches at the
+            # paper's CPU budget — batching changes no output
+            "config": {"workload": f"{args.config} FP16 greedy, {args.chunk}-sentence newstest-shaped "
+                                   f"chunk per rank per step, batch pruning rho=0.25 (reference arm: "
+                                   f"the oracle, O-fast FP32 NumPy, on a bounded slice of it)",
+                       "max_tokens": args.max_tokens, "max_sents": args.max_sents,
+                       "parallelism": f"sentence-sharded x{used} CPU processes",
+                       "oracle_batch_plan": "4096 tokens / 512 sentences per process"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
