@@ -339,25 +339,43 @@ __global__ void __launch_bounds__(256) k_layernorm_vec(const T* __restrict__ in,
                                                        float eps, const int* __restrict__ dR) {
   pdl_trigger();
   pdl_wait();
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  // grid-stride over rows with the next row's load issued before this row's reductions (a
+  // bounded grid instead of one short-lived warp per row)
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nrows = dR ? min(rows, *dR) : rows;
   if (row >= nrows) return;
-  float v[E];
+  float v[E], nx[E];
   ldrow<T, E>(in + (size_t)row * ldi + lane * E, v);
-  ln_contig<T, E>(v, 32 * E, g, b, eps, lane);
-  strow<T, E>(out + (size_t)row * ldo + lane * E, v);
+  for (;;) {
+    const int nr = row + nw;
+    if (nr < nrows) ldrow<T, E>(in + (size_t)nr * ldi + lane * E, nx);
+    ln_contig<T, E>(v, 32 * E, g, b, eps, lane);
+    strow<T, E>(out + (size_t)row * ldo + lane * E, v);
+    if (nr >= nrows) break;
+    row = nr;
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = nx[i];
+  }
 }
 
 template <class T>
 bool layernorm_vec(const T* in, int ldi, const T* g, const T* b, T* out, int ldo, int rows, int d,
                    float eps, const int* dR, cudaStream_t s) {
   const bool al = (ldi % 8 == 0) && (ldo % 8 == 0);
+  static const int cap = [] {   // one wave of resident 256-thread CTAs
+    int dev = 0, sms = 0, occ16 = 0;
+    NMT_CUDA(cudaGetDevice(&dev));
+    NMT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    NMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ16, k_layernorm_vec<T, 16>, 256, 0));
+    return std::max(1, occ16) * sms;
+  }();
+  const int grid = std::min(ceil_div(rows, 8), cap);
   if (d == 512 && al)
-    launch_k(k_layernorm_vec<T, 16>, ceil_div(rows, 8), 256, 0, s, in, ldi, g, b, out, ldo, rows,
-             eps, dR);
+    launch_k(k_layernorm_vec<T, 16>, grid, 256, 0, s, in, ldi, g, b, out, ldo, rows, eps, dR);
   else if (d == 256 && al)
-    launch_k(k_layernorm_vec<T, 8>, ceil_div(rows, 8), 256, 0, s, in, ldi, g, b, out, ldo, rows,
-             eps, dR);
+    launch_k(k_layernorm_vec<T, 8>, grid, 256, 0, s, in, ldi, g, b, out, ldo, rows, eps, dR);
   else
     return false;
   NMT_LAUNCH_CHECK();
