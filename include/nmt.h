@@ -329,6 +329,13 @@ nmt_status nmt_debug_fused_trace(nmt_model* m, uint64_t* h_out, int64_t cap);
  * TMEM freed} at h_out[8k + e].  Synchronises the device. */
 nmt_status nmt_debug_attn_trace(uint64_t* h_out, int64_t cap);
 
+/* Debug timeline of the persistent tcgen05 GEMM (environment variable NMT_GEMM_TRACE set at
+ * the launch; single-CTA units): for CTA c < 148 and its local unit k < 32, 8 globaltimer
+ * stamps at h_out[(c*32 + k)*8 + e]: {producer first / last load of the unit, MMA accumulator
+ * free / last commit, epilogue warp 4 waits / sees the accumulator, releases it, issues the
+ * unit's last store}.  Stamps persist until overwritten.  Synchronises the device. */
+nmt_status nmt_debug_gemm_trace(uint64_t* h_out, int64_t cap);
+
 /* ---- kernel-level entry points used by the unit parity tests ------------------- */
 /* C[M][N] = A[M][K] * B[N][K]^T (+bias[N]) (+R[M][N]) (relu) in the model precision
  * (FP16: tcgen05/TMEM/TMA tensor-core GEMM; FP32: SIMT), all pointers device, row-major

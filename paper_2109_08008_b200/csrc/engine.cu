@@ -1478,6 +1478,14 @@ nmt_status nmt_profile(nmt_model* m, int32_t mode, nmt_prof_entry* out, int32_t 
   });
 }
 
+nmt_status nmt_debug_gemm_trace(uint64_t* h_out, int64_t cap) {
+  return guard([&] {
+    NMT_REQUIRE(h_out && cap > 0, NMT_E_ARG, "null argument");
+    tc::gemm_trace(reinterpret_cast<unsigned long long*>(h_out),
+                   (int)std::min<int64_t>(cap, 148 * 32 * 8));
+  });
+}
+
 nmt_status nmt_debug_attn_trace(uint64_t* h_out, int64_t cap) {
   return guard([&] {
     NMT_REQUIRE(h_out && cap > 0, NMT_E_ARG, "null argument");

@@ -27,6 +27,23 @@
 namespace nmt {
 namespace tc {
 
+// Debug timeline (NMT_GEMM_TRACE set at the launch; single-CTA units only): CTA c, local unit
+// k < 32, 8 globaltimer stamps at g_gemm_trace[(c * 32 + k) * 8 + e]: 0 producer: first load
+// of the unit issued, 1 producer: last load issued, 2 MMA: accumulator free (tempty), 3 MMA:
+// last commit (tfull), 4 epilogue warp 4: starts waiting for tfull, 5 warp 4: tfull seen,
+// 6 warp 4: accumulator released, 7 warp 4: last store of the unit issued.
+__device__ unsigned long long g_gemm_trace[148 * 32 * 8];
+__device__ __forceinline__ unsigned long long gt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GT(k, e)                                                                        \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x < 148 && (k) < 32)                                        \
+      g_gemm_trace[((size_t)blockIdx.x * 32 + (k)) * 8 + (e)] = gt_now();               \
+  } while (0)
+
 // PAIR = true: a CTA pair (cluster of 2 on one TPC) computes 256 x BN output units with
 // tcgen05.mma.cta_group::2 (M = 256).  Each CTA stages its own 128 rows of A and BN/2 rows
 // of B per k-block, so every SM moves (128 + BN/2) * BK * 2 bytes per 2*128*BN*BK FLOP —
@@ -40,8 +57,11 @@ namespace tc {
 // epilogue): the large-row decode FFN2 keeps the association its small-row launches use.
 // AM: the vocab argmax epilogue by chunk maxima (its own instantiation: the extra arrays
 // would push the shared encoder-GEMM instantiation into spills).
+// PL: plain FP16 epilogue (bias, ReLU, TMA stores; no residual / LN statistics / argmax),
+// TMEM loads double-buffered: the next chunk's tcgen05.ld is in flight during this chunk's
+// math and staging (the epilogue is a latency chain of ~4 dependent steps per chunk).
 template <int BN, int STAGES, bool PAIR = false, int EW = 8, int NSTG = 1, bool BEAM = false,
-          int KS = 1, bool AM = false>
+          int KS = 1, bool AM = false, bool PL = false>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
@@ -150,11 +170,13 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           mbar_wait(&full[st], 0);
         }
       }
-      int it = 0;
-      for (int u = cid; u < units; u += ncl) {
+      int it = 0, lu = 0;
+      for (int u = cid; u < units; u += ncl, ++lu) {
         const int mi = p.nfast ? u / num_n : u % num_m, ni = p.nfast ? u % num_n : u / num_m;
         const int m0 = mi * UM + rank * BM, n0 = ni * BN + rank * (SM::BROWS);
         for (int kb = 0; kb < kb_total; ++kb, ++it) {
+          if (kb == 1) GT(lu, 0);
+          if (kb == kb_total - 1) GT(lu, 1);
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[st], ph ^ 1);
@@ -194,6 +216,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         const int acc = NACC == 2 ? (local & 1) : 0;
         const uint32_t aph = NACC == 2 ? (local >> 1) & 1 : local & 1;
         mbar_wait(&tempty[acc], aph ^ 1);   // epilogue(s) drained this accumulator
+        GT(local, 2);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d0 = tmem + acc * ACC_COLS;
         const int kps = kb_total / KS;   // KS = 2: k-blocks [0, kps) -> d0, [kps, 2 kps) -> d0 + BN
@@ -222,6 +245,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         }
         if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
         else mma_commit(&tfull[acc]);
+        GT(local, 3);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
@@ -307,7 +331,9 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         if (row_ok) ln = merge_stats(p.ln_st + (size_t)m * (p.K / 32), p.K / 32, p.ln_eps);
       }
       __syncwarp();
+      if (warp == 4 && lane == 0) GT(local, 4);
       mbar_wait(&tfull[acc], aph);
+      if (warp == 4 && lane == 0) GT(local, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16);
       unsigned long long best = 0ull;
@@ -371,6 +397,69 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         if (row_ok && best) atomicMax(p.argmax + m, best);
         continue;
       }
+      if constexpr (PL) {
+        constexpr int NCH = HALF / 32;
+        uint32_t rr[2][32];
+        __syncwarp();
+        tmem_ld32_nw(tbase + cb, rr[0]);
+#pragma unroll
+        for (int ci = 0; ci < NCH; ++ci) {
+          const int c0 = cb + ci * 32;
+          tmem_wait_ld(rr[ci & 1]);
+          if (ci + 1 < NCH) {
+            __syncwarp();
+            tmem_ld32_nw(tbase + c0 + 32, rr[(ci + 1) & 1]);
+          } else {   // every TMEM load of this warp has completed: release the accumulator
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (PAIR) mbar_arrive_cluster(acc ? te1 : te0);
+              else mbar_arrive(&tempty[acc]);
+              if (warp == 4) GT(local, 6);
+            }
+          }
+          if (n0 + c0 >= p.N) continue;   // warp-uniform
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[ci & 1][j]);
+          if (p.bias) {
+            const float* bp = bias_all ? sbias + n0 + c0 : sb + (c0 - cb);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b = *reinterpret_cast<const float4*>(bp + j);
+              v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
+            }
+          }
+          uint32_t h[16];
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat_relu(v[2 * i], v[2 * i + 1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) h[i] = pack_half2_sat(v[2 * i], v[2 * i + 1]);
+          }
+          uint8_t* stg = stg0 + (NSTG == 2 ? (kchunk & 1) * SM::STG : 0);
+          const int sw = (lane >> 1) & 3;
+          if (lane == 0) {
+            if constexpr (NSTG == 1) bulk_wait_read0();
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
+          ++kchunk;
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ sw) << 4)) =
+                make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&mapC, stg, n0 + c0, m0 + q * 32);
+            bulk_commit();
+          }
+        }
+        if (warp == 4 && lane == 0) GT(local, 7);
+        continue;
+      }
       BeamAcc bacc;
       if constexpr (BEAM) bacc.init();
 #pragma unroll
@@ -393,6 +482,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           if (lane == 0) {
             if constexpr (PAIR) mbar_arrive_cluster(acc ? te1 : te0);
             else mbar_arrive(&tempty[acc]);
+            if (warp == 4) GT(local, 6);
           }
         }
         if (p.dbg & 1) {
@@ -473,6 +563,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       // RALL: a unit that stored fewer than NSTG chunks (N edge) drains its stores, so every
       // staging tile is again last written NSTG groups back
       if (RALL && p.tstore && !rt && lane == 0 && n0 + cb + HALF > p.N) bulk_wait_read0();
+      if (warp == 4 && lane == 0) GT(local, 7);
       if (p.argmax && row_ok && best) atomicMax(p.argmax + m, best);
       if (BEAM && row_ok && n0 + cb < p.N) {   // this thread's segment of the row
         const int nseg = (p.N + HALF - 1) / HALF;
@@ -782,13 +873,14 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false, int KS = 1, bool AM = false>
+template <int BN, int STAGES, int EW = 8, int NSTG = 1, bool BEAM = false, int KS = 1, bool AM = false,
+          bool PL = false>
 void launch(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, false, EW, NSTG>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM, PL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
@@ -815,6 +907,8 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.ln_c = a.ln_c;
   p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
+  static const bool trace = getenv("NMT_GEMM_TRACE") != nullptr;   // debug timeline only
+  p.trace = trace && !BEAM;
   static const bool morder = getenv("NMT_GEMM_ORDER") && getenv("NMT_GEMM_ORDER")[0] == 'm';  // A/B only
   p.nfast = !morder;
   static const bool no_bpre = getenv("NMT_NO_BPRE") != nullptr;   // A/B only
@@ -827,18 +921,19 @@ void launch(const GemmArgs& a, cudaStream_t s) {
   p.rtma = NSTG >= 2 && p.tstore && a.R && !a.ln_st && !a.relu && (a.ldr % 8) == 0 &&
            (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && !no_rtma;
   const CUtensorMap mr = p.rtma ? make_map(a.R, a.M, a.N, a.ldr, 32, true) : CUtensorMap{};
-  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
+  if (PL && (a.R || a.ln_st || a.st_out || !p.tstore)) throw CudaError("gemm_tc: plain epilogue misuse");
+  launch_k(k_gemm_tc<BN, STAGES, false, EW, NSTG, BEAM, KS, AM, PL>, grid, 128 + 32 * EW, SM::BYTES, s, ma, mb, mc, mr, p);
   NMT_LAUNCH_CHECK();
 }
 
 // CTA-pair launch: clusters of 2 (one TPC), persistent over 256 x BN units.
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EW = 8, bool PL = false>
 void launch_pair(const GemmArgs& a, cudaStream_t s) {
-  using SM = Smem<BN, STAGES, true>;
+  using SM = Smem<BN, STAGES, true, EW>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, false, PL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
@@ -863,12 +958,14 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   p.ln_c = a.ln_c;
   p.ln_eps = a.ln_eps;
   p.dbg = getenv("NMT_GEMM_DBG") ? atoi(getenv("NMT_GEMM_DBG")) : 0;
+  static const bool trace = getenv("NMT_GEMM_TRACE") != nullptr;   // debug timeline only
+  p.trace = trace;
   p.nfast = 1;
   const int units = ceil_div(a.M, 2 * BM) * ceil_div(a.N, BN);
   const int pairs = std::min(units, num_sms() / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(128 + 32 * EW);
   cfg.dynamicSmemBytes = SM::BYTES;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -881,7 +978,9 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 2 : 1;
   const CUtensorMap mc = out_map(a, p);
-  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true>, ma, mb, mc, CUtensorMap{}, p));
+  if (PL && (a.R || a.ln_st || a.st_out || !p.tstore)) throw CudaError("gemm_tc: plain epilogue misuse");
+  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, false, PL>, ma, mb, mc,
+                              CUtensorMap{}, p));
   NMT_LAUNCH_CHECK();
 }
 
@@ -929,6 +1028,12 @@ void launch_cluster(const GemmArgs& a, cudaStream_t s) {
   cfg.numAttrs = g_pdl ? 2 : 1;
   NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc_cluster<STAGES>, ma, mb, p));
   NMT_LAUNCH_CHECK();
+}
+
+void gemm_trace(unsigned long long* h_out, int cap) {
+  NMT_CUDA(cudaDeviceSynchronize());
+  NMT_CUDA(cudaMemcpyFromSymbol(h_out, g_gemm_trace,
+                                sizeof(unsigned long long) * std::min(cap, 148 * 32 * 8)));
 }
 
 }  // namespace tc
@@ -1012,6 +1117,13 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     else if (c == "pair256x4") tc::launch_pair<256, 4>(a, s);
     else if (c == "pair256x5") tc::launch_pair<256, 5>(a, s);
     else if (c == "pair256x6") tc::launch_pair<256, 6>(a, s);
+    else if (c == "pair256x5w16") tc::launch_pair<256, 5, 16>(a, s);
+    else if (c.rfind("pl", 0) == 0 && (a.R || a.ln_st || a.st_out || a.argmax || a.logits || !a.C))
+      tc::launch<256, 4>(a, s);   // plain-epilogue configs apply to plain GEMMs only
+    else if (c == "pl256x4") tc::launch<256, 4, 8, 1, false, 1, false, true>(a, s);
+    else if (c == "plpair256x5") tc::launch_pair<256, 5, 8, true>(a, s);
+    else if (c == "plpair256x6") tc::launch_pair<256, 6, 8, true>(a, s);
+    else if (c == "pair256x4w16") tc::launch_pair<256, 4, 16>(a, s);
     else if (c == "512x2") tc::launch<512, 2>(a, s);
     else if (c == "256x3d") tc::launch<256, 3, 8, 2>(a, s);
     else if (c == "256x3q") tc::launch<256, 3, 8, 4>(a, s);
@@ -1023,6 +1135,14 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // CTA stages half of the B tile), 5 stages: 129 -> 121 us at M = 65520
     // (tools/gemm_bench.py); chosen from the weight shape only (batch invariance)
     tc::launch_pair<256, 5>(a, s);
+  } else if (!a.R && !a.ln_st && !a.st_out && !a.argmax && !a.logits && !a.dM && a.C &&
+             (a.ldc % 8) == 0 && (a.N % 8) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 &&
+             !getenv("NMT_NO_PLAIN_PAIR")) {
+    // encoder QKV / FFN1 / cross K/V (bias, ReLU, FP16 out): 256 x 256 CTA-pair units with the
+    // plain double-buffered-TMEM epilogue (tools/gemm_trace.py: the GEMMs are bound by shared-
+    // memory traffic; a pair stages half the B tile per CTA): QKV 103.7 -> 99.6, FFN1 135.2 ->
+    // 127.7, cross K/V 71.6 -> 69.5 us at M = 65520; chosen from the shape only
+    tc::launch_pair<256, 5, 8, true>(a, s);
   } else if (a.R && a.K <= 512 && !a.ln_st && !a.relu) {
     // residual GEMM with a short main loop (attention output projection): 3 stages and two
     // staging tiles per epilogue warp, the residual blocks TMA-loaded ahead of their chunk

@@ -98,6 +98,9 @@ void attn_encoder(const T* qkv, const int* len, const T* relk, const T* relv, T*
 void attn_encoder_umma(const __half* qkv, const int* len, const __half* relk, const __half* relv,
                        __half* out, int B, int S, int d, int H, int kclip, cudaStream_t s);
 void attn_umma_trace(unsigned long long* h_out, int cap);   // debug (nmt_debug_attn_trace)
+namespace tc {
+void gemm_trace(unsigned long long* h_out, int cap);   // debug (nmt_debug_gemm_trace)
+}
 // FP16 path of attn_encoder: Q K^T, q.A^K and P V + B A^V on tensor cores (attention_tc.cu).
 void attn_encoder_tc(const __half* qkv, const int* len, const __half* relk, const __half* relv,
                      __half* out, int B, int S, int d, int H, int kclip, int use_rpr,

@@ -211,6 +211,7 @@ struct Params {
   int tstore;         // FP16 C written by TMA stores (mapC), see k_gemm_tc
   int rtma;           // residual 32 x 32 blocks TMA-loaded into the staging tiles (mapR)
   int bpre;           // first-unit weight tiles requested before the PDL wait
+  int trace;          // NMT_GEMM_TRACE: per (CTA, local unit < 32) globaltimer stamps (g_gemm_trace)
   int nfast;          // unit order: 1 = column tiles of one row block on consecutive CTAs
                       // (the A row block is read from DRAM once and shared through L2)
   float2* st_out;     // LN folding, producer side (GemmArgs)

@@ -27,7 +27,7 @@ EXPORTS = ["nmt_load_weights", "nmt_get_config", "nmt_free_model", "nmt_encode",
            "nmt_translate_nbest", "nmt_ensemble_create", "nmt_ensemble_free",
            "nmt_translate_ensemble", "nmt_text_load", "nmt_text_free", "nmt_text_vocab_size",
            "nmt_text_encode", "nmt_text_decode", "nmt_dev_attn_encoder",
-           "nmt_profile_steps", "nmt_batch_free", "nmt_ntsd_inspect", "nmt_debug_fused_trace", "nmt_debug_attn_trace"]
+           "nmt_profile_steps", "nmt_batch_free", "nmt_ntsd_inspect", "nmt_debug_fused_trace", "nmt_debug_attn_trace", "nmt_debug_gemm_trace"]
 
 
 class ProfEntry(C.Structure):
