@@ -927,13 +927,13 @@ void launch(const GemmArgs& a, cudaStream_t s) {
 }
 
 // CTA-pair launch: clusters of 2 (one TPC), persistent over 256 x BN units.
-template <int BN, int STAGES, int EW = 8, bool PL = false>
+template <int BN, int STAGES, int EW = 8, bool PL = false, bool AM = false>
 void launch_pair(const GemmArgs& a, cudaStream_t s) {
   using SM = Smem<BN, STAGES, true, EW>;
   static_assert(SM::BYTES <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
   // thread-safe one-time attribute setup (C++11 static initialisation)
   static const bool attr = [&] {
-    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, false, PL>,
+    NMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, AM, PL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES));
     return true;
   }();
@@ -979,7 +979,7 @@ void launch_pair(const GemmArgs& a, cudaStream_t s) {
   cfg.numAttrs = g_pdl ? 2 : 1;
   const CUtensorMap mc = out_map(a, p);
   if (PL && (a.R || a.ln_st || a.st_out || !p.tstore)) throw CudaError("gemm_tc: plain epilogue misuse");
-  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, false, PL>, ma, mb, mc,
+  NMT_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, STAGES, true, EW, 1, false, 1, AM, PL>, ma, mb, mc,
                               CUtensorMap{}, p));
   NMT_LAUNCH_CHECK();
 }
@@ -1154,8 +1154,11 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   } else if (a.argmax && !a.logits && !a.C && !a.bias && !a.R && !a.ln_st &&
              !getenv("NMT_ARGMAX_SCAN")) {
     // vocab projection + argmax: the chunk-maximum epilogue (NMT_ARGMAX_SCAN: per-column
-    // scan, A/B only)
-    tc::launch<256, 4, 8, 1, false, 1, true>(a, s);
+    // scan, A/B only), on CTA-pair units (the argmax epilogue is light: the pair's shared-
+    // memory saving goes to the mainloop; NMT_NO_PAIR_VOCAB: single-CTA units, A/B only)
+    static const bool no_pair = getenv("NMT_NO_PAIR_VOCAB") != nullptr;
+    if (no_pair) tc::launch<256, 4, 8, 1, false, 1, true>(a, s);
+    else tc::launch_pair<256, 5, 8, false, true>(a, s);
   } else {
     // 128 x 256 tiles: 85 FLOP per staged byte at K = 512 (64 for 128 x 128)
     tc::launch<256, 4>(a, s);
