@@ -38,7 +38,7 @@ CHUNK = 192000          # 64 newstest2018-sized sets (2998 sentences each, PAPER
 BUCKETS = [(1, 16), (17, 64), (65, 148), (149, 512), (513, 2048), (2049, 8192), (8193, 16384)]
 T_WINDOW = (12, 20)     # "at t ~ 16"
 STEP_SENTS = 12000      # sentences of the step-timing run
-TRAFFIC_FILE = "profiles/r2x_enc_gemm_traffic.json"
+TRAFFIC_FILE = "profiles/r2y_enc_gemm_traffic.json"
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # Encoder GEMMs are dense contractions at N = 16K+ rows (tensor-bound).  Other classes take
 # the binding roof of their algorithmic FLOPs and bytes (decoder GEMMs / vocab projection:
