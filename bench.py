@@ -251,19 +251,20 @@ def c4_measure(args, reps=3):
     from paper_2109_08008_b200 import Model
     cfg = PRESETS["teacher-30-6"]
     W = generate_weights(cfg)
-    m = Model(cfg, W, precision="fp16", max_tokens=4096, max_sents=128, beam=4)
+    cw = 4   # concurrent batch workers: the 6-layer beam decode is a latency chain
+    m = Model(cfg, W, precision="fp16", max_tokens=4096, max_sents=128, beam=4, workspaces=cw)
     wl = newstest_like(512, cfg.vocab_size, start=0)
     d_ids = torch.from_numpy(wl.ids).cuda()
     d_out = torch.empty(wl.n, m.Tmax, dtype=torch.int32, device="cuda")
     d_len = torch.empty(wl.n, dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream()
-    m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4)   # graphs
+    m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4, workers=cw)   # graphs
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     gen = steps = 0
     for _ in range(reps):
-        st = m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4)
+        st = m.translate_device(d_ids, wl.off, d_out, d_len, caps=wl.caps, beam=4, workers=cw)
         gen += st["gen_tokens"]
         steps += st["decode_steps"]
     e1.record(s)
@@ -285,7 +286,7 @@ def c4_measure(args, reps=3):
                    "frac": round(1e3 * max(tt, th) / v["ms"], 4) if v["ms"] else None}
     del m
     return {"value": gen / reps / (ms / 1e3), "unit": UNIT, "model": "teacher-30-6 DLCL+RPR FP16",
-            "beam": 4, "sentences": wl.n, "max_tokens": 4096, "max_sents": 128,
+            "beam": 4, "sentences": wl.n, "max_tokens": 4096, "max_sents": 128, "workers": cw,
             "ms_per_pass": ms, "decode_steps_per_pass": steps // reps,
             "ms_per_decode_step": ms / max(1, steps // reps),
             "epilogue": "fused beam epilogue (no logits)" if os.environ.get("NMT_BEAM_EPI")

@@ -543,6 +543,22 @@ def test_concurrent_workers_identical():
     assert st["gen_tokens"] == st1["gen_tokens"]
 
 
+def test_concurrent_workers_identical_beam():
+    """Beam search (30-6 teacher, FP16, beam 4) with 4 concurrent batch workers (the C4
+    measurement's setting) gives the same hypotheses and scores as one worker."""
+    wl = newstest_like(96, 32000, start=4000)
+    caps = np.minimum(wl.caps, 40)
+    gm = gpu_model("teacher-30-6", "fp16", max_tokens=1024, max_sents=16, max_tgt_len=40, beam=4,
+                   workspaces=4)
+    ref, st1 = gm.translate(wl.ids, wl.off, caps=caps, beam=4)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        out, st = gm.translate(wl.ids, wl.off, caps=caps, beam=4, workers=4)
+    torch.cuda.synchronize()
+    assert out == ref
+    assert st["gen_tokens"] == st1["gen_tokens"] and st["batches"] == st1["batches"]
+
+
 def test_batch_invariance_fp32():
     """Sentence alone == sentence inside a bigger batch (PAPER.md:121 batching is exact)."""
     wl = newstest_like(16, 32000, start=50)
