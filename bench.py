@@ -687,7 +687,7 @@ def main():
                                    f"{args.workers} concurrent batch workers",
                        "max_tokens": args.max_tokens, "max_sents": args.max_sents,
                        "parallelism": f"sentence-sharded x{world}",
-                       "l2": "working set > L2 (262 MB FP16 weights + DLCL history)"},
+                       "l2": "working set > L2 (FP16 weights + DLCL history + batch activations)"},
             # device time of one decode step (its CUDA graph bracketed by event nodes,
             # finish/prune included), one worker, STEP_SENTS sentences of the chunk: mean over
             # all steps and median per live-row bucket at t in T_WINDOW
