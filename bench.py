@@ -573,7 +573,7 @@ def main():
             # whole-chunk throughput at the paper's budget (C3: 4096 tokens / 512 sentences,
             # PAPER.md:121, :138), same chunk, device-resident (one warm run); its own worker
             # count (small batches: 8 concurrent batches, tools/paper_workers.sh: 4 -> 1.09M,
-            # 6 -> 1.16M, 8 -> 1.21M)
+            # 6 -> 1.16M, 8 -> 1.21M; 12 / 16 -> 1.23M / 1.25M, within the spread)
             wl_p, d_ids_p = chunks[args.warmup]
             for rep in range(2):
                 barrier()

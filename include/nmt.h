@@ -70,8 +70,8 @@ typedef struct {
   int32_t max_sents;    /* sentences per batch (PAPER.md:138 uses 512)                           */
   int32_t max_tgt_len;  /* <= config max_tgt_len; decode steps per batch                          */
   int32_t beam;         /* 1 = greedy                                                              */
-  int32_t n_workspaces; /* arenas allocated at load (0 or 1 = one): the upper bound of
-                           nmt_translate_opts.n_workers (concurrent batch workers)                 */
+  int32_t n_workspaces; /* arenas allocated at load (0 or 1 = one, at most 16): the upper bound
+                           of nmt_translate_opts.n_workers (concurrent batch workers)              */
 } nmt_limits;
 
 typedef struct nmt_model nmt_model;   /* opaque: device weights + arena */

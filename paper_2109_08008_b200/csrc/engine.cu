@@ -409,7 +409,7 @@ nmt_model* load(const void* blob, size_t nbytes, int device, nmt_precision prec,
   auto& recs = P.recs;
   NMT_REQUIRE(lim->max_tokens >= 1 && lim->max_sents >= 1 && lim->max_tgt_len >= 1 &&
                   lim->max_tgt_len <= cfg.max_tgt_len && lim->beam >= 1 &&
-                  lim->n_workspaces >= 0 && lim->n_workspaces <= 8,
+                  lim->n_workspaces >= 0 && lim->n_workspaces <= 16,
               NMT_E_ARG, "bad limits");
   NMT_REQUIRE(lim->beam <= 4, NMT_E_UNSUPPORTED, "beam > 4 is not built");
   NMT_REQUIRE((size_t)lim->max_sents * lim->beam <= 16384, NMT_E_ARG, "max_sents*beam > 16384");
@@ -793,7 +793,7 @@ void translate_core(nmt_model* m, const int64_t* h_off, int64_t n, const nmt_tra
   const int every = o && o->prune_every > 0 ? o->prune_every : 1;
   const float ratio = o ? o->prune_ratio : 0.25f;
   const int sync_every = o && o->sync_every > 0 ? o->sync_every : 4;
-  const int W = o && o->n_workers > 1 ? std::min(o->n_workers, 8) : 1;
+  const int W = o && o->n_workers > 1 ? std::min(o->n_workers, 16) : 1;
   const int K = o && o->beam > 1 ? o->beam : 1;  // beam width; 1 = greedy
   const int NB = o && o->nbest > 1 ? o->nbest : 1;  // n-best lists
   NMT_REQUIRE(NB <= K, NMT_E_ARG, "nbest must be <= beam");
